@@ -1,0 +1,511 @@
+#!/usr/bin/env python
+"""Benchmark: decode tokens/s of a Mixtral-8x7B-shaped MoE layer, INT2 experts +
+rank-32 INT3 low-rank compensation on each token's top-1 expert (BASELINE.json
+configs[1]), plus the fraction of the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+A "step" is one MoE-layer forward (fused router -> LR down-projection ->
+tiled 2-bit W1/W3 SwiGLU kernel with U.(V.x) -> tiled W2 kernel with the
+weighted combine) over one decode batch of B synthetic tokens.  Steps rotate
+over L = 8 distinct resident layers (8 x 8 experts x 55.9 MB = 3.6 GB of
+codes), so every step streams its experts from HBM (inputs larger than the
+126 MB L2; no flush needed).  value = layer-tokens/s = K*B / device time.
+
+--impl reference times the reference CPU implementation of the path (the
+oracle port of moe.forward(..., "compensated"), oracle/lrc.py) on the host
+cores with the same metric, one token per step.
+
+Multi-GPU (torchrun): every rank runs the same per-GPU workload (replicas,
+weak scaling); time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+HIDDEN, FFN, E, TOPK, TOPN, RANK, BITS = 4096, 14336, 8, 2, 1, 32, 2
+METRIC = "decode tokens/s, Mixtral-8x7B MoE layer 2-bit+rank-r top-1; % of roofline"
+
+
+# ------------------------------------------------------------ byte / flop model --
+def packed_size_bytes(rows, cols, bits, include_metadata=False, group_size=64):
+    n = (rows * cols * bits + 7) // 8
+    if include_metadata:
+        n += rows * (-(-cols // group_size)) * 4
+    return n
+
+
+def expert_bytes(hidden, ffn, bits):
+    """w1 + w3 + w2 codes + fp16 scale/zero."""
+    return 2 * packed_size_bytes(ffn, hidden, bits, True) + packed_size_bytes(hidden, ffn, bits, True)
+
+
+def factor_bytes(rows, cols, r, factor_bits=3):
+    """U (rows, r) gs=min(64,r) + V (r, cols) gs=64, codes + fp16 metadata."""
+    codes = ((rows + cols) * r * factor_bits + 7) // 8
+    meta = 4 * (rows * -(-r // min(64, r)) + r * -(-cols // 64))
+    return codes + meta
+
+
+def comp_bytes(hidden, ffn, r, factor_bits=3):
+    if r == 0:
+        return 0
+    return 2 * factor_bytes(ffn, hidden, r, factor_bits) + factor_bytes(hidden, ffn, r, factor_bits)
+
+
+def layer_bytes(hidden, ffn, bits, rank, d_sel, d_comp, B, E, gate_elem=4, y_elem=2):
+    """Algorithmic HBM bytes of one layer step."""
+    return (d_sel * expert_bytes(hidden, ffn, bits) + d_comp * comp_bytes(hidden, ffn, rank)
+            + hidden * E * gate_elem + B * hidden * 2 + B * hidden * y_elem)
+
+
+def layer_flops(hidden, ffn, k, n, r, E):
+    """Per token: k*2*3*d*ffn + n*3*2*r*(d+ffn) + 2*d*E."""
+    return k * 2 * 3 * hidden * ffn + n * 3 * 2 * r * (hidden + ffn) + 2 * hidden * E
+
+
+def up_kernel_bytes(hidden, ffn, bits, rank, d_sel, d_comp, pairs, B):
+    """Dominant kernel (tiled W1|W3 + U1/U3 + V2-partial): algorithmic bytes per launch."""
+    w = 2 * packed_size_bytes(ffn, hidden, bits, True)
+    lr = 0
+    if rank:
+        lr = 2 * (((ffn * rank * 3) + 7) // 8 + 4 * ffn * -(-rank // min(64, rank))) + \
+            ((rank * ffn * 3 + 7) // 8 + 4 * rank * -(-ffn // 64))
+    return d_sel * w + d_comp * lr + B * hidden * 2 + pairs * ffn * 2
+
+
+def down_kernel_bytes(hidden, ffn, bits, rank, d_sel, d_comp, pairs, B):
+    w = packed_size_bytes(hidden, ffn, bits, True)
+    lr = ((hidden * rank * 3 + 7) // 8 + 4 * hidden * -(-rank // min(64, rank))) if rank else 0
+    return d_sel * w + d_comp * lr + pairs * ffn * 2 + B * hidden * 4
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------- clocks --
+class ClockSampler:
+    """NVML sampler of SM clocks and throttle reasons while the timed region runs."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, index=0, period=0.002):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.period = period
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ dist ---
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def dist_max(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ------------------------------------------------------------- our arm -----
+def run_ours(args, world, rank):
+    import torch
+
+    from paper_2512_17073_b200 import _lib
+    from paper_2512_17073_b200.synth import SynthLayer
+
+    _lib.load()
+    hbm, tf_burst, tf_sust, peak_kind = load_peaks()
+    B, L = args.batch, args.layers
+    torch.manual_seed(1234 + rank)
+    layers = [SynthLayer(HIDDEN, FFN, E, top_k=TOPK, bits=BITS, rank=RANK, seed=100 * l + rank,
+                         max_tokens=max(64, B)) for l in range(L)]
+    nx = 2 * L
+    xs = [torch.randn((B, HIDDEN), device="cuda").to(torch.bfloat16) for _ in range(nx)]
+    ys = [torch.empty((B, HIDDEN), dtype=torch.float32, device="cuda") for _ in range(L)]
+    idx = [torch.empty((B, TOPK), dtype=torch.int32, device="cuda") for _ in range(L)]
+    wts = [torch.empty((B, TOPK), dtype=torch.float32, device="cuda") for _ in range(L)]
+
+    def step(i):
+        l = i % L
+        layers[l].layer.forward(xs[i % nx], TOPK, TOPN, y=ys[l], topk_idx=idx[l], topk_w=wts[l])
+
+    # routing statistics of the exact step sequence (for the byte model)
+    def step_stats(i):
+        l = i % L
+        layers[l].layer.forward(xs[i % nx], TOPK, TOPN, y=ys[l], topk_idx=idx[l], topk_w=wts[l])
+        sel = idx[l].cpu().numpy()
+        return len(np.unique(sel)), len(np.unique(sel[:, :TOPN]))
+
+    cyc = {i: step_stats(i) for i in range(np.lcm(L, nx))}
+    ncyc = len(cyc)
+
+    def bytes_of(i, gate_elem=8, y_elem=4):
+        d_sel, d_comp = cyc[i % ncyc]
+        return layer_bytes(HIDDEN, FFN, BITS, RANK, d_sel, d_comp, B, E, gate_elem, y_elem)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    # capture the K timed steps into one CUDA graph (launch-bound layer: ~20 us)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for i in range(3):
+            step(i)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        for i in range(args.steps):
+            step(i)
+    launches = layers[0].layer.last_launches()
+    torch.cuda.synchronize()
+    g.replay()  # one untimed replay (graph upload)
+    torch.cuda.synchronize()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(index=torch.cuda.current_device()) as clk:
+        ev0.record()
+        g.replay()
+        ev1.record()
+        torch.cuda.synchronize()
+        if (ev0.elapsed_time(ev1)) < 200.0:  # keep sampling a little on the same workload
+            t0 = time.time()
+            while time.time() - t0 < 0.3:
+                g.replay()
+            torch.cuda.synchronize()
+    barrier(world)
+    ms = dist_max(ev0.elapsed_time(ev1), world)
+    ms_per_step = ms / args.steps
+    tok_s = world * args.steps * B / (ms / 1e3)
+
+    # layer roofline over the timed steps
+    tot_bytes = sum(bytes_of(i) for i in range(args.steps))
+    tot_flops = args.steps * B * layer_flops(HIDDEN, FFN, TOPK, TOPN, RANK, E)
+    t_roof = max(tot_bytes / (hbm * 1e9), tot_flops / (tf_sust * 1e12))
+    layer_frac = t_roof / (ms / 1e3)
+
+    # dominant-kernel roofline: per-phase CUDA events on the launching stream
+    for sl in layers:
+        sl.layer.set_profiling(True)
+    ph = {"route": [], "lr_down": [], "up": [], "down": []}
+    ubytes, dbytes = [], []
+    for i in range(4 * L):
+        step(i)
+        t = layers[i % L].layer.phase_ms()
+        for k, v in zip(ph, t):
+            ph[k].append(v)
+        d_sel, d_comp = cyc[i % ncyc]
+        ubytes.append(up_kernel_bytes(HIDDEN, FFN, BITS, RANK, d_sel, d_comp, B * TOPK, B))
+        dbytes.append(down_kernel_bytes(HIDDEN, FFN, BITS, RANK, d_sel, d_comp, B * TOPK, B))
+    for sl in layers:
+        sl.layer.set_profiling(False)
+    up_ms, down_ms = float(np.mean(ph["up"])), float(np.mean(ph["down"]))
+    dom = "up" if up_ms >= down_ms else "down"
+    dom_ms = up_ms if dom == "up" else down_ms
+    dom_bytes = float(np.mean(ubytes if dom == "up" else dbytes))
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None,
+                "kernel": f"tiled_kernel<{'UP' if dom == 'up' else 'DOWN'}> ({dom} projection)",
+                "bytes_per_launch": int(dom_bytes), "launch_ms": round(dom_ms, 5),
+                "peak_kind": peak_kind,
+                "phase_ms": {k: round(float(np.mean(v)), 5) for k, v in ph.items()},
+                "down_frac": round(float(np.mean(dbytes)) / (down_ms / 1e3) / 1e9 / hbm, 4)}
+    prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof_path):
+        tr = json.load(open(prof_path)).get(dom)
+        if tr:
+            roofline["traffic"] = tr
+
+    # end to end through the C-ABI with HOST buffers
+    xh = [torch.empty((B, HIDDEN), dtype=torch.bfloat16).pin_memory() for _ in range(nx)]
+    for i in range(nx):
+        xh[i].copy_(xs[i].cpu())
+    yh = [torch.empty((B, HIDDEN), dtype=torch.float32).pin_memory() for _ in range(L)]
+    for i in range(args.warmup):
+        layers[i % L].layer.forward_host(xh[i % nx], yh[i % L], TOPK, TOPN)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        layers[i % L].layer.forward_host(xh[i % nx], yh[i % L], TOPK, TOPN)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = dist_max(e0.elapsed_time(e1), world)
+    e2e = {"value": round(world * args.steps * B / (e2e_ms / 1e3), 1), "unit": "tokens/s",
+           "h2d_bytes_per_step": B * HIDDEN * 2, "d2h_bytes_per_step": B * HIDDEN * 4,
+           "ms_per_step": round(e2e_ms / args.steps, 5),
+           "path": "lrc_layer_forward_host (C-ABI, pinned host x/y, eager launches)"}
+
+    # batch sweep (decode batch 1..64, same rotation, graph-replayed)
+    sweep = {}
+    if args.sweep:
+        for Bs in (1, 2, 4, 8, 16, 32, 64):
+            sweep[str(Bs)] = sweep_point(layers, Bs, hbm, tf_sust)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_ours(layers[0], B)
+
+    out = {
+        "metric": METRIC, "value": round(tok_s, 1), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int2 codes, bf16 x, fp32 accum",
+        "data": "synthetic (random INT2 codes, fp16 scale/zero, INT3 rank-32 factors, random bf16 tokens)",
+        "config": {"workload": f"Mixtral-8x7B MoE layer (d=4096, ffn=14336, 8 experts top-2), INT2 gs64 "
+                               f"+ rank-32 INT3 LR on top-1, decode batch {B}, 1 GPU all-resident",
+                   "batch": B, "layers_rotated": L, "l2": "inputs larger than L2 (8 resident layers, 3.6 GB rotated)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "cuda_graph": True},
+        "roofline": roofline,
+        "roofline_layer": {"bound": "hbm", "frac": round(layer_frac, 4),
+                           "bytes_per_step": int(tot_bytes / args.steps),
+                           "achieved_gbs": round(tot_bytes / (ms / 1e3) / 1e9, 1), "peak": hbm},
+        "gpu_launches": launches * args.steps,
+        "e2e": e2e,
+        "clocks": clk.summary(),
+        "sweep": sweep,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(out))
+
+
+def sweep_point(layers, B, hbm, tf_sust, steps=200):
+    import torch
+
+    L = len(layers)
+    xs = [torch.randn((B, HIDDEN), device="cuda").to(torch.bfloat16) for _ in range(L)]
+    ys = [torch.empty((B, HIDDEN), dtype=torch.float32, device="cuda") for _ in range(L)]
+    idx = [torch.empty((B, TOPK), dtype=torch.int32, device="cuda") for _ in range(L)]
+    for sl in layers:
+        sl.layer.ensure_capacity(B, TOPK)
+    stats = []
+    for l in range(L):
+        layers[l].layer.forward(xs[l], TOPK, TOPN, y=ys[l], topk_idx=idx[l])
+        sel = idx[l].cpu().numpy()
+        stats.append((len(np.unique(sel)), len(np.unique(sel[:, :TOPN]))))
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for l in range(L):
+            layers[l].layer.forward(xs[l], TOPK, TOPN, y=ys[l], topk_idx=idx[l])
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        for i in range(steps):
+            l = i % L
+            layers[l].layer.forward(xs[l], TOPK, TOPN, y=ys[l], topk_idx=idx[l])
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    byts = sum(layer_bytes(HIDDEN, FFN, BITS, RANK, *stats[i % L], B, E, 8, 4) for i in range(steps))
+    fl = steps * B * layer_flops(HIDDEN, FFN, TOPK, TOPN, RANK, E)
+    roof = max(byts / (hbm * 1e9), fl / (tf_sust * 1e12))
+    return {"tokens_s": round(steps * B / (ms / 1e3), 1), "us_per_step": round(ms * 1e3 / steps, 2),
+            "gbs": round(byts / (ms / 1e3) / 1e9, 1), "frac": round(roof / (ms / 1e3), 4),
+            "d_sel_mean": round(float(np.mean([s[0] for s in stats])), 2)}
+
+
+# --------------------------------------------------------- CPU baselines ----
+def cpu_baseline_ours(sl, B, budget_s=25.0):
+    """Oracle (reference-algorithm port) on the same synthetic artifacts, host cores."""
+    import torch
+
+    from oracle import bridge, lrc
+
+    xs = lrc.to_bf16(np.random.default_rng(0).standard_normal((4, HIDDEN)))
+    sel = set()
+    for x in xs:
+        sel |= set(lrc.route(x, sl.gate, TOPK, TOPN)[1])
+    st = bridge.synth_store(sl, sorted(sel))
+    n, t0 = 0, time.time()
+    while n < len(xs) and (n == 0 or time.time() - t0 < budget_s):
+        lrc.forward(xs[n], sl.gate, None, TOPK, TOPN, "compensated", st)
+        n += 1
+    dt = time.time() - t0
+    del torch
+    return {"value": round(n / dt, 4), "unit": "tokens/s", "cores": int(os.environ["OPENBLAS_NUM_THREADS"]),
+            "kind": "port", "sample": f"{n} tokens x 1 C2 layer, oracle moe.forward(compensated) as-is "
+                                      f"(re-dequantizes per call, fp64 numpy/OpenBLAS)",
+            "seconds": round(dt, 2)}
+
+
+def host_synth_store(seed=0):
+    """Host-built synthetic C2 artifacts for the reference arm (lazy per expert)."""
+    from oracle import bridge, lrc
+
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((HIDDEN, E))
+    gate = g / np.linalg.norm(g, axis=0, keepdims=True) * 1.4
+
+    def qm(r, rows, cols, bits, gs, srange, zos):
+        codes = r.integers(0, 1 << bits, (rows, cols), dtype=np.uint8)
+        gpr = -(-cols // gs)
+        s = (r.random((rows, gpr)) * (srange[1] - srange[0]) + srange[0]).astype(np.float16).astype(np.float64)
+        z = (-zos * s).astype(np.float16).astype(np.float64)
+        return lrc.QM(rows, cols, bits, gs, codes, s, z)
+
+    def make(layer, expert):
+        r = np.random.default_rng(1000 + expert)
+        recs = {}
+        for p, (rows, cols) in (("w1", (FFN, HIDDEN)), ("w3", (FFN, HIDDEN)), ("w2", (HIDDEN, FFN))):
+            w = qm(r, rows, cols, BITS, 64, (1.4, 1.8), 1.5)
+            u = qm(r, rows, RANK, 3, 32, (0.014, 0.02), 3.5)
+            v = qm(r, RANK, cols, 3, 64, (0.03, 0.04), 3.5)
+            recs[p] = lrc.Rec(w, lrc.Comp(RANK, u, v, p))
+        return recs
+
+    return gate, bridge.LazyStore(make)
+
+
+def run_reference(args, world, rank):
+    """Reference arm: the reference's CPU algorithm (oracle port) on host cores."""
+    if rank != 0:
+        return
+    from oracle import lrc
+
+    gate, st = host_synth_store()
+    xs = lrc.to_bf16(np.random.default_rng(7).standard_normal((args.steps + args.warmup, HIDDEN)))
+    for i in range(args.warmup):
+        lrc.forward(xs[i], gate, None, TOPK, TOPN, "compensated", st)
+    t0 = time.time()
+    for i in range(args.steps):
+        lrc.forward(xs[args.warmup + i], gate, None, TOPK, TOPN, "compensated", st)
+    dt = time.time() - t0
+    v = args.steps / dt
+    cores = int(os.environ["OPENBLAS_NUM_THREADS"])
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3 / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "Mixtral-8x7B MoE layer (d=4096, ffn=14336, 8 experts top-2), INT2 "
+                               "+ rank-32 INT3 LR on top-1, decode batch 1", "batch": 1},
+        "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} tokens, oracle moe.forward(compensated) as-is"},
+        "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 2000 if args.impl == "ours" else 5
+    if args.warmup is None:
+        args.warmup = 10 if args.impl == "ours" else 1
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world, rank, _ = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

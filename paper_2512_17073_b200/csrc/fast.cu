@@ -1,0 +1,645 @@
+// Tiled low-bit expert kernels (2-bit codes, group size 64) for sm_100a.
+//
+// HBM layout ("T2 tiles"): a matrix (M, K) is cut into 16-row tiles and
+// 128-column group pairs.  Block (tile t, group-pair q, matrix i) is 640 B:
+//   [0,512)   codes: lane l holds 16 B = 4 words {A(g0), B(g0), A(g1), B(g1)}
+//             A = row t*16+gid, B = row t*16+gid+8 (gid = l>>2, tid = l&3);
+//             code (ks, p, e) of a word sits at bit 16e + 2(2ks+p) and is the
+//             weight at column g*64 + ks*16 + p*8 + tid*2 + e.
+//   [512,640) fp16 scale/zero: 16 B per gid {s,z}(A,g0) {s,z}(A,g1) {s,z}(B,g0) {s,z}(B,g1)
+// Blocks are ordered (t, q, i), so one row tile over a K range is one contiguous
+// byte range -> one cp.async.bulk per work item.  The codes are exactly the
+// reference's (lrc_tiles_unpack inverts the layout bit-exactly).
+//
+// In-register unpack: (w >> sh) & (3 << pos) | 0x43004300 yields two bf16
+// values 128 + 2^pos * c, which feed mma.sync m16n8k16 directly.  The 2^pos
+// multiplier is folded into the activation operand (x' = x / 2^pos, exact in
+// bf16) and the +128 bias into the fp32 accumulator seed (C = -128 * sum x').
+// Per group:  y += s * (sum c x) + z * sum x   (fp32, ref/quant.py:216-224).
+#include <algorithm>
+
+#include "common.cuh"
+#include "layer.cuh"
+
+namespace lrc {
+
+constexpr int kBlk = 640;
+constexpr int kCodeBytes = 512;
+constexpr int kSpanGP = 4;        // group pairs per warp span (512 columns)
+constexpr int kNW = 8;            // consumer warps
+constexpr int kThreads = (kNW + 1) * 32;
+
+int64_t tiles_bytes(int64_t rows, int64_t cols, int ni) {
+  int64_t rt = (rows + 15) / 16, gp = (cols + 127) / 128;
+  return rt * gp * ni * kBlk;
+}
+
+// ------------------------------------------------------------------ repack --
+__global__ void build_tiles_kernel(lrc_qmat m0, lrc_qmat m1, int ni, int64_t RT, int64_t GP,
+                                   uint8_t* __restrict__ tiles) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int lane = static_cast<int>(idx & 31);
+  const int64_t blk = idx >> 5;
+  if (blk >= RT * GP * ni) return;
+  const int i = static_cast<int>(blk % ni);
+  const int64_t tq = blk / ni;
+  const int64_t q = tq % GP, t = tq / GP;
+  const lrc_qmat& m = (i == 0) ? m0 : m1;
+  const int gid = lane >> 2, tid = lane & 3;
+  const int64_t nbytes = (static_cast<int64_t>(m.rows) * m.cols * m.bits + 7) >> 3;
+  uint32_t w[4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int rs = 0; rs < 2; ++rs) {
+      const int64_t r = t * 16 + gid + 8 * rs;
+      uint32_t word = 0;
+      for (int ks = 0; ks < 4; ++ks)
+        for (int p = 0; p < 2; ++p)
+          for (int e = 0; e < 2; ++e) {
+            const int64_t k = (2 * q + h) * 64 + ks * 16 + p * 8 + tid * 2 + e;
+            uint32_t c = 0;
+            if (r < m.rows && k < m.cols) c = read_code(m.packed, r * m.cols + k, m.bits, nbytes);
+            word |= c << (16 * e + 2 * (2 * ks + p));
+          }
+      w[h * 2 + rs] = word;
+    }
+  }
+  uint8_t* b = tiles + blk * kBlk;
+  *reinterpret_cast<uint4*>(b + lane * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+  if (lane < 8) {
+    const int gpr = (m.cols + m.group_size - 1) / m.group_size;
+    uint16_t v[8];
+#pragma unroll
+    for (int rs = 0; rs < 2; ++rs)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t r = t * 16 + lane + 8 * rs;
+        const int64_t g = 2 * q + h;
+        uint16_t s = 0, z = 0;
+        if (r < m.rows && g < gpr) {
+          s = m.scales[r * gpr + g];
+          z = m.zeros[r * gpr + g];
+        }
+        v[rs * 4 + h * 2] = s;
+        v[rs * 4 + h * 2 + 1] = z;
+      }
+    uint4 mv;
+    mv.x = v[0] | (uint32_t(v[1]) << 16);
+    mv.y = v[2] | (uint32_t(v[3]) << 16);
+    mv.z = v[4] | (uint32_t(v[5]) << 16);
+    mv.w = v[6] | (uint32_t(v[7]) << 16);
+    *reinterpret_cast<uint4*>(b + kCodeBytes + lane * 16) = mv;
+  }
+}
+
+__global__ void tiles_unpack_kernel(const uint8_t* __restrict__ tiles, int64_t rows, int64_t cols,
+                                    int ni, int which, int64_t GP, uint8_t* __restrict__ out) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= rows * cols) return;
+  const int64_t r = idx / cols, k = idx - r * cols;
+  const int64_t t = r / 16;
+  const int rr = static_cast<int>(r % 16), gid = rr & 7, rs = rr >> 3;
+  const int64_t g = k / 64, q = g / 2;
+  const int h = static_cast<int>(g & 1), w = static_cast<int>(k % 64);
+  const int ks = w / 16, p = (w % 16) / 8, tid = (w % 8) / 2, e = w % 2;
+  const int lane = gid * 4 + tid;
+  const uint8_t* b = tiles + ((t * GP + q) * ni + which) * kBlk;
+  const uint32_t word = reinterpret_cast<const uint32_t*>(b + lane * 16)[h * 2 + rs];
+  out[idx] = static_cast<uint8_t>((word >> (16 * e + 2 * (2 * ks + p))) & 3u);
+}
+
+// -------------------------------------------------------- PTX primitives ---
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kNW * 32) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(const void* p) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// code slot j = 2*ks + p of a word -> bf16x2 {128 + m*c_lo, 128 + m*c_hi},
+// m = 1,4,16,1,4,16,1,4 for j = 0..7
+template <int J>
+__device__ __forceinline__ uint32_t unpack_j(uint32_t w) {
+  constexpr int sh = (J < 3) ? 0 : ((J < 6) ? 6 : 12);
+  constexpr int pos = 2 * (J - ((J < 3) ? 0 : ((J < 6) ? 3 : 6)));
+  return ((w >> sh) & (0x00030003u << pos)) | 0x43004300u;
+}
+__device__ __forceinline__ float inv_mult(int j) {
+  // 1 / m for slot j
+  return (j % 3 == 0) ? 1.0f : ((j % 3 == 1) ? 0.25f : 0.0625f);
+}
+
+// --------------------------------------------------------- tiled kernel ---
+template <bool UP>
+struct TileCfg {
+  static constexpr int NI = UP ? 2 : 1;
+};
+
+struct TiledParams {
+  ExpertArgs a;
+  int M, K;            // rows / cols of the streamed matrix (per interleaved matrix)
+  int64_t GP, RT;      // group pairs per row, row tiles
+  int NS, SPC, nchunk; // spans, spans per chunk, chunks
+  int stage_bytes, nstage;
+  int xs_stride;       // bf16 elements per x' row
+};
+
+// shared memory carve-up (bytes)
+struct SmemMap {
+  int stages, xs, sums, red, bars, total;
+};
+
+template <int NT>
+__host__ __device__ inline SmemMap smem_map(const TiledParams& p, int ni) {
+  SmemMap m;
+  m.stages = 0;
+  m.xs = p.stage_bytes * p.nstage;
+  m.sums = m.xs + 8 * NT * p.xs_stride * 2;
+  const int groups = p.SPC * kSpanGP * 2;
+  m.red = m.sums + groups * 8 * NT * 8;
+  m.bars = m.red + ni * NT * 16 * 8 * 4;
+  m.total = m.bars + 2 * p.nstage * 8 + 64;
+  return m;
+}
+
+template <bool UP, int NT>
+__global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
+  constexpr int NI = TileCfg<UP>::NI;
+  constexpr int TPP = 8 * NT;  // tokens per pass
+  extern __shared__ __align__(128) uint8_t smem[];
+  const SmemMap SM = smem_map<NT>(P, NI);
+  uint8_t* stages = smem + SM.stages;
+  uint16_t* xs = reinterpret_cast<uint16_t*>(smem + SM.xs);
+  float2* sums = reinterpret_cast<float2*>(smem + SM.sums);  // [g_local][TPP] (X, Xm)
+  float* red = reinterpret_cast<float*>(smem + SM.red);      // [NI][NT][16][8]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM.bars);
+  uint64_t* empty = full + P.nstage;
+  __shared__ int s_prefix[LRC_MAX_EXPERTS + 1];
+  __shared__ int s_range[2];
+  __shared__ int s_comp_n[TPP], s_comp_slot[TPP], s_ncomp;
+  __shared__ float act_s[16 * TPP];
+
+  const ExpertArgs& A = P.a;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_active = A.plan.counts[0];
+
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int ai = 0; ai < n_active; ++ai) {
+      s_prefix[ai] = acc;
+      const int passes = (A.plan.active_cnt[ai] + TPP - 1) / TPP;
+      acc += passes * P.nchunk * static_cast<int>(P.RT);
+    }
+    s_prefix[n_active] = acc;
+    const int64_t total = acc;
+    s_range[0] = static_cast<int>(total * blockIdx.x / gridDim.x);
+    s_range[1] = static_cast<int>(total * (blockIdx.x + 1) / gridDim.x);
+    for (int s = 0; s < P.nstage; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kNW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < NI * NT * 128; i += blockDim.x) red[i] = 0.0f;
+  __syncthreads();
+  const int beg = s_range[0], end = s_range[1];
+  if (beg >= end) return;
+
+  // item -> (active index, pass, chunk, tile)
+  auto decode = [&](int it, int& ai, int& pass, int& chunk, int& tile) {
+    int lo = 0;
+    while (s_prefix[lo + 1] <= it) ++lo;
+    ai = lo;
+    int r = it - s_prefix[lo];
+    tile = r % static_cast<int>(P.RT);
+    r /= static_cast<int>(P.RT);
+    chunk = r % P.nchunk;
+    pass = r / P.nchunk;
+  };
+  auto chunk_gp = [&](int chunk, int& gp0, int& gp1) {
+    gp0 = chunk * P.SPC * kSpanGP;
+    gp1 = static_cast<int>(P.GP < static_cast<int64_t>(gp0) + P.SPC * kSpanGP ? P.GP : static_cast<int64_t>(gp0) + P.SPC * kSpanGP);
+  };
+
+  if (warp == kNW) {
+    // ===================== producer: one elected lane streams work items ====
+    if (lane == 0) {
+      for (int it = beg; it < end; ++it) {
+        const int k = it - beg;
+        const int s = k % P.nstage;
+        if (k >= P.nstage) mbar_wait(&empty[s], ((k / P.nstage) - 1) & 1);
+        int ai, pass, chunk, tile;
+        decode(it, ai, pass, chunk, tile);
+        int gp0, gp1;
+        chunk_gp(chunk, gp0, gp1);
+        const lrc_expert& E = A.experts[A.plan.active[ai]];
+        const uint8_t* base = UP ? E.up_tiles : E.down_tiles;
+        const uint8_t* src = base + ((static_cast<int64_t>(tile) * P.GP + gp0) * NI) * kBlk;
+        const uint32_t bytes = static_cast<uint32_t>((gp1 - gp0) * NI * kBlk);
+        mbar_expect_tx(&full[s], bytes);
+        bulk_g2s(stages + static_cast<size_t>(s) * P.stage_bytes, src, bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ============================ consumers ====================================
+  const int gid = lane >> 2, tid = lane & 3;
+  int cur_ai = -1, cur_pass = -1, cur_chunk = -1;
+  int pass_tok = 0;
+  for (int it = beg; it < end; ++it) {
+    const int k = it - beg;
+    const int s = k % P.nstage;
+    int ai, pass, chunk, tile;
+    decode(it, ai, pass, chunk, tile);
+    int gp0, gp1;
+    chunk_gp(chunk, gp0, gp1);
+    const int off = A.plan.active_off[ai], cnt = A.plan.active_cnt[ai];
+    const int e = A.plan.active[ai];
+    const lrc_expert& E = A.experts[e];
+    if (ai != cur_ai || pass != cur_pass || chunk != cur_chunk) {
+      // ---- rebuild the activation operand x' for (expert tokens of this pass, chunk)
+      consumer_sync();
+      cur_ai = ai;
+      cur_pass = pass;
+      cur_chunk = chunk;
+      pass_tok = min(TPP, cnt - pass * TPP);
+      if (threadIdx.x == 0) {
+        int nc = 0;
+        for (int n = 0; n < pass_tok; ++n) {
+          const int slot = A.plan.pair_comp[A.plan.pair_list[off + pass * TPP + n]];
+          if (slot >= 0) {
+            s_comp_n[nc] = n;
+            s_comp_slot[nc] = slot;
+            ++nc;
+          }
+        }
+        s_ncomp = nc;
+      }
+      const int kc = (gp1 - gp0) * 128;
+      const int k0 = gp0 * 128;
+      const int ng = (gp1 - gp0) * 2;
+      for (int i = threadIdx.x; i < ng * TPP; i += kNW * 32) sums[i] = make_float2(0.f, 0.f);
+      consumer_sync();
+      // each thread: 8 consecutive columns of one token row
+      const int per_row = kc / 8;
+      for (int i = threadIdx.x; i < TPP * per_row; i += kNW * 32) {
+        const int n = i / per_row, c8 = (i - n * per_row) * 8;
+        float v[8];
+        if (n < pass_tok) {
+          const int p = A.plan.pair_list[off + pass * TPP + n];
+          const int kk = k0 + c8;
+          if (UP) {
+            const uint16_t* src = A.x + static_cast<int64_t>(A.plan.pair_token[p]) * A.hidden;
+            if (kk + 8 <= P.K && (A.hidden % 8) == 0) {
+              uint4 raw = *reinterpret_cast<const uint4*>(src + kk);
+              const uint16_t* h = reinterpret_cast<const uint16_t*>(&raw);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[j] = bf2f(h[j]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[j] = (kk + j < P.K) ? bf2f(src[kk + j]) : 0.0f;
+            }
+          } else {
+            const uint16_t* src = A.a16 + static_cast<int64_t>(p) * A.ffn;
+            if (kk + 8 <= P.K && (A.ffn % 8) == 0) {
+              uint4 raw = *reinterpret_cast<const uint4*>(src + kk);
+              const uint16_t* h = reinterpret_cast<const uint16_t*>(&raw);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[j] = bf2f(h[j]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v[j] = (kk + j < P.K) ? bf2f(src[kk + j]) : 0.0f;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = 0.0f;
+        }
+        // slot j = (col % 64) / 8 is constant over the 8 columns
+        const int jslot = (c8 % 64) / 8;
+        const float im = inv_mult(jslot);
+        float xsum = 0.f, xpsum = 0.f;
+        uint16_t* row = xs + n * P.xs_stride + (c8 / 16) * 16;
+        const int pbit = (c8 % 16) / 8;  // p
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xp = v[j] * im;  // exact power-of-two scaling
+          xsum += v[j];
+          xpsum += xp;
+          const int tj = j / 2, ej = j % 2;
+          row[tj * 4 + pbit * 2 + ej] = f2bf(xp);
+        }
+        const int g_local = c8 / 64;
+        atomicAdd(&sums[g_local * TPP + n].x, xsum);
+        atomicAdd(&sums[g_local * TPP + n].y, -128.0f * xpsum);
+      }
+      consumer_sync();
+    }
+
+    // ---- wait for the weights of this item
+    mbar_wait(&full[s], (k / P.nstage) & 1);
+    const uint8_t* st = stages + static_cast<size_t>(s) * P.stage_bytes;
+
+    float acc[NI][NT][4];
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[i][nt][c] = 0.0f;
+
+    const int ngp = gp1 - gp0;
+    const int nspan = (ngp + kSpanGP - 1) / kSpanGP;
+    for (int sp = warp; sp < nspan; sp += kNW) {
+      const int q0 = sp * kSpanGP, q1 = min(ngp, q0 + kSpanGP);
+      for (int q = q0; q < q1; ++q) {
+        uint4 cw[NI], mw[NI];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const uint8_t* blk = st + (q * NI + i) * kBlk;
+          cw[i] = lds128(blk + lane * 16);
+          mw[i] = lds128(blk + kCodeBytes + gid * 16);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gl = q * 2 + h;  // group index within the chunk
+          float d[NI][NT][4];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const float2 xm0 = sums[gl * TPP + nt * 8 + 2 * tid];
+            const float2 xm1 = sums[gl * TPP + nt * 8 + 2 * tid + 1];
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+              d[i][nt][0] = xm0.y;
+              d[i][nt][1] = xm1.y;
+              d[i][nt][2] = xm0.y;
+              d[i][nt][3] = xm1.y;
+            }
+          }
+          const uint16_t* xrow = xs + gl * 64 + tid * 4;
+#define LRC_KSTEP(KS)                                                                      \
+  {                                                                                        \
+    uint32_t b0[NT], b1[NT];                                                               \
+    _Pragma("unroll") for (int nt = 0; nt < NT; ++nt) {                                    \
+      const uint2 bv = lds64(xrow + (nt * 8 + gid) * P.xs_stride + (KS) * 16);             \
+      b0[nt] = bv.x;                                                                       \
+      b1[nt] = bv.y;                                                                       \
+    }                                                                                      \
+    _Pragma("unroll") for (int i = 0; i < NI; ++i) {                                       \
+      const uint32_t wa = h ? cw[i].z : cw[i].x;                                           \
+      const uint32_t wb = h ? cw[i].w : cw[i].y;                                           \
+      const uint32_t a0 = unpack_j<2 * (KS)>(wa), a1 = unpack_j<2 * (KS)>(wb);             \
+      const uint32_t a2 = unpack_j<2 * (KS) + 1>(wa), a3 = unpack_j<2 * (KS) + 1>(wb);     \
+      _Pragma("unroll") for (int nt = 0; nt < NT; ++nt)                                    \
+          mma_bf16(d[i][nt], a0, a1, a2, a3, b0[nt], b1[nt]);                              \
+    }                                                                                      \
+  }
+          LRC_KSTEP(0)
+          LRC_KSTEP(1)
+          LRC_KSTEP(2)
+          LRC_KSTEP(3)
+#undef LRC_KSTEP
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            const uint32_t mA = h ? mw[i].y : mw[i].x;  // {s,z} row gid
+            const uint32_t mB = h ? mw[i].w : mw[i].z;  // {s,z} row gid+8
+            const float sA = h2f(mA & 0xffff), zA = h2f(mA >> 16);
+            const float sB = h2f(mB & 0xffff), zB = h2f(mB >> 16);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const float X0 = sums[gl * TPP + nt * 8 + 2 * tid].x;
+              const float X1 = sums[gl * TPP + nt * 8 + 2 * tid + 1].x;
+              acc[i][nt][0] = fmaf(sA, d[i][nt][0], fmaf(zA, X0, acc[i][nt][0]));
+              acc[i][nt][1] = fmaf(sA, d[i][nt][1], fmaf(zA, X1, acc[i][nt][1]));
+              acc[i][nt][2] = fmaf(sB, d[i][nt][2], fmaf(zB, X0, acc[i][nt][2]));
+              acc[i][nt][3] = fmaf(sB, d[i][nt][3], fmaf(zB, X1, acc[i][nt][3]));
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    // ---- cross-warp reduction into red[i][nt][row][col]
+    if (warp < nspan) {
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          float* rb = red + (i * NT + nt) * 128;
+          atomicAdd(&rb[gid * 8 + 2 * tid], acc[i][nt][0]);
+          atomicAdd(&rb[gid * 8 + 2 * tid + 1], acc[i][nt][1]);
+          atomicAdd(&rb[(gid + 8) * 8 + 2 * tid], acc[i][nt][2]);
+          atomicAdd(&rb[(gid + 8) * 8 + 2 * tid + 1], acc[i][nt][3]);
+        }
+    }
+    consumer_sync();
+
+    // ---- epilogue E1: low-rank up-projection U.t for the compensated tokens
+    // (ref/lowrank.py:165 applied to this tile's rows only).  16 lanes share a
+    // (token, matrix, row) and split the rank dimension.
+    if (s_ncomp > 0 && (UP || chunk == 0)) {
+      const int ntask = s_ncomp * NI * 16 * 16;
+      for (int o = threadIdx.x; o < ntask; o += kNW * 32) {
+        const int jl = o & 15, r = (o >> 4) & 15;
+        const int i = (o >> 8) % NI, c = (o >> 8) / NI;
+        const int n = s_comp_n[c], slot = s_comp_slot[c];
+        const int row = tile * 16 + r;
+        const lrc_qmat& U = UP ? (i == 0 ? E.u1 : E.u3) : E.u2;
+        const int proj = UP ? i : 2;
+        float v = 0.0f;
+        if (row < P.M && qmat_present(U)) {
+          const float* tp = A.t + (static_cast<int64_t>(slot) * 3 + proj) * A.maxr;
+          for (int j = jl; j < U.cols; j += 16) v = fmaf(qmat_elem(U, row, j), tp[j], v);
+        }
+#pragma unroll
+        for (int o2 = 8; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
+        if (jl == 0) red[(i * NT + (n >> 3)) * 128 + r * 8 + (n & 7)] += v;
+      }
+      consumer_sync();
+    }
+    // ---- E2: thread -> (row r, token n)
+    for (int o = threadIdx.x; o < 16 * TPP; o += kNW * 32) {
+      const int r = o & 15, n = o >> 4;
+      const int nt = n >> 3, col = n & 7;
+      const int row = tile * 16 + r;
+      float* r0 = red + (0 * NT + nt) * 128 + r * 8 + col;
+      const float v0 = *r0;
+      *r0 = 0.0f;
+      const bool valid = (n < pass_tok) && (row < P.M);
+      if (UP) {
+        float* r1 = red + ((NI - 1) * NT + nt) * 128 + r * 8 + col;
+        const float v1 = *r1;
+        *r1 = 0.0f;
+        float act = 0.0f;
+        if (valid) {
+          const int p = A.plan.pair_list[off + pass * TPP + n];
+          act = silu_f(v0) * v1;
+          A.a16[static_cast<int64_t>(p) * A.ffn + row] = f2bf(act);
+        }
+        act_s[r * TPP + n] = act;
+      } else if (valid) {
+        const int p = A.plan.pair_list[off + pass * TPP + n];
+        atomicAdd(&A.y[static_cast<int64_t>(A.plan.pair_token[p]) * A.hidden + row],
+                  A.plan.pair_w[p] * v0);
+      }
+    }
+    // ---- E3 (up only): partial t2 = V2[:, tile rows] . act for compensated tokens
+    if (UP && s_ncomp > 0 && qmat_present(E.v2)) {
+      consumer_sync();
+      const int r2 = E.v2.rows;
+      const int ntask = s_ncomp * r2 * 16;
+      for (int o = threadIdx.x; o < ntask; o += kNW * 32) {
+        const int rl = o & 15, j = (o >> 4) % r2, c = (o >> 4) / r2;
+        const int n = s_comp_n[c], slot = s_comp_slot[c];
+        const int row = tile * 16 + rl;
+        float v = (row < P.M) ? qmat_elem(E.v2, j, row) * act_s[rl * TPP + n] : 0.0f;
+#pragma unroll
+        for (int o2 = 8; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
+        if (rl == 0) atomicAdd(&A.t[(static_cast<int64_t>(slot) * 3 + 2) * A.maxr + j], v);
+      }
+    }
+    consumer_sync();
+  }
+}
+
+template <bool UP, int NT>
+static lrc_status launch_one(TiledParams& P, int num_sms, cudaStream_t st) {
+  constexpr int NI = TileCfg<UP>::NI;
+  const SmemMap m = smem_map<NT>(P, NI);
+  if (m.total > 227 * 1024) return fail(LRC_ERR_UNSUPPORTED, "tiled kernel: shared memory budget");
+  static int configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  auto fn = tiled_kernel<UP, NT>;
+  if (configured[UP][NT] < m.total) {
+    LRC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured[UP][NT] = 227 * 1024;
+  }
+  fn<<<num_sms, kThreads, m.total, st>>>(P);
+  LRC_CHECK_LAUNCH();
+  return LRC_OK;
+}
+
+static void plan_chunks(TiledParams& P, bool up) {
+  P.NS = static_cast<int>((P.GP + kSpanGP - 1) / kSpanGP);
+  if (up) {
+    P.nchunk = 1;
+    P.SPC = P.NS;
+  } else {
+    P.nchunk = (P.NS + kNW - 1) / kNW;
+    P.SPC = (P.NS + P.nchunk - 1) / P.nchunk;
+  }
+  P.xs_stride = P.SPC * kSpanGP * 128 + 16;
+}
+
+template <bool UP>
+static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, cudaStream_t st) {
+  TiledParams P{};
+  P.a = a;
+  P.M = UP ? a.ffn : a.hidden;
+  P.K = UP ? a.hidden : a.ffn;
+  P.GP = (P.K + 127) / 128;
+  P.RT = (P.M + 15) / 16;
+  plan_chunks(P, UP);
+  constexpr int NI = TileCfg<UP>::NI;
+  P.stage_bytes = P.SPC * kSpanGP * NI * kBlk;
+  const int nt = (max_tok <= 8) ? 1 : 2;
+  for (P.nstage = 4; P.nstage >= 2; --P.nstage) {
+    int total = (nt == 1) ? smem_map<1>(P, NI).total : smem_map<2>(P, NI).total;
+    if (total <= 227 * 1024) break;
+  }
+  if (P.nstage < 2) P.nstage = 2;
+  return (nt == 1) ? launch_one<UP, 1>(P, num_sms, st) : launch_one<UP, 2>(P, num_sms, st);
+}
+
+lrc_status launch_up_tiled(const ExpertArgs& a, int num_sms, int max_tok, cudaStream_t st) {
+  return launch_tiled<true>(a, num_sms, max_tok, st);
+}
+lrc_status launch_down_tiled(const ExpertArgs& a, int num_sms, int max_tok, cudaStream_t st) {
+  return launch_tiled<false>(a, num_sms, max_tok, st);
+}
+
+}  // namespace lrc
+
+using namespace lrc;
+
+extern "C" int64_t lrc_tiles_bytes(int64_t rows, int64_t cols, int interleave) {
+  return tiles_bytes(rows, cols, interleave);
+}
+
+extern "C" lrc_status lrc_build_tiles(const lrc_qmat* mats, int interleave, uint8_t* tiles,
+                                      void* stream) {
+  if (!mats || !tiles || interleave < 1 || interleave > 2)
+    return fail(LRC_ERR_INVALID, "build_tiles: bad arguments");
+  for (int i = 0; i < interleave; ++i) {
+    if (mats[i].bits != 2 || mats[i].group_size != 64 || mats[i].packed == nullptr)
+      return fail(LRC_ERR_UNSUPPORTED, "build_tiles: tiled layout needs 2-bit codes, group 64");
+    if (mats[i].rows != mats[0].rows || mats[i].cols != mats[0].cols)
+      return fail(LRC_ERR_INVALID, "build_tiles: interleaved matrices differ in shape");
+  }
+  const int64_t RT = (mats[0].rows + 15) / 16, GP = (mats[0].cols + 127) / 128;
+  const int64_t threads = RT * GP * interleave * 32;
+  build_tiles_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, as_stream(stream)>>>(
+      mats[0], mats[interleave - 1], interleave, RT, GP, tiles);
+  LRC_CHECK_LAUNCH();
+  return LRC_OK;
+}
+
+extern "C" lrc_status lrc_tiles_unpack(const uint8_t* tiles, int64_t rows, int64_t cols,
+                                       int interleave, int which, uint8_t* codes, void* stream) {
+  if (!tiles || !codes || rows <= 0 || cols <= 0 || which < 0 || which >= interleave)
+    return fail(LRC_ERR_INVALID, "tiles_unpack: bad arguments");
+  const int64_t GP = (cols + 127) / 128;
+  tiles_unpack_kernel<<<static_cast<unsigned>((rows * cols + 255) / 256), 256, 0,
+                        as_stream(stream)>>>(tiles, rows, cols, interleave, which, GP, codes);
+  LRC_CHECK_LAUNCH();
+  return LRC_OK;
+}

@@ -1,0 +1,524 @@
+// MoE layer object: workspace, generic (reference-layout) expert kernels, LR
+// kernels, and the forward orchestration.  Reference: ref/moe.py:196-259,
+// ref/lowrank.py:153-165.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "layer.cuh"
+
+namespace lrc {
+
+// ------------------------------------------------------------ LR kernels ---
+// t[slot][proj][j] = V_proj(e)[j, :] . x_b  for compensated pairs, proj in {w1, w3}
+__global__ void __launch_bounds__(256) lr_down_kernel(ExpertArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = blockIdx.x * 8 + warp;
+  const int per_slot = 2 * a.maxr;
+  const int slot = task / per_slot;
+  if (slot >= a.plan.counts[1]) return;
+  const int rem = task - slot * per_slot;
+  const int proj = rem / a.maxr, j = rem - proj * a.maxr;
+  const int p = a.plan.comp_list[slot];
+  const lrc_expert& E = a.experts[a.plan.pair_expert[p]];
+  const lrc_qmat& V = proj == 0 ? E.v1 : E.v3;
+  float acc = 0.0f;
+  if (qmat_present(V) && j < V.rows) {
+    const uint16_t* xb = a.x + static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden;
+    for (int k = lane; k < V.cols; k += 32) acc = fmaf(qmat_elem(V, j, k), bf2f(xb[k]), acc);
+    acc = warp_sum(acc);
+  }
+  if (lane == 0) a.t[(static_cast<int64_t>(slot) * 3 + proj) * a.maxr + j] = acc;
+}
+
+// U(row, :) . t  (warp-cooperative; all lanes return the sum)
+__device__ __forceinline__ float lr_up_dot(const lrc_qmat& U, int row, const float* t) {
+  float s = 0.0f;
+  for (int j = threadIdx.x & 31; j < U.cols; j += 32) s = fmaf(qmat_elem(U, row, j), t[j], s);
+  return warp_sum(s);
+}
+
+// --------------------------------------------------- generic expert kernels ---
+constexpr int kChunk = 8;
+
+__global__ void __launch_bounds__(256) up_generic_kernel(ExpertArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int n_active = a.plan.counts[0];
+  const int64_t total = static_cast<int64_t>(n_active) * a.ffn;
+  for (int64_t task = gw; task < total; task += nwarps) {
+    const int ai = static_cast<int>(task / a.ffn);
+    const int f = static_cast<int>(task - static_cast<int64_t>(ai) * a.ffn);
+    const lrc_expert& E = a.experts[a.plan.active[ai]];
+    const int off = a.plan.active_off[ai], cnt = a.plan.active_cnt[ai];
+    for (int c0 = 0; c0 < cnt; c0 += kChunk) {
+      const int nch = min(kChunk, cnt - c0);
+      float acc1[kChunk], acc3[kChunk];
+      const uint16_t* xp[kChunk];
+#pragma unroll
+      for (int i = 0; i < kChunk; ++i) {
+        acc1[i] = acc3[i] = 0.0f;
+        int p = a.plan.pair_list[off + c0 + min(i, nch - 1)];
+        xp[i] = a.x + static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden;
+      }
+      for (int k = lane; k < a.hidden; k += 32) {
+        const float w1v = qmat_elem(E.w1, f, k), w3v = qmat_elem(E.w3, f, k);
+#pragma unroll
+        for (int i = 0; i < kChunk; ++i) {
+          if (i < nch) {
+            const float xv = bf2f(xp[i][k]);
+            acc1[i] = fmaf(w1v, xv, acc1[i]);
+            acc3[i] = fmaf(w3v, xv, acc3[i]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kChunk; ++i) {
+        if (i < nch) {
+          float h1 = warp_sum(acc1[i]), h3 = warp_sum(acc3[i]);
+          const int p = a.plan.pair_list[off + c0 + i];
+          const int slot = a.plan.pair_comp[p];
+          if (slot >= 0) {
+            const float* tp = a.t + static_cast<int64_t>(slot) * 3 * a.maxr;
+            if (qmat_present(E.u1)) h1 += lr_up_dot(E.u1, f, tp);
+            if (qmat_present(E.u3)) h3 += lr_up_dot(E.u3, f, tp + a.maxr);
+          }
+          if (lane == 0) a.a32[static_cast<int64_t>(p) * a.ffn + f] = silu_f(h1) * h3;
+        }
+      }
+    }
+  }
+}
+
+// t[slot][2][j] = V2(e)[j, :] . a_p
+__global__ void __launch_bounds__(256) lr_mid_kernel(ExpertArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = blockIdx.x * 8 + warp;
+  const int slot = task / a.maxr;
+  if (slot >= a.plan.counts[1]) return;
+  const int j = task - slot * a.maxr;
+  const int p = a.plan.comp_list[slot];
+  const lrc_expert& E = a.experts[a.plan.pair_expert[p]];
+  float acc = 0.0f;
+  if (qmat_present(E.v2) && j < E.v2.rows) {
+    const float* ap = a.a32 + static_cast<int64_t>(p) * a.ffn;
+    for (int k = lane; k < E.v2.cols; k += 32) acc = fmaf(qmat_elem(E.v2, j, k), ap[k], acc);
+    acc = warp_sum(acc);
+  }
+  if (lane == 0) a.t[(static_cast<int64_t>(slot) * 3 + 2) * a.maxr + j] = acc;
+}
+
+__global__ void __launch_bounds__(256) down_generic_kernel(ExpertArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int n_active = a.plan.counts[0];
+  const int64_t total = static_cast<int64_t>(n_active) * a.hidden;
+  for (int64_t task = gw; task < total; task += nwarps) {
+    const int ai = static_cast<int>(task / a.hidden);
+    const int r = static_cast<int>(task - static_cast<int64_t>(ai) * a.hidden);
+    const lrc_expert& E = a.experts[a.plan.active[ai]];
+    const int off = a.plan.active_off[ai], cnt = a.plan.active_cnt[ai];
+    for (int c0 = 0; c0 < cnt; c0 += kChunk) {
+      const int nch = min(kChunk, cnt - c0);
+      float acc[kChunk];
+      const float* ap[kChunk];
+#pragma unroll
+      for (int i = 0; i < kChunk; ++i) {
+        acc[i] = 0.0f;
+        int p = a.plan.pair_list[off + c0 + min(i, nch - 1)];
+        ap[i] = a.a32 + static_cast<int64_t>(p) * a.ffn;
+      }
+      for (int k = lane; k < a.ffn; k += 32) {
+        const float wv = qmat_elem(E.w2, r, k);
+#pragma unroll
+        for (int i = 0; i < kChunk; ++i)
+          if (i < nch) acc[i] = fmaf(wv, ap[i][k], acc[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < kChunk; ++i) {
+        if (i < nch) {
+          float v = warp_sum(acc[i]);
+          const int p = a.plan.pair_list[off + c0 + i];
+          const int slot = a.plan.pair_comp[p];
+          if (slot >= 0 && qmat_present(E.u2))
+            v += lr_up_dot(E.u2, r, a.t + (static_cast<int64_t>(slot) * 3 + 2) * a.maxr);
+          if (lane == 0)
+            atomicAdd(&a.y[static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden + r],
+                      a.plan.pair_w[p] * v);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------- dense fp64 (reference) ---
+__global__ void dense_up_f64_kernel(const double* w1, const double* w3, int hidden, int ffn,
+                                    const double* x, int64_t B, double* act) {
+  const int lane = threadIdx.x & 31;
+  const int64_t task = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  if (task >= B * ffn) return;
+  const int64_t b = task / ffn;
+  const int f = static_cast<int>(task - b * ffn);
+  double h1 = 0.0, h3 = 0.0;
+  for (int k = lane; k < hidden; k += 32) {
+    const double xv = x[b * hidden + k];
+    h1 = fma(w1[static_cast<int64_t>(f) * hidden + k], xv, h1);
+    h3 = fma(w3[static_cast<int64_t>(f) * hidden + k], xv, h3);
+  }
+  h1 = warp_sum_d(h1);
+  h3 = warp_sum_d(h3);
+  if (lane == 0) act[task] = h1 / (1.0 + exp(-h1)) * h3;
+}
+
+__global__ void dense_down_f64_kernel(const double* w2, int hidden, int ffn, const double* act,
+                                      const double* mix, int64_t B, double* y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t task = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  if (task >= B * hidden) return;
+  const int64_t b = task / hidden;
+  const int r = static_cast<int>(task - b * hidden);
+  double acc = 0.0;
+  for (int k = lane; k < ffn; k += 32)
+    acc = fma(w2[static_cast<int64_t>(r) * ffn + k], act[b * ffn + k], acc);
+  acc = warp_sum_d(acc);
+  if (lane == 0) y[task] += (mix ? mix[b] : 1.0) * acc;
+}
+
+lrc_status launch_lr_down(const ExpertArgs& a, int np_bound, cudaStream_t st) {
+  if (a.maxr == 0) return LRC_OK;
+  int tasks = np_bound * 2 * a.maxr;
+  lr_down_kernel<<<(tasks + 7) / 8, 256, 0, st>>>(a);
+  LRC_CHECK_LAUNCH();
+  return LRC_OK;
+}
+
+}  // namespace lrc
+
+// =========================================================== layer object ===
+using namespace lrc;
+
+struct lrc_layer {
+  int hidden = 0, ffn = 0, E = 0, S = 0, max_tokens = 0, k_max = 0, maxr = 0;
+  int num_sms = 148;
+  bool tiled = false;
+  int last_launches = 0;
+  const double* gate_t = nullptr;
+  std::vector<lrc_expert> host_experts;
+  lrc_expert* d_experts = nullptr;
+  // workspace
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  PlanArgs plan{};
+  int32_t* topk_idx = nullptr;
+  float* topk_w = nullptr;
+  float* t = nullptr;
+  float* a32 = nullptr;
+  uint16_t* a16 = nullptr;
+  int max_pairs = 0;
+  // host-buffer staging + phase timing
+  uint16_t* x_stage = nullptr;
+  float* y_stage = nullptr;
+  bool profiling = false;
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+static bool has_comp(const lrc_expert& e) {
+  auto pres = [](const lrc_qmat& m) { return m.packed != nullptr || m.dense != nullptr; };
+  return pres(e.u1) || pres(e.u2) || pres(e.u3);
+}
+
+static int rank_of(const lrc_qmat& u) {
+  return (u.packed != nullptr || u.dense != nullptr) ? u.cols : 0;
+}
+
+static lrc_status validate_expert(const lrc_expert& e, int hidden, int ffn) {
+  auto chk = [](const lrc_qmat& m, int rows, int cols, const char* nm) -> lrc_status {
+    if (m.packed == nullptr && m.dense == nullptr)
+      return fail(LRC_ERR_MISSING, std::string("no artifact for projection ") + nm);
+    if (m.rows != rows || m.cols != cols)
+      return fail(LRC_ERR_INVALID, std::string("shape mismatch for ") + nm);
+    if (m.dense == nullptr && (m.bits < 1 || m.bits > 8 || m.group_size < 1 || !m.scales || !m.zeros))
+      return fail(LRC_ERR_INVALID, std::string("bad quantization params for ") + nm);
+    return LRC_OK;
+  };
+  lrc_status s;
+  if ((s = chk(e.w1, ffn, hidden, "w1")) != LRC_OK) return s;
+  if ((s = chk(e.w3, ffn, hidden, "w3")) != LRC_OK) return s;
+  if ((s = chk(e.w2, hidden, ffn, "w2")) != LRC_OK) return s;
+  const lrc_qmat* us[3] = {&e.u1, &e.u3, &e.u2};
+  const lrc_qmat* vs[3] = {&e.v1, &e.v3, &e.v2};
+  const int rows[3] = {ffn, ffn, hidden}, cols[3] = {hidden, hidden, ffn};
+  for (int i = 0; i < 3; ++i) {
+    int r = rank_of(*us[i]);
+    if (r == 0) continue;
+    if (us[i]->rows != rows[i] || vs[i]->rows != r || vs[i]->cols != cols[i] ||
+        (vs[i]->packed == nullptr && vs[i]->dense == nullptr))
+      return fail(LRC_ERR_INVALID, "compensator factor shapes incompatible with the projection");
+  }
+  return LRC_OK;
+}
+
+static lrc_status alloc_workspace(lrc_layer* L) {
+  const int NE = L->E + L->S;
+  const int NP = L->max_tokens * (L->k_max + L->S);
+  L->max_pairs = NP;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  size_t o_ticket = take(16), o_counts = take(16), o_hc = take(NE);
+  size_t o_pe = take(NP * 4), o_pw = take(NP * 4), o_pt = take(NP * 4), o_pc = take(NP * 4);
+  size_t o_pl = take(NP * 4), o_cl = take(NP * 4);
+  size_t o_act = take(NE * 4), o_aoff = take(NE * 4), o_acnt = take(NE * 4);
+  size_t o_tki = take(size_t(L->max_tokens) * L->k_max * 4);
+  size_t o_tkw = take(size_t(L->max_tokens) * L->k_max * 4);
+  size_t o_t = take(size_t(NP) * 3 * std::max(L->maxr, 1) * 4);
+  size_t o_a32 = take(size_t(NP) * L->ffn * 4);
+  size_t o_a16 = take(size_t(NP) * L->ffn * 2 + 64);
+  size_t o_xs = take(size_t(L->max_tokens) * L->hidden * 2);
+  size_t o_ys = take(size_t(L->max_tokens) * L->hidden * 4);
+  LRC_CUDA_TRY(cudaMalloc(&L->ws, off));
+  LRC_CUDA_TRY(cudaMemset(L->ws, 0, off));
+  L->ws_bytes = off;
+  char* base = static_cast<char*>(L->ws);
+  PlanArgs& p = L->plan;
+  p.ticket = reinterpret_cast<int*>(base + o_ticket);
+  p.counts = reinterpret_cast<int*>(base + o_counts);
+  p.has_comp = reinterpret_cast<uint8_t*>(base + o_hc);
+  p.pair_expert = reinterpret_cast<int*>(base + o_pe);
+  p.pair_w = reinterpret_cast<float*>(base + o_pw);
+  p.pair_token = reinterpret_cast<int*>(base + o_pt);
+  p.pair_comp = reinterpret_cast<int*>(base + o_pc);
+  p.pair_list = reinterpret_cast<int*>(base + o_pl);
+  p.comp_list = reinterpret_cast<int*>(base + o_cl);
+  p.active = reinterpret_cast<int*>(base + o_act);
+  p.active_off = reinterpret_cast<int*>(base + o_aoff);
+  p.active_cnt = reinterpret_cast<int*>(base + o_acnt);
+  p.num_experts = L->E;
+  p.num_shared = L->S;
+  L->topk_idx = reinterpret_cast<int32_t*>(base + o_tki);
+  L->topk_w = reinterpret_cast<float*>(base + o_tkw);
+  L->t = reinterpret_cast<float*>(base + o_t);
+  L->a32 = reinterpret_cast<float*>(base + o_a32);
+  L->a16 = reinterpret_cast<uint16_t*>(base + o_a16);
+  L->x_stage = reinterpret_cast<uint16_t*>(base + o_xs);
+  L->y_stage = reinterpret_cast<float*>(base + o_ys);
+  for (auto& e : L->ev) LRC_CUDA_TRY(cudaEventCreate(&e));
+  std::vector<uint8_t> hc(NE);
+  for (int e = 0; e < NE; ++e) hc[e] = has_comp(L->host_experts[e]) ? 1 : 0;
+  LRC_CUDA_TRY(cudaMemcpy(const_cast<uint8_t*>(p.has_comp), hc.data(), NE, cudaMemcpyHostToDevice));
+  return LRC_OK;
+}
+
+extern "C" lrc_status lrc_layer_create(const double* gate_t, int hidden, int ffn, int num_experts,
+                                       int num_shared, const lrc_expert* experts, int max_tokens,
+                                       int top_k, lrc_layer** out) {
+  if (!out || !gate_t || !experts) return fail(LRC_ERR_INVALID, "layer_create: null argument");
+  if (hidden <= 0 || ffn <= 0 || num_experts <= 0 || num_shared < 0 || max_tokens <= 0)
+    return fail(LRC_ERR_INVALID, "layer_create: bad dimensions");
+  if (num_experts + num_shared > LRC_MAX_EXPERTS)
+    return fail(LRC_ERR_UNSUPPORTED, "layer_create: at most 256 experts");
+  if (top_k < 0 || top_k > num_experts) return fail(LRC_ERR_INVALID, "top_k exceeds experts");
+  auto* L = new lrc_layer();
+  L->hidden = hidden;
+  L->ffn = ffn;
+  L->E = num_experts;
+  L->S = num_shared;
+  L->max_tokens = max_tokens;
+  L->k_max = std::max(top_k, 1);
+  L->gate_t = gate_t;
+  L->host_experts.assign(experts, experts + num_experts + num_shared);
+  bool tiled = true;
+  for (auto& e : L->host_experts) {
+    lrc_status s = validate_expert(e, hidden, ffn);
+    if (s != LRC_OK) {
+      delete L;
+      return s;
+    }
+    L->maxr = std::max({L->maxr, rank_of(e.u1), rank_of(e.u2), rank_of(e.u3)});
+    tiled = tiled && e.up_tiles != nullptr && e.down_tiles != nullptr;
+  }
+  L->tiled = tiled;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t bytes = sizeof(lrc_expert) * L->host_experts.size();
+  if (cudaMalloc(&L->d_experts, bytes) != cudaSuccess ||
+      cudaMemcpy(L->d_experts, L->host_experts.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+    delete L;
+    return fail(LRC_ERR_CUDA, "layer_create: expert table upload failed");
+  }
+  lrc_status s = alloc_workspace(L);
+  if (s != LRC_OK) {
+    cudaFree(L->d_experts);
+    delete L;
+    return s;
+  }
+  *out = L;
+  return LRC_OK;
+}
+
+extern "C" void lrc_layer_destroy(lrc_layer* L) {
+  if (!L) return;
+  cudaFree(L->d_experts);
+  cudaFree(L->ws);
+  for (auto& e : L->ev)
+    if (e) cudaEventDestroy(e);
+  delete L;
+}
+
+extern "C" lrc_status lrc_layer_set_expert(lrc_layer* L, int expert_id, const lrc_expert* e) {
+  if (!L || !e || expert_id < 0 || expert_id >= L->E + L->S)
+    return fail(LRC_ERR_INVALID, "set_expert: bad id");
+  lrc_status s = validate_expert(*e, L->hidden, L->ffn);
+  if (s != LRC_OK) return s;
+  if (std::max({rank_of(e->u1), rank_of(e->u2), rank_of(e->u3)}) > L->maxr)
+    return fail(LRC_ERR_UNSUPPORTED, "set_expert: rank above the layer's workspace rank");
+  L->host_experts[expert_id] = *e;
+  LRC_CUDA_TRY(cudaMemcpy(L->d_experts + expert_id, e, sizeof(lrc_expert), cudaMemcpyHostToDevice));
+  bool tiled = true;
+  for (auto& x : L->host_experts) tiled = tiled && x.up_tiles && x.down_tiles;
+  L->tiled = tiled;
+  return LRC_OK;
+}
+
+extern "C" int lrc_layer_last_launches(const lrc_layer* L) { return L ? L->last_launches : 0; }
+
+static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int top_k, int top_n,
+                               int renormalize, int compensate_shared, float* y, int32_t* topk_idx,
+                               float* topk_w, void* stream, bool allow_tiled) {
+  if (!L || !x || !y) return fail(LRC_ERR_INVALID, "forward: null argument");
+  if (top_k < 0 || top_n < 0 || top_n > top_k)
+    return fail(LRC_ERR_INVALID, "top_n must be <= top_k and both >= 0");
+  if (top_k > L->E) return fail(LRC_ERR_INVALID, "top_k exceeds the number of experts");
+  if (top_k > L->k_max) return fail(LRC_ERR_UNSUPPORTED, "top_k above the layer's workspace");
+  if (B < 0 || B > L->max_tokens) return fail(LRC_ERR_UNSUPPORTED, "B above max_tokens");
+  cudaStream_t st = as_stream(stream);
+  int launches = 0;
+  const bool prof = L->profiling;
+  if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[0], st));
+  LRC_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(float) * B * L->hidden, st));
+  if (B == 0) {
+    L->last_launches = 0;
+    return LRC_OK;
+  }
+  PlanArgs plan = L->plan;
+  plan.top_n = top_n;
+  plan.compensate_shared = compensate_shared;
+  int32_t* ti = topk_idx ? topk_idx : L->topk_idx;
+  float* tw = topk_w ? topk_w : L->topk_w;
+  lrc_status s = launch_route(L->gate_t, x, LRC_DTYPE_BF16, B, L->hidden, L->E, top_k,
+                              renormalize, nullptr, ti, tw, plan, st);
+  if (s != LRC_OK) return s;
+  ++launches;
+  if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[1], st));
+  const int P = top_k + L->S;
+  const int np_bound = static_cast<int>(B) * P;
+  ExpertArgs a{};
+  a.experts = L->d_experts;
+  a.plan = plan;
+  a.hidden = L->hidden;
+  a.ffn = L->ffn;
+  a.maxr = L->maxr;
+  a.x = x;
+  a.t = L->t;
+  a.a32 = L->a32;
+  a.a16 = L->a16;
+  a.y = y;
+  a.max_pairs = L->max_pairs;
+  if (allow_tiled && L->tiled && L->maxr)  // t2 is accumulated by the tiled up kernel
+    LRC_CUDA_TRY(cudaMemsetAsync(L->t, 0, sizeof(float) * np_bound * 3 * L->maxr, st));
+  if ((s = launch_lr_down(a, np_bound, st)) != LRC_OK) return s;
+  if (L->maxr) ++launches;
+  if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[2], st));
+  if (allow_tiled && L->tiled) {
+    const int tok_bound = static_cast<int>(std::min<int64_t>(B, L->max_tokens));
+    if ((s = launch_up_tiled(a, L->num_sms, tok_bound, st)) != LRC_OK) return s;
+    if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));
+    if ((s = launch_down_tiled(a, L->num_sms, tok_bound, st)) != LRC_OK) return s;
+    launches += 2;
+  } else {
+    const int grid = L->num_sms * 4;
+    up_generic_kernel<<<grid, 256, 0, st>>>(a);
+    LRC_CHECK_LAUNCH();
+    if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));
+    if (L->maxr) {
+      lr_mid_kernel<<<(np_bound * L->maxr + 7) / 8, 256, 0, st>>>(a);
+      LRC_CHECK_LAUNCH();
+      ++launches;
+    }
+    down_generic_kernel<<<grid, 256, 0, st>>>(a);
+    LRC_CHECK_LAUNCH();
+    launches += 2;
+  }
+  if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[4], st));
+  L->last_launches = launches;
+  return LRC_OK;
+}
+
+extern "C" lrc_status lrc_layer_forward(lrc_layer* L, const uint16_t* x, int64_t B, int top_k,
+                                        int top_n, int renormalize, int compensate_shared, float* y,
+                                        int32_t* topk_idx, float* topk_w, void* stream) {
+  return forward_impl(L, x, B, top_k, top_n, renormalize, compensate_shared, y, topk_idx, topk_w,
+                      stream, true);
+}
+
+extern "C" lrc_status lrc_layer_forward_generic(lrc_layer* L, const uint16_t* x, int64_t B,
+                                                int top_k, int top_n, int renormalize,
+                                                int compensate_shared, float* y, int32_t* topk_idx,
+                                                float* topk_w, void* stream) {
+  return forward_impl(L, x, B, top_k, top_n, renormalize, compensate_shared, y, topk_idx, topk_w,
+                      stream, false);
+}
+
+extern "C" lrc_status lrc_layer_forward_host(lrc_layer* L, const uint16_t* x_host, int64_t B,
+                                             int top_k, int top_n, int renormalize,
+                                             int compensate_shared, float* y_host, void* stream) {
+  if (!L || !x_host || !y_host) return fail(LRC_ERR_INVALID, "forward_host: null argument");
+  if (B < 0 || B > L->max_tokens) return fail(LRC_ERR_UNSUPPORTED, "B above max_tokens");
+  cudaStream_t st = as_stream(stream);
+  LRC_CUDA_TRY(cudaMemcpyAsync(L->x_stage, x_host, sizeof(uint16_t) * B * L->hidden,
+                               cudaMemcpyHostToDevice, st));
+  lrc_status s = forward_impl(L, L->x_stage, B, top_k, top_n, renormalize, compensate_shared,
+                              L->y_stage, nullptr, nullptr, stream, true);
+  if (s != LRC_OK) return s;
+  LRC_CUDA_TRY(cudaMemcpyAsync(y_host, L->y_stage, sizeof(float) * B * L->hidden,
+                               cudaMemcpyDeviceToHost, st));
+  return LRC_OK;
+}
+
+extern "C" lrc_status lrc_layer_set_profiling(lrc_layer* L, int enabled) {
+  if (!L) return fail(LRC_ERR_INVALID, "set_profiling: null layer");
+  L->profiling = enabled != 0;
+  return LRC_OK;
+}
+
+extern "C" lrc_status lrc_layer_phase_ms(lrc_layer* L, float* ms4) {
+  if (!L || !ms4) return fail(LRC_ERR_INVALID, "phase_ms: null argument");
+  LRC_CUDA_TRY(cudaEventSynchronize(L->ev[4]));
+  for (int i = 0; i < 4; ++i) LRC_CUDA_TRY(cudaEventElapsedTime(&ms4[i], L->ev[i], L->ev[i + 1]));
+  return LRC_OK;
+}
+
+extern "C" lrc_status lrc_dense_expert_f64(const double* w1, const double* w3, const double* w2,
+                                           int hidden, int ffn, const double* x, const double* mix,
+                                           int64_t B, double* y, void* stream) {
+  if (hidden <= 0 || ffn <= 0 || B < 0) return fail(LRC_ERR_INVALID, "dense_expert: bad shape");
+  if (B == 0) return LRC_OK;
+  cudaStream_t st = as_stream(stream);
+  double* act = nullptr;
+  LRC_CUDA_TRY(cudaMallocAsync(&act, sizeof(double) * B * ffn, st));
+  int64_t w1n = B * ffn * 32, w2n = B * hidden * 32;
+  dense_up_f64_kernel<<<static_cast<unsigned>((w1n + 255) / 256), 256, 0, st>>>(w1, w3, hidden, ffn,
+                                                                                 x, B, act);
+  dense_down_f64_kernel<<<static_cast<unsigned>((w2n + 255) / 256), 256, 0, st>>>(w2, hidden, ffn,
+                                                                                   act, mix, B, y);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(act, st);
+  if (e != cudaSuccess) return fail(LRC_ERR_CUDA, cudaGetErrorString(e));
+  return LRC_OK;
+}

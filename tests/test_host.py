@@ -1,0 +1,146 @@
+"""CPU-side tests: the C-ABI library loads and exports every declared symbol,
+host logic (configs, byte accounting, generators, traces) matches the reference."""
+
+import hashlib
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+G = np.load(os.path.join(ROOT, "tests", "golden", "golden.npz"))
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "lrc.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:lrc_status|int64_t|int|void|const char\*)\s+(lrc_\w+)\(",
+                                 src, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    import ctypes
+
+    from paper_2512_17073_b200 import _lib
+
+    lib = _lib.load()
+    names = header_functions()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in _lib.EXPORTED, n
+    assert lib.lrc_abi_version() == 1
+    # struct layout agrees with the header (ctypes mirrors the C ABI)
+    assert ctypes.sizeof(_lib.LrcQmat) == 48
+    assert ctypes.sizeof(_lib.LrcExpert) == 3 * 48 + 8 + 6 * 48 + 16
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    from paper_2512_17073_b200 import _lib
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_byte_accounting_c1():
+    """Acceptance c1 (ref tests/test_acceptance.py:40-54) + SURVEY 8(d) roofline bytes."""
+    from paper_2512_17073_b200 import lowrank, quant
+
+    assert 3 * quant.packed_size_bytes(4096, 14336, 2) == 44_040_192
+    r16 = 3 * lowrank.compensator_size_bytes(4096, 14336, 16)
+    assert r16 == 331_776 and round(r16 / 2**20, 3) == 0.316
+    r128 = 3 * lowrank.compensator_size_bytes(4096, 14336, 128)
+    assert r128 == 2_654_208 and round(r128 / 2**20, 2) == 2.53
+    assert 3 * quant.packed_size_bytes(4096, 14336, 2, include_metadata=True) == 55_050_240
+    assert 3 * quant.packed_size_bytes(4096, 14336, 3, include_metadata=True) == 77_070_336
+    assert quant.packed_size_bytes(4, 128, 2, include_metadata=True) == (4 * 128 * 2 + 7) // 8 + 32
+    with pytest.raises(quant.QuantizationError):
+        quant.packed_size_bytes(0, 4, 2)
+    with pytest.raises(lowrank.CompensatorError):
+        lowrank.compensator_size_bytes(-1, 4, 2)
+
+
+def test_roofline_bytes_formula():
+    import bench
+
+    b = bench.layer_bytes(hidden=4096, ffn=14336, bits=2, rank=32, d_sel=2, d_comp=1, B=1, E=8)
+    assert abs(b / 1e6 - 111.09) < 0.01  # C2 INT2 B=1 = 111.09 MB
+    assert bench.comp_bytes(4096, 14336, 32) == 839_680
+    f = bench.layer_flops(4096, 14336, 2, 1, 32, 8)
+    assert abs(f / 1e6 - 708.2) < 0.5  # 708.2 MFLOP per token
+
+
+def test_configs_validate():
+    from paper_2512_17073_b200 import moe, quant
+
+    with pytest.raises(quant.QuantizationError):
+        quant.QuantConfig(bits=5)
+    with pytest.raises(quant.QuantizationError):
+        quant.QuantConfig(bits=2, group_size=0)
+    with pytest.raises(quant.QuantizationError):
+        quant.QuantConfig(hqq_shrink_p=0.0)
+    with pytest.raises(moe.MoEError):
+        moe.ForwardConfig(top_k=1, top_n=2)
+    with pytest.raises(moe.MoEError):
+        moe.ForwardConfig(top_k=-1)
+    assert issubclass(moe.MissingArtifactError, KeyError)
+    assert issubclass(quant.QuantizationError, ValueError)
+
+
+def test_generator_bit_exact_with_reference():
+    from paper_2512_17073_b200 import moe
+
+    m = moe.gen_synthetic_model(seed=7, hidden=64, ffn=128, num_layers=2, num_experts=8,
+                                top_k=2, num_shared=1, tail_dofs=(4.0, math.inf), router_skew=1.4)
+    assert [sha(m.layers[0].gate), sha(m.layers[1].experts[3].w2),
+            sha(m.layers[1].shared_experts[0].w1)] == list(G["toy_sha"])
+    with pytest.raises(moe.MoEError):
+        moe.gen_synthetic_model(seed=0, hidden=4, ffn=4, num_layers=1, num_experts=2,
+                                tail_dofs=(2.0,))
+    np.testing.assert_array_equal(moe.gen_tokens(11, 64, 6), G["toy_x"])
+
+
+def test_trace_jsonl_round_trip(tmp_path):
+    from paper_2512_17073_b200 import moe
+
+    recs = [moe.TraceRecord(t, l, np.random.default_rng(t).random(4), [1, 2], [1])
+            for t in range(3) for l in range(2)]
+    tr = moe.RoutingTrace(recs)
+    tr.to_jsonl(tmp_path / "t.jsonl")
+    back = moe.RoutingTrace.from_jsonl(tmp_path / "t.jsonl")
+    assert len(back.records) == 6 and back.num_tokens() == 3 and back.num_layers() == 2
+    for a, b in zip(recs, back.records):
+        np.testing.assert_array_equal(a.scores, b.scores)
+        assert a.selected == b.selected
+    with pytest.raises(moe.MoEError):
+        moe.routing_stats(moe.RoutingTrace([]))
+
+
+def test_no_cpu_fallback_without_device():
+    """The product refuses to compute without CUDA instead of silently using the CPU."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    from paper_2512_17073_b200 import quant
+
+    with pytest.raises(RuntimeError):
+        quant.dequantize(quant.QuantizedMatrix(1, 4, 2, 64, np.zeros((1, 4), np.uint8),
+                                               np.ones((1, 1)), np.zeros((1, 1))))
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2512_17073_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith(".py") and f != "synth.py":
+                src = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
