@@ -556,12 +556,19 @@ template <bool UP, int NT>
 static lrc_status launch_one(TiledParams& P, int num_sms, cudaStream_t st) {
   constexpr int NI = TileCfg<UP>::NI;
   const SmemMap m = smem_map<NT>(P, NI);
-  if (m.total > 227 * 1024) return fail(LRC_ERR_UNSUPPORTED, "tiled kernel: shared memory budget");
-  static int configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
   auto fn = tiled_kernel<UP, NT>;
+  static int configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
   if (configured[UP][NT] < m.total) {
-    LRC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured[UP][NT] = 227 * 1024;
+    cudaFuncAttributes fa{};
+    LRC_CUDA_TRY(cudaFuncGetAttributes(&fa, fn));
+    int dev = 0, optin = 0;
+    LRC_CUDA_TRY(cudaGetDevice(&dev));
+    LRC_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (m.total + static_cast<int>(fa.sharedSizeBytes) > optin)
+      return fail(LRC_ERR_UNSUPPORTED, "tiled kernel: shared memory budget");
+    LRC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      optin - static_cast<int>(fa.sharedSizeBytes)));
+    configured[UP][NT] = optin - static_cast<int>(fa.sharedSizeBytes);
   }
   fn<<<num_sms, kThreads, m.total, st>>>(P);
   LRC_CHECK_LAUNCH();
@@ -594,7 +601,7 @@ static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, cu
   const int nt = (max_tok <= 8) ? 1 : 2;
   for (P.nstage = 4; P.nstage >= 2; --P.nstage) {
     int total = (nt == 1) ? smem_map<1>(P, NI).total : smem_map<2>(P, NI).total;
-    if (total <= 227 * 1024) break;
+    if (total <= 227 * 1024 - 4096) break;
   }
   if (P.nstage < 2) P.nstage = 2;
   return (nt == 1) ? launch_one<UP, 1>(P, num_sms, st) : launch_one<UP, 2>(P, num_sms, st);

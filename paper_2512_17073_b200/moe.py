@@ -318,9 +318,13 @@ def _forward_batch(xs: np.ndarray, layer: MoELayer, cfg: ForwardConfig, mode: st
                                        cfg.renormalize_topk)
         y = torch.zeros((B, layer.gate.shape[0]), dtype=torch.float64, device="cuda")
         idx_h = idx.cpu().numpy()
-        mix_d = mix.double()
+        sel = idx[:, : cfg.top_k].long()
+        mix_d = torch.gather(probs, 1, sel)  # fp64 mixing weights (ref/moe.py:234)
+        if cfg.renormalize_topk:
+            tot = mix_d.sum(dim=1, keepdim=True)
+            mix_d = torch.where(tot > 0, mix_d / tot, mix_d)
         for e in sorted({int(v) for v in idx_h[:, : cfg.top_k].ravel()}):
-            m = ((idx[:, : cfg.top_k] == e).double() * mix_d[:, : cfg.top_k]).sum(dim=1).contiguous()
+            m = ((sel == e).double() * mix_d).sum(dim=1).contiguous()
             _dense_expert_accum(layer.experts[e], xd, m, y)
         for s in layer.shared_experts:
             _dense_expert_accum(s, xd, None, y)

@@ -46,7 +46,7 @@ class SynthLayer:
 
     def __init__(self, hidden, ffn, num_experts, top_k=2, num_shared=0, bits=2, rank=32,
                  factor_bits=3, seed=0, router_skew=1.4, max_tokens=64, tiles=True,
-                 comp_experts=None):
+                 comp_experts=None, zero_weights=False):
         torch = _lib.device_required()
         self.hidden, self.ffn, self.E, self.S = hidden, ffn, num_experts, num_shared
         self.bits, self.rank, self.top_k = bits, rank, top_k
@@ -66,6 +66,9 @@ class SynthLayer:
             raw = {}
             for name, (r, c) in (("w1", (ffn, hidden)), ("w3", (ffn, hidden)), ("w2", (hidden, ffn))):
                 m, t = _qmat(self.keep, gen, r, c, bits, 64, wscale, qmax / 2.0)
+                if zero_weights:  # scale = zero = 0: only the low-rank path contributes
+                    t[1].zero_()
+                    t[2].zero_()
                 setattr(ex, name, m)
                 raw[name] = (*t, r, c, bits, 64)
             if rank > 0 and e in comp_experts:
