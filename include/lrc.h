@@ -101,6 +101,8 @@ typedef struct {
   lrc_qmat u1, v1, u3, v3, u2, v2;
   const uint8_t* up_tiles;
   const uint8_t* down_tiles;
+  const uint8_t* up_lr_tiles;   /* per 16-row tile: U1, U3 rows + V2^T rows (+ fp16 meta) */
+  const uint8_t* down_lr_tiles; /* per 16-row tile: U2 rows (+ fp16 meta)                 */
 } lrc_expert;
 
 /* Bytes of the fast tiled layout for a (rows, cols) 2-bit gs=64 matrix, with
@@ -108,6 +110,15 @@ typedef struct {
 int64_t lrc_tiles_bytes(int64_t rows, int64_t cols, int interleave);
 /* Repack `interleave` reference-format matrices into the tiled layout. */
 lrc_status lrc_build_tiles(const lrc_qmat* mats, int interleave, uint8_t* tiles, void* stream);
+/* Low-rank factor tiles: the rows of U1/U3/V2^T (up) and U2 (down) that belong
+ * to each 16-row weight tile, re-laid out contiguously (same 3-bit codes and
+ * fp16 metadata) so they stream into shared memory with the weight tile.
+ * Sizes are per expert (its factor ranks); requires factor group sizes that
+ * are multiples of 16 for V2.  *_bytes may be 0 (no compensator). */
+lrc_status lrc_lr_tiles_bytes(const lrc_expert* e, int hidden, int ffn, int64_t* up_bytes,
+                              int64_t* down_bytes);
+lrc_status lrc_build_lr_tiles(const lrc_expert* e, int hidden, int ffn, uint8_t* up_lr,
+                              uint8_t* down_lr, void* stream);
 /* Bit-exact inverse (codes of matrix `which`), for the K6 parity test. */
 lrc_status lrc_tiles_unpack(const uint8_t* tiles, int64_t rows, int64_t cols, int interleave,
                             int which, uint8_t* codes, void* stream);

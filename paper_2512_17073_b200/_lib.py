@@ -29,7 +29,7 @@ class LrcExpert(ctypes.Structure):
     _fields_ = [("w1", LrcQmat), ("w3", LrcQmat), ("w2", LrcQmat), ("rank", c_int32),
                 ("u1", LrcQmat), ("v1", LrcQmat), ("u3", LrcQmat), ("v3", LrcQmat),
                 ("u2", LrcQmat), ("v2", LrcQmat), ("up_tiles", c_void_p),
-                ("down_tiles", c_void_p)]
+                ("down_tiles", c_void_p), ("up_lr_tiles", c_void_p), ("down_lr_tiles", c_void_p)]
 
 
 # name -> (restype, argtypes)
@@ -48,6 +48,9 @@ _SIGS = {
                           c_void_p, c_void_p, c_void_p, c_void_p]),
     "lrc_tiles_bytes": (c_int64, [c_int64, c_int64, c_int]),
     "lrc_build_tiles": (c_int, [POINTER(LrcQmat), c_int, c_void_p, c_void_p]),
+    "lrc_lr_tiles_bytes": (c_int, [POINTER(LrcExpert), c_int, c_int, POINTER(c_int64),
+                                   POINTER(c_int64)]),
+    "lrc_build_lr_tiles": (c_int, [POINTER(LrcExpert), c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "lrc_tiles_unpack": (c_int, [c_void_p, c_int64, c_int64, c_int, c_int, c_void_p, c_void_p]),
     "lrc_layer_create": (c_int, [c_void_p, c_int, c_int, c_int, c_int, POINTER(LrcExpert), c_int,
                                  c_int, POINTER(c_void_p)]),

@@ -177,59 +177,158 @@ __device__ __forceinline__ float inv_mult(int j) {
   return (j % 3 == 0) ? 1.0f : ((j % 3 == 1) ? 0.25f : 0.0625f);
 }
 
-// --------------------------------------------------------- tiled kernel ---
-template <bool UP>
-struct TileCfg {
-  static constexpr int NI = UP ? 2 : 1;
-};
+// ------------------------------------------------------------- LR tiles ---
+// Stream of a 16-row tile of factor rows: element (rr, j) at index rr*r + j
+// (LSB-first, the factor's own bit width).  One thread per output byte.
+template <typename F>
+__device__ void fill_stream(uint8_t* dst, int nbytes, int bits, int count, F code_of) {
+  for (int b = threadIdx.x; b < nbytes; b += blockDim.x) {
+    uint32_t v = 0;
+    for (int t = 0; t < 8; ++t) {
+      const int gbit = b * 8 + t;
+      const int idx = gbit / bits;
+      if (idx < count) v |= ((code_of(idx) >> (gbit - idx * bits)) & 1u) << t;
+    }
+    dst[b] = static_cast<uint8_t>(v);
+  }
+}
 
+__device__ void fill_u_meta(uint8_t* dst, const lrc_qmat& u, int64_t row0) {
+  const int gpu = (u.cols + u.group_size - 1) / u.group_size;
+  uint16_t* d = reinterpret_cast<uint16_t*>(dst);
+  for (int i = threadIdx.x; i < 16 * gpu; i += blockDim.x) {
+    const int rr = i / gpu, g = i - rr * gpu;
+    const int64_t R = row0 + rr;
+    const bool ok = R < u.rows;
+    d[2 * i] = ok ? u.scales[R * gpu + g] : 0;
+    d[2 * i + 1] = ok ? u.zeros[R * gpu + g] : 0;
+  }
+}
+
+__device__ void fill_u_codes(uint8_t* dst, const lrc_qmat& u, int64_t row0) {
+  const int r = u.cols;
+  const int64_t nb = (static_cast<int64_t>(u.rows) * r * u.bits + 7) >> 3;
+  fill_stream(dst, (16 * r * u.bits + 7) / 8, u.bits, 16 * r, [&](int idx) -> uint32_t {
+    const int rr = idx / r, j = idx - rr * r;
+    const int64_t R = row0 + rr;
+    return R < u.rows ? read_code(u.packed, R * r + j, u.bits, nb) : 0u;
+  });
+}
+
+__global__ void build_lr_up_kernel(lrc_expert e, LrLayout L, uint8_t* __restrict__ out) {
+  const int64_t t = blockIdx.x;
+  uint8_t* base = out + t * L.up_total;
+  const int64_t row0 = t * 16;
+  if (factor_present(e.u1)) {
+    fill_u_codes(base + L.u1c, e.u1, row0);
+    fill_u_meta(base + L.u1m, e.u1, row0);
+  }
+  if (factor_present(e.u3)) {
+    fill_u_codes(base + L.u3c, e.u3, row0);
+    fill_u_meta(base + L.u3m, e.u3, row0);
+  }
+  if (factor_present(e.v2)) {
+    // V2^T rows: element (rr, j) = V2[j, row0 + rr]; group of the tile along ffn
+    const lrc_qmat& v = e.v2;
+    const int r2 = v.rows;
+    const int64_t nb = (static_cast<int64_t>(v.rows) * v.cols * v.bits + 7) >> 3;
+    fill_stream(base + L.v2c, (16 * r2 * v.bits + 7) / 8, v.bits, 16 * r2, [&](int idx) -> uint32_t {
+      const int rr = idx / r2, j = idx - rr * r2;
+      const int64_t f = row0 + rr;
+      return f < v.cols ? read_code(v.packed, static_cast<int64_t>(j) * v.cols + f, v.bits, nb) : 0u;
+    });
+    const int gpr = (v.cols + v.group_size - 1) / v.group_size;
+    const int64_t gv = row0 / v.group_size;
+    uint16_t* d = reinterpret_cast<uint16_t*>(base + L.v2m);
+    for (int j = threadIdx.x; j < r2; j += blockDim.x) {
+      d[2 * j] = v.scales[static_cast<int64_t>(j) * gpr + gv];
+      d[2 * j + 1] = v.zeros[static_cast<int64_t>(j) * gpr + gv];
+    }
+  }
+}
+
+__global__ void build_lr_down_kernel(lrc_expert e, LrLayout L, uint8_t* __restrict__ out) {
+  const int64_t t = blockIdx.x;
+  uint8_t* base = out + t * L.down_total;
+  if (factor_present(e.u2)) {
+    fill_u_codes(base + L.u2c, e.u2, t * 16);
+    fill_u_meta(base + L.u2m, e.u2, t * 16);
+  }
+}
+
+__device__ __forceinline__ float lr_deq(const uint8_t* codes, int idx, int bits, const uint8_t* meta,
+                                        int midx) {
+  const uint32_t c = read_code(codes, idx, bits, 1 << 30);
+  const uint32_t sz = *reinterpret_cast<const uint32_t*>(meta + midx * 4);
+  return fmaf(static_cast<float>(c), h2f(sz & 0xffff), h2f(sz >> 16));
+}
+
+// --------------------------------------------------------- tiled kernel ---
 struct TiledParams {
   ExpertArgs a;
-  int M, K;            // rows / cols of the streamed matrix (per interleaved matrix)
-  int64_t GP, RT;      // group pairs per row, row tiles
-  int NS, SPC, nchunk; // spans, spans per chunk, chunks
-  int stage_bytes, nstage;
-  int xs_stride;       // bf16 elements per x' row
+  int M, K;             // rows / cols of the streamed matrix (per interleaved matrix)
+  int64_t GP, RT;       // group pairs per row, row tiles
+  int NS, SPC, nchunk;  // spans, spans per chunk, chunks
+  int stage_bytes;      // weight bytes per stage
+  int lr_slot;          // low-rank tile bytes per stage (max over experts; 0 = none)
+  int nstage;
+  int xs_stride;        // bf16 elements per x' row
 };
 
-// shared memory carve-up (bytes)
 struct SmemMap {
-  int stages, xs, sums, red, bars, total;
+  int xs, sums, red, ts, act, lrs, bars, total;
 };
 
-template <int NT>
-__host__ __device__ inline SmemMap smem_map(const TiledParams& p, int ni) {
+__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+
+template <int NI, int NT>
+__host__ __device__ inline SmemMap smem_map(const TiledParams& p) {
+  constexpr int TPP = 8 * NT;
   SmemMap m;
-  m.stages = 0;
-  m.xs = p.stage_bytes * p.nstage;
-  m.sums = m.xs + 8 * NT * p.xs_stride * 2;
-  const int groups = p.SPC * kSpanGP * 2;
-  m.red = m.sums + groups * 8 * NT * 8;
-  m.bars = m.red + ni * NT * 16 * 8 * 4;
-  m.total = m.bars + 2 * p.nstage * 8 + 64;
+  int o = p.nstage * (p.stage_bytes + p.lr_slot);
+  m.xs = o;
+  o = align16(o + TPP * p.xs_stride * 2);
+  m.sums = o;
+  o = align16(o + p.SPC * kSpanGP * 2 * TPP * 8);
+  m.red = o;
+  o = align16(o + kNW * NI * NT * 128 * 4);
+  m.ts = o;
+  o = align16(o + TPP * NI * (p.a.maxr > 0 ? p.a.maxr : 1) * 4);
+  m.act = o;
+  o = align16(o + 16 * TPP * 4);
+  m.lrs = o;
+  o = align16(o + NI * 16 * TPP * 4);
+  m.bars = o;
+  m.total = o + 2 * p.nstage * 8;
   return m;
 }
 
 template <bool UP, int NT>
 __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
-  constexpr int NI = TileCfg<UP>::NI;
+  constexpr int NI = UP ? 2 : 1;
   constexpr int TPP = 8 * NT;  // tokens per pass
   extern __shared__ __align__(128) uint8_t smem[];
-  const SmemMap SM = smem_map<NT>(P, NI);
-  uint8_t* stages = smem + SM.stages;
+  const SmemMap SM = smem_map<NI, NT>(P);
+  uint8_t* stages = smem;
+  const int slot_bytes = P.stage_bytes + P.lr_slot;
   uint16_t* xs = reinterpret_cast<uint16_t*>(smem + SM.xs);
-  float2* sums = reinterpret_cast<float2*>(smem + SM.sums);  // [g_local][TPP] (X, Xm)
-  float* red = reinterpret_cast<float*>(smem + SM.red);      // [NI][NT][16][8]
+  float2* sums = reinterpret_cast<float2*>(smem + SM.sums);  // [g_local][TPP] (X, -128 X')
+  float* red = reinterpret_cast<float*>(smem + SM.red);      // [warp][NI][NT][16][8]
+  float* ts = reinterpret_cast<float*>(smem + SM.ts);        // [comp c][NI][maxr]
+  float* act_s = reinterpret_cast<float*>(smem + SM.act);    // [16][TPP]
+  float* lrs = reinterpret_cast<float*>(smem + SM.lrs);      // [NI][16][TPP(comp idx)]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM.bars);
   uint64_t* empty = full + P.nstage;
   __shared__ int s_prefix[LRC_MAX_EXPERTS + 1];
   __shared__ int s_range[2];
-  __shared__ int s_comp_n[TPP], s_comp_slot[TPP], s_ncomp;
-  __shared__ float act_s[16 * TPP];
+  __shared__ int s_comp_n[TPP], s_comp_slot[TPP], s_comp_of[TPP], s_ncomp;
+  __shared__ int s_r[3], s_ub[3], s_ugs[3], s_vb;
+  __shared__ LrLayout s_L;
 
   const ExpertArgs& A = P.a;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_active = A.plan.counts[0];
+  const int maxr = A.maxr;
 
   if (threadIdx.x == 0) {
     int acc = 0;
@@ -248,12 +347,10 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = threadIdx.x; i < NI * NT * 128; i += blockDim.x) red[i] = 0.0f;
   __syncthreads();
   const int beg = s_range[0], end = s_range[1];
   if (beg >= end) return;
 
-  // item -> (active index, pass, chunk, tile)
   auto decode = [&](int it, int& ai, int& pass, int& chunk, int& tile) {
     int lo = 0;
     while (s_prefix[lo + 1] <= it) ++lo;
@@ -266,26 +363,45 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   };
   auto chunk_gp = [&](int chunk, int& gp0, int& gp1) {
     gp0 = chunk * P.SPC * kSpanGP;
-    gp1 = static_cast<int>(P.GP < static_cast<int64_t>(gp0) + P.SPC * kSpanGP ? P.GP : static_cast<int64_t>(gp0) + P.SPC * kSpanGP);
+    const int64_t hi = static_cast<int64_t>(gp0) + P.SPC * kSpanGP;
+    gp1 = static_cast<int>(P.GP < hi ? P.GP : hi);
   };
 
   if (warp == kNW) {
     // ===================== producer: one elected lane streams work items ====
     if (lane == 0) {
+      int c_ai = -1, c_pass = -1, c_comp = 0;
       for (int it = beg; it < end; ++it) {
         const int k = it - beg;
         const int s = k % P.nstage;
         if (k >= P.nstage) mbar_wait(&empty[s], ((k / P.nstage) - 1) & 1);
         int ai, pass, chunk, tile;
         decode(it, ai, pass, chunk, tile);
+        if (ai != c_ai || pass != c_pass) {
+          c_ai = ai;
+          c_pass = pass;
+          c_comp = 0;
+          const int off = A.plan.active_off[ai];
+          const int n = min(TPP, A.plan.active_cnt[ai] - pass * TPP);
+          for (int j = 0; j < n; ++j) c_comp |= A.plan.pair_comp[A.plan.pair_list[off + pass * TPP + j]] >= 0;
+        }
         int gp0, gp1;
         chunk_gp(chunk, gp0, gp1);
         const lrc_expert& E = A.experts[A.plan.active[ai]];
         const uint8_t* base = UP ? E.up_tiles : E.down_tiles;
         const uint8_t* src = base + ((static_cast<int64_t>(tile) * P.GP + gp0) * NI) * kBlk;
         const uint32_t bytes = static_cast<uint32_t>((gp1 - gp0) * NI * kBlk);
-        mbar_expect_tx(&full[s], bytes);
-        bulk_g2s(stages + static_cast<size_t>(s) * P.stage_bytes, src, bytes, &full[s]);
+        uint32_t lr_bytes = 0;
+        const uint8_t* lr_src = nullptr;
+        if (P.lr_slot > 0 && c_comp && (UP || chunk == 0)) {
+          const LrLayout L = lr_layout(E);
+          lr_bytes = static_cast<uint32_t>(UP ? L.up_total : L.down_total);
+          lr_src = (UP ? E.up_lr_tiles : E.down_lr_tiles) + static_cast<int64_t>(tile) * lr_bytes;
+        }
+        uint8_t* dst = stages + static_cast<size_t>(s) * slot_bytes;
+        mbar_expect_tx(&full[s], bytes + lr_bytes);
+        bulk_g2s(dst, src, bytes, &full[s]);
+        if (lr_bytes) bulk_g2s(dst + P.stage_bytes, lr_src, lr_bytes, &full[s]);
       }
     }
     return;
@@ -303,91 +419,104 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     int gp0, gp1;
     chunk_gp(chunk, gp0, gp1);
     const int off = A.plan.active_off[ai], cnt = A.plan.active_cnt[ai];
-    const int e = A.plan.active[ai];
-    const lrc_expert& E = A.experts[e];
+    const lrc_expert& E = A.experts[A.plan.active[ai]];
     if (ai != cur_ai || pass != cur_pass || chunk != cur_chunk) {
-      // ---- rebuild the activation operand x' for (expert tokens of this pass, chunk)
+      // ---- (re)build the activation operand x' and the LR vectors for this group
       consumer_sync();
+      const bool new_pass = (ai != cur_ai || pass != cur_pass);
       cur_ai = ai;
       cur_pass = pass;
       cur_chunk = chunk;
       pass_tok = min(TPP, cnt - pass * TPP);
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == 0 && new_pass) {
         int nc = 0;
-        for (int n = 0; n < pass_tok; ++n) {
-          const int slot = A.plan.pair_comp[A.plan.pair_list[off + pass * TPP + n]];
-          if (slot >= 0) {
-            s_comp_n[nc] = n;
-            s_comp_slot[nc] = slot;
-            ++nc;
+        for (int n = 0; n < TPP; ++n) {
+          s_comp_of[n] = -1;
+          if (n < pass_tok) {
+            const int slot = A.plan.pair_comp[A.plan.pair_list[off + pass * TPP + n]];
+            if (slot >= 0) {
+              s_comp_of[n] = nc;
+              s_comp_n[nc] = n;
+              s_comp_slot[nc] = slot;
+              ++nc;
+            }
           }
         }
         s_ncomp = nc;
+        s_L = lr_layout(E);
+        const lrc_qmat* us[3] = {&E.u1, &E.u3, &E.u2};
+        for (int i = 0; i < 3; ++i) {
+          s_r[i] = factor_present(*us[i]) ? us[i]->cols : 0;
+          s_ub[i] = us[i]->bits;
+          s_ugs[i] = us[i]->group_size;
+        }
+        s_vb = E.v2.bits;
       }
-      const int kc = (gp1 - gp0) * 128;
       const int k0 = gp0 * 128;
       const int ng = (gp1 - gp0) * 2;
-      for (int i = threadIdx.x; i < ng * TPP; i += kNW * 32) sums[i] = make_float2(0.f, 0.f);
-      consumer_sync();
-      // each thread: 8 consecutive columns of one token row
-      const int per_row = kc / 8;
-      for (int i = threadIdx.x; i < TPP * per_row; i += kNW * 32) {
-        const int n = i / per_row, c8 = (i - n * per_row) * 8;
-        float v[8];
+      for (int task = threadIdx.x; task < TPP * ng; task += kNW * 32) {
+        const int n = task / ng, g = task - n * ng;
+        float xsum = 0.f, xpsum = 0.f;
+        uint32_t* dst = reinterpret_cast<uint32_t*>(xs + n * P.xs_stride + g * 64);
         if (n < pass_tok) {
           const int p = A.plan.pair_list[off + pass * TPP + n];
-          const int kk = k0 + c8;
-          if (UP) {
-            const uint16_t* src = A.x + static_cast<int64_t>(A.plan.pair_token[p]) * A.hidden;
-            if (kk + 8 <= P.K && (A.hidden % 8) == 0) {
-              uint4 raw = *reinterpret_cast<const uint4*>(src + kk);
-              const uint16_t* h = reinterpret_cast<const uint16_t*>(&raw);
+          const uint16_t* row = UP ? A.x + static_cast<int64_t>(A.plan.pair_token[p]) * A.hidden
+                                   : A.a16 + static_cast<int64_t>(p) * A.ffn;
+          const int kk = k0 + g * 64;
+          uint4 raw[8];
+          const bool vec = (kk + 64 <= P.K) && ((reinterpret_cast<uintptr_t>(row + kk) & 15) == 0);
+          if (vec) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) v[j] = bf2f(h[j]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) v[j] = (kk + j < P.K) ? bf2f(src[kk + j]) : 0.0f;
-            }
+            for (int c8 = 0; c8 < 8; ++c8) raw[c8] = __ldg(reinterpret_cast<const uint4*>(row + kk) + c8);
           } else {
-            const uint16_t* src = A.a16 + static_cast<int64_t>(p) * A.ffn;
-            if (kk + 8 <= P.K && (A.ffn % 8) == 0) {
-              uint4 raw = *reinterpret_cast<const uint4*>(src + kk);
-              const uint16_t* h = reinterpret_cast<const uint16_t*>(&raw);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) v[j] = bf2f(h[j]);
-            } else {
+            for (int c8 = 0; c8 < 8; ++c8) {
+              uint16_t h[8];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) v[j] = (kk + j < P.K) ? bf2f(src[kk + j]) : 0.0f;
+              for (int j = 0; j < 8; ++j) h[j] = (kk + c8 * 8 + j < P.K) ? row[kk + c8 * 8 + j] : 0;
+              raw[c8] = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16),
+                                   h[4] | (uint32_t(h[5]) << 16), h[6] | (uint32_t(h[7]) << 16));
+            }
+          }
+#pragma unroll
+          for (int c8 = 0; c8 < 8; ++c8) {
+            const float im = inv_mult(c8);  // slot j = c8 for columns c8*8 .. c8*8+7
+            const uint32_t w4[4] = {raw[c8].x, raw[c8].y, raw[c8].z, raw[c8].w};
+            // column c8*8 + 2*tj + e  ->  16-block (c8/2), position tj*4 + p*2 + e with p = c8&1
+#pragma unroll
+            for (int tj = 0; tj < 4; ++tj) {
+              const float lo = bf2f(w4[tj] & 0xffff), hi = bf2f(w4[tj] >> 16);
+              xsum += lo + hi;
+              const float plo = lo * im, phi = hi * im;
+              xpsum += plo + phi;
+              dst[((c8 >> 1) * 16 + tj * 4 + (c8 & 1) * 2) >> 1] =
+                  static_cast<uint32_t>(f2bf(plo)) | (static_cast<uint32_t>(f2bf(phi)) << 16);
             }
           }
         } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = 0.0f;
+#pragma unroll 8
+          for (int w = 0; w < 32; ++w) dst[w] = 0u;
         }
-        // slot j = (col % 64) / 8 is constant over the 8 columns
-        const int jslot = (c8 % 64) / 8;
-        const float im = inv_mult(jslot);
-        float xsum = 0.f, xpsum = 0.f;
-        uint16_t* row = xs + n * P.xs_stride + (c8 / 16) * 16;
-        const int pbit = (c8 % 16) / 8;  // p
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float xp = v[j] * im;  // exact power-of-two scaling
-          xsum += v[j];
-          xpsum += xp;
-          const int tj = j / 2, ej = j % 2;
-          row[tj * 4 + pbit * 2 + ej] = f2bf(xp);
+        sums[g * TPP + n] = make_float2(xsum, -128.0f * xpsum);
+      }
+      consumer_sync();
+      // low-rank input vectors of the compensated tokens (t1/t3 up, t2 down)
+      if (maxr > 0) {
+        const int ntask = s_ncomp * NI * maxr;
+        for (int task = threadIdx.x; task < ntask; task += kNW * 32) {
+          const int j = task % maxr, ci = task / maxr;
+          const int i = ci % NI, c = ci / NI;
+          const int proj = UP ? i : 2;
+          ts[task] = __ldcg(A.t + (static_cast<int64_t>(s_comp_slot[c]) * 3 + proj) * maxr + j);
         }
-        const int g_local = c8 / 64;
-        atomicAdd(&sums[g_local * TPP + n].x, xsum);
-        atomicAdd(&sums[g_local * TPP + n].y, -128.0f * xpsum);
       }
       consumer_sync();
     }
+    const bool item_lr = (P.lr_slot > 0) && (s_ncomp > 0) && (UP || chunk == 0);
 
     // ---- wait for the weights of this item
     mbar_wait(&full[s], (k / P.nstage) & 1);
-    const uint8_t* st = stages + static_cast<size_t>(s) * P.stage_bytes;
+    const uint8_t* st = stages + static_cast<size_t>(s) * slot_bytes;
 
     float acc[NI][NT][4];
 #pragma unroll
@@ -415,14 +544,14 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
           float d[NI][NT][4];
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            const float2 xm0 = sums[gl * TPP + nt * 8 + 2 * tid];
-            const float2 xm1 = sums[gl * TPP + nt * 8 + 2 * tid + 1];
+            const float xm0 = sums[gl * TPP + nt * 8 + 2 * tid].y;
+            const float xm1 = sums[gl * TPP + nt * 8 + 2 * tid + 1].y;
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
-              d[i][nt][0] = xm0.y;
-              d[i][nt][1] = xm1.y;
-              d[i][nt][2] = xm0.y;
-              d[i][nt][3] = xm1.y;
+              d[i][nt][0] = xm0;
+              d[i][nt][1] = xm1;
+              d[i][nt][2] = xm0;
+              d[i][nt][3] = xm1;
             }
           }
           const uint16_t* xrow = xs + gl * 64 + tid * 4;
@@ -467,59 +596,69 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    // ---- cross-warp reduction into red[i][nt][row][col]
-    if (warp < nspan) {
+    if (!item_lr) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // ---- per-warp partials (no shared atomics)
+    const int nw = min(nspan, kNW);
+    if (warp < nw) {
 #pragma unroll
       for (int i = 0; i < NI; ++i)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          float* rb = red + (i * NT + nt) * 128;
-          atomicAdd(&rb[gid * 8 + 2 * tid], acc[i][nt][0]);
-          atomicAdd(&rb[gid * 8 + 2 * tid + 1], acc[i][nt][1]);
-          atomicAdd(&rb[(gid + 8) * 8 + 2 * tid], acc[i][nt][2]);
-          atomicAdd(&rb[(gid + 8) * 8 + 2 * tid + 1], acc[i][nt][3]);
+          float* rb = red + ((warp * NI + i) * NT + nt) * 128;
+          rb[gid * 8 + 2 * tid] = acc[i][nt][0];
+          rb[gid * 8 + 2 * tid + 1] = acc[i][nt][1];
+          rb[(gid + 8) * 8 + 2 * tid] = acc[i][nt][2];
+          rb[(gid + 8) * 8 + 2 * tid + 1] = acc[i][nt][3];
         }
     }
     consumer_sync();
 
-    // ---- epilogue E1: low-rank up-projection U.t for the compensated tokens
-    // (ref/lowrank.py:165 applied to this tile's rows only).  16 lanes share a
-    // (token, matrix, row) and split the rank dimension.
-    if (s_ncomp > 0 && (UP || chunk == 0)) {
-      const int ntask = s_ncomp * NI * 16 * 16;
+    // ---- E1: low-rank up-projection U.t for the tile rows (ref/lowrank.py:165),
+    // factor rows read from the stage's LR slot; 16 lanes split the rank.
+    if (item_lr) {
+      const uint8_t* lr = st + P.stage_bytes;
+      const int ntask = s_ncomp * NI * 256;
       for (int o = threadIdx.x; o < ntask; o += kNW * 32) {
-        const int jl = o & 15, r = (o >> 4) & 15;
+        const int jl = o & 15, rr = (o >> 4) & 15;
         const int i = (o >> 8) % NI, c = (o >> 8) / NI;
-        const int n = s_comp_n[c], slot = s_comp_slot[c];
-        const int row = tile * 16 + r;
-        const lrc_qmat& U = UP ? (i == 0 ? E.u1 : E.u3) : E.u2;
-        const int proj = UP ? i : 2;
+        const int pi = UP ? i : 2;  // projection index into s_r (0 u1, 1 u3, 2 u2)
+        const int r = s_r[pi];
         float v = 0.0f;
-        if (row < P.M && qmat_present(U)) {
-          const float* tp = A.t + (static_cast<int64_t>(slot) * 3 + proj) * A.maxr;
-          for (int j = jl; j < U.cols; j += 16) v = fmaf(qmat_elem(U, row, j), tp[j], v);
+        if (r > 0) {
+          const uint8_t* codes = lr + (UP ? (i ? s_L.u3c : s_L.u1c) : s_L.u2c);
+          const uint8_t* meta = lr + (UP ? (i ? s_L.u3m : s_L.u1m) : s_L.u2m);
+          const int gpu = (r + s_ugs[pi] - 1) / s_ugs[pi];
+          const float* tv = ts + (c * NI + i) * maxr;
+          for (int j = jl; j < r; j += 16)
+            v = fmaf(lr_deq(codes, rr * r + j, s_ub[pi], meta, rr * gpu + j / s_ugs[pi]), tv[j], v);
         }
 #pragma unroll
         for (int o2 = 8; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
-        if (jl == 0) red[(i * NT + (n >> 3)) * 128 + r * 8 + (n & 7)] += v;
+        if (jl == 0) lrs[(i * 16 + rr) * TPP + c] = v;
       }
       consumer_sync();
     }
+
     // ---- E2: thread -> (row r, token n)
     for (int o = threadIdx.x; o < 16 * TPP; o += kNW * 32) {
       const int r = o & 15, n = o >> 4;
       const int nt = n >> 3, col = n & 7;
       const int row = tile * 16 + r;
-      float* r0 = red + (0 * NT + nt) * 128 + r * 8 + col;
-      const float v0 = *r0;
-      *r0 = 0.0f;
+      float v0 = 0.0f, v1 = 0.0f;
+      for (int w = 0; w < nw; ++w) {
+        v0 += red[((w * NI + 0) * NT + nt) * 128 + r * 8 + col];
+        if (UP) v1 += red[((w * NI + NI - 1) * NT + nt) * 128 + r * 8 + col];
+      }
+      const int c = s_comp_of[n];
+      if (item_lr && c >= 0) {
+        v0 += lrs[(0 * 16 + r) * TPP + c];
+        if (UP) v1 += lrs[((NI - 1) * 16 + r) * TPP + c];
+      }
       const bool valid = (n < pass_tok) && (row < P.M);
       if (UP) {
-        float* r1 = red + ((NI - 1) * NT + nt) * 128 + r * 8 + col;
-        const float v1 = *r1;
-        *r1 = 0.0f;
         float act = 0.0f;
         if (valid) {
           const int p = A.plan.pair_list[off + pass * TPP + n];
@@ -533,29 +672,38 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
                   A.plan.pair_w[p] * v0);
       }
     }
-    // ---- E3 (up only): partial t2 = V2[:, tile rows] . act for compensated tokens
-    if (UP && s_ncomp > 0 && qmat_present(E.v2)) {
+    // ---- E3 (up): partial t2 = V2[:, tile rows] . act for the compensated tokens
+    if (UP && item_lr && s_r[2] > 0) {
       consumer_sync();
-      const int r2 = E.v2.rows;
+      const uint8_t* lr = st + P.stage_bytes;
+      const int r2 = s_r[2];
       const int ntask = s_ncomp * r2 * 16;
-      for (int o = threadIdx.x; o < ntask; o += kNW * 32) {
-        const int rl = o & 15, j = (o >> 4) % r2, c = (o >> 4) / r2;
-        const int n = s_comp_n[c], slot = s_comp_slot[c];
-        const int row = tile * 16 + rl;
-        float v = (row < P.M) ? qmat_elem(E.v2, j, row) * act_s[rl * TPP + n] : 0.0f;
+      const int nround = (ntask + 31) & ~31;
+      for (int o = threadIdx.x; o < nround; o += kNW * 32) {
+        const int rl = o & 15;
+        float v = 0.0f;
+        int j = 0, c = 0;
+        if (o < ntask) {
+          j = (o >> 4) % r2;
+          c = (o >> 4) / r2;
+          v = lr_deq(lr + s_L.v2c, rl * r2 + j, s_vb, lr + s_L.v2m, j) *
+              act_s[rl * TPP + s_comp_n[c]];
+        }
 #pragma unroll
         for (int o2 = 8; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
-        if (rl == 0) atomicAdd(&A.t[(static_cast<int64_t>(slot) * 3 + 2) * A.maxr + j], v);
+        if (rl == 0 && o < ntask)
+          atomicAdd(&A.t[(static_cast<int64_t>(s_comp_slot[c]) * 3 + 2) * maxr + j], v);
       }
     }
     consumer_sync();
+    if (item_lr && lane == 0) mbar_arrive(&empty[s]);
   }
 }
 
 template <bool UP, int NT>
-static lrc_status launch_one(TiledParams& P, int num_sms, cudaStream_t st) {
-  constexpr int NI = TileCfg<UP>::NI;
-  const SmemMap m = smem_map<NT>(P, NI);
+static lrc_status launch_one(const TiledParams& P, int num_sms, cudaStream_t st) {
+  constexpr int NI = UP ? 2 : 1;
+  const SmemMap m = smem_map<NI, NT>(P);
   auto fn = tiled_kernel<UP, NT>;
   static int configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
   if (configured[UP][NT] < m.total) {
@@ -575,43 +723,52 @@ static lrc_status launch_one(TiledParams& P, int num_sms, cudaStream_t st) {
   return LRC_OK;
 }
 
-static void plan_chunks(TiledParams& P, bool up) {
-  P.NS = static_cast<int>((P.GP + kSpanGP - 1) / kSpanGP);
-  if (up) {
-    P.nchunk = 1;
-    P.SPC = P.NS;
-  } else {
-    P.nchunk = (P.NS + kNW - 1) / kNW;
-    P.SPC = (P.NS + P.nchunk - 1) / P.nchunk;
-  }
-  P.xs_stride = P.SPC * kSpanGP * 128 + 16;
-}
-
 template <bool UP>
-static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, cudaStream_t st) {
+static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, int lr_max,
+                               cudaStream_t st) {
+  constexpr int NI = UP ? 2 : 1;
   TiledParams P{};
   P.a = a;
   P.M = UP ? a.ffn : a.hidden;
   P.K = UP ? a.hidden : a.ffn;
   P.GP = (P.K + 127) / 128;
   P.RT = (P.M + 15) / 16;
-  plan_chunks(P, UP);
-  constexpr int NI = TileCfg<UP>::NI;
-  P.stage_bytes = P.SPC * kSpanGP * NI * kBlk;
-  const int nt = (max_tok <= 8) ? 1 : 2;
-  for (P.nstage = 4; P.nstage >= 2; --P.nstage) {
-    int total = (nt == 1) ? smem_map<1>(P, NI).total : smem_map<2>(P, NI).total;
-    if (total <= 227 * 1024 - 4096) break;
+  P.NS = static_cast<int>((P.GP + kSpanGP - 1) / kSpanGP);
+  if (UP) {  // the SwiGLU needs complete h1/h3: one chunk covers all of K
+    P.nchunk = 1;
+    P.SPC = P.NS;
+  } else {  // split K into <= 8-span chunks; partial outputs combine with atomics
+    P.nchunk = (P.NS + kNW - 1) / kNW;
+    P.SPC = (P.NS + P.nchunk - 1) / P.nchunk;
   }
-  if (P.nstage < 2) P.nstage = 2;
+  P.xs_stride = P.SPC * kSpanGP * 128 + 16;
+  P.stage_bytes = P.SPC * kSpanGP * NI * kBlk;
+  P.lr_slot = lr_max;
+  const int budget = 227 * 1024 - 6 * 1024;
+  auto fits = [&](int nt) {
+    return (nt == 1 ? smem_map<NI, 1>(P).total : smem_map<NI, 2>(P).total) <= budget;
+  };
+  int nt = 1;
+  if (max_tok > 8) {
+    for (P.nstage = 3; P.nstage >= 2; --P.nstage)
+      if (fits(2)) break;
+    if (P.nstage >= 2) nt = 2;
+  }
+  if (nt == 1) {
+    for (P.nstage = 4; P.nstage >= 2; --P.nstage)
+      if (fits(1)) break;
+    if (P.nstage < 2) return fail(LRC_ERR_UNSUPPORTED, "tiled kernel: K too large for smem");
+  }
   return (nt == 1) ? launch_one<UP, 1>(P, num_sms, st) : launch_one<UP, 2>(P, num_sms, st);
 }
 
-lrc_status launch_up_tiled(const ExpertArgs& a, int num_sms, int max_tok, cudaStream_t st) {
-  return launch_tiled<true>(a, num_sms, max_tok, st);
+lrc_status launch_up_tiled(const ExpertArgs& a, int num_sms, int max_tok, int lr_max,
+                           cudaStream_t st) {
+  return launch_tiled<true>(a, num_sms, max_tok, lr_max, st);
 }
-lrc_status launch_down_tiled(const ExpertArgs& a, int num_sms, int max_tok, cudaStream_t st) {
-  return launch_tiled<false>(a, num_sms, max_tok, st);
+lrc_status launch_down_tiled(const ExpertArgs& a, int num_sms, int max_tok, int lr_max,
+                             cudaStream_t st) {
+  return launch_tiled<false>(a, num_sms, max_tok, lr_max, st);
 }
 
 }  // namespace lrc
@@ -637,6 +794,50 @@ extern "C" lrc_status lrc_build_tiles(const lrc_qmat* mats, int interleave, uint
   build_tiles_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, as_stream(stream)>>>(
       mats[0], mats[interleave - 1], interleave, RT, GP, tiles);
   LRC_CHECK_LAUNCH();
+  return LRC_OK;
+}
+
+static lrc_status lr_tiles_check(const lrc_expert* e, int hidden, int ffn) {
+  const lrc_qmat* fs[6] = {&e->u1, &e->v1, &e->u3, &e->v3, &e->u2, &e->v2};
+  for (auto f : fs) {
+    if (!factor_present(*f)) continue;
+    if (f->dense != nullptr)
+      return fail(LRC_ERR_UNSUPPORTED, "lr tiles: raw (unquantized) factors use the generic path");
+    if (f->bits < 1 || f->bits > 8) return fail(LRC_ERR_INVALID, "lr tiles: bad factor bits");
+  }
+  if (factor_present(e->v2) && (e->v2.group_size % 16) != 0)
+    return fail(LRC_ERR_UNSUPPORTED, "lr tiles: V2 group size must be a multiple of 16");
+  (void)hidden;
+  (void)ffn;
+  return LRC_OK;
+}
+
+extern "C" lrc_status lrc_lr_tiles_bytes(const lrc_expert* e, int hidden, int ffn,
+                                         int64_t* up_bytes, int64_t* down_bytes) {
+  if (!e || !up_bytes || !down_bytes) return fail(LRC_ERR_INVALID, "lr_tiles_bytes: null");
+  lrc_status s = lr_tiles_check(e, hidden, ffn);
+  if (s != LRC_OK) return s;
+  const LrLayout L = lr_layout(*e);
+  *up_bytes = static_cast<int64_t>(L.up_total) * ((ffn + 15) / 16);
+  *down_bytes = static_cast<int64_t>(L.down_total) * ((hidden + 15) / 16);
+  return LRC_OK;
+}
+
+extern "C" lrc_status lrc_build_lr_tiles(const lrc_expert* e, int hidden, int ffn, uint8_t* up_lr,
+                                         uint8_t* down_lr, void* stream) {
+  if (!e) return fail(LRC_ERR_INVALID, "build_lr_tiles: null");
+  lrc_status s = lr_tiles_check(e, hidden, ffn);
+  if (s != LRC_OK) return s;
+  const LrLayout L = lr_layout(*e);
+  cudaStream_t st = as_stream(stream);
+  if (L.up_total > 0 && up_lr) {
+    build_lr_up_kernel<<<(ffn + 15) / 16, 256, 0, st>>>(*e, L, up_lr);
+    LRC_CHECK_LAUNCH();
+  }
+  if (L.down_total > 0 && down_lr) {
+    build_lr_down_kernel<<<(hidden + 15) / 16, 256, 0, st>>>(*e, L, down_lr);
+    LRC_CHECK_LAUNCH();
+  }
   return LRC_OK;
 }
 

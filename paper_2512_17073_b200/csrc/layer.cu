@@ -10,6 +10,42 @@
 namespace lrc {
 
 // ------------------------------------------------------------ LR kernels ---
+// Row j of a quantized V (group size 64, BITS-bit LSB-first stream) dotted with
+// a bf16 vector: each lane takes whole 64-code groups, loads the group's
+// 2*BITS words at once and decodes them with funnel shifts.
+template <int BITS>
+__device__ float vrow_dot_g64(const lrc_qmat& V, int j, const uint16_t* __restrict__ xb) {
+  constexpr int W = 2 * BITS;  // 32-bit words per 64-code group
+  const int lane = threadIdx.x & 31;
+  const int gpr = (V.cols + 63) / 64;
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(V.packed);
+  const int64_t nwords = ((static_cast<int64_t>(V.rows) * V.cols * BITS + 7) >> 3) >> 2;
+  float acc = 0.0f;
+  for (int g = lane; g < gpr; g += 32) {
+    const int64_t w0 = ((static_cast<int64_t>(j) * V.cols + g * 64) * BITS) >> 5;
+    uint32_t w[W + 1];
+#pragma unroll
+    for (int i = 0; i <= W; ++i) w[i] = (w0 + i < nwords) ? __ldg(words + w0 + i) : 0u;
+    const int nv = min(64, V.cols - g * 64);
+    const float s = h2f(V.scales[static_cast<int64_t>(j) * gpr + g]);
+    const float z = h2f(V.zeros[static_cast<int64_t>(j) * gpr + g]);
+    const uint16_t* xg = xb + g * 64;
+    float cx = 0.0f, sx = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      if (i < nv) {
+        const int bit = i * BITS;
+        const uint32_t c = __funnelshift_r(w[bit >> 5], w[(bit >> 5) + 1], bit & 31) & ((1u << BITS) - 1u);
+        const float xv = bf2f(xg[i]);
+        cx = fmaf(static_cast<float>(c), xv, cx);
+        sx += xv;
+      }
+    }
+    acc = fmaf(s, cx, fmaf(z, sx, acc));
+  }
+  return warp_sum(acc);
+}
+
 // t[slot][proj][j] = V_proj(e)[j, :] . x_b  for compensated pairs, proj in {w1, w3}
 __global__ void __launch_bounds__(256) lr_down_kernel(ExpertArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -25,8 +61,17 @@ __global__ void __launch_bounds__(256) lr_down_kernel(ExpertArgs a) {
   float acc = 0.0f;
   if (qmat_present(V) && j < V.rows) {
     const uint16_t* xb = a.x + static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden;
-    for (int k = lane; k < V.cols; k += 32) acc = fmaf(qmat_elem(V, j, k), bf2f(xb[k]), acc);
-    acc = warp_sum(acc);
+    const bool g64 = V.dense == nullptr && V.group_size == 64 && ((V.cols * V.bits) % 32) == 0;
+    if (g64 && V.bits == 3) {
+      acc = vrow_dot_g64<3>(V, j, xb);
+    } else if (g64 && V.bits == 2) {
+      acc = vrow_dot_g64<2>(V, j, xb);
+    } else if (g64 && V.bits == 4) {
+      acc = vrow_dot_g64<4>(V, j, xb);
+    } else {
+      for (int k = lane; k < V.cols; k += 32) acc = fmaf(qmat_elem(V, j, k), bf2f(xb[k]), acc);
+      acc = warp_sum(acc);
+    }
   }
   if (lane == 0) a.t[(static_cast<int64_t>(slot) * 3 + proj) * a.maxr + j] = acc;
 }
@@ -217,6 +262,9 @@ struct lrc_layer {
   float* a32 = nullptr;
   uint16_t* a16 = nullptr;
   int max_pairs = 0;
+  double* logits = nullptr;  // router scratch [max_tokens][E]
+  int* tile_ticket = nullptr;
+  int lr_up_max = 0, lr_down_max = 0;  // largest per-tile low-rank slot (bytes)
   // host-buffer staging + phase timing
   uint16_t* x_stage = nullptr;
   float* y_stage = nullptr;
@@ -260,6 +308,26 @@ static lrc_status validate_expert(const lrc_expert& e, int hidden, int ffn) {
   return LRC_OK;
 }
 
+// The tiled path needs T2 weight tiles for every expert and, for experts with
+// compensators, quantized factors re-laid out as LR tiles (raw fp32 factors ->
+// generic path).  Also records the largest LR slot the kernels must stage.
+static void refresh_tiled(lrc_layer* L) {
+  bool ok = true;
+  L->lr_up_max = L->lr_down_max = 0;
+  for (auto& e : L->host_experts) {
+    ok = ok && e.up_tiles != nullptr && e.down_tiles != nullptr;
+    if (!has_comp(e)) continue;
+    const lrc_qmat* fs[6] = {&e.u1, &e.v1, &e.u3, &e.v3, &e.u2, &e.v2};
+    for (auto f : fs) ok = ok && f->dense == nullptr;
+    const LrLayout lay = lr_layout(e);
+    ok = ok && (lay.up_total == 0 || e.up_lr_tiles != nullptr);
+    ok = ok && (lay.down_total == 0 || e.down_lr_tiles != nullptr);
+    L->lr_up_max = std::max(L->lr_up_max, lay.up_total);
+    L->lr_down_max = std::max(L->lr_down_max, lay.down_total);
+  }
+  L->tiled = ok;
+}
+
 static lrc_status alloc_workspace(lrc_layer* L) {
   const int NE = L->E + L->S;
   const int NP = L->max_tokens * (L->k_max + L->S);
@@ -281,6 +349,8 @@ static lrc_status alloc_workspace(lrc_layer* L) {
   size_t o_a16 = take(size_t(NP) * L->ffn * 2 + 64);
   size_t o_xs = take(size_t(L->max_tokens) * L->hidden * 2);
   size_t o_ys = take(size_t(L->max_tokens) * L->hidden * 4);
+  size_t o_lg = take(size_t(L->max_tokens) * L->E * 8);
+  size_t o_tt = take(size_t(route_tiles(L->max_tokens)) * 4 + 16);
   LRC_CUDA_TRY(cudaMalloc(&L->ws, off));
   LRC_CUDA_TRY(cudaMemset(L->ws, 0, off));
   L->ws_bytes = off;
@@ -307,6 +377,8 @@ static lrc_status alloc_workspace(lrc_layer* L) {
   L->a16 = reinterpret_cast<uint16_t*>(base + o_a16);
   L->x_stage = reinterpret_cast<uint16_t*>(base + o_xs);
   L->y_stage = reinterpret_cast<float*>(base + o_ys);
+  L->logits = reinterpret_cast<double*>(base + o_lg);
+  L->tile_ticket = reinterpret_cast<int*>(base + o_tt);
   for (auto& e : L->ev) LRC_CUDA_TRY(cudaEventCreate(&e));
   std::vector<uint8_t> hc(NE);
   for (int e = 0; e < NE; ++e) hc[e] = has_comp(L->host_experts[e]) ? 1 : 0;
@@ -332,7 +404,6 @@ extern "C" lrc_status lrc_layer_create(const double* gate_t, int hidden, int ffn
   L->k_max = std::max(top_k, 1);
   L->gate_t = gate_t;
   L->host_experts.assign(experts, experts + num_experts + num_shared);
-  bool tiled = true;
   for (auto& e : L->host_experts) {
     lrc_status s = validate_expert(e, hidden, ffn);
     if (s != LRC_OK) {
@@ -340,9 +411,8 @@ extern "C" lrc_status lrc_layer_create(const double* gate_t, int hidden, int ffn
       return s;
     }
     L->maxr = std::max({L->maxr, rank_of(e.u1), rank_of(e.u2), rank_of(e.u3)});
-    tiled = tiled && e.up_tiles != nullptr && e.down_tiles != nullptr;
   }
-  L->tiled = tiled;
+  refresh_tiled(L);
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -380,9 +450,7 @@ extern "C" lrc_status lrc_layer_set_expert(lrc_layer* L, int expert_id, const lr
     return fail(LRC_ERR_UNSUPPORTED, "set_expert: rank above the layer's workspace rank");
   L->host_experts[expert_id] = *e;
   LRC_CUDA_TRY(cudaMemcpy(L->d_experts + expert_id, e, sizeof(lrc_expert), cudaMemcpyHostToDevice));
-  bool tiled = true;
-  for (auto& x : L->host_experts) tiled = tiled && x.up_tiles && x.down_tiles;
-  L->tiled = tiled;
+  refresh_tiled(L);
   return LRC_OK;
 }
 
@@ -411,8 +479,22 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   plan.compensate_shared = compensate_shared;
   int32_t* ti = topk_idx ? topk_idx : L->topk_idx;
   float* tw = topk_w ? topk_w : L->topk_w;
-  lrc_status s = launch_route(L->gate_t, x, LRC_DTYPE_BF16, B, L->hidden, L->E, top_k,
-                              renormalize, nullptr, ti, tw, plan, st);
+  RouteArgs ra{};
+  ra.gate_t = L->gate_t;
+  ra.x = x;
+  ra.x_dtype = LRC_DTYPE_BF16;
+  ra.B = B;
+  ra.d = L->hidden;
+  ra.E = L->E;
+  ra.k = top_k;
+  ra.renorm = renormalize;
+  ra.probs = nullptr;
+  ra.topk_idx = ti;
+  ra.topk_w = tw;
+  ra.logits = L->logits;
+  ra.tile_ticket = L->tile_ticket;
+  ra.plan = plan;
+  lrc_status s = launch_route(ra, st);
   if (s != LRC_OK) return s;
   ++launches;
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[1], st));
@@ -437,9 +519,9 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[2], st));
   if (allow_tiled && L->tiled) {
     const int tok_bound = static_cast<int>(std::min<int64_t>(B, L->max_tokens));
-    if ((s = launch_up_tiled(a, L->num_sms, tok_bound, st)) != LRC_OK) return s;
+    if ((s = launch_up_tiled(a, L->num_sms, tok_bound, L->lr_up_max, st)) != LRC_OK) return s;
     if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));
-    if ((s = launch_down_tiled(a, L->num_sms, tok_bound, st)) != LRC_OK) return s;
+    if ((s = launch_down_tiled(a, L->num_sms, tok_bound, L->lr_down_max, st)) != LRC_OK) return s;
     launches += 2;
   } else {
     const int grid = L->num_sms * 4;

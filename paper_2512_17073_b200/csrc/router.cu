@@ -2,12 +2,20 @@
 // per-expert pair plan consumed by the expert kernels.
 // Reference: ref/moe.py:165-193 (route/softmax), ref/moe.py:234-258 (mixing,
 // shared experts).
+//
+// Grid (token tiles, experts): CTA (tile, e) computes the logits of up to
+// kTT tokens against gate row e with wide coalesced fp64 loads.  The last CTA
+// of a token tile (atomic ticket) runs softmax + stable top-k for the tile;
+// the last tile builds the pair plan -- one launch, no host round trip.
 #include <float.h>
 
 #include "common.cuh"
 #include "layer.cuh"
 
 namespace lrc {
+
+constexpr int kTT = 8;         // tokens per router CTA
+constexpr int kRThreads = 256;
 
 template <typename T>
 __device__ __forceinline__ double load_x(const T* x, int64_t i);
@@ -43,85 +51,98 @@ __device__ double pw_sum_small(const double* v, int n) {
   return __dadd_rn(pw_sum_small(v, n2), pw_sum_small(v + n2, n - n2));
 }
 
-// Route one token per CTA.  Writes probs (optional), topk idx / mixing weight.
-// When `plan` is non-null the last CTA to finish (atomic ticket) builds the
-// pair plan for the whole batch (no extra launch).
-template <typename T>
-__global__ void __launch_bounds__(256) route_kernel(const double* __restrict__ gate_t,
-                                                    const T* __restrict__ x, int64_t B, int d,
-                                                    int E, int k, int renorm,
-                                                    double* __restrict__ probs,
-                                                    int32_t* __restrict__ topk_idx,
-                                                    float* __restrict__ topk_w, PlanArgs plan) {
-  extern __shared__ double sm[];
-  double* xs = sm;           // d
-  double* logit = sm + d;    // E
-  const int64_t b = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) xs[i] = load_x<T>(x, b * d + i);
-  __syncthreads();
-  for (int e = warp; e < E; e += nw) {
-    const double* gr = gate_t + static_cast<int64_t>(e) * d;
-    double acc = 0.0;
-    for (int i = lane; i < d; i += 32) acc = fma(gr[i], xs[i], acc);
-    acc = warp_sum_d(acc);
-    if (lane == 0) logit[e] = acc;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // softmax exactly as ref/moe.py:165-168: z = l - max; e = exp(z); e / sum(e)
-    double mx = logit[0];
-    for (int e = 1; e < E; ++e) mx = fmax(mx, logit[e]);
-    for (int e = 0; e < E; ++e) logit[e] = exp(__dsub_rn(logit[e], mx));
-    double den = pw_sum_small(logit, E);
-    for (int e = 0; e < E; ++e) logit[e] = __ddiv_rn(logit[e], den);
-    if (probs)
-      for (int e = 0; e < E; ++e) probs[b * E + e] = logit[e];
-    // stable descending selection: strict '>' keeps the lower index on ties
-    // (np.argsort(-w, kind="stable"), ref/moe.py:190)
-    unsigned long long taken[4] = {0, 0, 0, 0};
-    double mix[64];
-    int sel[64];
-    double msum = 0.0;
-    for (int j = 0; j < k; ++j) {
-      int best = -1;
-      double bv = -DBL_MAX;
-      for (int e = 0; e < E; ++e) {
-        if ((taken[e >> 6] >> (e & 63)) & 1ull) continue;
-        if (best < 0 || logit[e] > bv) {
-          best = e;
-          bv = logit[e];
-        }
+// softmax (ref/moe.py:165-168) + stable descending top-k (np.argsort(-w,
+// kind="stable"), ref/moe.py:190: strict '>' keeps the lower index on ties).
+__device__ void select_topk(double* lg, int E, int k, int renorm, int64_t b, double* probs,
+                            int32_t* topk_idx, float* topk_w) {
+  double mx = lg[0];
+  for (int e = 1; e < E; ++e) mx = fmax(mx, lg[e]);
+  for (int e = 0; e < E; ++e) lg[e] = exp(__dsub_rn(lg[e], mx));
+  const double den = pw_sum_small(lg, E);
+  for (int e = 0; e < E; ++e) lg[e] = __ddiv_rn(lg[e], den);
+  if (probs)
+    for (int e = 0; e < E; ++e) probs[b * E + e] = lg[e];
+  unsigned long long taken[4] = {0, 0, 0, 0};
+  double mix[64];
+  for (int j = 0; j < k; ++j) {
+    int best = -1;
+    double bv = -DBL_MAX;
+    for (int e = 0; e < E; ++e) {
+      if ((taken[e >> 6] >> (e & 63)) & 1ull) continue;
+      if (best < 0 || lg[e] > bv) {
+        best = e;
+        bv = lg[e];
       }
-      taken[best >> 6] |= 1ull << (best & 63);
-      sel[j] = best;
-      mix[j] = bv;
     }
-    if (renorm) {
-      // mix.sum() in numpy order (pairwise over k values)
-      msum = pw_sum_small(mix, k);
-      if (msum > 0.0)
-        for (int j = 0; j < k; ++j) mix[j] = __ddiv_rn(mix[j], msum);
-    }
-    for (int j = 0; j < k; ++j) {
-      topk_idx[b * k + j] = sel[j];
-      topk_w[b * k + j] = static_cast<float>(mix[j]);
-    }
+    taken[best >> 6] |= 1ull << (best & 63);
+    topk_idx[b * k + j] = best;
+    mix[j] = bv;
   }
-  if (plan.ticket == nullptr) return;
-  // ---- last CTA builds the plan ----
-  __shared__ int is_last;
+  if (renorm) {  // ref/moe.py:234-236, mix.sum() in numpy order
+    const double s = pw_sum_small(mix, k);
+    if (s > 0.0)
+      for (int j = 0; j < k; ++j) mix[j] = __ddiv_rn(mix[j], s);
+  }
+  for (int j = 0; j < k; ++j) topk_w[b * k + j] = static_cast<float>(mix[j]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRThreads) gate_kernel(RouteArgs ra) {
+  extern __shared__ double sm_lg[];  // [kTT][E] (last CTA only)
+  __shared__ double s_red[kTT][kRThreads / 32];
+  __shared__ int s_last;
+  const int tile = blockIdx.x, e = blockIdx.y;
+  const int64_t b0 = static_cast<int64_t>(tile) * kTT;
+  const int64_t rem = ra.B - b0;
+  const int nb = rem < kTT ? static_cast<int>(rem) : kTT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const T* x = static_cast<const T*>(ra.x);
+  const double* g = ra.gate_t + static_cast<int64_t>(e) * ra.d;
+  double acc[kTT];
+#pragma unroll
+  for (int t = 0; t < kTT; ++t) acc[t] = 0.0;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < ra.d; i += kRThreads) {
+    const double gv = __ldg(g + i);
+#pragma unroll
+    for (int t = 0; t < kTT; ++t)
+      if (t < nb) acc[t] = fma(gv, load_x<T>(x, (b0 + t) * ra.d + i), acc[t]);
+  }
+#pragma unroll
+  for (int t = 0; t < kTT; ++t) {
+    const double v = warp_sum_d(acc[t]);
+    if (lane == 0) s_red[t][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < nb) {
+    double s = 0.0;
+    for (int w = 0; w < kRThreads / 32; ++w) s += s_red[threadIdx.x][w];
+    ra.logits[(b0 + threadIdx.x) * ra.E + e] = s;
+  }
+  // ---- last CTA of this token tile: softmax + top-k
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = atomicAdd(plan.ticket, 1);
-    is_last = (t == static_cast<int>(B) - 1);
-  }
+  if (threadIdx.x == 0) s_last = (atomicAdd(&ra.tile_ticket[tile], 1) == ra.E - 1);
   __syncthreads();
-  if (!is_last) return;
+  if (!s_last) return;
   __threadfence();
-  build_plan_block(plan, topk_idx, topk_w, static_cast<int>(B), k);
-  if (threadIdx.x == 0) *plan.ticket = 0;
+  for (int i = threadIdx.x; i < nb * ra.E; i += kRThreads)
+    sm_lg[i] = __ldcg(ra.logits + b0 * ra.E + i);
+  __syncthreads();
+  if (threadIdx.x < nb)
+    select_topk(sm_lg + threadIdx.x * ra.E, ra.E, ra.k, ra.renorm, b0 + threadIdx.x, ra.probs,
+                ra.topk_idx, ra.topk_w);
+  if (threadIdx.x == 0) ra.tile_ticket[tile] = 0;
+  if (ra.plan.ticket == nullptr) return;
+  // ---- last tile: build the pair plan for the whole batch
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(ra.plan.ticket, 1) == static_cast<int>(gridDim.x) - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  build_plan_block(ra.plan, ra.topk_idx, ra.topk_w, static_cast<int>(ra.B), ra.k);
+  if (threadIdx.x == 0) *ra.plan.ticket = 0;
 }
 
 // Pair plan: pair p = b*P + j, P = k + S.  j < k: routed expert topk_idx[b][j],
@@ -135,31 +156,23 @@ __device__ void build_plan_block(const PlanArgs& pa, const int32_t* topk_idx, co
   const int NE = pa.num_experts + pa.num_shared;
   __shared__ int s_cnt[LRC_MAX_EXPERTS];
   __shared__ int s_off[LRC_MAX_EXPERTS + 1];
-  __shared__ int s_warp[32];
-  __shared__ int s_ncomp;
   for (int e = threadIdx.x; e < NE; e += blockDim.x) s_cnt[e] = 0;
-  if (threadIdx.x == 0) s_ncomp = 0;
   __syncthreads();
-  // per-pair attributes
   for (int p = threadIdx.x; p < NP; p += blockDim.x) {
-    int b = p / P, j = p - b * P;
+    const int b = p / P, j = p - b * P;
     int e;
     float w;
-    int comp;
     if (j < k) {
-      e = topk_idx[b * k + j];
-      w = topk_w[b * k + j];
-      comp = (j < pa.top_n) && pa.has_comp[e];
+      e = __ldcg(topk_idx + b * k + j);
+      w = __ldcg(topk_w + b * k + j);
     } else {
       e = pa.num_experts + (j - k);
       w = 1.0f;
-      comp = pa.compensate_shared && pa.has_comp[e];
     }
     pa.pair_expert[p] = e;
     pa.pair_w[p] = w;
     pa.pair_token[p] = b;
     atomicAdd(&s_cnt[e], 1);
-    (void)comp;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -178,45 +191,37 @@ __device__ void build_plan_block(const PlanArgs& pa, const int32_t* topk_idx, co
     pa.counts[0] = na;
   }
   __syncthreads();
-  // stable scatter: walk pairs in order, one warp-synchronous pass per chunk
-  // of 32 pairs; each expert's cursor advances by the ballot prefix.
   const int lane = threadIdx.x & 31;
   if (threadIdx.x < 32) {
+    // stable scatter: one warp walks the pairs in order; experts present in a
+    // 32-pair chunk are serialised and each advances by its ballot prefix
+    int count = 0;
     for (int base = 0; base < NP; base += 32) {
-      int p = base + lane;
-      int e = (p < NP) ? pa.pair_expert[p] : -1;
+      const int p = base + lane;
+      const bool valid = p < NP;
+      const int e = valid ? pa.pair_expert[p] : -1;
       int pos = -1;
-      // serialise experts present in this chunk
-      unsigned pending = __ballot_sync(0xffffffffu, p < NP);
+      unsigned pending = __ballot_sync(0xffffffffu, valid);
       while (pending) {
-        int leader = __ffs(pending) - 1;
-        int le = __shfl_sync(0xffffffffu, e, leader);
-        unsigned same = __ballot_sync(0xffffffffu, e == le && p < NP);
-        if (e == le && p < NP) pos = s_off[le] + __popc(same & ((1u << lane) - 1u));
+        const int leader = __ffs(pending) - 1;
+        const int le = __shfl_sync(0xffffffffu, e, leader);
+        const unsigned same = __ballot_sync(0xffffffffu, valid && e == le);
+        if (valid && e == le) pos = s_off[le] + __popc(same & ((1u << lane) - 1u));
         __syncwarp();
         if (lane == leader) s_off[le] += __popc(same);
         __syncwarp();
         pending &= ~same;
       }
-      if (p < NP) pa.pair_list[pos] = p;
-    }
-  }
-  __syncthreads();
-  // compensated-pair slots (for the t = V.x buffers), in pair order
-  if (threadIdx.x < 32) {
-    int count = 0;
-    for (int base = 0; base < NP; base += 32) {
-      int p = base + lane;
+      if (valid) pa.pair_list[pos] = p;
+      // compensated-pair slots (for the t = V.x buffers), in pair order
       int comp = 0;
-      if (p < NP) {
-        int b = p / P, j = p - b * P;
-        int e = pa.pair_expert[p];
-        comp = (j < k) ? ((j < pa.top_n) && pa.has_comp[e])
-                       : (pa.compensate_shared && pa.has_comp[e]);
+      if (valid) {
+        const int j = p % P;
+        comp = (j < k) ? ((j < pa.top_n) && pa.has_comp[e]) : (pa.compensate_shared && pa.has_comp[e]);
       }
-      unsigned m = __ballot_sync(0xffffffffu, comp);
-      if (p < NP) {
-        int slot = comp ? count + __popc(m & ((1u << lane) - 1u)) : -1;
+      const unsigned m = __ballot_sync(0xffffffffu, comp);
+      if (valid) {
+        const int slot = comp ? count + __popc(m & ((1u << lane) - 1u)) : -1;
         pa.pair_comp[p] = slot;
         if (comp) pa.comp_list[slot] = p;
       }
@@ -224,34 +229,22 @@ __device__ void build_plan_block(const PlanArgs& pa, const int32_t* topk_idx, co
     }
     if (lane == 0) pa.counts[1] = count;
   }
-  (void)s_warp;
-  (void)s_ncomp;
 }
 
-static int route_smem(int d, int E) { return (d + E) * static_cast<int>(sizeof(double)); }
+int route_tiles(int64_t B) { return static_cast<int>((B + kTT - 1) / kTT); }
 
-lrc_status launch_route(const double* gate_t, const void* x, int x_dtype, int64_t B, int d, int E,
-                        int k, int renorm, double* probs, int32_t* topk_idx, float* topk_w,
-                        const PlanArgs& plan, cudaStream_t st) {
-  int smem = route_smem(d, E);
-  if (smem > 48 * 1024) {
-    static const void* fns[3] = {(const void*)route_kernel<double>, (const void*)route_kernel<float>,
-                                 (const void*)route_kernel<uint16_t>};
-    for (auto f : fns) LRC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  }
-  dim3 grid(static_cast<unsigned>(B));
-  switch (x_dtype) {
+lrc_status launch_route(const RouteArgs& ra, cudaStream_t st) {
+  const int smem = kTT * ra.E * static_cast<int>(sizeof(double));
+  dim3 grid(route_tiles(ra.B), ra.E);
+  switch (ra.x_dtype) {
     case LRC_DTYPE_F64:
-      route_kernel<double><<<grid, 256, smem, st>>>(gate_t, (const double*)x, B, d, E, k, renorm,
-                                                    probs, topk_idx, topk_w, plan);
+      gate_kernel<double><<<grid, kRThreads, smem, st>>>(ra);
       break;
     case LRC_DTYPE_F32:
-      route_kernel<float><<<grid, 256, smem, st>>>(gate_t, (const float*)x, B, d, E, k, renorm,
-                                                   probs, topk_idx, topk_w, plan);
+      gate_kernel<float><<<grid, kRThreads, smem, st>>>(ra);
       break;
     case LRC_DTYPE_BF16:
-      route_kernel<uint16_t><<<grid, 256, smem, st>>>(gate_t, (const uint16_t*)x, B, d, E, k,
-                                                      renorm, probs, topk_idx, topk_w, plan);
+      gate_kernel<uint16_t><<<grid, kRThreads, smem, st>>>(ra);
       break;
     default:
       return fail(LRC_ERR_INVALID, "route: unknown x dtype");
@@ -272,7 +265,28 @@ extern "C" lrc_status lrc_route(const double* gate_t, const void* x, int x_dtype
   if (top_k > E) return fail(LRC_ERR_INVALID, "top_k exceeds the number of experts");
   if (top_k > 64 || E > LRC_MAX_EXPERTS) return fail(LRC_ERR_UNSUPPORTED, "route: top_k <= 64, E <= 256");
   if (B == 0) return LRC_OK;
-  PlanArgs none{};
-  return launch_route(gate_t, x, x_dtype, B, d, E, top_k, renormalize, probs, topk_idx, topk_w,
-                      none, as_stream(stream));
+  cudaStream_t st = as_stream(stream);
+  // standalone call: scratch from the stream-ordered allocator
+  RouteArgs ra{};
+  ra.gate_t = gate_t;
+  ra.x = x;
+  ra.x_dtype = x_dtype;
+  ra.B = B;
+  ra.d = d;
+  ra.E = E;
+  ra.k = top_k;
+  ra.renorm = renormalize;
+  ra.probs = probs;
+  ra.topk_idx = topk_idx;
+  ra.topk_w = topk_w;
+  const int nt = route_tiles(B);
+  void* scratch = nullptr;
+  const size_t bytes = sizeof(double) * B * E + sizeof(int) * (nt + 1);
+  LRC_CUDA_TRY(cudaMallocAsync(&scratch, bytes, st));
+  LRC_CUDA_TRY(cudaMemsetAsync(scratch, 0, bytes, st));
+  ra.logits = static_cast<double*>(scratch);
+  ra.tile_ticket = reinterpret_cast<int*>(ra.logits + B * E);
+  lrc_status s = launch_route(ra, st);
+  cudaFreeAsync(scratch, st);
+  return s;
 }

@@ -95,6 +95,23 @@ def build_tiles(mats, keep: _Keep):
     return t
 
 
+def build_lr_tiles(ex: _lib.LrcExpert, hidden: int, ffn: int, keep: _Keep) -> bool:
+    """Low-rank factor tiles riding with the weight tiles (csrc/fast.cu); False if the
+    factors cannot be tiled (raw fp32 factors -> generic kernels)."""
+    torch = _lib.device_required()
+    lib = _lib.lib()
+    up, down = ctypes.c_int64(), ctypes.c_int64()
+    if lib.lrc_lr_tiles_bytes(ctypes.byref(ex), hidden, ffn, ctypes.byref(up), ctypes.byref(down)) != 0:
+        return False
+    tu = keep.add(torch.empty((max(up.value, 16),), dtype=torch.uint8, device="cuda"))
+    td = keep.add(torch.empty((max(down.value, 16),), dtype=torch.uint8, device="cuda"))
+    _lib.check(lib.lrc_build_lr_tiles(ctypes.byref(ex), hidden, ffn, _lib.ptr(tu), _lib.ptr(td),
+                                      _lib.stream_ptr()))
+    ex.up_lr_tiles = tu.data_ptr() if up.value else None
+    ex.down_lr_tiles = td.data_ptr() if down.value else None
+    return True
+
+
 def tiles_eligible(*mats: _lib.LrcQmat) -> bool:
     return all(m.bits == 2 and m.group_size == 64 and m.packed for m in mats)
 
@@ -223,6 +240,8 @@ class LRCMoELayer:
             if tiles and tiles_eligible(ex.w1, ex.w3, ex.w2):
                 ex.up_tiles = build_tiles([ex.w1, ex.w3], keep).data_ptr()
                 ex.down_tiles = build_tiles([ex.w2], keep).data_ptr()
+                if ex.rank:
+                    build_lr_tiles(ex, hidden, ffn, keep)
             experts.append(ex)
         return cls(gate, experts, hidden, ffn, num_experts, num_shared, keep, max_tokens, top_k,
                    frozenset(missing))

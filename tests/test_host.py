@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
     assert lib.lrc_abi_version() == 1
     # struct layout agrees with the header (ctypes mirrors the C ABI)
     assert ctypes.sizeof(_lib.LrcQmat) == 48
-    assert ctypes.sizeof(_lib.LrcExpert) == 3 * 48 + 8 + 6 * 48 + 16
+    assert ctypes.sizeof(_lib.LrcExpert) == 3 * 48 + 8 + 6 * 48 + 32
 
 
 def test_library_is_sm100a():
