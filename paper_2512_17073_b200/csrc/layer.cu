@@ -10,43 +10,7 @@
 namespace lrc {
 
 // ------------------------------------------------------------ LR kernels ---
-// Row j of a quantized V (group size 64, BITS-bit LSB-first stream) dotted with
-// a bf16 vector: each lane takes whole 64-code groups, loads the group's
-// 2*BITS words at once and decodes them with funnel shifts.
-template <int BITS>
-__device__ float vrow_dot_g64(const lrc_qmat& V, int j, const uint16_t* __restrict__ xb) {
-  constexpr int W = 2 * BITS;  // 32-bit words per 64-code group
-  const int lane = threadIdx.x & 31;
-  const int gpr = (V.cols + 63) / 64;
-  const uint32_t* words = reinterpret_cast<const uint32_t*>(V.packed);
-  const int64_t nwords = ((static_cast<int64_t>(V.rows) * V.cols * BITS + 7) >> 3) >> 2;
-  float acc = 0.0f;
-  for (int g = lane; g < gpr; g += 32) {
-    const int64_t w0 = ((static_cast<int64_t>(j) * V.cols + g * 64) * BITS) >> 5;
-    uint32_t w[W + 1];
-#pragma unroll
-    for (int i = 0; i <= W; ++i) w[i] = (w0 + i < nwords) ? __ldg(words + w0 + i) : 0u;
-    const int nv = min(64, V.cols - g * 64);
-    const float s = h2f(V.scales[static_cast<int64_t>(j) * gpr + g]);
-    const float z = h2f(V.zeros[static_cast<int64_t>(j) * gpr + g]);
-    const uint16_t* xg = xb + g * 64;
-    float cx = 0.0f, sx = 0.0f;
-#pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      if (i < nv) {
-        const int bit = i * BITS;
-        const uint32_t c = __funnelshift_r(w[bit >> 5], w[(bit >> 5) + 1], bit & 31) & ((1u << BITS) - 1u);
-        const float xv = bf2f(xg[i]);
-        cx = fmaf(static_cast<float>(c), xv, cx);
-        sx += xv;
-      }
-    }
-    acc = fmaf(s, cx, fmaf(z, sx, acc));
-  }
-  return warp_sum(acc);
-}
-
-// t[slot][proj][j] = V_proj(e)[j, :] . x_b  for compensated pairs, proj in {w1, w3}
+// t[b][e][proj][j] = V_proj(e)[j, :] . x_b  for compensated pairs, proj in {w1, w3}
 __global__ void __launch_bounds__(256) lr_down_kernel(ExpertArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int task = blockIdx.x * 8 + warp;
@@ -62,18 +26,30 @@ __global__ void __launch_bounds__(256) lr_down_kernel(ExpertArgs a) {
   if (qmat_present(V) && j < V.rows) {
     const uint16_t* xb = a.x + static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden;
     const bool g64 = V.dense == nullptr && V.group_size == 64 && ((V.cols * V.bits) % 32) == 0;
+    float av[1];
     if (g64 && V.bits == 3) {
-      acc = vrow_dot_g64<3>(V, j, xb);
+      vrow_dot_tokens<3, 1>(V, j, xb, a.hidden, 1, av);
+      acc = av[0];
     } else if (g64 && V.bits == 2) {
-      acc = vrow_dot_g64<2>(V, j, xb);
+      vrow_dot_tokens<2, 1>(V, j, xb, a.hidden, 1, av);
+      acc = av[0];
     } else if (g64 && V.bits == 4) {
-      acc = vrow_dot_g64<4>(V, j, xb);
+      vrow_dot_tokens<4, 1>(V, j, xb, a.hidden, 1, av);
+      acc = av[0];
     } else {
       for (int k = lane; k < V.cols; k += 32) acc = fmaf(qmat_elem(V, j, k), bf2f(xb[k]), acc);
       acc = warp_sum(acc);
     }
   }
-  if (lane == 0) a.t[(static_cast<int64_t>(slot) * 3 + proj) * a.maxr + j] = acc;
+  if (lane == 0)
+    a.t[((static_cast<int64_t>(a.plan.pair_token[p]) * a.ne + a.plan.pair_expert[p]) * 3 + proj) *
+            a.maxr + j] = acc;
+}
+
+// index of t[b][e][proj][0] for pair p
+__device__ __forceinline__ int64_t t_base(const ExpertArgs& a, int p, int proj) {
+  return ((static_cast<int64_t>(a.plan.pair_token[p]) * a.ne + a.plan.pair_expert[p]) * 3 + proj) *
+         a.maxr;
 }
 
 // U(row, :) . t  (warp-cooperative; all lanes return the sum)
@@ -125,7 +101,7 @@ __global__ void __launch_bounds__(256) up_generic_kernel(ExpertArgs a) {
           const int p = a.plan.pair_list[off + c0 + i];
           const int slot = a.plan.pair_comp[p];
           if (slot >= 0) {
-            const float* tp = a.t + static_cast<int64_t>(slot) * 3 * a.maxr;
+            const float* tp = a.t + t_base(a, p, 0);
             if (qmat_present(E.u1)) h1 += lr_up_dot(E.u1, f, tp);
             if (qmat_present(E.u3)) h3 += lr_up_dot(E.u3, f, tp + a.maxr);
           }
@@ -151,7 +127,7 @@ __global__ void __launch_bounds__(256) lr_mid_kernel(ExpertArgs a) {
     for (int k = lane; k < E.v2.cols; k += 32) acc = fmaf(qmat_elem(E.v2, j, k), ap[k], acc);
     acc = warp_sum(acc);
   }
-  if (lane == 0) a.t[(static_cast<int64_t>(slot) * 3 + 2) * a.maxr + j] = acc;
+  if (lane == 0) a.t[t_base(a, p, 2) + j] = acc;
 }
 
 __global__ void __launch_bounds__(256) down_generic_kernel(ExpertArgs a) {
@@ -188,7 +164,7 @@ __global__ void __launch_bounds__(256) down_generic_kernel(ExpertArgs a) {
           const int p = a.plan.pair_list[off + c0 + i];
           const int slot = a.plan.pair_comp[p];
           if (slot >= 0 && qmat_present(E.u2))
-            v += lr_up_dot(E.u2, r, a.t + (static_cast<int64_t>(slot) * 3 + 2) * a.maxr);
+            v += lr_up_dot(E.u2, r, a.t + t_base(a, p, 2));
           if (lane == 0)
             atomicAdd(&a.y[static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden + r],
                       a.plan.pair_w[p] * v);
@@ -265,6 +241,7 @@ struct lrc_layer {
   double* logits = nullptr;  // router scratch [max_tokens][E]
   int* tile_ticket = nullptr;
   int lr_up_max = 0, lr_down_max = 0;  // largest per-tile low-rank slot (bytes)
+  bool pdl = getenv("LRC_NO_PDL") == nullptr;  // programmatic dependent launch
   // host-buffer staging + phase timing
   uint16_t* x_stage = nullptr;
   float* y_stage = nullptr;
@@ -344,7 +321,7 @@ static lrc_status alloc_workspace(lrc_layer* L) {
   size_t o_act = take(NE * 4), o_aoff = take(NE * 4), o_acnt = take(NE * 4);
   size_t o_tki = take(size_t(L->max_tokens) * L->k_max * 4);
   size_t o_tkw = take(size_t(L->max_tokens) * L->k_max * 4);
-  size_t o_t = take(size_t(NP) * 3 * std::max(L->maxr, 1) * 4);
+  size_t o_t = take(size_t(L->max_tokens) * NE * 3 * std::max(L->maxr, 1) * 4);
   size_t o_a32 = take(size_t(NP) * L->ffn * 4);
   size_t o_a16 = take(size_t(NP) * L->ffn * 2 + 64);
   size_t o_xs = take(size_t(L->max_tokens) * L->hidden * 2);
@@ -469,7 +446,6 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   int launches = 0;
   const bool prof = L->profiling;
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[0], st));
-  LRC_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(float) * B * L->hidden, st));
   if (B == 0) {
     L->last_launches = 0;
     return LRC_OK;
@@ -494,6 +470,16 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   ra.logits = L->logits;
   ra.tile_ticket = L->tile_ticket;
   ra.plan = plan;
+  // one prologue launch: gate GEMV + softmax/top-k + plan, zeroing of y and the
+  // t2 accumulators, and (one token tile) the speculative low-rank V.x
+  const bool spec = L->maxr > 0 && B <= route_tiles(1) * 8 && route_tiles(B) == 1;
+  ra.experts = L->d_experts;
+  ra.t = L->t;
+  ra.ne = L->E + L->S;
+  ra.maxr = L->maxr;
+  ra.spec_blocks = spec ? 2 * ((L->maxr + 7) / 8) : 0;
+  ra.t2_zero = L->maxr ? L->t : nullptr;
+  ra.y_zero = y;
   lrc_status s = launch_route(ra, st);
   if (s != LRC_OK) return s;
   ++launches;
@@ -501,6 +487,7 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   const int P = top_k + L->S;
   const int np_bound = static_cast<int>(B) * P;
   ExpertArgs a{};
+  a.ne = L->E + L->S;
   a.experts = L->d_experts;
   a.plan = plan;
   a.hidden = L->hidden;
@@ -512,16 +499,21 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   a.a16 = L->a16;
   a.y = y;
   a.max_pairs = L->max_pairs;
-  if (allow_tiled && L->tiled && L->maxr)  // t2 is accumulated by the tiled up kernel
-    LRC_CUDA_TRY(cudaMemsetAsync(L->t, 0, sizeof(float) * np_bound * 3 * L->maxr, st));
-  if ((s = launch_lr_down(a, np_bound, st)) != LRC_OK) return s;
-  if (L->maxr) ++launches;
+  if (!spec && L->maxr) {  // exact V.x for the compensated pairs only
+    if ((s = launch_lr_down(a, np_bound, st)) != LRC_OK) return s;
+    ++launches;
+  }
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[2], st));
   if (allow_tiled && L->tiled) {
     const int tok_bound = static_cast<int>(std::min<int64_t>(B, L->max_tokens));
-    if ((s = launch_up_tiled(a, L->num_sms, tok_bound, L->lr_up_max, st)) != LRC_OK) return s;
+    // programmatic dependent launch: the next kernel's CTAs are scheduled as SMs
+    // free up and block in griddepcontrol.wait (no PDL while timing phases)
+    const bool pdl = !prof && L->pdl;
+    if ((s = launch_up_tiled(a, L->num_sms, tok_bound, L->lr_up_max, st, pdl)) != LRC_OK)
+      return s;
     if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));
-    if ((s = launch_down_tiled(a, L->num_sms, tok_bound, L->lr_down_max, st)) != LRC_OK) return s;
+    if ((s = launch_down_tiled(a, L->num_sms, tok_bound, L->lr_down_max, st, pdl)) != LRC_OK)
+      return s;
     launches += 2;
   } else {
     const int grid = L->num_sms * 4;

@@ -35,7 +35,81 @@ struct RouteArgs {
   double* logits;    // [B][E] scratch
   int* tile_ticket;  // [route_tiles(B)] zero-initialised, self-resetting
   PlanArgs plan;     // plan.ticket == nullptr -> routing only
+  // layer-forward extras (all null/0 for a standalone lrc_route)
+  const lrc_expert* experts;  // device table [ne]
+  float* t;                   // [B][ne][3][maxr] low-rank vectors
+  int ne, maxr;
+  int spec_blocks;            // V.x row blocks per expert computed speculatively (0 = none)
+  float* t2_zero;             // zero t[b][e][2][:] (tiled path accumulates into it)
+  float* y_zero;              // zero y rows
 };
+
+// Row j of a quantized V (group size 64, BITS-bit LSB-first stream) dotted
+// with nb bf16 token rows (stride ld): each lane takes whole 64-code groups,
+// loads the group's 2*BITS words at once and decodes them with funnel shifts;
+// x is read 8 columns (16 B) at a time.  acc[t] is warp-reduced on return.
+template <int BITS, int MAXT>
+__device__ void vrow_dot_tokens(const lrc_qmat& V, int j, const uint16_t* __restrict__ xt,
+                                int64_t ld, int nb, float (&acc)[MAXT]) {
+  constexpr int W = 2 * BITS;  // 32-bit words per 64-code group
+  const int lane = threadIdx.x & 31;
+  const int gpr = (V.cols + 63) / 64;
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(V.packed);
+  const int64_t nwords = ((static_cast<int64_t>(V.rows) * V.cols * BITS + 7) >> 3) >> 2;
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) acc[t] = 0.0f;
+  for (int g = lane; g < gpr; g += 32) {
+    const int64_t w0 = ((static_cast<int64_t>(j) * V.cols + g * 64) * BITS) >> 5;
+    uint32_t w[W + 1];
+#pragma unroll
+    for (int i = 0; i <= W; ++i) w[i] = (w0 + i < nwords) ? __ldg(words + w0 + i) : 0u;
+    const int nv = min(64, V.cols - g * 64);
+    const float s = h2f(V.scales[static_cast<int64_t>(j) * gpr + g]);
+    const float z = h2f(V.zeros[static_cast<int64_t>(j) * gpr + g]);
+    const bool vec = (nv == 64) && (ld % 8) == 0 && ((reinterpret_cast<uintptr_t>(xt) & 15) == 0);
+    float cx[MAXT], sx[MAXT];
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) cx[t] = sx[t] = 0.0f;
+#pragma unroll
+    for (int i8 = 0; i8 < 8; ++i8) {
+      float c[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int bit = (i8 * 8 + q) * BITS;
+        c[q] = static_cast<float>(__funnelshift_r(w[bit >> 5], w[(bit >> 5) + 1], bit & 31) &
+                                  ((1u << BITS) - 1u));
+      }
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) {
+        if (t < nb) {
+          const uint16_t* xr = xt + t * ld + g * 64 + i8 * 8;
+          float xv[8];
+          if (vec) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(xr));
+            const uint32_t u4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              xv[2 * q] = bf2f(u4[q] & 0xffff);
+              xv[2 * q + 1] = bf2f(u4[q] >> 16);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) xv[q] = (i8 * 8 + q < nv) ? bf2f(xr[q]) : 0.0f;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            cx[t] = fmaf(c[q], xv[q], cx[t]);
+            sx[t] += xv[q];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) acc[t] = fmaf(s, cx[t], fmaf(z, sx[t], acc[t]));
+  }
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) acc[t] = warp_sum(acc[t]);
+}
 
 __device__ void build_plan_block(const PlanArgs& pa, const int32_t* topk_idx,
                                  const float* topk_w, int B, int k);
@@ -53,6 +127,7 @@ struct ExpertArgs {
   uint16_t* a16;              // [NP][ffn] bf16 activations (tiled path)
   float* y;                   // [B][hidden] (accumulated)
   int max_pairs;
+  int ne;                     // experts incl. shared; t is [B][ne][3][maxr]
 };
 
 // Byte layout of the low-rank factor tiles that ride along with a weight tile
@@ -97,8 +172,8 @@ lrc_status launch_lr_down(const ExpertArgs& a, int np_bound, cudaStream_t st);
 // tiled kernels (fast.cu)
 int64_t tiles_bytes(int64_t rows, int64_t cols, int ni);
 lrc_status launch_up_tiled(const ExpertArgs& a, int num_sms, int max_tokens_per_expert,
-                           int lr_up_max, cudaStream_t st);
+                           int lr_up_max, cudaStream_t st, bool pdl);
 lrc_status launch_down_tiled(const ExpertArgs& a, int num_sms, int max_tokens_per_expert,
-                             int lr_down_max, cudaStream_t st);
+                             int lr_down_max, cudaStream_t st, bool pdl);
 
 }  // namespace lrc

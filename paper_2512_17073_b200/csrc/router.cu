@@ -86,43 +86,117 @@ __device__ void select_topk(double* lg, int E, int k, int renorm, int64_t b, dou
   for (int j = 0; j < k; ++j) topk_w[b * k + j] = static_cast<float>(mix[j]);
 }
 
+__device__ __forceinline__ void griddep_launch_dependents_r() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Speculative low-rank down-projection for a small batch (one token tile):
+// t[b][e][proj][j] = V_proj(e)[j, :] . x_b for rows j in block `blk` (8 rows,
+// one per warp; proj = blk / (r/8)), for every token of the tile, whether or
+// not e turns out to be one of b's top-n experts -- it removes a dependent
+// launch between the router and the expert kernels (ref/lowrank.py:165 with
+// the factored U.(V.x) order).  Costs < 1% extra bytes at decode sizes.
+__device__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* x, int64_t b0, int nb, int e,
+                             int blk) {
+  const lrc_expert& E = ra.experts[e];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rpb = 8;  // rows per block
+  const int nblk1 = (ra.maxr + rpb - 1) / rpb;
+  const int proj = blk / nblk1;
+  const int j = (blk - proj * nblk1) * rpb + warp;
+  const lrc_qmat& V = proj == 0 ? E.v1 : E.v3;
+  if (!factor_present(V) || j >= V.rows || V.dense != nullptr) {
+    // raw factors (test hook) are handled by the generic path; write zeros
+    if (lane < nb && j < ra.maxr) ra.t[(((b0 + lane) * ra.ne + e) * 3 + proj) * ra.maxr + j] = 0.0f;
+    return;
+  }
+  float acc[kTT];
+  const bool g64 = V.group_size == 64 && ((V.cols * V.bits) % 32) == 0;
+  if (g64 && V.bits == 3) {
+    vrow_dot_tokens<3, kTT>(V, j, x + b0 * ra.d, ra.d, nb, acc);
+  } else if (g64 && V.bits == 2) {
+    vrow_dot_tokens<2, kTT>(V, j, x + b0 * ra.d, ra.d, nb, acc);
+  } else if (g64 && V.bits == 4) {
+    vrow_dot_tokens<4, kTT>(V, j, x + b0 * ra.d, ra.d, nb, acc);
+  } else {
+    const int gs = V.group_size, gpr = (V.cols + gs - 1) / gs;
+    const int64_t nbytes = (static_cast<int64_t>(V.rows) * V.cols * V.bits + 7) >> 3;
+#pragma unroll
+    for (int t = 0; t < kTT; ++t) acc[t] = 0.0f;
+    for (int c = lane; c < V.cols; c += 32) {
+      const int64_t g = static_cast<int64_t>(j) * gpr + c / gs;
+      const float w = fmaf(static_cast<float>(read_code(V.packed, static_cast<int64_t>(j) * V.cols + c,
+                                                        V.bits, nbytes)),
+                           h2f(V.scales[g]), h2f(V.zeros[g]));
+#pragma unroll
+      for (int t = 0; t < kTT; ++t)
+        if (t < nb) acc[t] = fmaf(w, bf2f(x[(b0 + t) * ra.d + c]), acc[t]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kTT; ++t) {
+    const float v = warp_sum(acc[t]);
+    if (lane == 0 && t < nb) ra.t[(((b0 + t) * ra.ne + e) * 3 + proj) * ra.maxr + j] = v;
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kRThreads) gate_kernel(RouteArgs ra) {
   extern __shared__ double sm_lg[];  // [kTT][E] (last CTA only)
   __shared__ double s_red[kTT][kRThreads / 32];
   __shared__ int s_last;
-  const int tile = blockIdx.x, e = blockIdx.y;
+  // blockIdx.z == 0: gate logits of expert e (e < E) + zeroing of this tile's
+  // y rows / t2 block; blockIdx.z >= 1: speculative low-rank down-projection
+  // t = V.x for 8 rows of V1|V3 of expert e (small batches, see spec_lr_rows).
+  const int tile = blockIdx.x, e = blockIdx.y, z = blockIdx.z;
   const int64_t b0 = static_cast<int64_t>(tile) * kTT;
   const int64_t rem = ra.B - b0;
   const int nb = rem < kTT ? static_cast<int>(rem) : kTT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const T* x = static_cast<const T*>(ra.x);
-  const double* g = ra.gate_t + static_cast<int64_t>(e) * ra.d;
-  double acc[kTT];
+  griddep_launch_dependents_r();
+  if (z == 0) {
+    if (e < ra.E) {
+      const double* g = ra.gate_t + static_cast<int64_t>(e) * ra.d;
+      double acc[kTT];
 #pragma unroll
-  for (int t = 0; t < kTT; ++t) acc[t] = 0.0;
-#pragma unroll 4
-  for (int i = threadIdx.x; i < ra.d; i += kRThreads) {
-    const double gv = __ldg(g + i);
+      for (int t = 0; t < kTT; ++t) acc[t] = 0.0;
+      // all of this thread's gate loads are independent: unroll for memory-level parallelism
+#pragma unroll 8
+      for (int i = threadIdx.x; i < ra.d; i += kRThreads) {
+        const double gv = __ldg(g + i);
 #pragma unroll
-    for (int t = 0; t < kTT; ++t)
-      if (t < nb) acc[t] = fma(gv, load_x<T>(x, (b0 + t) * ra.d + i), acc[t]);
-  }
+        for (int t = 0; t < kTT; ++t)
+          if (t < nb) acc[t] = fma(gv, load_x<T>(x, (b0 + t) * ra.d + i), acc[t]);
+      }
 #pragma unroll
-  for (int t = 0; t < kTT; ++t) {
-    const double v = warp_sum_d(acc[t]);
-    if (lane == 0) s_red[t][warp] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x < nb) {
-    double s = 0.0;
-    for (int w = 0; w < kRThreads / 32; ++w) s += s_red[threadIdx.x][w];
-    ra.logits[(b0 + threadIdx.x) * ra.E + e] = s;
+      for (int t = 0; t < kTT; ++t) {
+        const double v = warp_sum_d(acc[t]);
+        if (lane == 0) s_red[t][warp] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x < nb) {
+        double s = 0.0;
+        for (int w = 0; w < kRThreads / 32; ++w) s += s_red[threadIdx.x][w];
+        ra.logits[(b0 + threadIdx.x) * ra.E + e] = s;
+      }
+    }
+    if (ra.t2_zero != nullptr && ra.maxr > 0)
+      for (int i = threadIdx.x; i < nb * ra.maxr; i += kRThreads) {
+        const int t = i / ra.maxr, j = i - t * ra.maxr;
+        ra.t2_zero[(((b0 + t) * ra.ne + e) * 3 + 2) * ra.maxr + j] = 0.0f;
+      }
+    if (ra.y_zero != nullptr && e == 0)
+      for (int64_t i = threadIdx.x; i < static_cast<int64_t>(nb) * ra.d; i += kRThreads)
+        ra.y_zero[b0 * ra.d + i] = 0.0f;
+  } else if constexpr (sizeof(T) == 2) {
+    spec_lr_rows(ra, reinterpret_cast<const uint16_t*>(x), b0, nb, e, z - 1);
   }
   // ---- last CTA of this token tile: softmax + top-k
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&ra.tile_ticket[tile], 1) == ra.E - 1);
+  if (threadIdx.x == 0)
+    s_last = (atomicAdd(&ra.tile_ticket[tile], 1) == static_cast<int>(gridDim.y * gridDim.z) - 1);
   __syncthreads();
   if (!s_last) return;
   __threadfence();
@@ -235,7 +309,7 @@ int route_tiles(int64_t B) { return static_cast<int>((B + kTT - 1) / kTT); }
 
 lrc_status launch_route(const RouteArgs& ra, cudaStream_t st) {
   const int smem = kTT * ra.E * static_cast<int>(sizeof(double));
-  dim3 grid(route_tiles(ra.B), ra.E);
+  dim3 grid(route_tiles(ra.B), ra.experts ? ra.ne : ra.E, 1 + ra.spec_blocks);
   switch (ra.x_dtype) {
     case LRC_DTYPE_F64:
       gate_kernel<double><<<grid, kRThreads, smem, st>>>(ra);

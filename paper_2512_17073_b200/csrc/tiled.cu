@@ -25,8 +25,8 @@ namespace lrc {
 
 constexpr int kBlk = 640;
 constexpr int kCodeBytes = 512;
-constexpr int kSpanGP = 4;        // group pairs per warp span (512 columns)
-constexpr int kNW = 8;            // consumer warps
+constexpr int kSpanGP = 2;        // group pairs per warp span (256 columns)
+constexpr int kNW = 16;           // consumer warps
 constexpr int kThreads = (kNW + 1) * 32;
 
 int64_t tiles_bytes(int64_t rows, int64_t cols, int ni) {
@@ -157,7 +157,7 @@ __device__ __forceinline__ uint2 lds64(const void* p) {
 }
 __device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
@@ -264,6 +264,11 @@ __device__ __forceinline__ float lr_deq(const uint8_t* codes, int idx, int bits,
 }
 
 // --------------------------------------------------------- tiled kernel ---
+// Work item = (active expert, token pass, K chunk, 16-row tile).  One CTA per
+// SM: warp kNW (producer) streams items with cp.async.bulk into a ring of
+// shared-memory stages; kNW consumer warps each own a 2-group-pair (256
+// column) span of the item, unpack the codes in registers and issue
+// mma.sync m16n8k16 with the activation operand x' from shared memory.
 struct TiledParams {
   ExpertArgs a;
   int M, K;             // rows / cols of the streamed matrix (per interleaved matrix)
@@ -303,6 +308,17 @@ __host__ __device__ inline SmemMap smem_map(const TiledParams& p) {
   return m;
 }
 
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ float2 h2f2(uint32_t w) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&w));
+}
+
 template <bool UP, int NT>
 __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   constexpr int NI = UP ? 2 : 1;
@@ -321,14 +337,20 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   uint64_t* empty = full + P.nstage;
   __shared__ int s_prefix[LRC_MAX_EXPERTS + 1];
   __shared__ int s_range[2];
-  __shared__ int s_comp_n[TPP], s_comp_slot[TPP], s_comp_of[TPP], s_ncomp;
+  __shared__ int s_comp_n[TPP], s_comp_tok[TPP], s_comp_of[TPP], s_ncomp;
   __shared__ int s_r[3], s_ub[3], s_ugs[3], s_vb;
   __shared__ LrLayout s_L;
 
   const ExpertArgs& A = P.a;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_active = A.plan.counts[0];
   const int maxr = A.maxr;
+  // The up kernel consumes the router's plan: wait for it.  The down kernel's
+  // plan is two launches old (complete before the up kernel passed its own
+  // wait), so its producer may start streaming W2 while the up kernel drains;
+  // its consumers wait before touching the up kernel's activations.
+  if (UP) griddep_wait();
+  griddep_launch_dependents();
+  const int n_active = A.plan.counts[0];
 
   if (threadIdx.x == 0) {
     int acc = 0;
@@ -409,8 +431,10 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
 
   // ============================ consumers ====================================
   const int gid = lane >> 2, tid = lane & 3;
+  const int ctid = threadIdx.x;  // consumer thread id, 0 .. kNW*32-1
+  if (!UP) griddep_wait();
   int cur_ai = -1, cur_pass = -1, cur_chunk = -1;
-  int pass_tok = 0;
+  int pass_tok = 0, cur_e = -1;
   for (int it = beg; it < end; ++it) {
     const int k = it - beg;
     const int s = k % P.nstage;
@@ -419,7 +443,6 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     int gp0, gp1;
     chunk_gp(chunk, gp0, gp1);
     const int off = A.plan.active_off[ai], cnt = A.plan.active_cnt[ai];
-    const lrc_expert& E = A.experts[A.plan.active[ai]];
     if (ai != cur_ai || pass != cur_pass || chunk != cur_chunk) {
       // ---- (re)build the activation operand x' and the LR vectors for this group
       consumer_sync();
@@ -427,17 +450,19 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       cur_ai = ai;
       cur_pass = pass;
       cur_chunk = chunk;
+      cur_e = A.plan.active[ai];
       pass_tok = min(TPP, cnt - pass * TPP);
-      if (threadIdx.x == 0 && new_pass) {
+      if (ctid == 0 && new_pass) {
+        const lrc_expert& E = A.experts[cur_e];
         int nc = 0;
         for (int n = 0; n < TPP; ++n) {
           s_comp_of[n] = -1;
           if (n < pass_tok) {
-            const int slot = A.plan.pair_comp[A.plan.pair_list[off + pass * TPP + n]];
-            if (slot >= 0) {
+            const int p = A.plan.pair_list[off + pass * TPP + n];
+            if (A.plan.pair_comp[p] >= 0) {
               s_comp_of[n] = nc;
               s_comp_n[nc] = n;
-              s_comp_slot[nc] = slot;
+              s_comp_tok[nc] = A.plan.pair_token[p];
               ++nc;
             }
           }
@@ -454,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       }
       const int k0 = gp0 * 128;
       const int ng = (gp1 - gp0) * 2;
-      for (int task = threadIdx.x; task < TPP * ng; task += kNW * 32) {
+      for (int task = ctid; task < TPP * ng; task += kNW * 32) {
         const int n = task / ng, g = task - n * ng;
         float xsum = 0.f, xpsum = 0.f;
         uint32_t* dst = reinterpret_cast<uint32_t*>(xs + n * P.xs_stride + g * 64);
@@ -463,26 +488,22 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
           const uint16_t* row = UP ? A.x + static_cast<int64_t>(A.plan.pair_token[p]) * A.hidden
                                    : A.a16 + static_cast<int64_t>(p) * A.ffn;
           const int kk = k0 + g * 64;
-          uint4 raw[8];
           const bool vec = (kk + 64 <= P.K) && ((reinterpret_cast<uintptr_t>(row + kk) & 15) == 0);
-          if (vec) {
-#pragma unroll
-            for (int c8 = 0; c8 < 8; ++c8) raw[c8] = __ldg(reinterpret_cast<const uint4*>(row + kk) + c8);
-          } else {
-#pragma unroll
-            for (int c8 = 0; c8 < 8; ++c8) {
+#pragma unroll 2
+          for (int c8 = 0; c8 < 8; ++c8) {
+            uint4 raw;
+            if (vec) {
+              raw = __ldg(reinterpret_cast<const uint4*>(row + kk) + c8);
+            } else {
               uint16_t h[8];
 #pragma unroll
               for (int j = 0; j < 8; ++j) h[j] = (kk + c8 * 8 + j < P.K) ? row[kk + c8 * 8 + j] : 0;
-              raw[c8] = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16),
-                                   h[4] | (uint32_t(h[5]) << 16), h[6] | (uint32_t(h[7]) << 16));
+              raw = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16),
+                               h[4] | (uint32_t(h[5]) << 16), h[6] | (uint32_t(h[7]) << 16));
             }
-          }
-#pragma unroll
-          for (int c8 = 0; c8 < 8; ++c8) {
             const float im = inv_mult(c8);  // slot j = c8 for columns c8*8 .. c8*8+7
-            const uint32_t w4[4] = {raw[c8].x, raw[c8].y, raw[c8].z, raw[c8].w};
-            // column c8*8 + 2*tj + e  ->  16-block (c8/2), position tj*4 + p*2 + e with p = c8&1
+            const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+            // column c8*8 + 2*tj + e -> 16-block c8/2, position tj*4 + (c8&1)*2 + e
 #pragma unroll
             for (int tj = 0; tj < 4; ++tj) {
               const float lo = bf2f(w4[tj] & 0xffff), hi = bf2f(w4[tj] >> 16);
@@ -503,11 +524,11 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       // low-rank input vectors of the compensated tokens (t1/t3 up, t2 down)
       if (maxr > 0) {
         const int ntask = s_ncomp * NI * maxr;
-        for (int task = threadIdx.x; task < ntask; task += kNW * 32) {
+        for (int task = ctid; task < ntask; task += kNW * 32) {
           const int j = task % maxr, ci = task / maxr;
           const int i = ci % NI, c = ci / NI;
           const int proj = UP ? i : 2;
-          ts[task] = __ldcg(A.t + (static_cast<int64_t>(s_comp_slot[c]) * 3 + proj) * maxr + j);
+          ts[task] = __ldcg(A.t + ((static_cast<int64_t>(s_comp_tok[c]) * A.ne + cur_e) * 3 + proj) * maxr + j);
         }
       }
       consumer_sync();
@@ -528,69 +549,70 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
 
     const int ngp = gp1 - gp0;
     const int nspan = (ngp + kSpanGP - 1) / kSpanGP;
+    const uint16_t* xlane = xs + gid * P.xs_stride + tid * 4;
     for (int sp = warp; sp < nspan; sp += kNW) {
       const int q0 = sp * kSpanGP, q1 = min(ngp, q0 + kSpanGP);
+#pragma unroll 2
       for (int q = q0; q < q1; ++q) {
+        const uint8_t* blk = st + q * NI * kBlk;
         uint4 cw[NI], mw[NI];
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
-          const uint8_t* blk = st + (q * NI + i) * kBlk;
-          cw[i] = lds128(blk + lane * 16);
-          mw[i] = lds128(blk + kCodeBytes + gid * 16);
+          cw[i] = *reinterpret_cast<const uint4*>(blk + i * kBlk + lane * 16);
+          mw[i] = *reinterpret_cast<const uint4*>(blk + i * kBlk + kCodeBytes + gid * 16);
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int gl = q * 2 + h;  // group index within the chunk
+          float4 xx[NT];
           float d[NI][NT][4];
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            const float xm0 = sums[gl * TPP + nt * 8 + 2 * tid].y;
-            const float xm1 = sums[gl * TPP + nt * 8 + 2 * tid + 1].y;
+            // (X, -128X') of this lane's two token columns
+            xx[nt] = *reinterpret_cast<const float4*>(sums + gl * TPP + nt * 8 + 2 * tid);
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
-              d[i][nt][0] = xm0;
-              d[i][nt][1] = xm1;
-              d[i][nt][2] = xm0;
-              d[i][nt][3] = xm1;
+              d[i][nt][0] = xx[nt].y;
+              d[i][nt][1] = xx[nt].w;
+              d[i][nt][2] = xx[nt].y;
+              d[i][nt][3] = xx[nt].w;
             }
           }
-          const uint16_t* xrow = xs + gl * 64 + tid * 4;
-#define LRC_KSTEP(KS)                                                                      \
-  {                                                                                        \
-    uint32_t b0[NT], b1[NT];                                                               \
-    _Pragma("unroll") for (int nt = 0; nt < NT; ++nt) {                                    \
-      const uint2 bv = lds64(xrow + (nt * 8 + gid) * P.xs_stride + (KS) * 16);             \
-      b0[nt] = bv.x;                                                                       \
-      b1[nt] = bv.y;                                                                       \
-    }                                                                                      \
-    _Pragma("unroll") for (int i = 0; i < NI; ++i) {                                       \
-      const uint32_t wa = h ? cw[i].z : cw[i].x;                                           \
-      const uint32_t wb = h ? cw[i].w : cw[i].y;                                           \
-      const uint32_t a0 = unpack_j<2 * (KS)>(wa), a1 = unpack_j<2 * (KS)>(wb);             \
-      const uint32_t a2 = unpack_j<2 * (KS) + 1>(wa), a3 = unpack_j<2 * (KS) + 1>(wb);     \
-      _Pragma("unroll") for (int nt = 0; nt < NT; ++nt)                                    \
-          mma_bf16(d[i][nt], a0, a1, a2, a3, b0[nt], b1[nt]);                              \
-    }                                                                                      \
-  }
-          LRC_KSTEP(0)
-          LRC_KSTEP(1)
-          LRC_KSTEP(2)
-          LRC_KSTEP(3)
-#undef LRC_KSTEP
+          const uint16_t* xg = xlane + gl * 64;
 #pragma unroll
-          for (int i = 0; i < NI; ++i) {
-            const uint32_t mA = h ? mw[i].y : mw[i].x;  // {s,z} row gid
-            const uint32_t mB = h ? mw[i].w : mw[i].z;  // {s,z} row gid+8
-            const float sA = h2f(mA & 0xffff), zA = h2f(mA >> 16);
-            const float sB = h2f(mB & 0xffff), zB = h2f(mB >> 16);
+          for (int ks = 0; ks < 4; ++ks) {
+            uint32_t b0[NT], b1[NT];
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
-              const float X0 = sums[gl * TPP + nt * 8 + 2 * tid].x;
-              const float X1 = sums[gl * TPP + nt * 8 + 2 * tid + 1].x;
-              acc[i][nt][0] = fmaf(sA, d[i][nt][0], fmaf(zA, X0, acc[i][nt][0]));
-              acc[i][nt][1] = fmaf(sA, d[i][nt][1], fmaf(zA, X1, acc[i][nt][1]));
-              acc[i][nt][2] = fmaf(sB, d[i][nt][2], fmaf(zB, X0, acc[i][nt][2]));
-              acc[i][nt][3] = fmaf(sB, d[i][nt][3], fmaf(zB, X1, acc[i][nt][3]));
+              const uint2 bv = *reinterpret_cast<const uint2*>(xg + nt * 8 * P.xs_stride + ks * 16);
+              b0[nt] = bv.x;
+              b1[nt] = bv.y;
+            }
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+              const uint32_t wa = h ? cw[i].z : cw[i].x;
+              const uint32_t wb = h ? cw[i].w : cw[i].y;
+              uint32_t a0, a1, a2, a3;
+              switch (ks) {
+                case 0: a0 = unpack_j<0>(wa); a1 = unpack_j<0>(wb); a2 = unpack_j<1>(wa); a3 = unpack_j<1>(wb); break;
+                case 1: a0 = unpack_j<2>(wa); a1 = unpack_j<2>(wb); a2 = unpack_j<3>(wa); a3 = unpack_j<3>(wb); break;
+                case 2: a0 = unpack_j<4>(wa); a1 = unpack_j<4>(wb); a2 = unpack_j<5>(wa); a3 = unpack_j<5>(wb); break;
+                default: a0 = unpack_j<6>(wa); a1 = unpack_j<6>(wb); a2 = unpack_j<7>(wa); a3 = unpack_j<7>(wb); break;
+              }
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) mma_bf16(d[i][nt], a0, a1, a2, a3, b0[nt], b1[nt]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            const float2 mA = h2f2(h ? mw[i].y : mw[i].x);  // {s, z} row gid
+            const float2 mB = h2f2(h ? mw[i].w : mw[i].z);  // {s, z} row gid+8
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              acc[i][nt][0] = fmaf(mA.x, d[i][nt][0], fmaf(mA.y, xx[nt].x, acc[i][nt][0]));
+              acc[i][nt][1] = fmaf(mA.x, d[i][nt][1], fmaf(mA.y, xx[nt].z, acc[i][nt][1]));
+              acc[i][nt][2] = fmaf(mB.x, d[i][nt][2], fmaf(mB.y, xx[nt].x, acc[i][nt][2]));
+              acc[i][nt][3] = fmaf(mB.x, d[i][nt][3], fmaf(mB.y, xx[nt].z, acc[i][nt][3]));
             }
           }
         }
@@ -608,10 +630,8 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           float* rb = red + ((warp * NI + i) * NT + nt) * 128;
-          rb[gid * 8 + 2 * tid] = acc[i][nt][0];
-          rb[gid * 8 + 2 * tid + 1] = acc[i][nt][1];
-          rb[(gid + 8) * 8 + 2 * tid] = acc[i][nt][2];
-          rb[(gid + 8) * 8 + 2 * tid + 1] = acc[i][nt][3];
+          *reinterpret_cast<float2*>(rb + gid * 8 + 2 * tid) = make_float2(acc[i][nt][0], acc[i][nt][1]);
+          *reinterpret_cast<float2*>(rb + (gid + 8) * 8 + 2 * tid) = make_float2(acc[i][nt][2], acc[i][nt][3]);
         }
     }
     consumer_sync();
@@ -621,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     if (item_lr) {
       const uint8_t* lr = st + P.stage_bytes;
       const int ntask = s_ncomp * NI * 256;
-      for (int o = threadIdx.x; o < ntask; o += kNW * 32) {
+      for (int o = ctid; o < ntask; o += kNW * 32) {
         const int jl = o & 15, rr = (o >> 4) & 15;
         const int i = (o >> 8) % NI, c = (o >> 8) / NI;
         const int pi = UP ? i : 2;  // projection index into s_r (0 u1, 1 u3, 2 u2)
@@ -643,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     }
 
     // ---- E2: thread -> (row r, token n)
-    for (int o = threadIdx.x; o < 16 * TPP; o += kNW * 32) {
+    for (int o = ctid; o < 16 * TPP; o += kNW * 32) {
       const int r = o & 15, n = o >> 4;
       const int nt = n >> 3, col = n & 7;
       const int row = tile * 16 + r;
@@ -679,7 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       const int r2 = s_r[2];
       const int ntask = s_ncomp * r2 * 16;
       const int nround = (ntask + 31) & ~31;
-      for (int o = threadIdx.x; o < nround; o += kNW * 32) {
+      for (int o = ctid; o < nround; o += kNW * 32) {
         const int rl = o & 15;
         float v = 0.0f;
         int j = 0, c = 0;
@@ -692,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
 #pragma unroll
         for (int o2 = 8; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
         if (rl == 0 && o < ntask)
-          atomicAdd(&A.t[(static_cast<int64_t>(s_comp_slot[c]) * 3 + 2) * maxr + j], v);
+          atomicAdd(&A.t[((static_cast<int64_t>(s_comp_tok[c]) * A.ne + cur_e) * 3 + 2) * maxr + j], v);
       }
     }
     consumer_sync();
@@ -701,7 +721,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
 }
 
 template <bool UP, int NT>
-static lrc_status launch_one(const TiledParams& P, int num_sms, cudaStream_t st) {
+static lrc_status launch_one(const TiledParams& P, int num_sms, cudaStream_t st, bool pdl) {
   constexpr int NI = UP ? 2 : 1;
   const SmemMap m = smem_map<NI, NT>(P);
   auto fn = tiled_kernel<UP, NT>;
@@ -718,14 +738,23 @@ static lrc_status launch_one(const TiledParams& P, int num_sms, cudaStream_t st)
                                       optin - static_cast<int>(fa.sharedSizeBytes)));
     configured[UP][NT] = optin - static_cast<int>(fa.sharedSizeBytes);
   }
-  fn<<<num_sms, kThreads, m.total, st>>>(P);
-  LRC_CHECK_LAUNCH();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(num_sms);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = m.total;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  LRC_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, P));
   return LRC_OK;
 }
 
 template <bool UP>
 static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, int lr_max,
-                               cudaStream_t st) {
+                               cudaStream_t st, bool pdl) {
   constexpr int NI = UP ? 2 : 1;
   TiledParams P{};
   P.a = a;
@@ -737,14 +766,14 @@ static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, in
   if (UP) {  // the SwiGLU needs complete h1/h3: one chunk covers all of K
     P.nchunk = 1;
     P.SPC = P.NS;
-  } else {  // split K into <= 8-span chunks; partial outputs combine with atomics
+  } else {  // split K into <= kNW-span chunks; partial outputs combine with atomics
     P.nchunk = (P.NS + kNW - 1) / kNW;
     P.SPC = (P.NS + P.nchunk - 1) / P.nchunk;
   }
   P.xs_stride = P.SPC * kSpanGP * 128 + 16;
   P.stage_bytes = P.SPC * kSpanGP * NI * kBlk;
   P.lr_slot = lr_max;
-  const int budget = 227 * 1024 - 6 * 1024;
+  const int budget = 227 * 1024 - 8 * 1024;
   auto fits = [&](int nt) {
     return (nt == 1 ? smem_map<NI, 1>(P).total : smem_map<NI, 2>(P).total) <= budget;
   };
@@ -759,16 +788,16 @@ static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, in
       if (fits(1)) break;
     if (P.nstage < 2) return fail(LRC_ERR_UNSUPPORTED, "tiled kernel: K too large for smem");
   }
-  return (nt == 1) ? launch_one<UP, 1>(P, num_sms, st) : launch_one<UP, 2>(P, num_sms, st);
+  return (nt == 1) ? launch_one<UP, 1>(P, num_sms, st, pdl) : launch_one<UP, 2>(P, num_sms, st, pdl);
 }
 
 lrc_status launch_up_tiled(const ExpertArgs& a, int num_sms, int max_tok, int lr_max,
-                           cudaStream_t st) {
-  return launch_tiled<true>(a, num_sms, max_tok, lr_max, st);
+                           cudaStream_t st, bool pdl) {
+  return launch_tiled<true>(a, num_sms, max_tok, lr_max, st, pdl);
 }
 lrc_status launch_down_tiled(const ExpertArgs& a, int num_sms, int max_tok, int lr_max,
-                             cudaStream_t st) {
-  return launch_tiled<false>(a, num_sms, max_tok, lr_max, st);
+                             cudaStream_t st, bool pdl) {
+  return launch_tiled<false>(a, num_sms, max_tok, lr_max, st, pdl);
 }
 
 }  // namespace lrc
