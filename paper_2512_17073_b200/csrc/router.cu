@@ -132,12 +132,12 @@ __device__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* x, int64_t b0,
       for (int t = 0; t < kTT; ++t)
         if (t < nb) acc[t] = fmaf(w, bf2f(x[(b0 + t) * ra.d + c]), acc[t]);
     }
+#pragma unroll
+    for (int t = 0; t < kTT; ++t) acc[t] = warp_sum(acc[t]);  // (vrow_dot_tokens reduces itself)
   }
 #pragma unroll
-  for (int t = 0; t < kTT; ++t) {
-    const float v = warp_sum(acc[t]);
-    if (lane == 0 && t < nb) ra.t[(((b0 + t) * ra.ne + e) * 3 + proj) * ra.maxr + j] = v;
-  }
+  for (int t = 0; t < kTT; ++t)
+    if (lane == 0 && t < nb) ra.t[(((b0 + t) * ra.ne + e) * 3 + proj) * ra.maxr + j] = acc[t];
 }
 
 template <typename T>

@@ -338,6 +338,14 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   __shared__ int s_prefix[LRC_MAX_EXPERTS + 1];
   __shared__ int s_range[2];
   __shared__ int s_comp_n[TPP], s_comp_tok[TPP], s_comp_of[TPP], s_ncomp;
+  // per active expert (filled in parallel at kernel start) and per token pass
+  __shared__ int s_aoff[LRC_MAX_EXPERTS], s_acnt[LRC_MAX_EXPERTS], s_ae[LRC_MAX_EXPERTS];
+  __shared__ const uint8_t* s_wsrc[LRC_MAX_EXPERTS];
+  __shared__ const uint8_t* s_lsrc[LRC_MAX_EXPERTS];
+  __shared__ int s_lbytes[LRC_MAX_EXPERTS];
+  __shared__ int s_ppair[TPP], s_ptok[TPP];
+  __shared__ float s_pw[TPP];
+  __shared__ int s_dirty;
   __shared__ int s_r[3], s_ub[3], s_ugs[3], s_vb;
   __shared__ LrLayout s_L;
 
@@ -352,11 +360,24 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   griddep_launch_dependents();
   const int n_active = A.plan.counts[0];
 
+  for (int ai = threadIdx.x; ai < n_active; ai += blockDim.x) {
+    const int e = A.plan.active[ai];
+    const lrc_expert& E = A.experts[e];
+    s_aoff[ai] = A.plan.active_off[ai];
+    s_acnt[ai] = A.plan.active_cnt[ai];
+    s_ae[ai] = e;
+    s_wsrc[ai] = UP ? E.up_tiles : E.down_tiles;
+    const LrLayout L = lr_layout(E);
+    s_lbytes[ai] = UP ? L.up_total : L.down_total;
+    s_lsrc[ai] = UP ? E.up_lr_tiles : E.down_lr_tiles;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
+    s_dirty = TPP;
     int acc = 0;
     for (int ai = 0; ai < n_active; ++ai) {
       s_prefix[ai] = acc;
-      const int passes = (A.plan.active_cnt[ai] + TPP - 1) / TPP;
+      const int passes = (s_acnt[ai] + TPP - 1) / TPP;
       acc += passes * P.nchunk * static_cast<int>(P.RT);
     }
     s_prefix[n_active] = acc;
@@ -403,22 +424,19 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
           c_ai = ai;
           c_pass = pass;
           c_comp = 0;
-          const int off = A.plan.active_off[ai];
-          const int n = min(TPP, A.plan.active_cnt[ai] - pass * TPP);
+          const int off = s_aoff[ai];
+          const int n = min(TPP, s_acnt[ai] - pass * TPP);
           for (int j = 0; j < n; ++j) c_comp |= A.plan.pair_comp[A.plan.pair_list[off + pass * TPP + j]] >= 0;
         }
         int gp0, gp1;
         chunk_gp(chunk, gp0, gp1);
-        const lrc_expert& E = A.experts[A.plan.active[ai]];
-        const uint8_t* base = UP ? E.up_tiles : E.down_tiles;
-        const uint8_t* src = base + ((static_cast<int64_t>(tile) * P.GP + gp0) * NI) * kBlk;
+        const uint8_t* src = s_wsrc[ai] + ((static_cast<int64_t>(tile) * P.GP + gp0) * NI) * kBlk;
         const uint32_t bytes = static_cast<uint32_t>((gp1 - gp0) * NI * kBlk);
         uint32_t lr_bytes = 0;
         const uint8_t* lr_src = nullptr;
-        if (P.lr_slot > 0 && c_comp && (UP || chunk == 0)) {
-          const LrLayout L = lr_layout(E);
-          lr_bytes = static_cast<uint32_t>(UP ? L.up_total : L.down_total);
-          lr_src = (UP ? E.up_lr_tiles : E.down_lr_tiles) + static_cast<int64_t>(tile) * lr_bytes;
+        if (P.lr_slot > 0 && c_comp && (UP || chunk == 0) && s_lbytes[ai] > 0) {
+          lr_bytes = static_cast<uint32_t>(s_lbytes[ai]);
+          lr_src = s_lsrc[ai] + static_cast<int64_t>(tile) * lr_bytes;
         }
         uint8_t* dst = stages + static_cast<size_t>(s) * slot_bytes;
         mbar_expect_tx(&full[s], bytes + lr_bytes);
@@ -442,29 +460,43 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     decode(it, ai, pass, chunk, tile);
     int gp0, gp1;
     chunk_gp(chunk, gp0, gp1);
-    const int off = A.plan.active_off[ai], cnt = A.plan.active_cnt[ai];
     if (ai != cur_ai || pass != cur_pass || chunk != cur_chunk) {
+      const int off = s_aoff[ai], cnt = s_acnt[ai];
       // ---- (re)build the activation operand x' and the LR vectors for this group
       consumer_sync();
       const bool new_pass = (ai != cur_ai || pass != cur_pass);
       cur_ai = ai;
       cur_pass = pass;
       cur_chunk = chunk;
-      cur_e = A.plan.active[ai];
+      cur_e = s_ae[ai];
       pass_tok = min(TPP, cnt - pass * TPP);
+      if (ctid < TPP && new_pass) {  // per-token pass data into shared memory
+        const int n = ctid;
+        int p = -1, tok = 0, cmp = 0;
+        float w = 0.0f;
+        if (n < pass_tok) {
+          p = A.plan.pair_list[off + pass * TPP + n];
+          tok = A.plan.pair_token[p];
+          w = A.plan.pair_w[p];
+          cmp = A.plan.pair_comp[p] >= 0;
+        }
+        s_ppair[n] = p;
+        s_ptok[n] = tok;
+        s_pw[n] = w;
+        s_comp_of[n] = cmp;  // flag for now; ranked below
+      }
+      consumer_sync();
       if (ctid == 0 && new_pass) {
         const lrc_expert& E = A.experts[cur_e];
         int nc = 0;
         for (int n = 0; n < TPP; ++n) {
-          s_comp_of[n] = -1;
-          if (n < pass_tok) {
-            const int p = A.plan.pair_list[off + pass * TPP + n];
-            if (A.plan.pair_comp[p] >= 0) {
-              s_comp_of[n] = nc;
-              s_comp_n[nc] = n;
-              s_comp_tok[nc] = A.plan.pair_token[p];
-              ++nc;
-            }
+          if (s_comp_of[n]) {
+            s_comp_of[n] = nc;
+            s_comp_n[nc] = n;
+            s_comp_tok[nc] = s_ptok[n];
+            ++nc;
+          } else {
+            s_comp_of[n] = -1;
           }
         }
         s_ncomp = nc;
@@ -479,13 +511,14 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       }
       const int k0 = gp0 * 128;
       const int ng = (gp1 - gp0) * 2;
-      for (int task = ctid; task < TPP * ng; task += kNW * 32) {
+      const int nrows = max(pass_tok, s_dirty);  // rows beyond pass_tok only if dirty
+      for (int task = ctid; task < nrows * ng; task += kNW * 32) {
         const int n = task / ng, g = task - n * ng;
         float xsum = 0.f, xpsum = 0.f;
         uint32_t* dst = reinterpret_cast<uint32_t*>(xs + n * P.xs_stride + g * 64);
         if (n < pass_tok) {
-          const int p = A.plan.pair_list[off + pass * TPP + n];
-          const uint16_t* row = UP ? A.x + static_cast<int64_t>(A.plan.pair_token[p]) * A.hidden
+          const int p = s_ppair[n];
+          const uint16_t* row = UP ? A.x + static_cast<int64_t>(s_ptok[n]) * A.hidden
                                    : A.a16 + static_cast<int64_t>(p) * A.ffn;
           const int kk = k0 + g * 64;
           const bool vec = (kk + 64 <= P.K) && ((reinterpret_cast<uintptr_t>(row + kk) & 15) == 0);
@@ -521,6 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
         sums[g * TPP + n] = make_float2(xsum, -128.0f * xpsum);
       }
       consumer_sync();
+      if (ctid == 0) s_dirty = pass_tok;
       // low-rank input vectors of the compensated tokens (t1/t3 up, t2 down)
       if (maxr > 0) {
         const int ntask = s_ncomp * NI * maxr;
@@ -681,15 +715,12 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       if (UP) {
         float act = 0.0f;
         if (valid) {
-          const int p = A.plan.pair_list[off + pass * TPP + n];
           act = silu_f(v0) * v1;
-          A.a16[static_cast<int64_t>(p) * A.ffn + row] = f2bf(act);
+          A.a16[static_cast<int64_t>(s_ppair[n]) * A.ffn + row] = f2bf(act);
         }
         act_s[r * TPP + n] = act;
       } else if (valid) {
-        const int p = A.plan.pair_list[off + pass * TPP + n];
-        atomicAdd(&A.y[static_cast<int64_t>(A.plan.pair_token[p]) * A.hidden + row],
-                  A.plan.pair_w[p] * v0);
+        atomicAdd(&A.y[static_cast<int64_t>(s_ptok[n]) * A.hidden + row], s_pw[n] * v0);
       }
     }
     // ---- E3 (up): partial t2 = V2[:, tile rows] . act for the compensated tokens
