@@ -319,6 +319,11 @@ __device__ __forceinline__ float2 h2f2(uint32_t w) {
   return __half22float2(*reinterpret_cast<const __half2*>(&w));
 }
 
+struct ItemDesc {
+  int ai, pass, chunk, tile, lr, pad0, pad1, pad2;
+};
+constexpr int kMaxStages = 8;
+
 template <bool UP, int NT>
 __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   constexpr int NI = UP ? 2 : 1;
@@ -335,10 +340,10 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   float* lrs = reinterpret_cast<float*>(smem + SM.lrs);      // [NI][16][TPP(comp idx)]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM.bars);
   uint64_t* empty = full + P.nstage;
+  __shared__ ItemDesc s_desc[kMaxStages];
   __shared__ int s_prefix[LRC_MAX_EXPERTS + 1];
   __shared__ int s_range[2];
   __shared__ int s_comp_n[TPP], s_comp_tok[TPP], s_comp_of[TPP], s_ncomp;
-  // per active expert (filled in parallel at kernel start) and per token pass
   __shared__ int s_aoff[LRC_MAX_EXPERTS], s_acnt[LRC_MAX_EXPERTS], s_ae[LRC_MAX_EXPERTS];
   __shared__ const uint8_t* s_wsrc[LRC_MAX_EXPERTS];
   __shared__ const uint8_t* s_lsrc[LRC_MAX_EXPERTS];
@@ -359,7 +364,6 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   if (UP) griddep_wait();
   griddep_launch_dependents();
   const int n_active = A.plan.counts[0];
-
   for (int ai = threadIdx.x; ai < n_active; ai += blockDim.x) {
     const int e = A.plan.active[ai];
     const lrc_expert& E = A.experts[e];
@@ -377,8 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     int acc = 0;
     for (int ai = 0; ai < n_active; ++ai) {
       s_prefix[ai] = acc;
-      const int passes = (s_acnt[ai] + TPP - 1) / TPP;
-      acc += passes * P.nchunk * static_cast<int>(P.RT);
+      acc += ((s_acnt[ai] + TPP - 1) / TPP) * P.nchunk * static_cast<int>(P.RT);
     }
     s_prefix[n_active] = acc;
     const int64_t total = acc;
@@ -394,32 +397,19 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   const int beg = s_range[0], end = s_range[1];
   if (beg >= end) return;
 
-  auto decode = [&](int it, int& ai, int& pass, int& chunk, int& tile) {
-    int lo = 0;
-    while (s_prefix[lo + 1] <= it) ++lo;
-    ai = lo;
-    int r = it - s_prefix[lo];
-    tile = r % static_cast<int>(P.RT);
-    r /= static_cast<int>(P.RT);
-    chunk = r % P.nchunk;
-    pass = r / P.nchunk;
-  };
-  auto chunk_gp = [&](int chunk, int& gp0, int& gp1) {
-    gp0 = chunk * P.SPC * kSpanGP;
-    const int64_t hi = static_cast<int64_t>(gp0) + P.SPC * kSpanGP;
-    gp1 = static_cast<int>(P.GP < hi ? P.GP : hi);
-  };
-
   if (warp == kNW) {
     // ===================== producer: one elected lane streams work items ====
     if (lane == 0) {
-      int c_ai = -1, c_pass = -1, c_comp = 0;
+      int c_ai = -1, c_pass = -1, c_comp = 0, ai = 0;
       for (int it = beg; it < end; ++it) {
         const int k = it - beg;
         const int s = k % P.nstage;
         if (k >= P.nstage) mbar_wait(&empty[s], ((k / P.nstage) - 1) & 1);
-        int ai, pass, chunk, tile;
-        decode(it, ai, pass, chunk, tile);
+        while (s_prefix[ai + 1] <= it) ++ai;
+        int r = it - s_prefix[ai];
+        const int tile = r % static_cast<int>(P.RT);
+        r /= static_cast<int>(P.RT);
+        const int chunk = r % P.nchunk, pass = r / P.nchunk;
         if (ai != c_ai || pass != c_pass) {
           c_ai = ai;
           c_pass = pass;
@@ -428,20 +418,18 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
           const int n = min(TPP, s_acnt[ai] - pass * TPP);
           for (int j = 0; j < n; ++j) c_comp |= A.plan.pair_comp[A.plan.pair_list[off + pass * TPP + j]] >= 0;
         }
-        int gp0, gp1;
-        chunk_gp(chunk, gp0, gp1);
+        const int gp0 = chunk * P.SPC * kSpanGP;
+        const int gp1 = static_cast<int>(min(P.GP, static_cast<int64_t>(gp0) + P.SPC * kSpanGP));
         const uint8_t* src = s_wsrc[ai] + ((static_cast<int64_t>(tile) * P.GP + gp0) * NI) * kBlk;
         const uint32_t bytes = static_cast<uint32_t>((gp1 - gp0) * NI * kBlk);
-        uint32_t lr_bytes = 0;
-        const uint8_t* lr_src = nullptr;
-        if (P.lr_slot > 0 && c_comp && (UP || chunk == 0) && s_lbytes[ai] > 0) {
-          lr_bytes = static_cast<uint32_t>(s_lbytes[ai]);
-          lr_src = s_lsrc[ai] + static_cast<int64_t>(tile) * lr_bytes;
-        }
+        const bool lr = P.lr_slot > 0 && c_comp && (UP || chunk == 0) && s_lbytes[ai] > 0;
+        const uint32_t lr_bytes = lr ? static_cast<uint32_t>(s_lbytes[ai]) : 0u;
+        s_desc[s] = ItemDesc{ai, pass, chunk, tile, lr ? 1 : 0, gp0, gp1, 0};
         uint8_t* dst = stages + static_cast<size_t>(s) * slot_bytes;
-        mbar_expect_tx(&full[s], bytes + lr_bytes);
+        mbar_expect_tx(&full[s], bytes + lr_bytes);  // release: orders the descriptor store
         bulk_g2s(dst, src, bytes, &full[s]);
-        if (lr_bytes) bulk_g2s(dst + P.stage_bytes, lr_src, lr_bytes, &full[s]);
+        if (lr) bulk_g2s(dst + P.stage_bytes, s_lsrc[ai] + static_cast<int64_t>(tile) * lr_bytes,
+                         lr_bytes, &full[s]);
       }
     }
     return;
@@ -451,63 +439,64 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   const int gid = lane >> 2, tid = lane & 3;
   const int ctid = threadIdx.x;  // consumer thread id, 0 .. kNW*32-1
   if (!UP) griddep_wait();
-  int cur_ai = -1, cur_pass = -1, cur_chunk = -1;
-  int pass_tok = 0, cur_e = -1;
-  for (int it = beg; it < end; ++it) {
-    const int k = it - beg;
+  int cur_ai = -1, cur_pass = -1, cur_chunk = -1, pass_tok = 0, cur_e = -1;
+  const uint16_t* xlane = xs + gid * P.xs_stride + tid * 4;
+  const int nitems = end - beg;
+  for (int k = 0; k < nitems; ++k) {
     const int s = k % P.nstage;
-    int ai, pass, chunk, tile;
-    decode(it, ai, pass, chunk, tile);
-    int gp0, gp1;
-    chunk_gp(chunk, gp0, gp1);
-    if (ai != cur_ai || pass != cur_pass || chunk != cur_chunk) {
-      const int off = s_aoff[ai], cnt = s_acnt[ai];
-      // ---- (re)build the activation operand x' and the LR vectors for this group
-      consumer_sync();
-      const bool new_pass = (ai != cur_ai || pass != cur_pass);
-      cur_ai = ai;
-      cur_pass = pass;
-      cur_chunk = chunk;
-      cur_e = s_ae[ai];
-      pass_tok = min(TPP, cnt - pass * TPP);
-      if (ctid < TPP && new_pass) {  // per-token pass data into shared memory
-        const int n = ctid;
-        int p = -1, tok = 0, cmp = 0;
-        float w = 0.0f;
-        if (n < pass_tok) {
-          p = A.plan.pair_list[off + pass * TPP + n];
-          tok = A.plan.pair_token[p];
-          w = A.plan.pair_w[p];
-          cmp = A.plan.pair_comp[p] >= 0;
-        }
-        s_ppair[n] = p;
-        s_ptok[n] = tok;
-        s_pw[n] = w;
-        s_comp_of[n] = cmp;  // flag for now; ranked below
-      }
-      consumer_sync();
-      if (ctid == 0 && new_pass) {
-        const lrc_expert& E = A.experts[cur_e];
-        int nc = 0;
-        for (int n = 0; n < TPP; ++n) {
-          if (s_comp_of[n]) {
-            s_comp_of[n] = nc;
-            s_comp_n[nc] = n;
-            s_comp_tok[nc] = s_ptok[n];
-            ++nc;
-          } else {
-            s_comp_of[n] = -1;
+    mbar_wait(&full[s], (k / P.nstage) & 1);  // acquire: descriptor + bytes visible
+    const ItemDesc dsc = s_desc[s];
+    const int gp0 = dsc.pad0, gp1 = dsc.pad1, tile = dsc.tile;
+    if (dsc.ai != cur_ai || dsc.pass != cur_pass || dsc.chunk != cur_chunk) {
+      // ---- (re)build the activation operand x' and the LR vectors for this group.
+      // All consumers passed the previous item's final barrier, so xs/sums/ts are free.
+      const bool new_pass = (dsc.ai != cur_ai || dsc.pass != cur_pass);
+      const int off = s_aoff[dsc.ai], cnt = s_acnt[dsc.ai];
+      cur_ai = dsc.ai;
+      cur_pass = dsc.pass;
+      cur_chunk = dsc.chunk;
+      cur_e = s_ae[dsc.ai];
+      pass_tok = min(TPP, cnt - cur_pass * TPP);
+      if (new_pass) {
+        if (ctid < TPP) {  // per-token pass data into shared memory
+          const int n = ctid;
+          int p = -1, tok = 0, cmp = 0;
+          float w = 0.0f;
+          if (n < pass_tok) {
+            p = A.plan.pair_list[off + cur_pass * TPP + n];
+            tok = A.plan.pair_token[p];
+            w = A.plan.pair_w[p];
+            cmp = A.plan.pair_comp[p] >= 0;
           }
+          s_ppair[n] = p;
+          s_ptok[n] = tok;
+          s_pw[n] = w;
+          s_comp_of[n] = cmp;
         }
-        s_ncomp = nc;
-        s_L = lr_layout(E);
-        const lrc_qmat* us[3] = {&E.u1, &E.u3, &E.u2};
-        for (int i = 0; i < 3; ++i) {
-          s_r[i] = factor_present(*us[i]) ? us[i]->cols : 0;
-          s_ub[i] = us[i]->bits;
-          s_ugs[i] = us[i]->group_size;
+        consumer_sync();
+        if (ctid == 0) {
+          const lrc_expert& E = A.experts[cur_e];
+          int nc = 0;
+          for (int n = 0; n < TPP; ++n) {
+            if (s_comp_of[n]) {
+              s_comp_of[n] = nc;
+              s_comp_n[nc] = n;
+              s_comp_tok[nc] = s_ptok[n];
+              ++nc;
+            } else {
+              s_comp_of[n] = -1;
+            }
+          }
+          s_ncomp = nc;
+          s_L = lr_layout(E);
+          const lrc_qmat* us[3] = {&E.u1, &E.u3, &E.u2};
+          for (int i = 0; i < 3; ++i) {
+            s_r[i] = factor_present(*us[i]) ? us[i]->cols : 0;
+            s_ub[i] = us[i]->bits;
+            s_ugs[i] = us[i]->group_size;
+          }
+          s_vb = E.v2.bits;
         }
-        s_vb = E.v2.bits;
       }
       const int k0 = gp0 * 128;
       const int ng = (gp1 - gp0) * 2;
@@ -517,9 +506,8 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
         float xsum = 0.f, xpsum = 0.f;
         uint32_t* dst = reinterpret_cast<uint32_t*>(xs + n * P.xs_stride + g * 64);
         if (n < pass_tok) {
-          const int p = s_ppair[n];
           const uint16_t* row = UP ? A.x + static_cast<int64_t>(s_ptok[n]) * A.hidden
-                                   : A.a16 + static_cast<int64_t>(p) * A.ffn;
+                                   : A.a16 + static_cast<int64_t>(s_ppair[n]) * A.ffn;
           const int kk = k0 + g * 64;
           const bool vec = (kk + 64 <= P.K) && ((reinterpret_cast<uintptr_t>(row + kk) & 15) == 0);
 #pragma unroll 2
@@ -567,12 +555,9 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       }
       consumer_sync();
     }
-    const bool item_lr = (P.lr_slot > 0) && (s_ncomp > 0) && (UP || chunk == 0);
-
-    // ---- wait for the weights of this item
-    mbar_wait(&full[s], (k / P.nstage) & 1);
     const uint8_t* st = stages + static_cast<size_t>(s) * slot_bytes;
 
+    // ---------------------------------------------------------- MMA core ----
     float acc[NI][NT][4];
 #pragma unroll
     for (int i = 0; i < NI; ++i)
@@ -583,7 +568,6 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
 
     const int ngp = gp1 - gp0;
     const int nspan = (ngp + kSpanGP - 1) / kSpanGP;
-    const uint16_t* xlane = xs + gid * P.xs_stride + tid * 4;
     for (int sp = warp; sp < nspan; sp += kNW) {
       const int q0 = sp * kSpanGP, q1 = min(ngp, q0 + kSpanGP);
 #pragma unroll 2
@@ -612,6 +596,17 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
               d[i][nt][3] = xx[nt].w;
             }
           }
+          // shared shifts of the two code words per matrix (j>=3 slots)
+          uint32_t wa[NI][3], wb[NI][3];
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            wa[i][0] = h ? cw[i].z : cw[i].x;
+            wb[i][0] = h ? cw[i].w : cw[i].y;
+            wa[i][1] = wa[i][0] >> 6;
+            wb[i][1] = wb[i][0] >> 6;
+            wa[i][2] = wa[i][0] >> 12;
+            wb[i][2] = wb[i][0] >> 12;
+          }
           const uint16_t* xg = xlane + gl * 64;
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
@@ -622,17 +617,14 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
               b0[nt] = bv.x;
               b1[nt] = bv.y;
             }
+            // slot j = 2ks (regs a0/a1) and 2ks+1 (a2/a3): word (j/3 shift), mask 3 << 2*(j%3)
+            constexpr uint32_t M = 0x43004300u;
+            const int j0 = 2 * ks, j1 = 2 * ks + 1;
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
-              const uint32_t wa = h ? cw[i].z : cw[i].x;
-              const uint32_t wb = h ? cw[i].w : cw[i].y;
-              uint32_t a0, a1, a2, a3;
-              switch (ks) {
-                case 0: a0 = unpack_j<0>(wa); a1 = unpack_j<0>(wb); a2 = unpack_j<1>(wa); a3 = unpack_j<1>(wb); break;
-                case 1: a0 = unpack_j<2>(wa); a1 = unpack_j<2>(wb); a2 = unpack_j<3>(wa); a3 = unpack_j<3>(wb); break;
-                case 2: a0 = unpack_j<4>(wa); a1 = unpack_j<4>(wb); a2 = unpack_j<5>(wa); a3 = unpack_j<5>(wb); break;
-                default: a0 = unpack_j<6>(wa); a1 = unpack_j<6>(wb); a2 = unpack_j<7>(wa); a3 = unpack_j<7>(wb); break;
-              }
+              const uint32_t m0 = 0x00030003u << (2 * (j0 % 3)), m1 = 0x00030003u << (2 * (j1 % 3));
+              const uint32_t a0 = (wa[i][j0 / 3] & m0) | M, a1 = (wb[i][j0 / 3] & m0) | M;
+              const uint32_t a2 = (wa[i][j1 / 3] & m1) | M, a3 = (wb[i][j1 / 3] & m1) | M;
 #pragma unroll
               for (int nt = 0; nt < NT; ++nt) mma_bf16(d[i][nt], a0, a1, a2, a3, b0[nt], b1[nt]);
             }
@@ -652,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
         }
       }
     }
-    if (!item_lr) {
+    if (!dsc.lr) {  // weights consumed: hand the stage back right away
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
@@ -668,35 +660,44 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
           *reinterpret_cast<float2*>(rb + (gid + 8) * 8 + 2 * tid) = make_float2(acc[i][nt][2], acc[i][nt][3]);
         }
     }
-    consumer_sync();
+    consumer_sync();  // (A) partials complete
 
-    // ---- E1: low-rank up-projection U.t for the tile rows (ref/lowrank.py:165),
-    // factor rows read from the stage's LR slot; 16 lanes split the rank.
-    if (item_lr) {
-      const uint8_t* lr = st + P.stage_bytes;
-      const int ntask = s_ncomp * NI * 256;
-      for (int o = ctid; o < ntask; o += kNW * 32) {
-        const int jl = o & 15, rr = (o >> 4) & 15;
-        const int i = (o >> 8) % NI, c = (o >> 8) / NI;
-        const int pi = UP ? i : 2;  // projection index into s_r (0 u1, 1 u3, 2 u2)
+    // ---- E1 (one warp): low-rank up-projection U.t for the tile rows
+    // (ref/lowrank.py:165), factor rows from the stage's LR slot.  Lane =
+    // (matrix i, row rr); loops over the compensated tokens of the pass.
+    if (dsc.lr) {
+      if (warp == 0 && lane < NI * 16) {
+        const uint8_t* lr = st + P.stage_bytes;
+        const int rr = lane & 15, i = lane >> 4;
+        const int pi = UP ? i : 2;
         const int r = s_r[pi];
-        float v = 0.0f;
-        if (r > 0) {
-          const uint8_t* codes = lr + (UP ? (i ? s_L.u3c : s_L.u1c) : s_L.u2c);
-          const uint8_t* meta = lr + (UP ? (i ? s_L.u3m : s_L.u1m) : s_L.u2m);
-          const int gpu = (r + s_ugs[pi] - 1) / s_ugs[pi];
-          const float* tv = ts + (c * NI + i) * maxr;
-          for (int j = jl; j < r; j += 16)
-            v = fmaf(lr_deq(codes, rr * r + j, s_ub[pi], meta, rr * gpu + j / s_ugs[pi]), tv[j], v);
+        for (int c = 0; c < s_ncomp; ++c) {
+          float v = 0.0f;
+          if (r > 0) {
+            const uint8_t* codes = lr + (UP ? (i ? s_L.u3c : s_L.u1c) : s_L.u2c);
+            const uint8_t* meta = lr + (UP ? (i ? s_L.u3m : s_L.u1m) : s_L.u2m);
+            const int gsu = s_ugs[pi], bits = s_ub[pi];
+            const int gpu = (r + gsu - 1) / gsu;
+            const float* tv = ts + (c * NI + i) * maxr;
+            for (int g = 0; g < gpu; ++g) {
+              const uint32_t sz = *reinterpret_cast<const uint32_t*>(meta + (rr * gpu + g) * 4);
+              const float2 f = h2f2(sz);
+              float cx = 0.0f, sx = 0.0f;
+              const int j1 = min(r, (g + 1) * gsu);
+              for (int j = g * gsu; j < j1; ++j) {
+                cx = fmaf(static_cast<float>(read_code(codes, rr * r + j, bits, 1 << 30)), tv[j], cx);
+                sx += tv[j];
+              }
+              v = fmaf(f.x, cx, fmaf(f.y, sx, v));
+            }
+          }
+          lrs[(i * 16 + rr) * TPP + c] = v;
         }
-#pragma unroll
-        for (int o2 = 8; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
-        if (jl == 0) lrs[(i * 16 + rr) * TPP + c] = v;
       }
-      consumer_sync();
+      consumer_sync();  // (B) LR terms ready
     }
 
-    // ---- E2: thread -> (row r, token n)
+    // ---- E2: thread -> (row r, token n): reduce the warp partials, epilogue
     for (int o = ctid; o < 16 * TPP; o += kNW * 32) {
       const int r = o & 15, n = o >> 4;
       const int nt = n >> 3, col = n & 7;
@@ -707,7 +708,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
         if (UP) v1 += red[((w * NI + NI - 1) * NT + nt) * 128 + r * 8 + col];
       }
       const int c = s_comp_of[n];
-      if (item_lr && c >= 0) {
+      if (dsc.lr && c >= 0) {
         v0 += lrs[(0 * 16 + r) * TPP + c];
         if (UP) v1 += lrs[((NI - 1) * 16 + r) * TPP + c];
       }
@@ -723,31 +724,33 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
         atomicAdd(&A.y[static_cast<int64_t>(s_ptok[n]) * A.hidden + row], s_pw[n] * v0);
       }
     }
-    // ---- E3 (up): partial t2 = V2[:, tile rows] . act for the compensated tokens
-    if (UP && item_lr && s_r[2] > 0) {
-      consumer_sync();
+    consumer_sync();  // (C) red / lrs / act_s consumed
+
+    // ---- E3 (up, one warp, overlaps the next item): partial t2 = V2[:, tile
+    // rows] . act for the compensated tokens; lane = rank index j.
+    if (UP && dsc.lr && warp == kNW - 1 && s_r[2] > 0) {
       const uint8_t* lr = st + P.stage_bytes;
-      const int r2 = s_r[2];
-      const int ntask = s_ncomp * r2 * 16;
-      const int nround = (ntask + 31) & ~31;
-      for (int o = ctid; o < nround; o += kNW * 32) {
-        const int rl = o & 15;
-        float v = 0.0f;
-        int j = 0, c = 0;
-        if (o < ntask) {
-          j = (o >> 4) % r2;
-          c = (o >> 4) / r2;
-          v = lr_deq(lr + s_L.v2c, rl * r2 + j, s_vb, lr + s_L.v2m, j) *
-              act_s[rl * TPP + s_comp_n[c]];
+      const int r2 = s_r[2], vb = s_vb;
+      for (int j = lane; j < r2; j += 32) {
+        const float2 f = h2f2(*reinterpret_cast<const uint32_t*>(lr + s_L.v2m + j * 4));
+        for (int c = 0; c < s_ncomp; ++c) {
+          const int n = s_comp_n[c];
+          float cx = 0.0f, sx = 0.0f;
+#pragma unroll 4
+          for (int rl = 0; rl < 16; ++rl) {
+            const float a = act_s[rl * TPP + n];
+            cx = fmaf(static_cast<float>(read_code(lr + s_L.v2c, rl * r2 + j, vb, 1 << 30)), a, cx);
+            sx += a;
+          }
+          atomicAdd(&A.t[((static_cast<int64_t>(s_comp_tok[c]) * A.ne + cur_e) * 3 + 2) * maxr + j],
+                    fmaf(f.x, cx, f.y * sx));
         }
-#pragma unroll
-        for (int o2 = 8; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
-        if (rl == 0 && o < ntask)
-          atomicAdd(&A.t[((static_cast<int64_t>(s_comp_tok[c]) * A.ne + cur_e) * 3 + 2) * maxr + j], v);
       }
     }
-    consumer_sync();
-    if (item_lr && lane == 0) mbar_arrive(&empty[s]);
+    if (dsc.lr) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
   }
 }
 
@@ -804,7 +807,7 @@ static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, in
   P.xs_stride = P.SPC * kSpanGP * 128 + 16;
   P.stage_bytes = P.SPC * kSpanGP * NI * kBlk;
   P.lr_slot = lr_max;
-  const int budget = 227 * 1024 - 8 * 1024;
+  const int budget = 227 * 1024 - 12 * 1024;  // static shared (~10 KB) + slack
   auto fits = [&](int nt) {
     return (nt == 1 ? smem_map<NI, 1>(P).total : smem_map<NI, 2>(P).total) <= budget;
   };
