@@ -17,6 +17,7 @@
 // bf16) and the +128 bias into the fp32 accumulator seed (C = -128 * sum x').
 // Per group:  y += s * (sum c x) + z * sum x   (fp32, ref/quant.py:216-224).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "layer.cuh"
@@ -25,9 +26,9 @@ namespace lrc {
 
 constexpr int kBlk = 640;
 constexpr int kCodeBytes = 512;
-constexpr int kSpanGP = 2;        // group pairs per warp span (256 columns)
-constexpr int kNW = 16;           // consumer warps
-constexpr int kThreads = (kNW + 1) * 32;
+constexpr int kSpanGP = 4;        // group pairs per warp span (512 columns)
+constexpr int kNW = 8;            // consumer warps (+1 epilogue warp, +1 producer warp)
+constexpr int kThreads = (kNW + 2) * 32;
 
 int64_t tiles_bytes(int64_t rows, int64_t cols, int ni) {
   int64_t rt = (rows + 15) / 16, gp = (cols + 127) / 128;
@@ -278,7 +279,11 @@ struct TiledParams {
   int lr_slot;          // low-rank tile bytes per stage (max over experts; 0 = none)
   int nstage;
   int xs_stride;        // bf16 elements per x' row
+  int xs_rows;          // x' rows held in shared memory (<= 8*NT)
+  int debug;            // LRC_TILED_DEBUG: bit0 skip MMA core
 };
+
+constexpr int kNRed = 2;  // partial-sum ring depth (consumers -> epilogue warp)
 
 struct SmemMap {
   int xs, sums, red, ts, act, lrs, bars, total;
@@ -292,11 +297,11 @@ __host__ __device__ inline SmemMap smem_map(const TiledParams& p) {
   SmemMap m;
   int o = p.nstage * (p.stage_bytes + p.lr_slot);
   m.xs = o;
-  o = align16(o + TPP * p.xs_stride * 2);
+  o = align16(o + (p.xs_rows + 1) * p.xs_stride * 2);  // +1: shared zero row
   m.sums = o;
   o = align16(o + p.SPC * kSpanGP * 2 * TPP * 8);
   m.red = o;
-  o = align16(o + kNW * NI * NT * 128 * 4);
+  o = align16(o + kNRed * kNW * NI * NT * 128 * 4);
   m.ts = o;
   o = align16(o + TPP * NI * (p.a.maxr > 0 ? p.a.maxr : 1) * 4);
   m.act = o;
@@ -304,7 +309,7 @@ __host__ __device__ inline SmemMap smem_map(const TiledParams& p) {
   m.lrs = o;
   o = align16(o + NI * 16 * TPP * 4);
   m.bars = o;
-  m.total = o + 2 * p.nstage * 8;
+  m.total = o + (2 * p.nstage + 2 * kNRed) * 8;
   return m;
 }
 
@@ -319,39 +324,63 @@ __device__ __forceinline__ float2 h2f2(uint32_t w) {
   return __half22float2(*reinterpret_cast<const __half2*>(&w));
 }
 
+// exact float of a small unsigned code without the XU pipe: 2^23 + c, minus 2^23
+__device__ __forceinline__ float code_f(uint32_t c) {
+  return __uint_as_float(0x4B000000u | c) - 8388608.0f;
+}
+
+// code at bit offset `bit` of a shared-memory bitstream (4-byte aligned base)
+__device__ __forceinline__ uint32_t smem_code(const uint32_t* w, int bit, uint32_t mask) {
+  return __funnelshift_r(w[bit >> 5], w[(bit >> 5) + 1], bit & 31) & mask;
+}
+
+// (w & m) | 0x43004300 in ONE lop3 (nvcc otherwise splits it: one immediate per LOP3)
+__device__ __forceinline__ uint32_t lop_and_or(uint32_t w, uint32_t m) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "r"(m), "r"(0x43004300u));
+  return r;
+}
+
 struct ItemDesc {
-  int ai, pass, chunk, tile, lr, pad0, pad1, pad2;
+  int ai, pass, chunk, tile, lr, gp0, gp1, pad;
 };
 constexpr int kMaxStages = 8;
 
+// Warp roles: warps [0, kNW) consume (MMA over a K span of each item), warp
+// kNW is the epilogue warp (cross-warp reduction, low-rank terms, SwiGLU /
+// combine), warp kNW+1 produces (cp.async.bulk).  Consumers never block on the
+// epilogue: partials go through a kNRed-deep mbarrier ring.
 template <bool UP, int NT>
 __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   constexpr int NI = UP ? 2 : 1;
   constexpr int TPP = 8 * NT;  // tokens per pass
+  constexpr int kEpi = kNW, kProd = kNW + 1;
   extern __shared__ __align__(128) uint8_t smem[];
   const SmemMap SM = smem_map<NI, NT>(P);
   uint8_t* stages = smem;
   const int slot_bytes = P.stage_bytes + P.lr_slot;
   uint16_t* xs = reinterpret_cast<uint16_t*>(smem + SM.xs);
   float2* sums = reinterpret_cast<float2*>(smem + SM.sums);  // [g_local][TPP] (X, -128 X')
-  float* red = reinterpret_cast<float*>(smem + SM.red);      // [warp][NI][NT][16][8]
+  float* red = reinterpret_cast<float*>(smem + SM.red);      // [ring][warp][NI][NT][16][8]
   float* ts = reinterpret_cast<float*>(smem + SM.ts);        // [comp c][NI][maxr]
-  float* act_s = reinterpret_cast<float*>(smem + SM.act);    // [16][TPP]
+  float* act_s = reinterpret_cast<float*>(smem + SM.act);    // [TPP][16]
   float* lrs = reinterpret_cast<float*>(smem + SM.lrs);      // [NI][16][TPP(comp idx)]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM.bars);
   uint64_t* empty = full + P.nstage;
+  uint64_t* rfull = empty + P.nstage;
+  uint64_t* rempty = rfull + kNRed;
   __shared__ ItemDesc s_desc[kMaxStages];
   __shared__ int s_prefix[LRC_MAX_EXPERTS + 1];
   __shared__ int s_range[2];
-  __shared__ int s_comp_n[TPP], s_comp_tok[TPP], s_comp_of[TPP], s_ncomp;
   __shared__ int s_aoff[LRC_MAX_EXPERTS], s_acnt[LRC_MAX_EXPERTS], s_ae[LRC_MAX_EXPERTS];
   __shared__ const uint8_t* s_wsrc[LRC_MAX_EXPERTS];
   __shared__ const uint8_t* s_lsrc[LRC_MAX_EXPERTS];
   __shared__ int s_lbytes[LRC_MAX_EXPERTS];
-  __shared__ int s_ppair[TPP], s_ptok[TPP];
-  __shared__ float s_pw[TPP];
-  __shared__ int s_dirty;
-  __shared__ int s_r[3], s_ub[3], s_ugs[3], s_vb;
+  __shared__ int s_cpair[TPP], s_ctok[TPP];  // consumer-owned pass data
+  // epilogue-owned pass data
+  __shared__ int s_epair[TPP], s_etok[TPP], s_ecomp_of[TPP], s_ecomp_n[TPP], s_ecomp_tok[TPP];
+  __shared__ float s_ew[TPP];
+  __shared__ int s_encomp, s_r[3], s_ub[3], s_ugs[3], s_vb;
   __shared__ LrLayout s_L;
 
   const ExpertArgs& A = P.a;
@@ -360,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   // The up kernel consumes the router's plan: wait for it.  The down kernel's
   // plan is two launches old (complete before the up kernel passed its own
   // wait), so its producer may start streaming W2 while the up kernel drains;
-  // its consumers wait before touching the up kernel's activations.
+  // its consumers / epilogue wait before touching the up kernel's outputs.
   if (UP) griddep_wait();
   griddep_launch_dependents();
   const int n_active = A.plan.counts[0];
@@ -377,7 +406,6 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    s_dirty = TPP;
     int acc = 0;
     for (int ai = 0; ai < n_active; ++ai) {
       s_prefix[ai] = acc;
@@ -389,15 +417,23 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     s_range[1] = static_cast<int>(total * (blockIdx.x + 1) / gridDim.x);
     for (int s = 0; s < P.nstage; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kNW);
+      mbar_init(&empty[s], kNW + 1);  // consumers + epilogue (LR slot)
+    }
+    for (int r = 0; r < kNRed; ++r) {
+      mbar_init(&rfull[r], kNW);
+      mbar_init(&rempty[r], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // the shared zero row read by MMA lanes whose token column is empty
+  for (int i = threadIdx.x; i < P.xs_stride / 2; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(xs + P.xs_rows * P.xs_stride)[i] = 0u;
   __syncthreads();
   const int beg = s_range[0], end = s_range[1];
   if (beg >= end) return;
+  const int nitems = end - beg;
 
-  if (warp == kNW) {
+  if (warp == kProd) {
     // ===================== producer: one elected lane streams work items ====
     if (lane == 0) {
       int c_ai = -1, c_pass = -1, c_comp = 0, ai = 0;
@@ -435,59 +471,50 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     return;
   }
 
-  // ============================ consumers ====================================
-  const int gid = lane >> 2, tid = lane & 3;
-  const int ctid = threadIdx.x;  // consumer thread id, 0 .. kNW*32-1
-  if (!UP) griddep_wait();
-  int cur_ai = -1, cur_pass = -1, cur_chunk = -1, pass_tok = 0, cur_e = -1;
-  const uint16_t* xlane = xs + gid * P.xs_stride + tid * 4;
-  const int nitems = end - beg;
-  for (int k = 0; k < nitems; ++k) {
-    const int s = k % P.nstage;
-    mbar_wait(&full[s], (k / P.nstage) & 1);  // acquire: descriptor + bytes visible
-    const ItemDesc dsc = s_desc[s];
-    const int gp0 = dsc.pad0, gp1 = dsc.pad1, tile = dsc.tile;
-    if (dsc.ai != cur_ai || dsc.pass != cur_pass || dsc.chunk != cur_chunk) {
-      // ---- (re)build the activation operand x' and the LR vectors for this group.
-      // All consumers passed the previous item's final barrier, so xs/sums/ts are free.
-      const bool new_pass = (dsc.ai != cur_ai || dsc.pass != cur_pass);
-      const int off = s_aoff[dsc.ai], cnt = s_acnt[dsc.ai];
-      cur_ai = dsc.ai;
-      cur_pass = dsc.pass;
-      cur_chunk = dsc.chunk;
-      cur_e = s_ae[dsc.ai];
-      pass_tok = min(TPP, cnt - cur_pass * TPP);
-      if (new_pass) {
-        if (ctid < TPP) {  // per-token pass data into shared memory
-          const int n = ctid;
+  if (warp == kEpi) {
+    // ================== epilogue warp: reduce, low-rank terms, SwiGLU/combine ===
+    if (!UP) griddep_wait();  // t2 comes from the up kernel
+    int cur_ai = -1, cur_pass = -1, pass_tok = 0, cur_e = -1;
+    for (int k = 0; k < nitems; ++k) {
+      const int s = k % P.nstage, rs = k % kNRed;
+      mbar_wait(&rfull[rs], (k / kNRed) & 1);
+      const ItemDesc dsc = s_desc[s];
+      const uint8_t* st = stages + static_cast<size_t>(s) * slot_bytes;
+      if (dsc.ai != cur_ai || dsc.pass != cur_pass) {
+        cur_ai = dsc.ai;
+        cur_pass = dsc.pass;
+        cur_e = s_ae[dsc.ai];
+        pass_tok = min(TPP, s_acnt[dsc.ai] - cur_pass * TPP);
+        const int off = s_aoff[dsc.ai];
+        if (lane < TPP) {
           int p = -1, tok = 0, cmp = 0;
           float w = 0.0f;
-          if (n < pass_tok) {
-            p = A.plan.pair_list[off + cur_pass * TPP + n];
+          if (lane < pass_tok) {
+            p = A.plan.pair_list[off + cur_pass * TPP + lane];
             tok = A.plan.pair_token[p];
             w = A.plan.pair_w[p];
             cmp = A.plan.pair_comp[p] >= 0;
           }
-          s_ppair[n] = p;
-          s_ptok[n] = tok;
-          s_pw[n] = w;
-          s_comp_of[n] = cmp;
+          s_epair[lane] = p;
+          s_etok[lane] = tok;
+          s_ew[lane] = w;
+          s_ecomp_of[lane] = cmp;
         }
-        consumer_sync();
-        if (ctid == 0) {
+        __syncwarp();
+        if (lane == 0) {
           const lrc_expert& E = A.experts[cur_e];
           int nc = 0;
           for (int n = 0; n < TPP; ++n) {
-            if (s_comp_of[n]) {
-              s_comp_of[n] = nc;
-              s_comp_n[nc] = n;
-              s_comp_tok[nc] = s_ptok[n];
+            if (s_ecomp_of[n]) {
+              s_ecomp_of[n] = nc;
+              s_ecomp_n[nc] = n;
+              s_ecomp_tok[nc] = s_etok[n];
               ++nc;
             } else {
-              s_comp_of[n] = -1;
+              s_ecomp_of[n] = -1;
             }
           }
-          s_ncomp = nc;
+          s_encomp = nc;
           s_L = lr_layout(E);
           const lrc_qmat* us[3] = {&E.u1, &E.u3, &E.u2};
           for (int i = 0; i < 3; ++i) {
@@ -497,17 +524,141 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
           }
           s_vb = E.v2.bits;
         }
+        __syncwarp();
+        if (maxr > 0) {  // low-rank input vectors (t1/t3 up, t2 down) of the comp tokens
+          const int ntask = s_encomp * NI * maxr;
+          for (int task = lane; task < ntask; task += 32) {
+            const int j = task % maxr, ci = task / maxr;
+            const int i = ci % NI, c = ci / NI;
+            const int proj = UP ? i : 2;
+            ts[task] = __ldcg(A.t + ((static_cast<int64_t>(s_ecomp_tok[c]) * A.ne + cur_e) * 3 + proj) * maxr + j);
+          }
+        }
+        __syncwarp();
+      }
+      const int nw = min((dsc.gp1 - dsc.gp0 + kSpanGP - 1) / kSpanGP, kNW);
+      const float* rb = red + static_cast<size_t>(rs) * kNW * NI * NT * 128;
+      const int rr = lane & 15, il = lane >> 4;  // lane -> (matrix, row)
+      const bool lane_on = il < NI;
+      // ---- E1: low-rank up-projection U.t for this tile's rows (ref/lowrank.py:165)
+      if (dsc.lr && lane_on) {
+        const int pi = UP ? il : 2;
+        const int r = s_r[pi];
+        const uint8_t* lr = st + P.stage_bytes;
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(lr + (UP ? (il ? s_L.u3c : s_L.u1c) : s_L.u2c));
+        const uint8_t* meta = lr + (UP ? (il ? s_L.u3m : s_L.u1m) : s_L.u2m);
+        const int bits = s_ub[pi], gsu = s_ugs[pi];
+        const uint32_t mask = (1u << bits) - 1u;
+        const int gpu = (r + gsu - 1) / gsu;
+        for (int c = 0; c < s_encomp; ++c) {
+          const float* tv = ts + (c * NI + il) * maxr;
+          float v = 0.0f;
+          for (int g = 0; g < gpu; ++g) {
+            const float2 f = h2f2(*reinterpret_cast<const uint32_t*>(meta + (rr * gpu + g) * 4));
+            float cx = 0.0f, sx = 0.0f;
+            const int j1 = min(r, (g + 1) * gsu);
+#pragma unroll 8
+            for (int j = g * gsu; j < j1; ++j) {
+              cx = fmaf(code_f(smem_code(cw, (rr * r + j) * bits, mask)), tv[j], cx);
+              sx += tv[j];
+            }
+            v = fmaf(f.x, cx, fmaf(f.y, sx, v));
+          }
+          lrs[(il * 16 + rr) * TPP + c] = v;
+        }
+      }
+      __syncwarp();
+      // ---- E2: reduce the consumer partials per (matrix, row, token) and finish
+      for (int n = 0; n < pass_tok; ++n) {
+        const int nt = n >> 3, col = n & 7;
+        float v = 0.0f;
+        if (lane_on) {
+          for (int w = 0; w < nw; ++w) v += rb[((w * NI + il) * NT + nt) * 128 + rr * 8 + col];
+          const int c = s_ecomp_of[n];
+          if (dsc.lr && c >= 0) v += lrs[(il * 16 + rr) * TPP + c];
+        }
+        const int row = dsc.tile * 16 + rr;
+        if (UP) {
+          const float h3 = __shfl_down_sync(0xffffffffu, v, 16);
+          if (lane < 16) {
+            const float act = (row < P.M) ? silu_f(v) * h3 : 0.0f;
+            act_s[n * 16 + rr] = act;
+            if (row < P.M) A.a16[static_cast<int64_t>(s_epair[n]) * A.ffn + row] = f2bf(act);
+          }
+        } else if (lane < 16 && row < P.M) {
+          atomicAdd(&A.y[static_cast<int64_t>(s_etok[n]) * A.hidden + row], s_ew[n] * v);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rempty[rs]);  // partial slot free for the consumers
+      // ---- E3 (up): partial t2 = V2[:, tile rows] . act for the comp tokens
+      if (UP && dsc.lr && s_r[2] > 0) {
+        const int r2 = s_r[2], vb = s_vb;
+        const uint32_t vmask = (1u << vb) - 1u;
+        const uint8_t* lr = st + P.stage_bytes;
+        const uint32_t* vw = reinterpret_cast<const uint32_t*>(lr + s_L.v2c);
+        for (int j = lane; j < r2; j += 32) {
+          const float2 f = h2f2(*reinterpret_cast<const uint32_t*>(lr + s_L.v2m + j * 4));
+          for (int c = 0; c < s_encomp; ++c) {
+            const float* an = act_s + s_ecomp_n[c] * 16;
+            float cx = 0.0f, sx = 0.0f;
+#pragma unroll
+            for (int rl = 0; rl < 16; ++rl) {  // V2^T tile is j-major: code (j, rl) at j*16 + rl
+              cx = fmaf(code_f(smem_code(vw, (j * 16 + rl) * vb, vmask)), an[rl], cx);
+              sx += an[rl];
+            }
+            atomicAdd(&A.t[((static_cast<int64_t>(s_ecomp_tok[c]) * A.ne + cur_e) * 3 + 2) * maxr + j],
+                      fmaf(f.x, cx, f.y * sx));
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // LR slot read: stage may be refilled
+    }
+    return;
+  }
+
+  // ============================ consumers ====================================
+  const int gid = lane >> 2, tid = lane & 3;
+  const int ctid = threadIdx.x;  // consumer thread id, 0 .. kNW*32-1
+  if (!UP) griddep_wait();  // a16 comes from the up kernel
+  int cur_ai = -1, cur_pass = -1, cur_chunk = -1, pass_tok = 0;
+  for (int k = 0; k < nitems; ++k) {
+    const int s = k % P.nstage;
+    mbar_wait(&full[s], (k / P.nstage) & 1);  // acquire: descriptor + bytes visible
+    const ItemDesc dsc = s_desc[s];
+    const int gp0 = dsc.gp0, gp1 = dsc.gp1;
+    if (dsc.ai != cur_ai || dsc.pass != cur_pass || dsc.chunk != cur_chunk) {
+      // ---- (re)build the activation operand x' (consumers only)
+      consumer_sync();  // every consumer is past the previous item's MMA
+      const bool new_pass = (dsc.ai != cur_ai || dsc.pass != cur_pass);
+      cur_ai = dsc.ai;
+      cur_pass = dsc.pass;
+      cur_chunk = dsc.chunk;
+      pass_tok = min(TPP, s_acnt[dsc.ai] - cur_pass * TPP);
+      if (new_pass) {
+        if (ctid < TPP) {
+          int p = -1, tok = 0;
+          if (ctid < pass_tok) {
+            p = A.plan.pair_list[s_aoff[dsc.ai] + cur_pass * TPP + ctid];
+            tok = A.plan.pair_token[p];
+          }
+          s_cpair[ctid] = p;
+          s_ctok[ctid] = tok;
+        }
+        consumer_sync();
       }
       const int k0 = gp0 * 128;
       const int ng = (gp1 - gp0) * 2;
-      const int nrows = max(pass_tok, s_dirty);  // rows beyond pass_tok only if dirty
-      for (int task = ctid; task < nrows * ng; task += kNW * 32) {
+      // only real token rows are built; empty columns read the shared zero row
+      // (their sums are never used: MMA columns are independent)
+      for (int task = ctid; task < pass_tok * ng; task += kNW * 32) {
         const int n = task / ng, g = task - n * ng;
         float xsum = 0.f, xpsum = 0.f;
         uint32_t* dst = reinterpret_cast<uint32_t*>(xs + n * P.xs_stride + g * 64);
-        if (n < pass_tok) {
-          const uint16_t* row = UP ? A.x + static_cast<int64_t>(s_ptok[n]) * A.hidden
-                                   : A.a16 + static_cast<int64_t>(s_ppair[n]) * A.ffn;
+        {
+          const uint16_t* row = UP ? A.x + static_cast<int64_t>(s_ctok[n]) * A.hidden
+                                   : A.a16 + static_cast<int64_t>(s_cpair[n]) * A.ffn;
           const int kk = k0 + g * 64;
           const bool vec = (kk + 64 <= P.K) && ((reinterpret_cast<uintptr_t>(row + kk) & 15) == 0);
 #pragma unroll 2
@@ -535,23 +686,8 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
                   static_cast<uint32_t>(f2bf(plo)) | (static_cast<uint32_t>(f2bf(phi)) << 16);
             }
           }
-        } else {
-#pragma unroll 8
-          for (int w = 0; w < 32; ++w) dst[w] = 0u;
         }
         sums[g * TPP + n] = make_float2(xsum, -128.0f * xpsum);
-      }
-      consumer_sync();
-      if (ctid == 0) s_dirty = pass_tok;
-      // low-rank input vectors of the compensated tokens (t1/t3 up, t2 down)
-      if (maxr > 0) {
-        const int ntask = s_ncomp * NI * maxr;
-        for (int task = ctid; task < ntask; task += kNW * 32) {
-          const int j = task % maxr, ci = task / maxr;
-          const int i = ci % NI, c = ci / NI;
-          const int proj = UP ? i : 2;
-          ts[task] = __ldcg(A.t + ((static_cast<int64_t>(s_comp_tok[c]) * A.ne + cur_e) * 3 + proj) * maxr + j);
-        }
       }
       consumer_sync();
     }
@@ -568,7 +704,14 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
 
     const int ngp = gp1 - gp0;
     const int nspan = (ngp + kSpanGP - 1) / kSpanGP;
-    for (int sp = warp; sp < nspan; sp += kNW) {
+    // B-fragment row of this lane per N-tile: token column nt*8+gid, or the zero row
+    const uint16_t* xrow[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int n = nt * 8 + gid;
+      xrow[nt] = xs + (n < pass_tok ? n : P.xs_rows) * P.xs_stride + tid * 4;
+    }
+    for (int sp = warp; sp < ((P.debug & 1) ? 0 : nspan); sp += kNW) {
       const int q0 = sp * kSpanGP, q1 = min(ngp, q0 + kSpanGP);
 #pragma unroll 2
       for (int q = q0; q < q1; ++q) {
@@ -596,7 +739,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
               d[i][nt][3] = xx[nt].w;
             }
           }
-          // shared shifts of the two code words per matrix (j>=3 slots)
+          // the two code words per matrix and their shifted copies (j >= 3 slots)
           uint32_t wa[NI][3], wb[NI][3];
 #pragma unroll
           for (int i = 0; i < NI; ++i) {
@@ -607,24 +750,22 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
             wa[i][2] = wa[i][0] >> 12;
             wb[i][2] = wb[i][0] >> 12;
           }
-          const uint16_t* xg = xlane + gl * 64;
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             uint32_t b0[NT], b1[NT];
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
-              const uint2 bv = *reinterpret_cast<const uint2*>(xg + nt * 8 * P.xs_stride + ks * 16);
+              const uint2 bv = *reinterpret_cast<const uint2*>(xrow[nt] + gl * 64 + ks * 16);
               b0[nt] = bv.x;
               b1[nt] = bv.y;
             }
             // slot j = 2ks (regs a0/a1) and 2ks+1 (a2/a3): word (j/3 shift), mask 3 << 2*(j%3)
-            constexpr uint32_t M = 0x43004300u;
             const int j0 = 2 * ks, j1 = 2 * ks + 1;
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
               const uint32_t m0 = 0x00030003u << (2 * (j0 % 3)), m1 = 0x00030003u << (2 * (j1 % 3));
-              const uint32_t a0 = (wa[i][j0 / 3] & m0) | M, a1 = (wb[i][j0 / 3] & m0) | M;
-              const uint32_t a2 = (wa[i][j1 / 3] & m1) | M, a3 = (wb[i][j1 / 3] & m1) | M;
+              const uint32_t a0 = lop_and_or(wa[i][j0 / 3], m0), a1 = lop_and_or(wb[i][j0 / 3], m0);
+              const uint32_t a2 = lop_and_or(wa[i][j1 / 3], m1), a3 = lop_and_or(wb[i][j1 / 3], m1);
 #pragma unroll
               for (int nt = 0; nt < NT; ++nt) mma_bf16(d[i][nt], a0, a1, a2, a3, b0[nt], b1[nt]);
             }
@@ -644,113 +785,24 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
         }
       }
     }
-    if (!dsc.lr) {  // weights consumed: hand the stage back right away
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-    // ---- per-warp partials (no shared atomics)
-    const int nw = min(nspan, kNW);
-    if (warp < nw) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // weights consumed
+    // ---- partials to the epilogue ring (slot reused every kNRed items)
+    const int rs = k % kNRed;
+    mbar_wait(&rempty[rs], ((k / kNRed) & 1) ^ 1);
+    if (warp < nspan) {
+      float* rb = red + (static_cast<size_t>(rs) * kNW + warp) * NI * NT * 128;
 #pragma unroll
       for (int i = 0; i < NI; ++i)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          float* rb = red + ((warp * NI + i) * NT + nt) * 128;
-          *reinterpret_cast<float2*>(rb + gid * 8 + 2 * tid) = make_float2(acc[i][nt][0], acc[i][nt][1]);
-          *reinterpret_cast<float2*>(rb + (gid + 8) * 8 + 2 * tid) = make_float2(acc[i][nt][2], acc[i][nt][3]);
+          float* q = rb + (i * NT + nt) * 128;
+          *reinterpret_cast<float2*>(q + gid * 8 + 2 * tid) = make_float2(acc[i][nt][0], acc[i][nt][1]);
+          *reinterpret_cast<float2*>(q + (gid + 8) * 8 + 2 * tid) = make_float2(acc[i][nt][2], acc[i][nt][3]);
         }
     }
-    consumer_sync();  // (A) partials complete
-
-    // ---- E1 (one warp): low-rank up-projection U.t for the tile rows
-    // (ref/lowrank.py:165), factor rows from the stage's LR slot.  Lane =
-    // (matrix i, row rr); loops over the compensated tokens of the pass.
-    if (dsc.lr) {
-      if (warp == 0 && lane < NI * 16) {
-        const uint8_t* lr = st + P.stage_bytes;
-        const int rr = lane & 15, i = lane >> 4;
-        const int pi = UP ? i : 2;
-        const int r = s_r[pi];
-        for (int c = 0; c < s_ncomp; ++c) {
-          float v = 0.0f;
-          if (r > 0) {
-            const uint8_t* codes = lr + (UP ? (i ? s_L.u3c : s_L.u1c) : s_L.u2c);
-            const uint8_t* meta = lr + (UP ? (i ? s_L.u3m : s_L.u1m) : s_L.u2m);
-            const int gsu = s_ugs[pi], bits = s_ub[pi];
-            const int gpu = (r + gsu - 1) / gsu;
-            const float* tv = ts + (c * NI + i) * maxr;
-            for (int g = 0; g < gpu; ++g) {
-              const uint32_t sz = *reinterpret_cast<const uint32_t*>(meta + (rr * gpu + g) * 4);
-              const float2 f = h2f2(sz);
-              float cx = 0.0f, sx = 0.0f;
-              const int j1 = min(r, (g + 1) * gsu);
-              for (int j = g * gsu; j < j1; ++j) {
-                cx = fmaf(static_cast<float>(read_code(codes, rr * r + j, bits, 1 << 30)), tv[j], cx);
-                sx += tv[j];
-              }
-              v = fmaf(f.x, cx, fmaf(f.y, sx, v));
-            }
-          }
-          lrs[(i * 16 + rr) * TPP + c] = v;
-        }
-      }
-      consumer_sync();  // (B) LR terms ready
-    }
-
-    // ---- E2: thread -> (row r, token n): reduce the warp partials, epilogue
-    for (int o = ctid; o < 16 * TPP; o += kNW * 32) {
-      const int r = o & 15, n = o >> 4;
-      const int nt = n >> 3, col = n & 7;
-      const int row = tile * 16 + r;
-      float v0 = 0.0f, v1 = 0.0f;
-      for (int w = 0; w < nw; ++w) {
-        v0 += red[((w * NI + 0) * NT + nt) * 128 + r * 8 + col];
-        if (UP) v1 += red[((w * NI + NI - 1) * NT + nt) * 128 + r * 8 + col];
-      }
-      const int c = s_comp_of[n];
-      if (dsc.lr && c >= 0) {
-        v0 += lrs[(0 * 16 + r) * TPP + c];
-        if (UP) v1 += lrs[((NI - 1) * 16 + r) * TPP + c];
-      }
-      const bool valid = (n < pass_tok) && (row < P.M);
-      if (UP) {
-        float act = 0.0f;
-        if (valid) {
-          act = silu_f(v0) * v1;
-          A.a16[static_cast<int64_t>(s_ppair[n]) * A.ffn + row] = f2bf(act);
-        }
-        act_s[r * TPP + n] = act;
-      } else if (valid) {
-        atomicAdd(&A.y[static_cast<int64_t>(s_ptok[n]) * A.hidden + row], s_pw[n] * v0);
-      }
-    }
-    consumer_sync();  // (C) red / lrs / act_s consumed
-
-    // ---- E3 (up, one warp, overlaps the next item): partial t2 = V2[:, tile
-    // rows] . act for the compensated tokens; lane = rank index j.
-    if (UP && dsc.lr && warp == kNW - 1 && s_r[2] > 0) {
-      const uint8_t* lr = st + P.stage_bytes;
-      const int r2 = s_r[2], vb = s_vb;
-      for (int j = lane; j < r2; j += 32) {
-        const float2 f = h2f2(*reinterpret_cast<const uint32_t*>(lr + s_L.v2m + j * 4));
-        for (int c = 0; c < s_ncomp; ++c) {
-          const int n = s_comp_n[c];
-          float cx = 0.0f, sx = 0.0f;
-#pragma unroll 4
-          for (int rl = 0; rl < 16; ++rl) {
-            const float a = act_s[rl * TPP + n];
-            cx = fmaf(static_cast<float>(read_code(lr + s_L.v2c, rl * r2 + j, vb, 1 << 30)), a, cx);
-            sx += a;
-          }
-          atomicAdd(&A.t[((static_cast<int64_t>(s_comp_tok[c]) * A.ne + cur_e) * 3 + 2) * maxr + j],
-                    fmaf(f.x, cx, f.y * sx));
-        }
-      }
-    }
-    if (dsc.lr) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&rfull[rs]);
   }
 }
 
@@ -807,8 +859,10 @@ static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, in
   P.xs_stride = P.SPC * kSpanGP * 128 + 16;
   P.stage_bytes = P.SPC * kSpanGP * NI * kBlk;
   P.lr_slot = lr_max;
+  P.debug = getenv("LRC_TILED_DEBUG") ? atoi(getenv("LRC_TILED_DEBUG")) : 0;
   const int budget = 227 * 1024 - 12 * 1024;  // static shared (~10 KB) + slack
   auto fits = [&](int nt) {
+    P.xs_rows = min(8 * nt, max(max_tok, 1));  // x' rows actually needed
     return (nt == 1 ? smem_map<NI, 1>(P).total : smem_map<NI, 2>(P).total) <= budget;
   };
   int nt = 1;
@@ -822,6 +876,7 @@ static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, in
       if (fits(1)) break;
     if (P.nstage < 2) return fail(LRC_ERR_UNSUPPORTED, "tiled kernel: K too large for smem");
   }
+  fits(nt);  // final x' row count for the chosen N-tiling
   return (nt == 1) ? launch_one<UP, 1>(P, num_sms, st, pdl) : launch_one<UP, 2>(P, num_sms, st, pdl);
 }
 
