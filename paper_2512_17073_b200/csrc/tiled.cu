@@ -229,12 +229,13 @@ __global__ void build_lr_up_kernel(lrc_expert e, LrLayout L, uint8_t* __restrict
     fill_u_meta(base + L.u3m, e.u3, row0);
   }
   if (factor_present(e.v2)) {
-    // V2^T rows: element (rr, j) = V2[j, row0 + rr]; group of the tile along ffn
+    // V2^T tile, j-major: element (j, rr) = V2[j, row0 + rr] at index j*16 + rr
+    // (one lane per rank index j reads 16 consecutive codes); group along ffn
     const lrc_qmat& v = e.v2;
     const int r2 = v.rows;
     const int64_t nb = (static_cast<int64_t>(v.rows) * v.cols * v.bits + 7) >> 3;
     fill_stream(base + L.v2c, (16 * r2 * v.bits + 7) / 8, v.bits, 16 * r2, [&](int idx) -> uint32_t {
-      const int rr = idx / r2, j = idx - rr * r2;
+      const int j = idx / 16, rr = idx - j * 16;
       const int64_t f = row0 + rr;
       return f < v.cols ? read_code(v.packed, static_cast<int64_t>(j) * v.cols + f, v.bits, nb) : 0u;
     });
@@ -280,7 +281,7 @@ struct TiledParams {
   int nstage;
   int xs_stride;        // bf16 elements per x' row
   int xs_rows;          // x' rows held in shared memory (<= 8*NT)
-  int debug;            // LRC_TILED_DEBUG: bit0 skip MMA core
+  int debug;            // LRC_TILED_DEBUG: bit0 skip MMA core, bit1 skip epilogue math
 };
 
 constexpr int kNRed = 2;  // partial-sum ring depth (consumers -> epilogue warp)
@@ -541,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       const int rr = lane & 15, il = lane >> 4;  // lane -> (matrix, row)
       const bool lane_on = il < NI;
       // ---- E1: low-rank up-projection U.t for this tile's rows (ref/lowrank.py:165)
-      if (dsc.lr && lane_on) {
+      if (dsc.lr && lane_on && !(P.debug & 2)) {
         const int pi = UP ? il : 2;
         const int r = s_r[pi];
         const uint8_t* lr = st + P.stage_bytes;
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       }
       __syncwarp();
       // ---- E2: reduce the consumer partials per (matrix, row, token) and finish
-      for (int n = 0; n < pass_tok; ++n) {
+      for (int n = 0; n < ((P.debug & 2) ? 0 : pass_tok); ++n) {
         const int nt = n >> 3, col = n & 7;
         float v = 0.0f;
         if (lane_on) {
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&rempty[rs]);  // partial slot free for the consumers
       // ---- E3 (up): partial t2 = V2[:, tile rows] . act for the comp tokens
-      if (UP && dsc.lr && s_r[2] > 0) {
+      if (UP && dsc.lr && s_r[2] > 0 && !(P.debug & 2)) {
         const int r2 = s_r[2], vb = s_vb;
         const uint32_t vmask = (1u << vb) - 1u;
         const uint8_t* lr = st + P.stage_bytes;
