@@ -142,8 +142,10 @@ __host__ __device__ inline bool factor_present(const lrc_qmat& m) {
 }
 __host__ __device__ inline LrLayout lr_layout(const lrc_expert& e) {
   LrLayout L{};
+  // codes are re-laid out as 4-bit nibbles (factor bits <= 4): word-aligned
+  // rows, shift-only decode in the epilogue warp
   auto codes = [](const lrc_qmat& m, int r) {
-    return factor_present(m) ? pad16((16 * r * m.bits + 7) / 8) : 0;
+    return factor_present(m) ? pad16((16 * r * 4 + 7) / 8) : 0;
   };
   auto umeta = [](const lrc_qmat& u) {
     return factor_present(u) ? pad16(16 * ((u.cols + u.group_size - 1) / u.group_size) * 4) : 0;

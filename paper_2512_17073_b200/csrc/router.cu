@@ -86,6 +86,59 @@ __device__ void select_topk(double* lg, int E, int k, int renorm, int64_t b, dou
   for (int j = 0; j < k; ++j) topk_w[b * k + j] = static_cast<float>(mix[j]);
 }
 
+// Warp-parallel variant (one warp per token): exp and the top-k argmax run
+// across lanes; the softmax denominator keeps numpy's pairwise order (lane 0)
+// so weights stay bit-identical to select_topk.
+__device__ void select_topk_warp(double* lg, int E, int k, int renorm, int64_t b, double* probs,
+                                 int32_t* topk_idx, float* topk_w) {
+  const int lane = threadIdx.x & 31;
+  double mx = -DBL_MAX;
+  for (int e = lane; e < E; e += 32) mx = fmax(mx, lg[e]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  for (int e = lane; e < E; e += 32) lg[e] = exp(__dsub_rn(lg[e], mx));
+  __syncwarp();
+  double den = 0.0;
+  if (lane == 0) den = pw_sum_small(lg, E);
+  den = __shfl_sync(0xffffffffu, den, 0);
+  for (int e = lane; e < E; e += 32) {
+    lg[e] = __ddiv_rn(lg[e], den);
+    if (probs) probs[b * E + e] = lg[e];
+  }
+  __syncwarp();
+  uint32_t taken = 0;  // bit m: element lane + 32m already selected
+  double mix[64];
+  for (int j = 0; j < k; ++j) {
+    double bv = -DBL_MAX;
+    int be = 0x7fffffff;
+    for (int m = 0, e = lane; e < E; ++m, e += 32)
+      if (!((taken >> m) & 1u) && (lg[e] > bv || be == 0x7fffffff)) {
+        bv = lg[e];
+        be = e;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      if (oe != 0x7fffffff && (be == 0x7fffffff || ov > bv || (ov == bv && oe < be))) {
+        bv = ov;
+        be = oe;
+      }
+    }
+    if ((be & 31) == lane) taken |= 1u << (be >> 5);
+    mix[j] = bv;
+    if (lane == 0) topk_idx[b * k + j] = be;
+  }
+  if (lane == 0) {
+    if (renorm) {  // ref/moe.py:234-236, mix.sum() in numpy order
+      const double s = pw_sum_small(mix, k);
+      if (s > 0.0)
+        for (int j = 0; j < k; ++j) mix[j] = __ddiv_rn(mix[j], s);
+    }
+    for (int j = 0; j < k; ++j) topk_w[b * k + j] = static_cast<float>(mix[j]);
+  }
+}
+
 __device__ __forceinline__ void griddep_launch_dependents_r() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
@@ -203,9 +256,9 @@ __global__ void __launch_bounds__(kRThreads) gate_kernel(RouteArgs ra) {
   for (int i = threadIdx.x; i < nb * ra.E; i += kRThreads)
     sm_lg[i] = __ldcg(ra.logits + b0 * ra.E + i);
   __syncthreads();
-  if (threadIdx.x < nb)
-    select_topk(sm_lg + threadIdx.x * ra.E, ra.E, ra.k, ra.renorm, b0 + threadIdx.x, ra.probs,
-                ra.topk_idx, ra.topk_w);
+  if (warp < nb)
+    select_topk_warp(sm_lg + warp * ra.E, ra.E, ra.k, ra.renorm, b0 + warp, ra.probs, ra.topk_idx,
+                     ra.topk_w);
   if (threadIdx.x == 0) ra.tile_ticket[tile] = 0;
   if (ra.plan.ticket == nullptr) return;
   // ---- last tile: build the pair plan for the whole batch

@@ -209,7 +209,7 @@ __device__ void fill_u_meta(uint8_t* dst, const lrc_qmat& u, int64_t row0) {
 __device__ void fill_u_codes(uint8_t* dst, const lrc_qmat& u, int64_t row0) {
   const int r = u.cols;
   const int64_t nb = (static_cast<int64_t>(u.rows) * r * u.bits + 7) >> 3;
-  fill_stream(dst, (16 * r * u.bits + 7) / 8, u.bits, 16 * r, [&](int idx) -> uint32_t {
+  fill_stream(dst, (16 * r * 4 + 7) / 8, 4, 16 * r, [&](int idx) -> uint32_t {
     const int rr = idx / r, j = idx - rr * r;
     const int64_t R = row0 + rr;
     return R < u.rows ? read_code(u.packed, R * r + j, u.bits, nb) : 0u;
@@ -234,7 +234,7 @@ __global__ void build_lr_up_kernel(lrc_expert e, LrLayout L, uint8_t* __restrict
     const lrc_qmat& v = e.v2;
     const int r2 = v.rows;
     const int64_t nb = (static_cast<int64_t>(v.rows) * v.cols * v.bits + 7) >> 3;
-    fill_stream(base + L.v2c, (16 * r2 * v.bits + 7) / 8, v.bits, 16 * r2, [&](int idx) -> uint32_t {
+    fill_stream(base + L.v2c, (16 * r2 * 4 + 7) / 8, 4, 16 * r2, [&](int idx) -> uint32_t {
       const int j = idx / 16, rr = idx - j * 16;
       const int64_t f = row0 + rr;
       return f < v.cols ? read_code(v.packed, static_cast<int64_t>(j) * v.cols + f, v.bits, nb) : 0u;
@@ -340,6 +340,19 @@ __device__ __forceinline__ uint32_t lop_and_or(uint32_t w, uint32_t m) {
   uint32_t r;
   asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "r"(m), "r"(0x43004300u));
   return r;
+}
+
+// (w & m) | c in one lop3
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t w, uint32_t m, uint32_t c) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "r"(m), "r"(c));
+  return r;
+}
+// nibble Q of w as the float 1 + c/16 (no int->float conversion): c*t = 16*(v*t - t)
+template <int Q>
+__device__ __forceinline__ float nib_f(uint32_t w) {
+  const uint32_t sh = (4 * Q <= 19) ? (w << (19 - 4 * Q)) : (w >> (4 * Q - 19));
+  return __uint_as_float(lop3_and_or(sh, 0x00780000u, 0x3F800000u));
 }
 
 struct ItemDesc {
@@ -548,20 +561,38 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
         const uint8_t* lr = st + P.stage_bytes;
         const uint32_t* cw = reinterpret_cast<const uint32_t*>(lr + (UP ? (il ? s_L.u3c : s_L.u1c) : s_L.u2c));
         const uint8_t* meta = lr + (UP ? (il ? s_L.u3m : s_L.u1m) : s_L.u2m);
-        const int bits = s_ub[pi], gsu = s_ugs[pi];
-        const uint32_t mask = (1u << bits) - 1u;
+        const int gsu = s_ugs[pi];  // LR tile codes are 4-bit nibbles
         const int gpu = (r + gsu - 1) / gsu;
+        const bool fast = (r % 8) == 0 && (gsu % 8) == 0;
         for (int c = 0; c < s_encomp; ++c) {
           const float* tv = ts + (c * NI + il) * maxr;
           float v = 0.0f;
           for (int g = 0; g < gpu; ++g) {
             const float2 f = h2f2(*reinterpret_cast<const uint32_t*>(meta + (rr * gpu + g) * 4));
             float cx = 0.0f, sx = 0.0f;
-            const int j1 = min(r, (g + 1) * gsu);
-#pragma unroll 8
-            for (int j = g * gsu; j < j1; ++j) {
-              cx = fmaf(code_f(smem_code(cw, (rr * r + j) * bits, mask)), tv[j], cx);
-              sx += tv[j];
+            const int j0 = g * gsu, j1 = min(r, (g + 1) * gsu);
+            if (fast) {
+              float vx = 0.0f;
+              for (int j = j0; j < j1; j += 8) {
+                const uint32_t w = cw[(rr * r + j) >> 3];
+                const float4 t0 = *reinterpret_cast<const float4*>(tv + j);
+                const float4 t1 = *reinterpret_cast<const float4*>(tv + j + 4);
+                vx = fmaf(nib_f<0>(w), t0.x, vx);
+                vx = fmaf(nib_f<1>(w), t0.y, vx);
+                vx = fmaf(nib_f<2>(w), t0.z, vx);
+                vx = fmaf(nib_f<3>(w), t0.w, vx);
+                vx = fmaf(nib_f<4>(w), t1.x, vx);
+                vx = fmaf(nib_f<5>(w), t1.y, vx);
+                vx = fmaf(nib_f<6>(w), t1.z, vx);
+                vx = fmaf(nib_f<7>(w), t1.w, vx);
+                sx += (t0.x + t0.y) + (t0.z + t0.w) + (t1.x + t1.y) + (t1.z + t1.w);
+              }
+              cx = 16.0f * (vx - sx);
+            } else {
+              for (int j = j0; j < j1; ++j) {
+                cx = fmaf(code_f(smem_code(cw, (rr * r + j) * 4, 0xFu)), tv[j], cx);
+                sx += tv[j];
+              }
             }
             v = fmaf(f.x, cx, fmaf(f.y, sx, v));
           }
@@ -594,20 +625,35 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       if (lane == 0) mbar_arrive(&rempty[rs]);  // partial slot free for the consumers
       // ---- E3 (up): partial t2 = V2[:, tile rows] . act for the comp tokens
       if (UP && dsc.lr && s_r[2] > 0 && !(P.debug & 2)) {
-        const int r2 = s_r[2], vb = s_vb;
-        const uint32_t vmask = (1u << vb) - 1u;
+        const int r2 = s_r[2];
         const uint8_t* lr = st + P.stage_bytes;
         const uint32_t* vw = reinterpret_cast<const uint32_t*>(lr + s_L.v2c);
         for (int j = lane; j < r2; j += 32) {
           const float2 f = h2f2(*reinterpret_cast<const uint32_t*>(lr + s_L.v2m + j * 4));
+          // V2^T tile is j-major nibbles: codes (j, rl), rl = 0..15, in words 2j, 2j+1
+          const uint32_t w0 = vw[2 * j], w1 = vw[2 * j + 1];
           for (int c = 0; c < s_encomp; ++c) {
-            const float* an = act_s + s_ecomp_n[c] * 16;
-            float cx = 0.0f, sx = 0.0f;
-#pragma unroll
-            for (int rl = 0; rl < 16; ++rl) {  // V2^T tile is j-major: code (j, rl) at j*16 + rl
-              cx = fmaf(code_f(smem_code(vw, (j * 16 + rl) * vb, vmask)), an[rl], cx);
-              sx += an[rl];
-            }
+            const float4* an = reinterpret_cast<const float4*>(act_s + s_ecomp_n[c] * 16);
+            const float4 a0 = an[0], a1 = an[1], a2 = an[2], a3 = an[3];
+            float vx = nib_f<0>(w0) * a0.x;
+            vx = fmaf(nib_f<1>(w0), a0.y, vx);
+            vx = fmaf(nib_f<2>(w0), a0.z, vx);
+            vx = fmaf(nib_f<3>(w0), a0.w, vx);
+            vx = fmaf(nib_f<4>(w0), a1.x, vx);
+            vx = fmaf(nib_f<5>(w0), a1.y, vx);
+            vx = fmaf(nib_f<6>(w0), a1.z, vx);
+            vx = fmaf(nib_f<7>(w0), a1.w, vx);
+            vx = fmaf(nib_f<0>(w1), a2.x, vx);
+            vx = fmaf(nib_f<1>(w1), a2.y, vx);
+            vx = fmaf(nib_f<2>(w1), a2.z, vx);
+            vx = fmaf(nib_f<3>(w1), a2.w, vx);
+            vx = fmaf(nib_f<4>(w1), a3.x, vx);
+            vx = fmaf(nib_f<5>(w1), a3.y, vx);
+            vx = fmaf(nib_f<6>(w1), a3.z, vx);
+            vx = fmaf(nib_f<7>(w1), a3.w, vx);
+            const float sx = ((a0.x + a0.y) + (a0.z + a0.w)) + ((a1.x + a1.y) + (a1.z + a1.w)) +
+                             ((a2.x + a2.y) + (a2.z + a2.w)) + ((a3.x + a3.y) + (a3.z + a3.w));
+            const float cx = 16.0f * (vx - sx);
             atomicAdd(&A.t[((static_cast<int64_t>(s_ecomp_tok[c]) * A.ne + cur_e) * 3 + 2) * maxr + j],
                       fmaf(f.x, cx, f.y * sx));
           }
@@ -922,7 +968,8 @@ static lrc_status lr_tiles_check(const lrc_expert* e, int hidden, int ffn) {
     if (!factor_present(*f)) continue;
     if (f->dense != nullptr)
       return fail(LRC_ERR_UNSUPPORTED, "lr tiles: raw (unquantized) factors use the generic path");
-    if (f->bits < 1 || f->bits > 8) return fail(LRC_ERR_INVALID, "lr tiles: bad factor bits");
+    if (f->bits < 1 || f->bits > 4)
+      return fail(LRC_ERR_UNSUPPORTED, "lr tiles: factor codes wider than 4 bits use the generic path");
   }
   if (factor_present(e->v2) && (e->v2.group_size % 16) != 0)
     return fail(LRC_ERR_UNSUPPORTED, "lr tiles: V2 group size must be a multiple of 16");
