@@ -158,14 +158,24 @@ __device__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* x, int64_t b0,
   const int proj = blk / nblk1;
   const int j = (blk - proj * nblk1) * rpb + warp;
   const lrc_qmat& V = proj == 0 ? E.v1 : E.v3;
-  if (!factor_present(V) || j >= V.rows || V.dense != nullptr) {
-    // raw factors (test hook) are handled by the generic path; write zeros
+  if (!factor_present(V) || j >= V.rows) {
     if (lane < nb && j < ra.maxr) ra.t[(((b0 + lane) * ra.ne + e) * 3 + proj) * ra.maxr + j] = 0.0f;
     return;
   }
   float acc[kTT];
-  const bool g64 = V.group_size == 64 && ((V.cols * V.bits) % 32) == 0;
-  if (g64 && V.bits == 3) {
+  const bool g64 = V.dense == nullptr && V.group_size == 64 && ((V.cols * V.bits) % 32) == 0;
+  if (V.dense != nullptr) {  // raw fp32 factors (the reference's quantize_factors=False hook)
+#pragma unroll
+    for (int t = 0; t < kTT; ++t) acc[t] = 0.0f;
+    for (int c = lane; c < V.cols; c += 32) {
+      const float w = V.dense[static_cast<int64_t>(j) * V.cols + c];
+#pragma unroll
+      for (int t = 0; t < kTT; ++t)
+        if (t < nb) acc[t] = fmaf(w, bf2f(x[(b0 + t) * ra.d + c]), acc[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < kTT; ++t) acc[t] = warp_sum(acc[t]);
+  } else if (g64 && V.bits == 3) {
     vrow_dot_tokens<3, kTT>(V, j, x + b0 * ra.d, ra.d, nb, acc);
   } else if (g64 && V.bits == 2) {
     vrow_dot_tokens<2, kTT>(V, j, x + b0 * ra.d, ra.d, nb, acc);
