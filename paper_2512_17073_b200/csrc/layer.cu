@@ -2,6 +2,7 @@
 // kernels, and the forward orchestration.  Reference: ref/moe.py:196-259,
 // ref/lowrank.py:153-165.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -210,6 +211,11 @@ __global__ void dense_down_f64_kernel(const double* w2, int hidden, int ffn, con
 lrc_status launch_lr_down(const ExpertArgs& a, int np_bound, cudaStream_t st) {
   if (a.maxr == 0) return LRC_OK;
   int tasks = np_bound * 2 * a.maxr;
+  static bool carve = false;
+  if (!carve && getenv("LRC_NO_CARVEOUT") == nullptr) {  // match the tiled kernels' L1/smem split
+    LRC_CUDA_TRY(cudaFuncSetAttribute(lr_down_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    carve = true;
+  }
   lr_down_kernel<<<(tasks + 7) / 8, 256, 0, st>>>(a);
   LRC_CHECK_LAUNCH();
   return LRC_OK;

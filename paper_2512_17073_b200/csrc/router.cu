@@ -1,20 +1,25 @@
-// K1: fused router -- gate GEMV (fp64) + softmax + stable top-k/top-n, and the
-// per-expert pair plan consumed by the expert kernels.
+// K1: fused router prologue -- gate GEMV (fp64) + softmax + stable top-k/top-n,
+// the per-expert pair plan consumed by the expert kernels, zeroing of the
+// accumulated outputs, and (single token tile) the speculative low-rank
+// down-projection t = V.x.
 // Reference: ref/moe.py:165-193 (route/softmax), ref/moe.py:234-258 (mixing,
-// shared experts).
+// shared experts), ref/lowrank.py:165 (factored U.(V.x) order).
 //
-// Grid (token tiles, experts): CTA (tile, e) computes the logits of up to
-// kTT tokens against gate row e with wide coalesced fp64 loads.  The last CTA
-// of a token tile (atomic ticket) runs softmax + stable top-k for the tile;
-// the last tile builds the pair plan -- one launch, no host round trip.
+// Grid (token tiles, experts, 1 + V.x row blocks).  CTA (tile, e, 0) computes
+// the logits of up to kTT tokens against gate row e; CTAs (tile, e, z>0) the
+// speculative V.x rows.  The last CTA of a token tile (atomic ticket) runs the
+// warp-parallel softmax + top-k for the tile; the last tile builds the pair
+// plan -- one launch, no host round trip.  Code is kept compact on purpose:
+// cold straight-line paths in a huge kernel stall on instruction fetch.
 #include <float.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "layer.cuh"
 
 namespace lrc {
 
-constexpr int kTT = 8;         // tokens per router CTA
+constexpr int kTT = 8;  // tokens per router CTA
 constexpr int kRThreads = 256;
 
 template <typename T>
@@ -29,7 +34,7 @@ __device__ __forceinline__ double load_x<uint16_t>(const uint16_t* x, int64_t i)
 }
 
 // numpy pairwise order for a short fp64 vector (softmax denominator, E <= 256).
-__device__ double pw_sum_small(const double* v, int n) {
+__device__ __noinline__ double pw_sum_small(const double* v, int n) {
   if (n < 8) {
     double r = 0.0;
     for (int i = 0; i < n; ++i) r = __dadd_rn(r, v[i]);
@@ -51,50 +56,15 @@ __device__ double pw_sum_small(const double* v, int n) {
   return __dadd_rn(pw_sum_small(v, n2), pw_sum_small(v + n2, n - n2));
 }
 
-// softmax (ref/moe.py:165-168) + stable descending top-k (np.argsort(-w,
-// kind="stable"), ref/moe.py:190: strict '>' keeps the lower index on ties).
-__device__ void select_topk(double* lg, int E, int k, int renorm, int64_t b, double* probs,
-                            int32_t* topk_idx, float* topk_w) {
-  double mx = lg[0];
-  for (int e = 1; e < E; ++e) mx = fmax(mx, lg[e]);
-  for (int e = 0; e < E; ++e) lg[e] = exp(__dsub_rn(lg[e], mx));
-  const double den = pw_sum_small(lg, E);
-  for (int e = 0; e < E; ++e) lg[e] = __ddiv_rn(lg[e], den);
-  if (probs)
-    for (int e = 0; e < E; ++e) probs[b * E + e] = lg[e];
-  unsigned long long taken[4] = {0, 0, 0, 0};
-  double mix[64];
-  for (int j = 0; j < k; ++j) {
-    int best = -1;
-    double bv = -DBL_MAX;
-    for (int e = 0; e < E; ++e) {
-      if ((taken[e >> 6] >> (e & 63)) & 1ull) continue;
-      if (best < 0 || lg[e] > bv) {
-        best = e;
-        bv = lg[e];
-      }
-    }
-    taken[best >> 6] |= 1ull << (best & 63);
-    topk_idx[b * k + j] = best;
-    mix[j] = bv;
-  }
-  if (renorm) {  // ref/moe.py:234-236, mix.sum() in numpy order
-    const double s = pw_sum_small(mix, k);
-    if (s > 0.0)
-      for (int j = 0; j < k; ++j) mix[j] = __ddiv_rn(mix[j], s);
-  }
-  for (int j = 0; j < k; ++j) topk_w[b * k + j] = static_cast<float>(mix[j]);
-}
-
-// Warp-parallel variant (one warp per token): exp and the top-k argmax run
-// across lanes; the softmax denominator keeps numpy's pairwise order (lane 0)
-// so weights stay bit-identical to select_topk.
-__device__ void select_topk_warp(double* lg, int E, int k, int renorm, int64_t b, double* probs,
-                                 int32_t* topk_idx, float* topk_w) {
+// One warp per token: softmax exactly as ref/moe.py:165-168 (z = l - max,
+// exp, divide by the numpy-ordered sum), then k rounds of warp argmax with the
+// stable tie rule of np.argsort(-w, kind="stable") (ref/moe.py:190): equal
+// weights go to the lower expert index.  lg has E weights + 64 scratch.
+__device__ __noinline__ void select_topk_warp(double* lg, int E, int k, int renorm, int64_t b,
+                                              double* probs, int32_t* topk_idx, float* topk_w) {
   const int lane = threadIdx.x & 31;
   double mx = -DBL_MAX;
   for (int e = lane; e < E; e += 32) mx = fmax(mx, lg[e]);
-#pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   for (int e = lane; e < E; e += 32) lg[e] = exp(__dsub_rn(lg[e], mx));
   __syncwarp();
@@ -107,16 +77,14 @@ __device__ void select_topk_warp(double* lg, int E, int k, int renorm, int64_t b
   }
   __syncwarp();
   uint32_t taken = 0;  // bit m: element lane + 32m already selected
-  double mix[64];
   for (int j = 0; j < k; ++j) {
     double bv = -DBL_MAX;
     int be = 0x7fffffff;
     for (int m = 0, e = lane; e < E; ++m, e += 32)
-      if (!((taken >> m) & 1u) && (lg[e] > bv || be == 0x7fffffff)) {
+      if (!((taken >> m) & 1u) && (be == 0x7fffffff || lg[e] > bv)) {
         bv = lg[e];
         be = e;
       }
-#pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
       const int oe = __shfl_xor_sync(0xffffffffu, be, o);
@@ -126,10 +94,14 @@ __device__ void select_topk_warp(double* lg, int E, int k, int renorm, int64_t b
       }
     }
     if ((be & 31) == lane) taken |= 1u << (be >> 5);
-    mix[j] = bv;
-    if (lane == 0) topk_idx[b * k + j] = be;
+    if (lane == 0) {
+      topk_idx[b * k + j] = be;
+      lg[E + j] = bv;  // scratch after the E weights
+    }
   }
+  __syncwarp();
   if (lane == 0) {
+    double* mix = lg + E;
     if (renorm) {  // ref/moe.py:234-236, mix.sum() in numpy order
       const double s = pw_sum_small(mix, k);
       if (s > 0.0)
@@ -143,74 +115,86 @@ __device__ __forceinline__ void griddep_launch_dependents_r() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Speculative low-rank down-projection for a small batch (one token tile):
-// t[b][e][proj][j] = V_proj(e)[j, :] . x_b for rows j in block `blk` (8 rows,
-// one per warp; proj = blk / (r/8)), for every token of the tile, whether or
-// not e turns out to be one of b's top-n experts -- it removes a dependent
-// launch between the router and the expert kernels (ref/lowrank.py:165 with
-// the factored U.(V.x) order).  Costs < 1% extra bytes at decode sizes.
-__device__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* x, int64_t b0, int nb, int e,
-                             int blk) {
+// Speculative t[b][e][proj][j] = V_proj(e)[j, :] . x_b for the 8 rows of
+// block `blk` (one warp per row) and every token of the tile, whether or not
+// e becomes one of b's top-n experts: removes a dependent launch between the
+// router and the expert kernels (< 1% extra bytes at decode sizes).  x rows
+// come from shared memory (xs: nb x d bf16); each lane preloads the code words
+// of its whole groups, then loops over tokens.
+__device__ __noinline__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* xs, int64_t b0,
+                                          int nb, int e, int blk) {
   const lrc_expert& E = ra.experts[e];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rpb = 8;  // rows per block
-  const int nblk1 = (ra.maxr + rpb - 1) / rpb;
+  const int nblk1 = (ra.maxr + 7) / 8;
   const int proj = blk / nblk1;
-  const int j = (blk - proj * nblk1) * rpb + warp;
+  const int j = (blk - proj * nblk1) * 8 + warp;
+  if (j >= ra.maxr) return;
   const lrc_qmat& V = proj == 0 ? E.v1 : E.v3;
+  float* tout = ra.t + ((b0 * ra.ne + e) * 3 + proj) * ra.maxr + j;
+  const int64_t tstride = static_cast<int64_t>(ra.ne) * 3 * ra.maxr;
   if (!factor_present(V) || j >= V.rows) {
-    if (lane < nb && j < ra.maxr) ra.t[(((b0 + lane) * ra.ne + e) * 3 + proj) * ra.maxr + j] = 0.0f;
+    if (lane < nb) tout[lane * tstride] = 0.0f;
     return;
   }
-  float acc[kTT];
-  const bool g64 = V.dense == nullptr && V.group_size == 64 && ((V.cols * V.bits) % 32) == 0;
-  if (V.dense != nullptr) {  // raw fp32 factors (the reference's quantize_factors=False hook)
+  const bool fast = V.dense == nullptr && V.group_size == 64 && V.bits == 3 &&
+                    ((V.cols * 3) % 32) == 0 && V.cols <= 64 * 64;
+  if (fast) {
+    // 3-bit codes, group 64 = 6 words; up to 2 groups per lane (cols <= 4096)
+    const int gpr = V.cols / 64 + ((V.cols % 64) != 0);
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(V.packed);
+    const int64_t nwords = ((static_cast<int64_t>(V.rows) * V.cols * 3 + 7) >> 3) >> 2;
+    uint32_t w[2][7];
+    float s[2], z[2];
+    int nv[2];
 #pragma unroll
-    for (int t = 0; t < kTT; ++t) acc[t] = 0.0f;
-    for (int c = lane; c < V.cols; c += 32) {
-      const float w = V.dense[static_cast<int64_t>(j) * V.cols + c];
+    for (int h = 0; h < 2; ++h) {
+      const int g = lane + 32 * h;
+      nv[h] = (g < gpr) ? min(64, V.cols - g * 64) : 0;
+      const int64_t w0 = ((static_cast<int64_t>(j) * V.cols + g * 64) * 3) >> 5;
 #pragma unroll
-      for (int t = 0; t < kTT; ++t)
-        if (t < nb) acc[t] = fmaf(w, bf2f(x[(b0 + t) * ra.d + c]), acc[t]);
+      for (int i = 0; i < 7; ++i) w[h][i] = (nv[h] > 0 && w0 + i < nwords) ? __ldg(words + w0 + i) : 0u;
+      s[h] = nv[h] > 0 ? h2f(V.scales[static_cast<int64_t>(j) * gpr + g]) : 0.0f;
+      z[h] = nv[h] > 0 ? h2f(V.zeros[static_cast<int64_t>(j) * gpr + g]) : 0.0f;
     }
+    for (int t = 0; t < nb; ++t) {
+      const uint16_t* xr = xs + t * ra.d;
+      float acc = 0.0f;
 #pragma unroll
-    for (int t = 0; t < kTT; ++t) acc[t] = warp_sum(acc[t]);
-  } else if (g64 && V.bits == 3) {
-    vrow_dot_tokens<3, kTT>(V, j, x + b0 * ra.d, ra.d, nb, acc);
-  } else if (g64 && V.bits == 2) {
-    vrow_dot_tokens<2, kTT>(V, j, x + b0 * ra.d, ra.d, nb, acc);
-  } else if (g64 && V.bits == 4) {
-    vrow_dot_tokens<4, kTT>(V, j, x + b0 * ra.d, ra.d, nb, acc);
-  } else {
-    const int gs = V.group_size, gpr = (V.cols + gs - 1) / gs;
-    const int64_t nbytes = (static_cast<int64_t>(V.rows) * V.cols * V.bits + 7) >> 3;
+      for (int h = 0; h < 2; ++h) {
+        float cx = 0.0f, sx = 0.0f;
+        const uint16_t* xg = xr + (lane + 32 * h) * 64;
 #pragma unroll
-    for (int t = 0; t < kTT; ++t) acc[t] = 0.0f;
-    for (int c = lane; c < V.cols; c += 32) {
-      const int64_t g = static_cast<int64_t>(j) * gpr + c / gs;
-      const float w = fmaf(static_cast<float>(read_code(V.packed, static_cast<int64_t>(j) * V.cols + c,
-                                                        V.bits, nbytes)),
-                           h2f(V.scales[g]), h2f(V.zeros[g]));
-#pragma unroll
-      for (int t = 0; t < kTT; ++t)
-        if (t < nb) acc[t] = fmaf(w, bf2f(x[(b0 + t) * ra.d + c]), acc[t]);
+        for (int i = 0; i < 64; ++i) {
+          if (i < nv[h]) {
+            const int bit = i * 3;
+            const float c = static_cast<float>(
+                __funnelshift_r(w[h][bit >> 5], w[h][(bit >> 5) + 1], bit & 31) & 7u);
+            const float xv = bf2f(xg[i]);
+            cx = fmaf(c, xv, cx);
+            sx += xv;
+          }
+        }
+        acc = fmaf(s[h], cx, fmaf(z[h], sx, acc));
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) tout[t * tstride] = acc;
     }
-#pragma unroll
-    for (int t = 0; t < kTT; ++t) acc[t] = warp_sum(acc[t]);  // (vrow_dot_tokens reduces itself)
+    return;
   }
-#pragma unroll
-  for (int t = 0; t < kTT; ++t)
-    if (lane == 0 && t < nb) ra.t[(((b0 + t) * ra.ne + e) * 3 + proj) * ra.maxr + j] = acc[t];
+  for (int t = 0; t < nb; ++t) {  // generic: any bits / group size / raw fp32 factors
+    const uint16_t* xr = xs + t * ra.d;
+    float acc = 0.0f;
+    for (int c = lane; c < V.cols; c += 32) acc = fmaf(qmat_elem(V, j, c), bf2f(xr[c]), acc);
+    acc = warp_sum(acc);
+    if (lane == 0) tout[t * tstride] = acc;
+  }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kRThreads) gate_kernel(RouteArgs ra) {
-  extern __shared__ double sm_lg[];  // [kTT][E] (last CTA only)
+__global__ void __launch_bounds__(kRThreads) route_kernel(RouteArgs ra) {
+  extern __shared__ __align__(16) uint8_t rsm[];  // [kTT*(E+64)] f64 logits | x tile (bf16)
   __shared__ double s_red[kTT][kRThreads / 32];
   __shared__ int s_last;
-  // blockIdx.z == 0: gate logits of expert e (e < E) + zeroing of this tile's
-  // y rows / t2 block; blockIdx.z >= 1: speculative low-rank down-projection
-  // t = V.x for 8 rows of V1|V3 of expert e (small batches, see spec_lr_rows).
   const int tile = blockIdx.x, e = blockIdx.y, z = blockIdx.z;
   const int64_t b0 = static_cast<int64_t>(tile) * kTT;
   const int64_t rem = ra.B - b0;
@@ -224,8 +208,7 @@ __global__ void __launch_bounds__(kRThreads) gate_kernel(RouteArgs ra) {
       double acc[kTT];
 #pragma unroll
       for (int t = 0; t < kTT; ++t) acc[t] = 0.0;
-      // all of this thread's gate loads are independent: unroll for memory-level parallelism
-#pragma unroll 8
+#pragma unroll 4
       for (int i = threadIdx.x; i < ra.d; i += kRThreads) {
         const double gv = __ldg(g + i);
 #pragma unroll
@@ -253,7 +236,18 @@ __global__ void __launch_bounds__(kRThreads) gate_kernel(RouteArgs ra) {
       for (int64_t i = threadIdx.x; i < static_cast<int64_t>(nb) * ra.d; i += kRThreads)
         ra.y_zero[b0 * ra.d + i] = 0.0f;
   } else if constexpr (sizeof(T) == 2) {
-    spec_lr_rows(ra, reinterpret_cast<const uint16_t*>(x), b0, nb, e, z - 1);
+    // stage the tile's token rows once (16-byte copies), then the V.x rows
+    uint16_t* xs = reinterpret_cast<uint16_t*>(rsm);
+    const uint16_t* xg = reinterpret_cast<const uint16_t*>(x) + b0 * ra.d;
+    if ((ra.d % 8) == 0 && (reinterpret_cast<uintptr_t>(xg) & 15) == 0) {
+      const int n16 = (nb * ra.d) / 8;
+      for (int i = threadIdx.x; i < n16; i += kRThreads)
+        reinterpret_cast<uint4*>(xs)[i] = __ldg(reinterpret_cast<const uint4*>(xg) + i);
+    } else {
+      for (int i = threadIdx.x; i < nb * ra.d; i += kRThreads) xs[i] = xg[i];
+    }
+    __syncthreads();
+    spec_lr_rows(ra, xs, b0, nb, e, z - 1);
   }
   // ---- last CTA of this token tile: softmax + top-k
   __threadfence();
@@ -263,11 +257,13 @@ __global__ void __launch_bounds__(kRThreads) gate_kernel(RouteArgs ra) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  double* lg = reinterpret_cast<double*>(rsm);  // per token: E weights + 64 scratch
+  const int ldl = ra.E + 64;
   for (int i = threadIdx.x; i < nb * ra.E; i += kRThreads)
-    sm_lg[i] = __ldcg(ra.logits + b0 * ra.E + i);
+    lg[(i / ra.E) * ldl + i % ra.E] = __ldcg(ra.logits + b0 * ra.E + i);
   __syncthreads();
   if (warp < nb)
-    select_topk_warp(sm_lg + warp * ra.E, ra.E, ra.k, ra.renorm, b0 + warp, ra.probs, ra.topk_idx,
+    select_topk_warp(lg + warp * ldl, ra.E, ra.k, ra.renorm, b0 + warp, ra.probs, ra.topk_idx,
                      ra.topk_w);
   if (threadIdx.x == 0) ra.tile_ticket[tile] = 0;
   if (ra.plan.ticket == nullptr) return;
@@ -286,8 +282,8 @@ __global__ void __launch_bounds__(kRThreads) gate_kernel(RouteArgs ra) {
 // weight topk_w, compensated iff j < n.  j >= k: shared expert E + (j-k),
 // weight 1, compensated iff compensate_shared (ref/moe.py:249-258).
 // Pairs are grouped by expert, ascending pair id inside each expert (stable).
-__device__ void build_plan_block(const PlanArgs& pa, const int32_t* topk_idx, const float* topk_w,
-                                 int B, int k) {
+__device__ __noinline__ void build_plan_block(const PlanArgs& pa, const int32_t* topk_idx,
+                                              const float* topk_w, int B, int k) {
   const int P = k + pa.num_shared;
   const int NP = B * P;
   const int NE = pa.num_experts + pa.num_shared;
@@ -350,7 +346,7 @@ __device__ void build_plan_block(const PlanArgs& pa, const int32_t* topk_idx, co
         pending &= ~same;
       }
       if (valid) pa.pair_list[pos] = p;
-      // compensated-pair slots (for the t = V.x buffers), in pair order
+      // compensated-pair slots, in pair order
       int comp = 0;
       if (valid) {
         const int j = p % P;
@@ -371,17 +367,34 @@ __device__ void build_plan_block(const PlanArgs& pa, const int32_t* topk_idx, co
 int route_tiles(int64_t B) { return static_cast<int>((B + kTT - 1) / kTT); }
 
 lrc_status launch_route(const RouteArgs& ra, cudaStream_t st) {
-  const int smem = kTT * ra.E * static_cast<int>(sizeof(double));
+  // logits scratch (kTT tokens x (E + 64) doubles) shares dynamic smem with the
+  // bf16 x tile of the speculative V.x CTAs
+  int smem = kTT * (ra.E + 64) * static_cast<int>(sizeof(double));
+  if (ra.spec_blocks > 0) smem = max(smem, kTT * ra.d * 2);
+  static int configured = -1;
+  if (configured < smem) {
+    const void* fns[3] = {(const void*)route_kernel<double>, (const void*)route_kernel<float>,
+                          (const void*)route_kernel<uint16_t>};
+    for (auto f : fns) {
+      if (smem > 48 * 1024)
+        LRC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      // same L1/shared split as the tiled expert kernels: no carveout switch
+      // (SM drain + reconfiguration) between the launches of a layer
+      if (getenv("LRC_NO_CARVEOUT") == nullptr)
+        LRC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
+    configured = smem;
+  }
   dim3 grid(route_tiles(ra.B), ra.experts ? ra.ne : ra.E, 1 + ra.spec_blocks);
   switch (ra.x_dtype) {
     case LRC_DTYPE_F64:
-      gate_kernel<double><<<grid, kRThreads, smem, st>>>(ra);
+      route_kernel<double><<<grid, kRThreads, smem, st>>>(ra);
       break;
     case LRC_DTYPE_F32:
-      gate_kernel<float><<<grid, kRThreads, smem, st>>>(ra);
+      route_kernel<float><<<grid, kRThreads, smem, st>>>(ra);
       break;
     case LRC_DTYPE_BF16:
-      gate_kernel<uint16_t><<<grid, kRThreads, smem, st>>>(ra);
+      route_kernel<uint16_t><<<grid, kRThreads, smem, st>>>(ra);
       break;
     default:
       return fail(LRC_ERR_INVALID, "route: unknown x dtype");
