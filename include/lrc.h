@@ -164,6 +164,11 @@ lrc_status lrc_layer_forward_host(lrc_layer* layer, const uint16_t* x_host, int6
  * {route, lr_down, up, down} durations in milliseconds. */
 lrc_status lrc_layer_set_profiling(lrc_layer* layer, int enabled);
 lrc_status lrc_layer_phase_ms(lrc_layer* layer, float* ms4);
+/* Debug: %globaltimer (ns) stamps, 8 per CTA, of the last launch of the router
+ * (which = 0; enabled by LRC_ROUTE_STAMPS=1 in the environment) or of the
+ * tiled kernels (which = 1: [down, up][256 CTAs][8]; LRC_TILED_DEBUG bit 3).
+ * Copies n values and clears the device buffer. */
+lrc_status lrc_debug_stamps(int which, uint64_t* host, int n);
 
 /* Dense fp64 expert (mode="reference", ref/moe.py:241-243):
  * y (B, hidden) += w[b] * w2 @ (silu(w1 @ x_b) * (w3 @ x_b)); w may be NULL (=1). */

@@ -325,6 +325,7 @@ static lrc_status alloc_workspace(lrc_layer* L) {
   size_t o_pe = take(NP * 4), o_pw = take(NP * 4), o_pt = take(NP * 4), o_pc = take(NP * 4);
   size_t o_pl = take(NP * 4), o_cl = take(NP * 4);
   size_t o_act = take(NE * 4), o_aoff = take(NE * 4), o_acnt = take(NE * 4);
+  size_t o_arec = take(NE * sizeof(ActiveRec));
   size_t o_tki = take(size_t(L->max_tokens) * L->k_max * 4);
   size_t o_tkw = take(size_t(L->max_tokens) * L->k_max * 4);
   size_t o_t = take(size_t(L->max_tokens) * NE * 3 * std::max(L->maxr, 1) * 4);
@@ -351,6 +352,8 @@ static lrc_status alloc_workspace(lrc_layer* L) {
   p.active = reinterpret_cast<int*>(base + o_act);
   p.active_off = reinterpret_cast<int*>(base + o_aoff);
   p.active_cnt = reinterpret_cast<int*>(base + o_acnt);
+  p.arec = reinterpret_cast<ActiveRec*>(base + o_arec);
+  p.experts = L->d_experts;
   p.num_experts = L->E;
   p.num_shared = L->S;
   L->topk_idx = reinterpret_cast<int32_t*>(base + o_tki);

@@ -6,6 +6,18 @@
 
 namespace lrc {
 
+// Everything the tiled kernels need about one active expert, written by the
+// plan builder so their setup is a single dependent round trip.
+struct ActiveRec {
+  const uint8_t* up_tiles;
+  const uint8_t* down_tiles;
+  const uint8_t* up_lr_tiles;
+  const uint8_t* down_lr_tiles;
+  int e, off, cnt;
+  uint32_t cmask;  // bit q: pairs [8q, 8q+8) of the expert hold a compensated pair (q >= 31 -> bit 31)
+  int up_lr_bytes, down_lr_bytes, pad[2];
+};
+
 // Pair plan (see build_plan_block in router.cu).
 struct PlanArgs {
   int* ticket;
@@ -21,6 +33,8 @@ struct PlanArgs {
   int* active_off;          // [E+S] offset into pair_list
   int* active_cnt;          // [E+S]
   int* counts;              // [0] n_active, [1] n_comp
+  ActiveRec* arec;          // [E+S] per active expert (layer forward only; null otherwise)
+  const lrc_expert* experts;  // device table [E+S] (with arec)
 };
 
 struct RouteArgs {
@@ -42,6 +56,7 @@ struct RouteArgs {
   int spec_blocks;            // V.x row blocks per expert computed speculatively (0 = none)
   float* t2_zero;             // zero t[b][e][2][:] (tiled path accumulates into it)
   float* y_zero;              // zero y rows
+  int stamp;                  // LRC_ROUTE_STAMPS: per-CTA %globaltimer stamps (debug)
 };
 
 // Row j of a quantized V (group size 64, BITS-bit LSB-first stream) dotted
@@ -167,6 +182,8 @@ __host__ __device__ inline LrLayout lr_layout(const lrc_expert& e) {
   L.down_total = o;
   return L;
 }
+
+void tiled_stamps_copy(uint64_t* host, int n);  // debug (tiled.cu)
 
 // generic kernels (layer.cu)
 lrc_status launch_lr_down(const ExpertArgs& a, int np_bound, cudaStream_t st);

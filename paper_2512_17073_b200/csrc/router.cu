@@ -21,6 +21,7 @@ namespace lrc {
 
 constexpr int kTT = 8;  // tokens per router CTA
 constexpr int kRThreads = 256;
+constexpr int kStampCtas = 1024;
 
 template <typename T>
 __device__ __forceinline__ double load_x(const T* x, int64_t i);
@@ -115,7 +116,11 @@ __device__ __forceinline__ void griddep_launch_dependents_r() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Speculative t[b][e][proj][j] = V_proj(e)[j, :] . x_b for the 8 rows of
+// Padded shared-memory x row: 64-column groups at a stride of 66 elements.
+__host__ __device__ inline int xs_row_elems(int d) { return ((d + 63) / 64) * 66; }
+__device__ inline int xs_col(int c) { return (c >> 6) * 66 + (c & 63); }
+
+// Speculative t[b][e][proj][j] =V_proj(e)[j, :] . x_b for the 8 rows of
 // block `blk` (one warp per row) and every token of the tile, whether or not
 // e becomes one of b's top-n experts: removes a dependent launch between the
 // router and the expert kernels (< 1% extra bytes at decode sizes).  x rows
@@ -156,22 +161,27 @@ __device__ __noinline__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* x
       s[h] = nv[h] > 0 ? h2f(V.scales[static_cast<int64_t>(j) * gpr + g]) : 0.0f;
       z[h] = nv[h] > 0 ? h2f(V.zeros[static_cast<int64_t>(j) * gpr + g]) : 0.0f;
     }
+    const int ldx = xs_row_elems(ra.d);
     for (int t = 0; t < nb; ++t) {
-      const uint16_t* xr = xs + t * ra.d;
+      const uint32_t* xr = reinterpret_cast<const uint32_t*>(xs + t * ldx);
       float acc = 0.0f;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float cx = 0.0f, sx = 0.0f;
-        const uint16_t* xg = xr + (lane + 32 * h) * 64;
+        const uint32_t* xg = xr + (lane + 32 * h) * 33;
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          if (i < nv[h]) {
-            const int bit = i * 3;
-            const float c = static_cast<float>(
-                __funnelshift_r(w[h][bit >> 5], w[h][(bit >> 5) + 1], bit & 31) & 7u);
-            const float xv = bf2f(xg[i]);
-            cx = fmaf(c, xv, cx);
-            sx += xv;
+        for (int i2 = 0; i2 < 32; ++i2) {
+          if (2 * i2 < nv[h]) {
+            const uint32_t xw = xg[i2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int bit = (2 * i2 + q) * 3;
+              const float c = static_cast<float>(
+                  __funnelshift_r(w[h][bit >> 5], w[h][(bit >> 5) + 1], bit & 31) & 7u);
+              const float xv = q ? __uint_as_float(xw & 0xffff0000u) : __uint_as_float(xw << 16);
+              cx = fmaf(c, xv, cx);
+              sx += xv;
+            }
           }
         }
         acc = fmaf(s[h], cx, fmaf(z[h], sx, acc));
@@ -181,17 +191,29 @@ __device__ __noinline__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* x
     }
     return;
   }
+  const int ldx = xs_row_elems(ra.d);
   for (int t = 0; t < nb; ++t) {  // generic: any bits / group size / raw fp32 factors
-    const uint16_t* xr = xs + t * ra.d;
+    const uint16_t* xr = xs + t * ldx;
     float acc = 0.0f;
-    for (int c = lane; c < V.cols; c += 32) acc = fmaf(qmat_elem(V, j, c), bf2f(xr[c]), acc);
+    for (int c = lane; c < V.cols; c += 32) acc = fmaf(qmat_elem(V, j, c), bf2f(xr[xs_col(c)]), acc);
     acc = warp_sum(acc);
     if (lane == 0) tout[t * tstride] = acc;
   }
 }
 
+__device__ unsigned long long g_route_stamps[kStampCtas * 8];
+#define RSTAMP(k)                                                                     \
+  do {                                                                                \
+    if (ra.stamp && threadIdx.x == 0) {                                               \
+      const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      if (cta < kStampCtas) g_route_stamps[cta * 8 + (k)] = t_;                       \
+    }                                                                                 \
+  } while (0)
+
 template <typename T>
-__global__ void __launch_bounds__(kRThreads) route_kernel(RouteArgs ra) {
+__global__ void __launch_bounds__(kRThreads) route_kernel(const __grid_constant__ RouteArgs ra) {
   extern __shared__ __align__(16) uint8_t rsm[];  // [kTT*(E+64)] f64 logits | x tile (bf16)
   __shared__ double s_red[kTT][kRThreads / 32];
   __shared__ int s_last;
@@ -201,6 +223,7 @@ __global__ void __launch_bounds__(kRThreads) route_kernel(RouteArgs ra) {
   const int nb = rem < kTT ? static_cast<int>(rem) : kTT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const T* x = static_cast<const T*>(ra.x);
+  RSTAMP(0);
   griddep_launch_dependents_r();
   if (z == 0) {
     if (e < ra.E) {
@@ -227,6 +250,7 @@ __global__ void __launch_bounds__(kRThreads) route_kernel(RouteArgs ra) {
         ra.logits[(b0 + threadIdx.x) * ra.E + e] = s;
       }
     }
+    RSTAMP(6);
     if (ra.t2_zero != nullptr && ra.maxr > 0)
       for (int i = threadIdx.x; i < nb * ra.maxr; i += kRThreads) {
         const int t = i / ra.maxr, j = i - t * ra.maxr;
@@ -237,24 +261,36 @@ __global__ void __launch_bounds__(kRThreads) route_kernel(RouteArgs ra) {
         ra.y_zero[b0 * ra.d + i] = 0.0f;
   } else if constexpr (sizeof(T) == 2) {
     // stage the tile's token rows once (16-byte copies), then the V.x rows
+    // padded layout: 64-column groups at a stride of 33 words, so lanes that
+    // each walk their own group hit distinct banks
     uint16_t* xs = reinterpret_cast<uint16_t*>(rsm);
     const uint16_t* xg = reinterpret_cast<const uint16_t*>(x) + b0 * ra.d;
-    if ((ra.d % 8) == 0 && (reinterpret_cast<uintptr_t>(xg) & 15) == 0) {
-      const int n16 = (nb * ra.d) / 8;
-      for (int i = threadIdx.x; i < n16; i += kRThreads)
-        reinterpret_cast<uint4*>(xs)[i] = __ldg(reinterpret_cast<const uint4*>(xg) + i);
+    const int ldx = xs_row_elems(ra.d);
+    if ((ra.d % 64) == 0 && (reinterpret_cast<uintptr_t>(xg) & 3) == 0) {
+      const int wpr = ra.d / 2;  // words per token row
+      uint32_t* xs32 = reinterpret_cast<uint32_t*>(xs);
+      const uint32_t* xg32 = reinterpret_cast<const uint32_t*>(xg);
+      for (int i = threadIdx.x; i < nb * wpr; i += kRThreads) {
+        const int t = i / wpr, w = i - t * wpr;
+        xs32[t * (ldx / 2) + (w >> 5) * 33 + (w & 31)] = __ldg(xg32 + i);
+      }
     } else {
-      for (int i = threadIdx.x; i < nb * ra.d; i += kRThreads) xs[i] = xg[i];
+      for (int i = threadIdx.x; i < nb * ra.d; i += kRThreads) {
+        const int t = i / ra.d, c = i - t * ra.d;
+        xs[t * ldx + xs_col(c)] = xg[i];
+      }
     }
     __syncthreads();
     spec_lr_rows(ra, xs, b0, nb, e, z - 1);
   }
   // ---- last CTA of this token tile: softmax + top-k
+  RSTAMP(1);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0)
     s_last = (atomicAdd(&ra.tile_ticket[tile], 1) == static_cast<int>(gridDim.y * gridDim.z) - 1);
   __syncthreads();
+  RSTAMP(2);
   if (!s_last) return;
   __threadfence();
   double* lg = reinterpret_cast<double*>(rsm);  // per token: E weights + 64 scratch
@@ -266,16 +302,20 @@ __global__ void __launch_bounds__(kRThreads) route_kernel(RouteArgs ra) {
     select_topk_warp(lg + warp * ldl, ra.E, ra.k, ra.renorm, b0 + warp, ra.probs, ra.topk_idx,
                      ra.topk_w);
   if (threadIdx.x == 0) ra.tile_ticket[tile] = 0;
+  RSTAMP(3);
   if (ra.plan.ticket == nullptr) return;
   // ---- last tile: build the pair plan for the whole batch
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = (atomicAdd(ra.plan.ticket, 1) == static_cast<int>(gridDim.x) - 1);
   __syncthreads();
+  RSTAMP(4);
   if (!s_last) return;
   __threadfence();
   build_plan_block(ra.plan, ra.topk_idx, ra.topk_w, static_cast<int>(ra.B), ra.k);
   if (threadIdx.x == 0) *ra.plan.ticket = 0;
+  __syncthreads();
+  RSTAMP(5);
 }
 
 // Pair plan: pair p = b*P + j, P = k + S.  j < k: routed expert topk_idx[b][j],
@@ -317,6 +357,20 @@ __device__ __noinline__ void build_plan_block(const PlanArgs& pa, const int32_t*
         pa.active[na] = e;
         pa.active_off[na] = s_off[e];
         pa.active_cnt[na] = s_cnt[e];
+        if (pa.arec != nullptr) {
+          const lrc_expert& X = pa.experts[e];
+          const LrLayout L = lr_layout(X);
+          ActiveRec& R = pa.arec[na];
+          R.up_tiles = X.up_tiles;
+          R.down_tiles = X.down_tiles;
+          R.up_lr_tiles = X.up_lr_tiles;
+          R.down_lr_tiles = X.down_lr_tiles;
+          R.e = e;
+          R.off = s_off[e];
+          R.cnt = s_cnt[e];
+          R.up_lr_bytes = L.up_total;
+          R.down_lr_bytes = L.down_total;
+        }
         ++na;
       }
     }
@@ -362,15 +416,35 @@ __device__ __noinline__ void build_plan_block(const PlanArgs& pa, const int32_t*
     }
     if (lane == 0) pa.counts[1] = count;
   }
+  if (pa.arec == nullptr) return;
+  // compensated-pair mask per active expert, 8-pair granularity (one warp each)
+  __syncthreads();
+  const int na = pa.counts[0];
+  for (int a = threadIdx.x >> 5; a < na; a += blockDim.x >> 5) {
+    const int off = pa.active_off[a], cnt = pa.active_cnt[a];
+    uint32_t mask = 0;
+    for (int j0 = 0; j0 < cnt; j0 += 32) {
+      const int j = j0 + lane;
+      const bool c = j < cnt && pa.pair_comp[pa.pair_list[off + j]] >= 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, c);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if ((bal >> (8 * q)) & 0xffu) mask |= 1u << min((j0 >> 3) + q, 31);
+    }
+    if (lane == 0) pa.arec[a].cmask = mask;
+  }
 }
 
 int route_tiles(int64_t B) { return static_cast<int>((B + kTT - 1) / kTT); }
 
-lrc_status launch_route(const RouteArgs& ra, cudaStream_t st) {
+lrc_status launch_route(const RouteArgs& ra_in, cudaStream_t st) {
+  static const int stamps = getenv("LRC_ROUTE_STAMPS") != nullptr;
+  RouteArgs ra = ra_in;
+  ra.stamp = stamps;
   // logits scratch (kTT tokens x (E + 64) doubles) shares dynamic smem with the
   // bf16 x tile of the speculative V.x CTAs
   int smem = kTT * (ra.E + 64) * static_cast<int>(sizeof(double));
-  if (ra.spec_blocks > 0) smem = max(smem, kTT * ra.d * 2);
+  if (ra.spec_blocks > 0) smem = max(smem, kTT * xs_row_elems(ra.d) * 2);
   static int configured = -1;
   if (configured < smem) {
     const void* fns[3] = {(const void*)route_kernel<double>, (const void*)route_kernel<float>,
@@ -404,6 +478,21 @@ lrc_status launch_route(const RouteArgs& ra, cudaStream_t st) {
 }
 
 }  // namespace lrc
+
+extern "C" lrc_status lrc_debug_stamps(int which, uint64_t* host, int n) {
+  using namespace lrc;
+  if (n < 0 || n > (which == 0 ? kStampCtas * 8 : 2 * 256 * 8 + 2 * 64 * 6)) return fail(LRC_ERR_INVALID, "stamps: bad count");
+  LRC_CUDA_TRY(cudaDeviceSynchronize());
+  if (which != 0) {
+    tiled_stamps_copy(host, n);
+    return LRC_OK;
+  }
+  LRC_CUDA_TRY(cudaMemcpyFromSymbol(host, g_route_stamps, sizeof(uint64_t) * n));
+  void* dev = nullptr;  // cleared after each read: CTAs that skip a point leave 0
+  LRC_CUDA_TRY(cudaGetSymbolAddress(&dev, g_route_stamps));
+  LRC_CUDA_TRY(cudaMemset(dev, 0, sizeof(g_route_stamps)));
+  return LRC_OK;
+}
 
 extern "C" lrc_status lrc_route(const double* gate_t, const void* x, int x_dtype, int64_t B, int d,
                                 int E, int top_k, int top_n, int renormalize, double* probs,

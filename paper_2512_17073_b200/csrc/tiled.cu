@@ -28,7 +28,8 @@ constexpr int kBlk = 640;
 constexpr int kCodeBytes = 512;
 constexpr int kSpanGP = 4;        // group pairs per warp span (512 columns)
 constexpr int kNW = 8;            // consumer warps (+1 epilogue warp, +1 producer warp)
-constexpr int kThreads = (kNW + 2) * 32;
+constexpr int kNEpi = 2;          // epilogue warps: item k -> warp kNW + k % kNEpi
+constexpr int kThreads = (kNW + kNEpi + 1) * 32;
 
 int64_t tiles_bytes(int64_t rows, int64_t cols, int ni) {
   int64_t rt = (rows + 15) / 16, gp = (cols + 127) / 128;
@@ -134,12 +135,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
+// Weight tiles are read exactly once per step: stream them with an L2
+// evict-first policy so they do not evict the small hot state every kernel of
+// the layer touches (code, parameters, gate, activations, the pair plan).
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol, bool hint) {
+  if (hint)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kNW * 32) : "memory");
@@ -284,7 +301,8 @@ struct TiledParams {
   int debug;            // LRC_TILED_DEBUG: bit0 skip MMA core, bit1 skip epilogue math
 };
 
-constexpr int kNRed = 2;  // partial-sum ring depth (consumers -> epilogue warp)
+constexpr int kNRed = 2;  // partial-sum ring depth (consumers -> epilogue warps)
+static_assert(kNRed == kNEpi, "partial slot k % kNRed belongs to epilogue warp k % kNEpi");
 
 struct SmemMap {
   int xs, sums, red, ts, act, lrs, bars, total;
@@ -304,11 +322,11 @@ __host__ __device__ inline SmemMap smem_map(const TiledParams& p) {
   m.red = o;
   o = align16(o + kNRed * kNW * NI * NT * 128 * 4);
   m.ts = o;
-  o = align16(o + TPP * NI * (p.a.maxr > 0 ? p.a.maxr : 1) * 4);
+  o = align16(o + kNEpi * TPP * NI * (p.a.maxr > 0 ? p.a.maxr : 1) * 4);
   m.act = o;
-  o = align16(o + 16 * TPP * 4);
+  o = align16(o + kNEpi * 16 * TPP * 4);
   m.lrs = o;
-  o = align16(o + NI * 16 * TPP * 4);
+  o = align16(o + kNEpi * NI * 16 * TPP * 4);
   m.bars = o;
   m.total = o + (2 * p.nstage + 2 * kNRed) * 8;
   return m;
@@ -355,6 +373,22 @@ __device__ __forceinline__ float nib_f(uint32_t w) {
   return __uint_as_float(lop3_and_or(sh, 0x00780000u, 0x3F800000u));
 }
 
+// Per-pass state of one epilogue warp.
+template <int TPP>
+struct EpiPass {
+  int epair[TPP], etok[TPP], ecomp_of[TPP], ecomp_n[TPP], ecomp_tok[TPP];
+  float ew[TPP];
+  int encomp, r[3], ub[3], ugs[3], vb;
+  LrLayout L;
+};
+
+// does pass `pass` (TPP = 8 * tpp8 pairs) hold a compensated pair? (ActiveRec::cmask)
+__device__ __forceinline__ bool pass_has_comp(uint32_t m, int pass, int tpp8) {
+  bool c = false;
+  for (int q = pass * tpp8; q < (pass + 1) * tpp8; ++q) c |= ((m >> min(q, 31)) & 1u) != 0;
+  return c;
+}
+
 struct ItemDesc {
   int ai, pass, chunk, tile, lr, gp0, gp1, pad;
 };
@@ -364,11 +398,33 @@ constexpr int kMaxStages = 8;
 // kNW is the epilogue warp (cross-warp reduction, low-rank terms, SwiGLU /
 // combine), warp kNW+1 produces (cp.async.bulk).  Consumers never block on the
 // epilogue: partials go through a kNRed-deep mbarrier ring.
+// LRC_TILED_DEBUG bit 3: %globaltimer stamps per CTA (lrc_debug_stamps)
+constexpr int kTStampCtas = 256;
+__device__ unsigned long long g_tiled_stamps[2][kTStampCtas][8];
+// CTA 0 per item: issue, consumer pre-wait, data, MMA core done, partials posted, epi done
+__device__ unsigned long long g_item_stamps[2][64][6];
+#define ISTAMP(k, j)                                                      \
+  do {                                                                    \
+    if ((P.debug & 8) && blockIdx.x == 0 && (k) < 64) {                   \
+      unsigned long long t_;                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));              \
+      g_item_stamps[UP][k][j] = t_;                                       \
+    }                                                                     \
+  } while (0)
+#define TSTAMP(k)                                                          \
+  do {                                                                     \
+    if (P.debug & 8) {                                                     \
+      unsigned long long t_;                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));               \
+      if (blockIdx.x < kTStampCtas) g_tiled_stamps[UP][blockIdx.x][k] = t_; \
+    }                                                                      \
+  } while (0)
+
 template <bool UP, int NT>
-__global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
+__global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constant__ TiledParams P) {
   constexpr int NI = UP ? 2 : 1;
   constexpr int TPP = 8 * NT;  // tokens per pass
-  constexpr int kEpi = kNW, kProd = kNW + 1;
+  constexpr int kEpi0 = kNW, kProd = kNW + kNEpi;
   extern __shared__ __align__(128) uint8_t smem[];
   const SmemMap SM = smem_map<NI, NT>(P);
   uint8_t* stages = smem;
@@ -390,12 +446,9 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   __shared__ const uint8_t* s_wsrc[LRC_MAX_EXPERTS];
   __shared__ const uint8_t* s_lsrc[LRC_MAX_EXPERTS];
   __shared__ int s_lbytes[LRC_MAX_EXPERTS];
+  __shared__ uint32_t s_acmask[LRC_MAX_EXPERTS];
   __shared__ int s_cpair[TPP], s_ctok[TPP];  // consumer-owned pass data
-  // epilogue-owned pass data
-  __shared__ int s_epair[TPP], s_etok[TPP], s_ecomp_of[TPP], s_ecomp_n[TPP], s_ecomp_tok[TPP];
-  __shared__ float s_ew[TPP];
-  __shared__ int s_encomp, s_r[3], s_ub[3], s_ugs[3], s_vb;
-  __shared__ LrLayout s_L;
+  __shared__ EpiPass<TPP> s_ep[kNEpi];       // epilogue-owned pass data (per warp)
 
   const ExpertArgs& A = P.a;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -404,19 +457,22 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   // plan is two launches old (complete before the up kernel passed its own
   // wait), so its producer may start streaming W2 while the up kernel drains;
   // its consumers / epilogue wait before touching the up kernel's outputs.
+  if (threadIdx.x == 0) TSTAMP(0);
   if (UP) griddep_wait();
   griddep_launch_dependents();
+  if (threadIdx.x == 0) TSTAMP(1);
+  // one round trip: the active count and every active-expert record (records
+  // past n_active are stale and ignored) are loaded concurrently
   const int n_active = A.plan.counts[0];
-  for (int ai = threadIdx.x; ai < n_active; ai += blockDim.x) {
-    const int e = A.plan.active[ai];
-    const lrc_expert& E = A.experts[e];
-    s_aoff[ai] = A.plan.active_off[ai];
-    s_acnt[ai] = A.plan.active_cnt[ai];
-    s_ae[ai] = e;
-    s_wsrc[ai] = UP ? E.up_tiles : E.down_tiles;
-    const LrLayout L = lr_layout(E);
-    s_lbytes[ai] = UP ? L.up_total : L.down_total;
-    s_lsrc[ai] = UP ? E.up_lr_tiles : E.down_lr_tiles;
+  for (int ai = threadIdx.x; ai < min(A.ne, LRC_MAX_EXPERTS); ai += blockDim.x) {
+    const ActiveRec R = A.plan.arec[ai];
+    s_aoff[ai] = R.off;
+    s_acnt[ai] = R.cnt;
+    s_ae[ai] = R.e;
+    s_wsrc[ai] = UP ? R.up_tiles : R.down_tiles;
+    s_lbytes[ai] = UP ? R.up_lr_bytes : R.down_lr_bytes;
+    s_lsrc[ai] = UP ? R.up_lr_tiles : R.down_lr_tiles;
+    s_acmask[ai] = R.cmask;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -431,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     s_range[1] = static_cast<int>(total * (blockIdx.x + 1) / gridDim.x);
     for (int s = 0; s < P.nstage; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kNW + 1);  // consumers + epilogue (LR slot)
+      mbar_init(&empty[s], kNW + 1);  // consumers + the item's epilogue warp (LR slot)
     }
     for (int r = 0; r < kNRed; ++r) {
       mbar_init(&rfull[r], kNW);
@@ -443,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   for (int i = threadIdx.x; i < P.xs_stride / 2; i += blockDim.x)
     reinterpret_cast<uint32_t*>(xs + P.xs_rows * P.xs_stride)[i] = 0u;
   __syncthreads();
+  if (threadIdx.x == 0) TSTAMP(2);
   const int beg = s_range[0], end = s_range[1];
   if (beg >= end) return;
   const int nitems = end - beg;
@@ -450,24 +507,18 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   if (warp == kProd) {
     // ===================== producer: one elected lane streams work items ====
     if (lane == 0) {
-      int c_ai = -1, c_pass = -1, c_comp = 0, ai = 0;
+      const bool hint = (P.debug & 4) == 0;  // LRC_TILED_DEBUG bit 2: plain L2 policy
+      const uint64_t pol = l2_evict_first_policy();
+      int ai = 0, s = 0, ph = 0;
       for (int it = beg; it < end; ++it) {
         const int k = it - beg;
-        const int s = k % P.nstage;
-        if (k >= P.nstage) mbar_wait(&empty[s], ((k / P.nstage) - 1) & 1);
+        if (k >= P.nstage) mbar_wait(&empty[s], ph ^ 1);
         while (s_prefix[ai + 1] <= it) ++ai;
         int r = it - s_prefix[ai];
         const int tile = r % static_cast<int>(P.RT);
         r /= static_cast<int>(P.RT);
         const int chunk = r % P.nchunk, pass = r / P.nchunk;
-        if (ai != c_ai || pass != c_pass) {
-          c_ai = ai;
-          c_pass = pass;
-          c_comp = 0;
-          const int off = s_aoff[ai];
-          const int n = min(TPP, s_acnt[ai] - pass * TPP);
-          for (int j = 0; j < n; ++j) c_comp |= A.plan.pair_comp[A.plan.pair_list[off + pass * TPP + j]] >= 0;
-        }
+        const bool c_comp = pass_has_comp(s_acmask[ai], pass, NT);
         const int gp0 = chunk * P.SPC * kSpanGP;
         const int gp1 = static_cast<int>(min(P.GP, static_cast<int64_t>(gp0) + P.SPC * kSpanGP));
         const uint8_t* src = s_wsrc[ai] + ((static_cast<int64_t>(tile) * P.GP + gp0) * NI) * kBlk;
@@ -477,29 +528,45 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
         s_desc[s] = ItemDesc{ai, pass, chunk, tile, lr ? 1 : 0, gp0, gp1, 0};
         uint8_t* dst = stages + static_cast<size_t>(s) * slot_bytes;
         mbar_expect_tx(&full[s], bytes + lr_bytes);  // release: orders the descriptor store
-        bulk_g2s(dst, src, bytes, &full[s]);
+        bulk_g2s(dst, src, bytes, &full[s], pol, hint);
         if (lr) bulk_g2s(dst + P.stage_bytes, s_lsrc[ai] + static_cast<int64_t>(tile) * lr_bytes,
-                         lr_bytes, &full[s]);
+                         lr_bytes, &full[s], pol, hint);
+        if (k == 0) TSTAMP(3);
+        ISTAMP(k, 0);
+        if (++s == P.nstage) {
+          s = 0;
+          ph ^= 1;
+        }
       }
+      TSTAMP(4);
     }
     return;
   }
 
-  if (warp == kEpi) {
-    // ================== epilogue warp: reduce, low-rank terms, SwiGLU/combine ===
+  if (warp >= kEpi0 && warp < kEpi0 + kNEpi) {
+    // ====== epilogue warps: reduce, low-rank terms, SwiGLU / combine ========
+    // Item k belongs to warp kEpi0 + k % kNEpi and partial slot k % kNRed.  The
+    // pass setup of an item (pair lists, t vectors) is done from the item index
+    // before its partials are awaited, off the critical path.
+    const int ew = warp - kEpi0;
+    EpiPass<TPP>& EP = s_ep[ew];
+    float* tsw = ts + ew * TPP * NI * (maxr > 0 ? maxr : 1);
+    float* actw = act_s + ew * 16 * TPP;
+    float* lrsw = lrs + ew * NI * 16 * TPP;
     if (!UP) griddep_wait();  // t2 comes from the up kernel
-    int cur_ai = -1, cur_pass = -1, pass_tok = 0, cur_e = -1;
-    for (int k = 0; k < nitems; ++k) {
-      const int s = k % P.nstage, rs = k % kNRed;
-      mbar_wait(&rfull[rs], (k / kNRed) & 1);
-      const ItemDesc dsc = s_desc[s];
-      const uint8_t* st = stages + static_cast<size_t>(s) * slot_bytes;
-      if (dsc.ai != cur_ai || dsc.pass != cur_pass) {
-        cur_ai = dsc.ai;
-        cur_pass = dsc.pass;
-        cur_e = s_ae[dsc.ai];
-        pass_tok = min(TPP, s_acnt[dsc.ai] - cur_pass * TPP);
-        const int off = s_aoff[dsc.ai];
+    int cur_ai = -1, cur_pass = -1, pass_tok = 0, cur_e = -1, ai = 0;
+    int s = ew % P.nstage;
+    for (int k = ew; k < nitems; k += kNEpi) {
+      const int rs = k % kNRed;
+      const int it = beg + k;
+      while (s_prefix[ai + 1] <= it) ++ai;
+      const int pass = ((it - s_prefix[ai]) / static_cast<int>(P.RT)) / P.nchunk;
+      if (ai != cur_ai || pass != cur_pass) {
+        cur_ai = ai;
+        cur_pass = pass;
+        cur_e = s_ae[ai];
+        pass_tok = min(TPP, s_acnt[ai] - cur_pass * TPP);
+        const int off = s_aoff[ai];
         if (lane < TPP) {
           int p = -1, tok = 0, cmp = 0;
           float w = 0.0f;
@@ -509,47 +576,51 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
             w = A.plan.pair_w[p];
             cmp = A.plan.pair_comp[p] >= 0;
           }
-          s_epair[lane] = p;
-          s_etok[lane] = tok;
-          s_ew[lane] = w;
-          s_ecomp_of[lane] = cmp;
+          EP.epair[lane] = p;
+          EP.etok[lane] = tok;
+          EP.ew[lane] = w;
+          EP.ecomp_of[lane] = cmp;
+        } else if (lane == 31) {
+          const lrc_expert& E = A.experts[cur_e];
+          EP.L = lr_layout(E);
+          const lrc_qmat* us[3] = {&E.u1, &E.u3, &E.u2};
+          for (int i = 0; i < 3; ++i) {
+            EP.r[i] = factor_present(*us[i]) ? us[i]->cols : 0;
+            EP.ub[i] = us[i]->bits;
+            EP.ugs[i] = us[i]->group_size;
+          }
+          EP.vb = E.v2.bits;
         }
         __syncwarp();
         if (lane == 0) {
-          const lrc_expert& E = A.experts[cur_e];
           int nc = 0;
           for (int n = 0; n < TPP; ++n) {
-            if (s_ecomp_of[n]) {
-              s_ecomp_of[n] = nc;
-              s_ecomp_n[nc] = n;
-              s_ecomp_tok[nc] = s_etok[n];
+            if (EP.ecomp_of[n]) {
+              EP.ecomp_of[n] = nc;
+              EP.ecomp_n[nc] = n;
+              EP.ecomp_tok[nc] = EP.etok[n];
               ++nc;
             } else {
-              s_ecomp_of[n] = -1;
+              EP.ecomp_of[n] = -1;
             }
           }
-          s_encomp = nc;
-          s_L = lr_layout(E);
-          const lrc_qmat* us[3] = {&E.u1, &E.u3, &E.u2};
-          for (int i = 0; i < 3; ++i) {
-            s_r[i] = factor_present(*us[i]) ? us[i]->cols : 0;
-            s_ub[i] = us[i]->bits;
-            s_ugs[i] = us[i]->group_size;
-          }
-          s_vb = E.v2.bits;
+          EP.encomp = nc;
         }
         __syncwarp();
         if (maxr > 0) {  // low-rank input vectors (t1/t3 up, t2 down) of the comp tokens
-          const int ntask = s_encomp * NI * maxr;
+          const int ntask = EP.encomp * NI * maxr;
           for (int task = lane; task < ntask; task += 32) {
             const int j = task % maxr, ci = task / maxr;
             const int i = ci % NI, c = ci / NI;
             const int proj = UP ? i : 2;
-            ts[task] = __ldcg(A.t + ((static_cast<int64_t>(s_ecomp_tok[c]) * A.ne + cur_e) * 3 + proj) * maxr + j);
+            tsw[task] = __ldcg(A.t + ((static_cast<int64_t>(EP.ecomp_tok[c]) * A.ne + cur_e) * 3 + proj) * maxr + j);
           }
         }
         __syncwarp();
       }
+      mbar_wait(&rfull[rs], (k / kNRed) & 1);
+      const ItemDesc dsc = s_desc[s];
+      const uint8_t* st = stages + static_cast<size_t>(s) * slot_bytes;
       const int nw = min((dsc.gp1 - dsc.gp0 + kSpanGP - 1) / kSpanGP, kNW);
       const float* rb = red + static_cast<size_t>(rs) * kNW * NI * NT * 128;
       const int rr = lane & 15, il = lane >> 4;  // lane -> (matrix, row)
@@ -557,15 +628,15 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       // ---- E1: low-rank up-projection U.t for this tile's rows (ref/lowrank.py:165)
       if (dsc.lr && lane_on && !(P.debug & 2)) {
         const int pi = UP ? il : 2;
-        const int r = s_r[pi];
+        const int r = EP.r[pi];
         const uint8_t* lr = st + P.stage_bytes;
-        const uint32_t* cw = reinterpret_cast<const uint32_t*>(lr + (UP ? (il ? s_L.u3c : s_L.u1c) : s_L.u2c));
-        const uint8_t* meta = lr + (UP ? (il ? s_L.u3m : s_L.u1m) : s_L.u2m);
-        const int gsu = s_ugs[pi];  // LR tile codes are 4-bit nibbles
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(lr + (UP ? (il ? EP.L.u3c : EP.L.u1c) : EP.L.u2c));
+        const uint8_t* meta = lr + (UP ? (il ? EP.L.u3m : EP.L.u1m) : EP.L.u2m);
+        const int gsu = EP.ugs[pi];  // LR tile codes are 4-bit nibbles
         const int gpu = (r + gsu - 1) / gsu;
         const bool fast = (r % 8) == 0 && (gsu % 8) == 0;
-        for (int c = 0; c < s_encomp; ++c) {
-          const float* tv = ts + (c * NI + il) * maxr;
+        for (int c = 0; c < EP.encomp; ++c) {
+          const float* tv = tsw + (c * NI + il) * maxr;
           float v = 0.0f;
           for (int g = 0; g < gpu; ++g) {
             const float2 f = h2f2(*reinterpret_cast<const uint32_t*>(meta + (rr * gpu + g) * 4));
@@ -596,7 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
             }
             v = fmaf(f.x, cx, fmaf(f.y, sx, v));
           }
-          lrs[(il * 16 + rr) * TPP + c] = v;
+          lrsw[(il * 16 + rr) * TPP + c] = v;
         }
       }
       __syncwarp();
@@ -605,35 +676,37 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
         const int nt = n >> 3, col = n & 7;
         float v = 0.0f;
         if (lane_on) {
-          for (int w = 0; w < nw; ++w) v += rb[((w * NI + il) * NT + nt) * 128 + rr * 8 + col];
-          const int c = s_ecomp_of[n];
-          if (dsc.lr && c >= 0) v += lrs[(il * 16 + rr) * TPP + c];
+#pragma unroll
+          for (int w = 0; w < kNW; ++w)
+            if (w < nw) v += rb[((w * NI + il) * NT + nt) * 128 + rr * 8 + col];
+          const int c = EP.ecomp_of[n];
+          if (dsc.lr && c >= 0) v += lrsw[(il * 16 + rr) * TPP + c];
         }
         const int row = dsc.tile * 16 + rr;
         if (UP) {
           const float h3 = __shfl_down_sync(0xffffffffu, v, 16);
           if (lane < 16) {
             const float act = (row < P.M) ? silu_f(v) * h3 : 0.0f;
-            act_s[n * 16 + rr] = act;
-            if (row < P.M) A.a16[static_cast<int64_t>(s_epair[n]) * A.ffn + row] = f2bf(act);
+            actw[n * 16 + rr] = act;
+            if (row < P.M) A.a16[static_cast<int64_t>(EP.epair[n]) * A.ffn + row] = f2bf(act);
           }
         } else if (lane < 16 && row < P.M) {
-          atomicAdd(&A.y[static_cast<int64_t>(s_etok[n]) * A.hidden + row], s_ew[n] * v);
+          atomicAdd(&A.y[static_cast<int64_t>(EP.etok[n]) * A.hidden + row], EP.ew[n] * v);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&rempty[rs]);  // partial slot free for the consumers
       // ---- E3 (up): partial t2 = V2[:, tile rows] . act for the comp tokens
-      if (UP && dsc.lr && s_r[2] > 0 && !(P.debug & 2)) {
-        const int r2 = s_r[2];
+      if (UP && dsc.lr && EP.r[2] > 0 && !(P.debug & 2)) {
+        const int r2 = EP.r[2];
         const uint8_t* lr = st + P.stage_bytes;
-        const uint32_t* vw = reinterpret_cast<const uint32_t*>(lr + s_L.v2c);
+        const uint32_t* vw = reinterpret_cast<const uint32_t*>(lr + EP.L.v2c);
         for (int j = lane; j < r2; j += 32) {
-          const float2 f = h2f2(*reinterpret_cast<const uint32_t*>(lr + s_L.v2m + j * 4));
+          const float2 f = h2f2(*reinterpret_cast<const uint32_t*>(lr + EP.L.v2m + j * 4));
           // V2^T tile is j-major nibbles: codes (j, rl), rl = 0..15, in words 2j, 2j+1
           const uint32_t w0 = vw[2 * j], w1 = vw[2 * j + 1];
-          for (int c = 0; c < s_encomp; ++c) {
-            const float4* an = reinterpret_cast<const float4*>(act_s + s_ecomp_n[c] * 16);
+          for (int c = 0; c < EP.encomp; ++c) {
+            const float4* an = reinterpret_cast<const float4*>(actw + EP.ecomp_n[c] * 16);
             const float4 a0 = an[0], a1 = an[1], a2 = an[2], a3 = an[3];
             float vx = nib_f<0>(w0) * a0.x;
             vx = fmaf(nib_f<1>(w0), a0.y, vx);
@@ -654,14 +727,18 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
             const float sx = ((a0.x + a0.y) + (a0.z + a0.w)) + ((a1.x + a1.y) + (a1.z + a1.w)) +
                              ((a2.x + a2.y) + (a2.z + a2.w)) + ((a3.x + a3.y) + (a3.z + a3.w));
             const float cx = 16.0f * (vx - sx);
-            atomicAdd(&A.t[((static_cast<int64_t>(s_ecomp_tok[c]) * A.ne + cur_e) * 3 + 2) * maxr + j],
+            atomicAdd(&A.t[((static_cast<int64_t>(EP.ecomp_tok[c]) * A.ne + cur_e) * 3 + 2) * maxr + j],
                       fmaf(f.x, cx, f.y * sx));
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);  // LR slot read: stage may be refilled
+      if (lane == 0) ISTAMP(k, 5);
+      s += kNEpi;
+      while (s >= P.nstage) s -= P.nstage;
     }
+    if (lane == 0) TSTAMP(7);
     return;
   }
 
@@ -670,9 +747,12 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
   const int ctid = threadIdx.x;  // consumer thread id, 0 .. kNW*32-1
   if (!UP) griddep_wait();  // a16 comes from the up kernel
   int cur_ai = -1, cur_pass = -1, cur_chunk = -1, pass_tok = 0;
+  int s = 0, ph = 0;
   for (int k = 0; k < nitems; ++k) {
-    const int s = k % P.nstage;
-    mbar_wait(&full[s], (k / P.nstage) & 1);  // acquire: descriptor + bytes visible
+    if (ctid == 0) ISTAMP(k, 1);
+    mbar_wait(&full[s], ph);  // acquire: descriptor + bytes visible
+    if (k == 0 && ctid == 0) TSTAMP(5);
+    if (ctid == 0) ISTAMP(k, 2);
     const ItemDesc dsc = s_desc[s];
     const int gp0 = dsc.gp0, gp1 = dsc.gp1;
     if (dsc.ai != cur_ai || dsc.pass != cur_pass || dsc.chunk != cur_chunk) {
@@ -699,29 +779,44 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
       const int ng = (gp1 - gp0) * 2;
       // only real token rows are built; empty columns read the shared zero row
       // (their sums are never used: MMA columns are independent)
-      for (int task = ctid; task < pass_tok * ng; task += kNW * 32) {
-        const int n = task / ng, g = task - n * ng;
-        float xsum = 0.f, xpsum = 0.f;
-        uint32_t* dst = reinterpret_cast<uint32_t*>(xs + n * P.xs_stride + g * 64);
-        {
-          const uint16_t* row = UP ? A.x + static_cast<int64_t>(s_ctok[n]) * A.hidden
-                                   : A.a16 + static_cast<int64_t>(s_cpair[n]) * A.ffn;
-          const int kk = k0 + g * 64;
-          const bool vec = (kk + 64 <= P.K) && ((reinterpret_cast<uintptr_t>(row + kk) & 15) == 0);
-#pragma unroll 2
-          for (int c8 = 0; c8 < 8; ++c8) {
-            uint4 raw;
-            if (vec) {
-              raw = __ldg(reinterpret_cast<const uint4*>(row + kk) + c8);
+      // one 16-byte x load per thread-task (8 columns), two tasks in flight per
+      // thread; the 8 lanes of a (token, group) reduce its sums by shuffles
+      const int ntask = pass_tok * ng * 8;
+      for (int base = 0; base < ntask; base += 2 * kNW * 32) {
+        uint4 raw[2];
+        int tn[2], tg[2];
+        bool ok[2];
+        const int c8 = ctid & 7;  // == task & 7 (base is a multiple of 8)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int task = base + u * kNW * 32 + ctid;
+          ok[u] = task < ntask;
+          const int ng8 = ok[u] ? (task >> 3) : 0;
+          tn[u] = ng8 / ng;
+          tg[u] = ng8 - tn[u] * ng;
+          raw[u] = make_uint4(0u, 0u, 0u, 0u);
+          if (ok[u]) {
+            const uint16_t* row = UP ? A.x + static_cast<int64_t>(s_ctok[tn[u]]) * A.hidden
+                                     : A.a16 + static_cast<int64_t>(s_cpair[tn[u]]) * A.ffn;
+            const int kk = k0 + tg[u] * 64 + c8 * 8;
+            if (kk + 8 <= P.K && (reinterpret_cast<uintptr_t>(row + kk) & 15) == 0) {
+              raw[u] = __ldg(reinterpret_cast<const uint4*>(row + kk));
             } else {
               uint16_t h[8];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) h[j] = (kk + c8 * 8 + j < P.K) ? row[kk + c8 * 8 + j] : 0;
-              raw = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16),
-                               h[4] | (uint32_t(h[5]) << 16), h[6] | (uint32_t(h[7]) << 16));
+              for (int j = 0; j < 8; ++j) h[j] = (kk + j < P.K) ? row[kk + j] : 0;
+              raw[u] = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16),
+                                  h[4] | (uint32_t(h[5]) << 16), h[6] | (uint32_t(h[7]) << 16));
             }
-            const float im = inv_mult(c8);  // slot j = c8 for columns c8*8 .. c8*8+7
-            const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+          }
+        }
+        const float im = inv_mult(c8);  // slot j = c8 for columns c8*8 .. c8*8+7
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          float xsum = 0.f, xpsum = 0.f;
+          if (ok[u]) {
+            uint32_t* dst = reinterpret_cast<uint32_t*>(xs + tn[u] * P.xs_stride + tg[u] * 64);
+            const uint32_t w4[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
             // column c8*8 + 2*tj + e -> 16-block c8/2, position tj*4 + (c8&1)*2 + e
 #pragma unroll
             for (int tj = 0; tj < 4; ++tj) {
@@ -733,8 +828,13 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
                   static_cast<uint32_t>(f2bf(plo)) | (static_cast<uint32_t>(f2bf(phi)) << 16);
             }
           }
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) {
+            xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
+            xpsum += __shfl_xor_sync(0xffffffffu, xpsum, o);
+          }
+          if (ok[u] && c8 == 0) sums[tg[u] * TPP + tn[u]] = make_float2(xsum, -128.0f * xpsum);
         }
-        sums[g * TPP + n] = make_float2(xsum, -128.0f * xpsum);
       }
       consumer_sync();
     }
@@ -834,6 +934,11 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // weights consumed
+    if (ctid == 0) ISTAMP(k, 3);
+    if (++s == P.nstage) {
+      s = 0;
+      ph ^= 1;
+    }
     // ---- partials to the epilogue ring (slot reused every kNRed items)
     const int rs = k % kNRed;
     mbar_wait(&rempty[rs], ((k / kNRed) & 1) ^ 1);
@@ -850,6 +955,22 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(TiledParams P) {
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&rfull[rs]);
+    if (ctid == 0) ISTAMP(k, 4);
+  }
+  if (ctid == 0) TSTAMP(6);
+}
+
+void tiled_stamps_copy(uint64_t* host, int n) {
+  const int n0 = 2 * kTStampCtas * 8;
+  if (n > n0) {
+    cudaMemcpyFromSymbol(host + n0, g_item_stamps, sizeof(uint64_t) * (n - n0));
+    void* dev = nullptr;
+    if (cudaGetSymbolAddress(&dev, g_item_stamps) == cudaSuccess) cudaMemset(dev, 0, sizeof(g_item_stamps));
+    n = n0;
+  }
+  if (cudaMemcpyFromSymbol(host, g_tiled_stamps, sizeof(uint64_t) * n) == cudaSuccess) {
+    void* dev = nullptr;
+    if (cudaGetSymbolAddress(&dev, g_tiled_stamps) == cudaSuccess) cudaMemset(dev, 0, sizeof(g_tiled_stamps));
   }
 }
 

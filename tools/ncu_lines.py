@@ -10,6 +10,12 @@ import sys
 rows = list(csv.reader(open(sys.argv[1])))
 want = sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+# optional "file.cu:LO-HI": only report lines in that range (percent of the range)
+rng = None
+if len(sys.argv) > 4:
+    f, lohi = sys.argv[4].split(":")
+    lo, hi = map(int, lohi.split("-"))
+    rng = (f, lo, hi)
 cur_file = cur_fn = None
 hdr = None
 agg = collections.defaultdict(lambda: [0, 0, ""])
@@ -36,6 +42,8 @@ for r in rows:
         agg[k][0] += s
         agg[k][1] += e
         agg[k][2] = r[1][:88]
+if rng:
+    agg = {k: v for k, v in agg.items() if k[0] == rng[0] and rng[1] <= k[1] <= rng[2]}
 tot = sum(v[0] for v in agg.values()) or 1
 toti = sum(v[1] for v in agg.values()) or 1
 print("samples", tot, "instructions", toti)
