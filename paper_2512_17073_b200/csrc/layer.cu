@@ -489,6 +489,10 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   ra.spec_blocks = spec ? 2 * ((L->maxr + 7) / 8) : 0;
   ra.t2_zero = L->maxr ? L->t : nullptr;
   ra.y_zero = y;
+  // PDL: the router's constant-data prologue (expert tables, gate rows, code
+  // warm-up) overlaps the previous kernel's tail; it waits before touching x,
+  // y, t or the plan
+  ra.pdl = (!prof && L->pdl) ? 1 : 0;
   lrc_status s = launch_route(ra, st);
   if (s != LRC_OK) return s;
   ++launches;

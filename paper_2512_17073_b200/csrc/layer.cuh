@@ -57,6 +57,7 @@ struct RouteArgs {
   float* t2_zero;             // zero t[b][e][2][:] (tiled path accumulates into it)
   float* y_zero;              // zero y rows
   int stamp;                  // LRC_ROUTE_STAMPS: per-CTA %globaltimer stamps (debug)
+  int pdl;                    // launched as a programmatic dependent of the previous kernel
 };
 
 // Row j of a quantized V (group size 64, BITS-bit LSB-first stream) dotted
@@ -126,8 +127,6 @@ __device__ void vrow_dot_tokens(const lrc_qmat& V, int j, const uint16_t* __rest
   for (int t = 0; t < MAXT; ++t) acc[t] = warp_sum(acc[t]);
 }
 
-__device__ void build_plan_block(const PlanArgs& pa, const int32_t* topk_idx,
-                                 const float* topk_w, int B, int k);
 int route_tiles(int64_t B);
 lrc_status launch_route(const RouteArgs& ra, cudaStream_t st);
 

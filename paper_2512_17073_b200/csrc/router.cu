@@ -5,12 +5,15 @@
 // Reference: ref/moe.py:165-193 (route/softmax), ref/moe.py:234-258 (mixing,
 // shared experts), ref/lowrank.py:165 (factored U.(V.x) order).
 //
-// Grid (token tiles, experts, 1 + V.x row blocks).  CTA (tile, e, 0) computes
-// the logits of up to kTT tokens against gate row e; CTAs (tile, e, z>0) the
-// speculative V.x rows.  The last CTA of a token tile (atomic ticket) runs the
-// warp-parallel softmax + top-k for the tile; the last tile builds the pair
-// plan -- one launch, no host round trip.  Code is kept compact on purpose:
-// cold straight-line paths in a huge kernel stall on instruction fetch.
+// Grid (token tiles x kCl, 1 + aux rows), clusters of kCl CTAs along x: row 0
+// of a tile's cluster computes its logits (CTA r: experts r, r + kCl, ...) and
+// stores them into the leader CTA's shared memory (DSMEM); after one cluster
+// barrier the leader runs the warp-parallel softmax + top-k and, for a single
+// token tile, builds the pair plan straight from shared memory (several
+// tiles: the last leader, by atomic ticket).  Aux rows zero the accumulated
+// outputs and compute the speculative V.x rows.  One launch, no host round
+// trip, and at decode sizes no global-memory handoff inside the kernel: every
+// dependent global round trip costs ~1 us while the weight stream saturates HBM.
 #include <float.h>
 #include <stdlib.h>
 
@@ -61,8 +64,16 @@ __device__ __noinline__ double pw_sum_small(const double* v, int n) {
 // exp, divide by the numpy-ordered sum), then k rounds of warp argmax with the
 // stable tie rule of np.argsort(-w, kind="stable") (ref/moe.py:190): equal
 // weights go to the lower expert index.  lg has E weights + 64 scratch.
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __noinline__ void select_topk_warp(double* lg, int E, int k, int renorm, int64_t b,
-                                              double* probs, int32_t* topk_idx, float* topk_w) {
+                                              double* probs, int32_t* topk_idx, float* topk_w,
+                                              int32_t* s_idx, float* s_w,
+                                              unsigned long long* dbg_stamp = nullptr) {
   const int lane = threadIdx.x & 31;
   double mx = -DBL_MAX;
   for (int e = lane; e < E; e += 32) mx = fmax(mx, lg[e]);
@@ -77,6 +88,7 @@ __device__ __noinline__ void select_topk_warp(double* lg, int E, int k, int reno
     if (probs) probs[b * E + e] = lg[e];
   }
   __syncwarp();
+  if (dbg_stamp != nullptr && lane == 0) *dbg_stamp = globaltimer();
   uint32_t taken = 0;  // bit m: element lane + 32m already selected
   for (int j = 0; j < k; ++j) {
     double bv = -DBL_MAX;
@@ -97,10 +109,12 @@ __device__ __noinline__ void select_topk_warp(double* lg, int E, int k, int reno
     if ((be & 31) == lane) taken |= 1u << (be >> 5);
     if (lane == 0) {
       topk_idx[b * k + j] = be;
+      s_idx[j] = be;
       lg[E + j] = bv;  // scratch after the E weights
     }
   }
   __syncwarp();
+  if (dbg_stamp != nullptr && lane == 0) dbg_stamp[5] = globaltimer();
   if (lane == 0) {
     double* mix = lg + E;
     if (renorm) {  // ref/moe.py:234-236, mix.sum() in numpy order
@@ -108,13 +122,17 @@ __device__ __noinline__ void select_topk_warp(double* lg, int E, int k, int reno
       if (s > 0.0)
         for (int j = 0; j < k; ++j) mix[j] = __ddiv_rn(mix[j], s);
     }
-    for (int j = 0; j < k; ++j) topk_w[b * k + j] = static_cast<float>(mix[j]);
+    for (int j = 0; j < k; ++j) {
+      topk_w[b * k + j] = static_cast<float>(mix[j]);
+      s_w[j] = static_cast<float>(mix[j]);
+    }
   }
 }
 
 __device__ __forceinline__ void griddep_launch_dependents_r() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+__device__ __forceinline__ void griddep_wait_r() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Padded shared-memory x row: 64-column groups at a stride of 66 elements.
 __host__ __device__ inline int xs_row_elems(int d) { return ((d + 63) / 64) * 66; }
@@ -126,8 +144,12 @@ __device__ inline int xs_col(int c) { return (c >> 6) * 66 + (c & 63); }
 // router and the expert kernels (< 1% extra bytes at decode sizes).  x rows
 // come from shared memory (xs: nb x d bf16); each lane preloads the code words
 // of its whole groups, then loops over tokens.
-__device__ __noinline__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* xs, int64_t b0,
-                                          int nb, int e, int blk) {
+__device__ __forceinline__ float code_f(uint32_t c) {  // exact float of a small code
+  return __uint_as_float(0x4B000000u | c) - 8388608.0f;
+}
+
+__device__ __noinline__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* xs, const float* xsum,
+                                          int64_t b0, int nb, int e, int blk) {
   const lrc_expert& E = ra.experts[e];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nblk1 = (ra.maxr + 7) / 8;
@@ -161,33 +183,47 @@ __device__ __noinline__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* x
       s[h] = nv[h] > 0 ? h2f(V.scales[static_cast<int64_t>(j) * gpr + g]) : 0.0f;
       z[h] = nv[h] > 0 ? h2f(V.zeros[static_cast<int64_t>(j) * gpr + g]) : 0.0f;
     }
+    // each code is decoded once (exact float via the 2^23 magic, no XU
+    // conversion) and applied to every token of the tile; sum(x) per group
+    // comes precomputed from the staging pass (xsum[t][g])
     const int ldx = xs_row_elems(ra.d);
-    for (int t = 0; t < nb; ++t) {
-      const uint32_t* xr = reinterpret_cast<const uint32_t*>(xs + t * ldx);
-      float acc = 0.0f;
+    const uint32_t* xs32 = reinterpret_cast<const uint32_t*>(xs);
+    float acc[kTT];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float cx = 0.0f, sx = 0.0f;
-        const uint32_t* xg = xr + (lane + 32 * h) * 33;
+    for (int t = 0; t < kTT; ++t) acc[t] = 0.0f;
 #pragma unroll
-        for (int i2 = 0; i2 < 32; ++i2) {
-          if (2 * i2 < nv[h]) {
-            const uint32_t xw = xg[i2];
+    for (int h = 0; h < 2; ++h) {
+      if (nv[h] == 0) continue;
+      const int g = lane + 32 * h;
+      float cx[kTT];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int bit = (2 * i2 + q) * 3;
-              const float c = static_cast<float>(
-                  __funnelshift_r(w[h][bit >> 5], w[h][(bit >> 5) + 1], bit & 31) & 7u);
-              const float xv = q ? __uint_as_float(xw & 0xffff0000u) : __uint_as_float(xw << 16);
-              cx = fmaf(c, xv, cx);
-              sx += xv;
+      for (int t = 0; t < kTT; ++t) cx[t] = 0.0f;
+      // two chunks of 32 codes = exactly 3 words each (static word indices)
+      for (int ch = 0; ch < 2; ++ch) {
+        if (32 * ch >= nv[h]) break;
+        const uint32_t q[4] = {ch ? w[h][3] : w[h][0], ch ? w[h][4] : w[h][1], ch ? w[h][5] : w[h][2],
+                               ch ? w[h][6] : w[h][3]};
+#pragma unroll
+        for (int i2 = 0; i2 < 16; ++i2) {
+          const int bit0 = 6 * i2, bit1 = bit0 + 3;
+          const float c0 = code_f(__funnelshift_r(q[bit0 >> 5], q[(bit0 >> 5) + 1], bit0 & 31) & 7u);
+          const float c1 = code_f(__funnelshift_r(q[bit1 >> 5], q[(bit1 >> 5) + 1], bit1 & 31) & 7u);
+#pragma unroll
+          for (int t = 0; t < kTT; ++t)
+            if (t < nb) {
+              const uint32_t xw = xs32[t * (ldx / 2) + g * 33 + 16 * ch + i2];
+              cx[t] = fmaf(c0, __uint_as_float(xw << 16), fmaf(c1, __uint_as_float(xw & 0xffff0000u), cx[t]));
             }
-          }
         }
-        acc = fmaf(s[h], cx, fmaf(z[h], sx, acc));
       }
-      acc = warp_sum(acc);
-      if (lane == 0) tout[t * tstride] = acc;
+#pragma unroll
+      for (int t = 0; t < kTT; ++t)
+        if (t < nb) acc[t] = fmaf(s[h], cx[t], fmaf(z[h], xsum[t * 64 + g], acc[t]));
+    }
+#pragma unroll
+    for (int t = 0; t < kTT; ++t) {
+      const float v = warp_sum(acc[t]);
+      if (lane == 0 && t < nb) tout[t * tstride] = v;
     }
     return;
   }
@@ -212,12 +248,103 @@ __device__ unsigned long long g_route_stamps[kStampCtas * 8];
     }                                                                                 \
   } while (0)
 
+constexpr int kCl = 8;  // CTAs per router cluster: one cluster per token tile
+
+// barrier of the kRThreads worker threads (the warm-up warp never joins)
+__device__ __forceinline__ void wsync() { asm volatile("bar.sync 1, %0;" ::"n"(kRThreads) : "memory"); }
+
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// store v into CTA `rank`'s shared memory at the address of `p` in its layout
+__device__ __forceinline__ void st_cl_f64(const double* p, uint32_t rank, double v) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_cl_u64(const uint64_t* p, uint32_t rank, uint64_t v) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(ra), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_cl_u8(const uint8_t* p, uint32_t rank, uint8_t v) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(ra), "h"(static_cast<unsigned short>(v)) : "memory");
+}
+
 template <typename T>
-__global__ void __launch_bounds__(kRThreads) route_kernel(const __grid_constant__ RouteArgs ra) {
-  extern __shared__ __align__(16) uint8_t rsm[];  // [kTT*(E+64)] f64 logits | x tile (bf16)
+__device__ __forceinline__ void load_x2(const T* x, int64_t i, double& a, double& b);
+template <>
+__device__ __forceinline__ void load_x2<double>(const double* x, int64_t i, double& a, double& b) {
+  const double2 v = __ldg(reinterpret_cast<const double2*>(x + i));
+  a = v.x;
+  b = v.y;
+}
+template <>
+__device__ __forceinline__ void load_x2<float>(const float* x, int64_t i, double& a, double& b) {
+  const float2 v = __ldg(reinterpret_cast<const float2*>(x + i));
+  a = v.x;
+  b = v.y;
+}
+template <>
+__device__ __forceinline__ void load_x2<uint16_t>(const uint16_t* x, int64_t i, double& a, double& b) {
+  const uint32_t v = __ldg(reinterpret_cast<const unsigned int*>(x + i));
+  a = bf2f(v & 0xffffu);
+  b = bf2f(v >> 16);
+}
+
+// Per-expert tile pointers the plan builder copies into ActiveRec.
+struct ExpertTiles {
+  const uint8_t* up;
+  const uint8_t* down;
+  const uint8_t* up_lr;
+  const uint8_t* down_lr;
+  int up_lr_bytes, down_lr_bytes;
+};
+
+__device__ __noinline__ void build_plan_block(const PlanArgs& pa, const int32_t* tk_idx,
+                                              const float* tk_w, const uint8_t* hc,
+                                              const ExpertTiles* et, int B, int k);
+__device__ __noinline__ void build_plan_warp(const PlanArgs& pa, const int32_t* tk_idx,
+                                             const float* tk_w, const uint8_t* hc,
+                                             const ExpertTiles* et, int B, int k);
+
+// Scratch of the warm-up warp: select + warp plan run once on dummy data while
+// the logits are computed, so the leader's serial tail finds its code in the
+// SM's instruction cache (a cold line costs an L2 round trip, ~150 ns each).
+struct WarmScratch {
+  double lg[LRC_MAX_EXPERTS + 64];
+  int32_t idx[64];
+  float w[64];
+  int pe[32], pt[32], pc[32], pl[32], cl[32], act[32], aoff[32], acnt[32], cnt[4];
+  float pw[32];
+  ActiveRec arec[32];
+};
+__device__ __noinline__ void warm_tail(const RouteArgs& ra, WarmScratch& ws, const uint8_t* hc,
+                                       const ExpertTiles* et);
+
+template <typename T>
+__global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_constant__ RouteArgs ra) {
+  extern __shared__ __align__(16) uint8_t rsm[];  // leader: [kTT][E+64] f64 logits | aux: x tile
   __shared__ double s_red[kTT][kRThreads / 32];
   __shared__ int s_last;
-  const int tile = blockIdx.x, e = blockIdx.y, z = blockIdx.z;
+  __shared__ int32_t s_tidx[kTT * 64];
+  __shared__ float s_tw[kTT * 64];
+  __shared__ uint8_t s_hc[LRC_MAX_EXPERTS];
+  __shared__ ExpertTiles s_et[LRC_MAX_EXPERTS];
+  __shared__ WarmScratch s_warm;
+  const int rank = static_cast<int>(cl_rank());
+  const int tile = blockIdx.x / kCl, ntiles = gridDim.x / kCl, row = blockIdx.y;
   const int64_t b0 = static_cast<int64_t>(tile) * kTT;
   const int64_t rem = ra.B - b0;
   const int nb = rem < kTT ? static_cast<int>(rem) : kTT;
@@ -225,159 +352,272 @@ __global__ void __launch_bounds__(kRThreads) route_kernel(const __grid_constant_
   const T* x = static_cast<const T*>(ra.x);
   RSTAMP(0);
   griddep_launch_dependents_r();
-  if (z == 0) {
-    if (e < ra.E) {
-      const double* g = ra.gate_t + static_cast<int64_t>(e) * ra.d;
-      double acc[kTT];
+  if (warp == kRThreads / 32) {  // warm-up warp: leader of a row-0 cluster only
+    if (row == 0) {
+      // arrive on the cluster barrier first (never waits): the logits handoff
+      // must not wait for this warp's cold instruction fetches
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+      if (rank == 0 && ra.plan.ticket != nullptr) warm_tail(ra, s_warm, s_hc, s_et);
+    }
+    return;
+  }
+  if (row > 0) {
+    // ---- aux CTAs: speculative V.x rows (single tile) + zeroing of the outputs
+    if (ra.pdl) griddep_wait_r();  // x, y and t belong to the previous kernel until here
+    const int aux = (row - 1) * kCl + rank, naux = (gridDim.y - 1) * kCl;
+    if (ra.y_zero != nullptr) {
+      const int64_t n = static_cast<int64_t>(nb) * ra.d;
+      for (int64_t i = static_cast<int64_t>(aux) * kRThreads + threadIdx.x; i < n;
+           i += static_cast<int64_t>(naux) * kRThreads)
+        ra.y_zero[b0 * ra.d + i] = 0.0f;
+    }
+    if (ra.t2_zero != nullptr && ra.maxr > 0) {
+      const int n = nb * ra.ne * ra.maxr;
+      for (int i = aux * kRThreads + threadIdx.x; i < n; i += naux * kRThreads) {
+        const int t = i / (ra.ne * ra.maxr), r2 = i - t * ra.ne * ra.maxr;
+        const int e = r2 / ra.maxr, j = r2 - e * ra.maxr;
+        ra.t2_zero[(((b0 + t) * ra.ne + e) * 3 + 2) * ra.maxr + j] = 0.0f;
+      }
+    }
+    if constexpr (sizeof(T) == 2) {
+      if (ra.spec_blocks > 0 && aux < ra.ne * ra.spec_blocks) {
+        // stage the tile's token rows (padded: 64-column groups at a stride of
+        // 33 words, so lanes that each walk their own group hit distinct banks)
+        uint16_t* xs = reinterpret_cast<uint16_t*>(rsm);
+        const uint16_t* xg = reinterpret_cast<const uint16_t*>(x) + b0 * ra.d;
+        const int ldx = xs_row_elems(ra.d);
+        if ((ra.d % 64) == 0 && (reinterpret_cast<uintptr_t>(xg) & 3) == 0) {
+          const int wpr = ra.d / 2;  // words per token row
+          uint32_t* xs32 = reinterpret_cast<uint32_t*>(xs);
+          const uint32_t* xg32 = reinterpret_cast<const uint32_t*>(xg);
+          constexpr int U = 8;  // loads in flight per thread: one round trip per 8 KB
+          for (int base = 0; base < nb * wpr; base += U * kRThreads) {
+            uint32_t v[U];
 #pragma unroll
-      for (int t = 0; t < kTT; ++t) acc[t] = 0.0;
-#pragma unroll 4
+            for (int u = 0; u < U; ++u) {
+              const int i = base + u * kRThreads + threadIdx.x;
+              v[u] = i < nb * wpr ? __ldg(xg32 + i) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int i = base + u * kRThreads + threadIdx.x;
+              if (i < nb * wpr) {
+                const int t = i / wpr, w = i - t * wpr;
+                xs32[t * (ldx / 2) + (w >> 5) * 33 + (w & 31)] = v[u];
+              }
+            }
+          }
+        } else {
+          for (int i = threadIdx.x; i < nb * ra.d; i += kRThreads) {
+            const int t = i / ra.d, c = i - t * ra.d;
+            xs[t * ldx + xs_col(c)] = xg[i];
+          }
+        }
+        wsync();
+        // per (token, 64-column group) sums of x for the zero-point term
+        float* xsum = reinterpret_cast<float*>(rsm + kTT * ldx * 2);
+        const int gpr = (ra.d + 63) / 64;
+        if (gpr <= 64)
+          for (int i = threadIdx.x; i < nb * gpr; i += kRThreads) {
+            const int t = i / gpr, g = i - t * gpr;
+            const uint32_t* r = reinterpret_cast<const uint32_t*>(xs) + t * (ldx / 2) + g * 33;
+            const int nw = min(32, (ra.d - g * 64 + 1) / 2);
+            float a = 0.0f;
+            for (int q = 0; q < nw; ++q) a += __uint_as_float(r[q] << 16) + __uint_as_float(r[q] & 0xffff0000u);
+            xsum[t * 64 + g] = a;
+          }
+        wsync();
+        spec_lr_rows(ra, xs, xsum, b0, nb, aux % ra.ne, aux / ra.ne);
+      }
+    }
+    RSTAMP(1);
+    return;
+  }
+  // ---- logits: cluster CTA `rank` takes experts rank, rank + kCl, ...; every
+  // gate load of a row is in flight at once (pairs, 8 per thread for d = 4096)
+  const bool leader = rank == 0;
+  const int NE = ra.plan.num_experts + ra.plan.num_shared;
+  if (rank == 1 && ra.plan.ticket != nullptr) {
+    // plan inputs for the leader, fetched by a helper CTA while the leader
+    // computes its logits, stored into the leader's shared memory (DSMEM)
+    for (int e = threadIdx.x; e < NE; e += kRThreads) {
+      st_cl_u8(&s_hc[e], 0, ra.plan.has_comp[e]);
+      if (ra.plan.arec != nullptr) {
+        const lrc_expert& X = ra.plan.experts[e];
+        const LrLayout L = lr_layout(X);
+        const ExpertTiles et{X.up_tiles, X.down_tiles, X.up_lr_tiles, X.down_lr_tiles, L.up_total, L.down_total};
+        static_assert(sizeof(ExpertTiles) == 40, "ExpertTiles layout");
+        const uint64_t* src = reinterpret_cast<const uint64_t*>(&et);
+        uint64_t* dst = reinterpret_cast<uint64_t*>(&s_et[e]);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) st_cl_u64(dst + q, 0, src[q]);
+      }
+    }
+  }
+  if (ra.pdl) {
+    // the gate rows are constant: pull this CTA's into L1 while the previous
+    // kernel drains, then wait before reading x
+    for (int e = rank; e < ra.E; e += kCl)
+      for (int l = threadIdx.x; l < (ra.d * 8 + 127) / 128; l += kRThreads)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(ra.gate_t + static_cast<int64_t>(e) * ra.d + l * 16));
+    griddep_wait_r();
+  }
+  double* lg = reinterpret_cast<double*>(rsm);  // leader's layout: per token E weights + 64 scratch
+  const int ldl = ra.E + 64;
+  for (int e = rank; e < ra.E; e += kCl) {
+    const double* g = ra.gate_t + static_cast<int64_t>(e) * ra.d;
+    double acc[kTT];
+#pragma unroll
+    for (int t = 0; t < kTT; ++t) acc[t] = 0.0;
+    if ((ra.d & 1) == 0) {
+      // explicit batches: the U gate pairs and U x pairs per token are all in
+      // flight before the first use (a runtime-bounded loop would serialise)
+      constexpr int U = 8;
+      const int np = ra.d >> 1;
+      for (int base = 0; base < np; base += U * kRThreads) {
+        double2 gv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i2 = base + u * kRThreads + threadIdx.x;
+          gv[u] = i2 < np ? __ldg(reinterpret_cast<const double2*>(g) + i2) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int t = 0; t < kTT; ++t)
+          if (t < nb) {
+            double xa[U], xb[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int i2 = base + u * kRThreads + threadIdx.x;
+              if (i2 < np) {
+                load_x2<T>(x, (b0 + t) * ra.d + 2 * i2, xa[u], xb[u]);
+              } else {
+                xa[u] = xb[u] = 0.0;
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[t] = fma(gv[u].y, xb[u], fma(gv[u].x, xa[u], acc[t]));
+          }
+      }
+    } else {
       for (int i = threadIdx.x; i < ra.d; i += kRThreads) {
         const double gv = __ldg(g + i);
 #pragma unroll
         for (int t = 0; t < kTT; ++t)
           if (t < nb) acc[t] = fma(gv, load_x<T>(x, (b0 + t) * ra.d + i), acc[t]);
       }
+    }
+    if (rank != 0) RSTAMP(3);
 #pragma unroll
-      for (int t = 0; t < kTT; ++t) {
-        const double v = warp_sum_d(acc[t]);
-        if (lane == 0) s_red[t][warp] = v;
-      }
-      __syncthreads();
-      if (threadIdx.x < nb) {
-        double s = 0.0;
-        for (int w = 0; w < kRThreads / 32; ++w) s += s_red[threadIdx.x][w];
-        ra.logits[(b0 + threadIdx.x) * ra.E + e] = s;
-      }
+    for (int t = 0; t < kTT; ++t) {
+      const double v = warp_sum_d(acc[t]);
+      if (lane == 0) s_red[t][warp] = v;
     }
-    RSTAMP(6);
-    if (ra.t2_zero != nullptr && ra.maxr > 0)
-      for (int i = threadIdx.x; i < nb * ra.maxr; i += kRThreads) {
-        const int t = i / ra.maxr, j = i - t * ra.maxr;
-        ra.t2_zero[(((b0 + t) * ra.ne + e) * 3 + 2) * ra.maxr + j] = 0.0f;
-      }
-    if (ra.y_zero != nullptr && e == 0)
-      for (int64_t i = threadIdx.x; i < static_cast<int64_t>(nb) * ra.d; i += kRThreads)
-        ra.y_zero[b0 * ra.d + i] = 0.0f;
-  } else if constexpr (sizeof(T) == 2) {
-    // stage the tile's token rows once (16-byte copies), then the V.x rows
-    // padded layout: 64-column groups at a stride of 33 words, so lanes that
-    // each walk their own group hit distinct banks
-    uint16_t* xs = reinterpret_cast<uint16_t*>(rsm);
-    const uint16_t* xg = reinterpret_cast<const uint16_t*>(x) + b0 * ra.d;
-    const int ldx = xs_row_elems(ra.d);
-    if ((ra.d % 64) == 0 && (reinterpret_cast<uintptr_t>(xg) & 3) == 0) {
-      const int wpr = ra.d / 2;  // words per token row
-      uint32_t* xs32 = reinterpret_cast<uint32_t*>(xs);
-      const uint32_t* xg32 = reinterpret_cast<const uint32_t*>(xg);
-      for (int i = threadIdx.x; i < nb * wpr; i += kRThreads) {
-        const int t = i / wpr, w = i - t * wpr;
-        xs32[t * (ldx / 2) + (w >> 5) * 33 + (w & 31)] = __ldg(xg32 + i);
-      }
-    } else {
-      for (int i = threadIdx.x; i < nb * ra.d; i += kRThreads) {
-        const int t = i / ra.d, c = i - t * ra.d;
-        xs[t * ldx + xs_col(c)] = xg[i];
-      }
+    wsync();
+    if (rank != 0) RSTAMP(4);
+    if (threadIdx.x < nb) {
+      double sum = 0.0;
+      for (int w = 0; w < kRThreads / 32; ++w) sum += s_red[threadIdx.x][w];
+      st_cl_f64(lg + threadIdx.x * ldl + e, 0, sum);  // into the leader's shared memory
     }
-    __syncthreads();
-    spec_lr_rows(ra, xs, b0, nb, e, z - 1);
+    wsync();
+    if (rank != 0) RSTAMP(5);
   }
-  // ---- last CTA of this token tile: softmax + top-k
-  RSTAMP(1);
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0)
-    s_last = (atomicAdd(&ra.tile_ticket[tile], 1) == static_cast<int>(gridDim.y * gridDim.z) - 1);
-  __syncthreads();
-  RSTAMP(2);
-  if (!s_last) return;
-  __threadfence();
-  double* lg = reinterpret_cast<double*>(rsm);  // per token: E weights + 64 scratch
-  const int ldl = ra.E + 64;
-  for (int i = threadIdx.x; i < nb * ra.E; i += kRThreads)
-    lg[(i / ra.E) * ldl + i % ra.E] = __ldcg(ra.logits + b0 * ra.E + i);
-  __syncthreads();
+  cl_sync();  // release/acquire: the leader sees every logit
+  RSTAMP(6);
+  if (!leader) return;
+  // ---- leader: softmax + top-k (warp per token), then the pair plan
   if (warp < nb)
     select_topk_warp(lg + warp * ldl, ra.E, ra.k, ra.renorm, b0 + warp, ra.probs, ra.topk_idx,
-                     ra.topk_w);
-  if (threadIdx.x == 0) ra.tile_ticket[tile] = 0;
+                     ra.topk_w, s_tidx + warp * ra.k, s_tw + warp * ra.k,
+                     (ra.stamp && warp == 0 && blockIdx.y * gridDim.x + blockIdx.x < kStampCtas)
+                         ? &g_route_stamps[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + 2]
+                         : nullptr);
   RSTAMP(3);
   if (ra.plan.ticket == nullptr) return;
-  // ---- last tile: build the pair plan for the whole batch
+  wsync();
+  if (ntiles == 1) {  // decode: the whole plan from shared memory, no ticket
+    if (ra.B * (ra.k + ra.plan.num_shared) <= 32) {
+      if (warp == 0) build_plan_warp(ra.plan, s_tidx, s_tw, s_hc, s_et, static_cast<int>(ra.B), ra.k);
+    } else {
+      build_plan_block(ra.plan, s_tidx, s_tw, s_hc, s_et, static_cast<int>(ra.B), ra.k);
+    }
+    RSTAMP(5);
+    return;
+  }
+  // several token tiles: the last leader builds the plan from the global top-k
   __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(ra.plan.ticket, 1) == static_cast<int>(gridDim.x) - 1);
-  __syncthreads();
+  wsync();
+  if (threadIdx.x == 0) s_last = (atomicAdd(ra.plan.ticket, 1) == ntiles - 1);
+  wsync();
   RSTAMP(4);
   if (!s_last) return;
   __threadfence();
-  build_plan_block(ra.plan, ra.topk_idx, ra.topk_w, static_cast<int>(ra.B), ra.k);
+  build_plan_block(ra.plan, ra.topk_idx, ra.topk_w, s_hc, s_et, static_cast<int>(ra.B), ra.k);
   if (threadIdx.x == 0) *ra.plan.ticket = 0;
-  __syncthreads();
   RSTAMP(5);
 }
 
-// Pair plan: pair p = b*P + j, P = k + S.  j < k: routed expert topk_idx[b][j],
-// weight topk_w, compensated iff j < n.  j >= k: shared expert E + (j-k),
+// Pair plan: pair p = b*P + j, P = k + S.  j < k: routed expert tk_idx[b][j],
+// weight tk_w, compensated iff j < n.  j >= k: shared expert E + (j-k),
 // weight 1, compensated iff compensate_shared (ref/moe.py:249-258).
 // Pairs are grouped by expert, ascending pair id inside each expert (stable).
-__device__ __noinline__ void build_plan_block(const PlanArgs& pa, const int32_t* topk_idx,
-                                              const float* topk_w, int B, int k) {
+// tk_idx / tk_w may point to shared (single tile) or global memory; hc and et
+// are the has-comp flags and tile pointers staged in shared memory.
+__device__ __noinline__ void build_plan_block(const PlanArgs& pa, const int32_t* tk_idx,
+                                              const float* tk_w, const uint8_t* hc,
+                                              const ExpertTiles* et, int B, int k) {
   const int P = k + pa.num_shared;
   const int NP = B * P;
   const int NE = pa.num_experts + pa.num_shared;
   __shared__ int s_cnt[LRC_MAX_EXPERTS];
   __shared__ int s_off[LRC_MAX_EXPERTS + 1];
-  for (int e = threadIdx.x; e < NE; e += blockDim.x) s_cnt[e] = 0;
-  __syncthreads();
-  for (int p = threadIdx.x; p < NP; p += blockDim.x) {
+  __shared__ int s_start[LRC_MAX_EXPERTS];
+  __shared__ int s_act[LRC_MAX_EXPERTS];
+  __shared__ uint32_t s_cm[LRC_MAX_EXPERTS];
+  __shared__ int s_na;
+  for (int e = threadIdx.x; e < NE; e += kRThreads) {
+    s_cnt[e] = 0;
+    s_cm[e] = 0;
+  }
+  wsync();
+  auto pair_of = [&](int p, int& e, float& w) {
     const int b = p / P, j = p - b * P;
-    int e;
-    float w;
     if (j < k) {
-      e = __ldcg(topk_idx + b * k + j);
-      w = __ldcg(topk_w + b * k + j);
+      e = tk_idx[b * k + j];
+      w = tk_w[b * k + j];
     } else {
       e = pa.num_experts + (j - k);
       w = 1.0f;
     }
+  };
+  for (int p = threadIdx.x; p < NP; p += kRThreads) {
+    int e;
+    float w;
+    pair_of(p, e, w);
     pa.pair_expert[p] = e;
     pa.pair_w[p] = w;
-    pa.pair_token[p] = b;
+    pa.pair_token[p] = p / P;
     atomicAdd(&s_cnt[e], 1);
   }
-  __syncthreads();
+  wsync();
   if (threadIdx.x == 0) {
     int acc = 0, na = 0;
     for (int e = 0; e < NE; ++e) {
       s_off[e] = acc;
-      acc += s_cnt[e];
+      s_start[e] = acc;
       if (s_cnt[e] > 0) {
         pa.active[na] = e;
-        pa.active_off[na] = s_off[e];
+        pa.active_off[na] = acc;
         pa.active_cnt[na] = s_cnt[e];
-        if (pa.arec != nullptr) {
-          const lrc_expert& X = pa.experts[e];
-          const LrLayout L = lr_layout(X);
-          ActiveRec& R = pa.arec[na];
-          R.up_tiles = X.up_tiles;
-          R.down_tiles = X.down_tiles;
-          R.up_lr_tiles = X.up_lr_tiles;
-          R.down_lr_tiles = X.down_lr_tiles;
-          R.e = e;
-          R.off = s_off[e];
-          R.cnt = s_cnt[e];
-          R.up_lr_bytes = L.up_total;
-          R.down_lr_bytes = L.down_total;
-        }
-        ++na;
+        s_act[na++] = e;
       }
+      acc += s_cnt[e];
     }
     s_off[NE] = acc;
+    s_na = na;
     pa.counts[0] = na;
   }
-  __syncthreads();
+  wsync();
   const int lane = threadIdx.x & 31;
   if (threadIdx.x < 32) {
     // stable scatter: one warp walks the pairs in order; experts present in a
@@ -386,7 +626,9 @@ __device__ __noinline__ void build_plan_block(const PlanArgs& pa, const int32_t*
     for (int base = 0; base < NP; base += 32) {
       const int p = base + lane;
       const bool valid = p < NP;
-      const int e = valid ? pa.pair_expert[p] : -1;
+      int e = -1;
+      float w;
+      if (valid) pair_of(p, e, w);
       int pos = -1;
       unsigned pending = __ballot_sync(0xffffffffu, valid);
       while (pending) {
@@ -404,35 +646,134 @@ __device__ __noinline__ void build_plan_block(const PlanArgs& pa, const int32_t*
       int comp = 0;
       if (valid) {
         const int j = p % P;
-        comp = (j < k) ? ((j < pa.top_n) && pa.has_comp[e]) : (pa.compensate_shared && pa.has_comp[e]);
+        comp = (j < k) ? ((j < pa.top_n) && hc[e]) : (pa.compensate_shared && hc[e]);
       }
       const unsigned m = __ballot_sync(0xffffffffu, comp);
       if (valid) {
         const int slot = comp ? count + __popc(m & ((1u << lane) - 1u)) : -1;
         pa.pair_comp[p] = slot;
-        if (comp) pa.comp_list[slot] = p;
+        if (comp) {
+          pa.comp_list[slot] = p;
+          atomicOr(&s_cm[e], 1u << min((pos - s_start[e]) >> 3, 31));
+        }
       }
       count += __popc(m);
     }
     if (lane == 0) pa.counts[1] = count;
   }
   if (pa.arec == nullptr) return;
-  // compensated-pair mask per active expert, 8-pair granularity (one warp each)
-  __syncthreads();
-  const int na = pa.counts[0];
-  for (int a = threadIdx.x >> 5; a < na; a += blockDim.x >> 5) {
-    const int off = pa.active_off[a], cnt = pa.active_cnt[a];
-    uint32_t mask = 0;
-    for (int j0 = 0; j0 < cnt; j0 += 32) {
-      const int j = j0 + lane;
-      const bool c = j < cnt && pa.pair_comp[pa.pair_list[off + j]] >= 0;
-      const unsigned bal = __ballot_sync(0xffffffffu, c);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if ((bal >> (8 * q)) & 0xffu) mask |= 1u << min((j0 >> 3) + q, 31);
-    }
-    if (lane == 0) pa.arec[a].cmask = mask;
+  wsync();
+  for (int a = threadIdx.x; a < s_na; a += kRThreads) {
+    const int e = s_act[a];
+    const ExpertTiles& T = et[e];
+    ActiveRec R;
+    R.up_tiles = T.up;
+    R.down_tiles = T.down;
+    R.up_lr_tiles = T.up_lr;
+    R.down_lr_tiles = T.down_lr;
+    R.e = e;
+    R.off = s_start[e];
+    R.cnt = s_cnt[e];
+    R.cmask = s_cm[e];
+    R.up_lr_bytes = T.up_lr_bytes;
+    R.down_lr_bytes = T.down_lr_bytes;
+    R.pad[0] = R.pad[1] = 0;
+    pa.arec[a] = R;
   }
+}
+
+// Decode plan (B * (k + S) <= 32 pairs): one pair per lane, warp-synchronous
+// (match / ballot / reduce), same output as build_plan_block.
+__device__ __noinline__ void build_plan_warp(const PlanArgs& pa, const int32_t* tk_idx,
+                                             const float* tk_w, const uint8_t* hc,
+                                             const ExpertTiles* et, int B, int k) {
+  const int lane = threadIdx.x & 31;
+  const int P = k + pa.num_shared, NP = B * P;
+  const bool valid = lane < NP;
+  int e = 0x7fffffff, j = 0;
+  if (valid) {
+    const int b = lane / P;
+    j = lane - b * P;
+    float w;
+    if (j < k) {
+      e = tk_idx[b * k + j];
+      w = tk_w[b * k + j];
+    } else {
+      e = pa.num_experts + (j - k);
+      w = 1.0f;
+    }
+    pa.pair_expert[lane] = e;
+    pa.pair_w[lane] = w;
+    pa.pair_token[lane] = b;
+  }
+  const unsigned same = __match_any_sync(0xffffffffu, e);  // lanes of my expert, in pair order
+  const int cnt = __popc(same), rk = __popc(same & ((1u << lane) - 1u));
+  int off = 0, nbelow = 0;  // pairs / distinct experts with a smaller id
+  for (int q = 0; q < 32; ++q) {
+    const int eq = __shfl_sync(0xffffffffu, e, q);
+    const unsigned sq = __shfl_sync(0xffffffffu, same, q);
+    off += eq < e;
+    nbelow += (eq < e) && ((sq & ((1u << q) - 1u)) == 0u);
+  }
+  const bool comp = valid && ((j < k) ? (j < pa.top_n && hc[e] != 0) : (pa.compensate_shared && hc[e] != 0));
+  const unsigned cm = __ballot_sync(0xffffffffu, comp);
+  if (valid) {
+    pa.pair_list[off + rk] = lane;
+    const int slot = comp ? __popc(cm & ((1u << lane) - 1u)) : -1;
+    pa.pair_comp[lane] = slot;
+    if (comp) pa.comp_list[slot] = lane;
+  }
+  const uint32_t cmask = __reduce_or_sync(same, comp ? (1u << min(rk >> 3, 31)) : 0u);
+  const bool first = valid && rk == 0;
+  if (first) {
+    pa.active[nbelow] = e;
+    pa.active_off[nbelow] = off;
+    pa.active_cnt[nbelow] = cnt;
+    if (pa.arec != nullptr) {
+      const ExpertTiles& T = et[e];
+      ActiveRec R;
+      R.up_tiles = T.up;
+      R.down_tiles = T.down;
+      R.up_lr_tiles = T.up_lr;
+      R.down_lr_tiles = T.down_lr;
+      R.e = e;
+      R.off = off;
+      R.cnt = cnt;
+      R.cmask = cmask;
+      R.up_lr_bytes = T.up_lr_bytes;
+      R.down_lr_bytes = T.down_lr_bytes;
+      R.pad[0] = R.pad[1] = 0;
+      pa.arec[nbelow] = R;
+    }
+  }
+  const int na = __popc(__ballot_sync(0xffffffffu, first));
+  if (lane == 0) {
+    pa.counts[0] = na;
+    pa.counts[1] = __popc(cm);
+  }
+}
+
+__device__ __noinline__ void warm_tail(const RouteArgs& ra, WarmScratch& ws, const uint8_t* hc,
+                                       const ExpertTiles* et) {
+  const int lane = threadIdx.x & 31;
+  const int E = min(ra.E, LRC_MAX_EXPERTS);
+  for (int e = lane; e < E; e += 32) ws.lg[e] = 0.001 * e;
+  __syncwarp();
+  select_topk_warp(ws.lg, E, ra.k, ra.renorm, 0, nullptr, ws.idx, ws.w, ws.idx, ws.w);
+  __syncwarp();
+  PlanArgs d = ra.plan;  // same scalars, outputs redirected to the scratch
+  d.pair_expert = ws.pe;
+  d.pair_w = ws.pw;
+  d.pair_token = ws.pt;
+  d.pair_comp = ws.pc;
+  d.pair_list = ws.pl;
+  d.comp_list = ws.cl;
+  d.active = ws.act;
+  d.active_off = ws.aoff;
+  d.active_cnt = ws.acnt;
+  d.counts = ws.cnt;
+  d.arec = ws.arec;
+  if (ra.k + ra.plan.num_shared <= 32) build_plan_warp(d, ws.idx, ws.w, hc, et, 1, ra.k);
 }
 
 int route_tiles(int64_t B) { return static_cast<int>((B + kTT - 1) / kTT); }
@@ -441,10 +782,10 @@ lrc_status launch_route(const RouteArgs& ra_in, cudaStream_t st) {
   static const int stamps = getenv("LRC_ROUTE_STAMPS") != nullptr;
   RouteArgs ra = ra_in;
   ra.stamp = stamps;
-  // logits scratch (kTT tokens x (E + 64) doubles) shares dynamic smem with the
-  // bf16 x tile of the speculative V.x CTAs
+  // leader: logits scratch (kTT tokens x (E + 64) doubles); aux CTAs: the bf16
+  // x tile of the speculative V.x rows
   int smem = kTT * (ra.E + 64) * static_cast<int>(sizeof(double));
-  if (ra.spec_blocks > 0) smem = max(smem, kTT * xs_row_elems(ra.d) * 2);
+  if (ra.spec_blocks > 0) smem = max(smem, kTT * xs_row_elems(ra.d) * 2 + kTT * 64 * 4);
   static int configured = -1;
   if (configured < smem) {
     const void* fns[3] = {(const void*)route_kernel<double>, (const void*)route_kernel<float>,
@@ -459,21 +800,36 @@ lrc_status launch_route(const RouteArgs& ra_in, cudaStream_t st) {
     }
     configured = smem;
   }
-  dim3 grid(route_tiles(ra.B), ra.experts ? ra.ne : ra.E, 1 + ra.spec_blocks);
+  // grid: x = token tiles x kCl (one cluster per tile), y = 1 + aux rows
+  const int spec_rows = ra.spec_blocks > 0 ? (ra.ne * ra.spec_blocks + kCl - 1) / kCl : 0;
+  const int zero_rows = (ra.y_zero != nullptr || ra.t2_zero != nullptr) ? 1 : 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(route_tiles(ra.B) * kCl, 1 + max(spec_rows, zero_rows), 1);
+  cfg.blockDim = dim3(kRThreads + 32);  // + the warm-up warp
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ra.pdl ? 2 : 1;
   switch (ra.x_dtype) {
     case LRC_DTYPE_F64:
-      route_kernel<double><<<grid, kRThreads, smem, st>>>(ra);
+      LRC_CUDA_TRY(cudaLaunchKernelEx(&cfg, route_kernel<double>, ra));
       break;
     case LRC_DTYPE_F32:
-      route_kernel<float><<<grid, kRThreads, smem, st>>>(ra);
+      LRC_CUDA_TRY(cudaLaunchKernelEx(&cfg, route_kernel<float>, ra));
       break;
     case LRC_DTYPE_BF16:
-      route_kernel<uint16_t><<<grid, kRThreads, smem, st>>>(ra);
+      LRC_CUDA_TRY(cudaLaunchKernelEx(&cfg, route_kernel<uint16_t>, ra));
       break;
     default:
       return fail(LRC_ERR_INVALID, "route: unknown x dtype");
   }
-  LRC_CHECK_LAUNCH();
   return LRC_OK;
 }
 

@@ -29,9 +29,10 @@ def grab(which, n):
     return buf.astype(np.int64)
 
 
-for i in range(10):
-    torch.cuda._sleep(1_000_000)
-    layers[i % 4].layer.forward(x, 2, 1)
+# back-to-back steps over the 4 layers (like the bench); stamps of the last step
+for rep in range(3):
+    for i in range(16):
+        layers[i % 4].layer.forward(x, 2, 1)
     torch.cuda.synchronize()
     r = grab(0, 1024 * 8).reshape(1024, 8)
     t = grab(1, 2 * 256 * 8).reshape(2, 256, 8)
@@ -48,7 +49,10 @@ def show(name, v):
 
 
 print(f"B={B}  router CTAs={r.shape[0]}")
-for k, n in enumerate(["entry", "work done", "tile ticket", "select done", "plan ticket", "plan done", "logits done"]):
+nl = r[1:8]  # non-leader logit CTAs of row 0 (x = 1..7)
+for k, n in ((3, "nonleader: loads+fma done"), (4, "nonleader: reduce done"), (5, "nonleader: dsmem done")):
+    show(n, nl[:, k])
+for k, n in enumerate(["entry", "work done", "sel: softmax done", "select done", "plan ticket", "plan done", "logits done", "sel: top-k done"]):
     show("route " + n, r[:, k])
 for up, nm in ((1, "up"), (0, "down")):
     for k, n in enumerate(["entry", "griddep passed", "setup done", "prod first issue", "prod last issue",
@@ -56,6 +60,9 @@ for up, nm in ((1, "up"), (0, "down")):
         show(f"{nm} {n}", t[up, :148, k])
 
 # per-item stamps of CTA 0 (last step): issue / data / MMA done / epilogue done
+for i in range(16):
+    layers[i % 4].layer.forward(x, 2, 1)
+torch.cuda.synchronize()
 t = grab(1, 2 * 256 * 8 + 2 * 64 * 6)[2 * 256 * 8:].reshape(2, 64, 6)
 for up, nm in ((1, "up"), (0, "down")):
     it = t[up]
