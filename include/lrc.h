@@ -145,6 +145,15 @@ lrc_status lrc_layer_set_expert(lrc_layer* layer, int expert_id, const lrc_exper
 lrc_status lrc_layer_forward(lrc_layer* layer, const uint16_t* x, int64_t B, int top_k,
                              int top_n, int renormalize, int compensate_shared, float* y,
                              int32_t* topk_idx, float* topk_w, void* stream);
+/* Expert-parallel receive side: the routing is GIVEN.  Row b of
+ * x goes to expert[b] (0 <= expert < num_experts + num_shared) with mixing
+ * weight weight[b]; the low-rank term is applied iff comp[b] != 0 and the
+ * expert has a compensator.  y[b] = weight[b] * E_expert[b](x_b) -- the source
+ * rank sums its rows back per token (ref/moe.py:237-258 split by expert
+ * owner).  No implicit shared experts.  expert/weight/comp are device arrays. */
+lrc_status lrc_layer_forward_pairs(lrc_layer* layer, const uint16_t* x, int64_t B,
+                                   const int32_t* expert, const float* weight, const uint8_t* comp,
+                                   float* y, void* stream);
 /* Same computation through the generic (reference-layout) kernels even when
  * tiles exist -- used as an internal cross-check. */
 lrc_status lrc_layer_forward_generic(lrc_layer* layer, const uint16_t* x, int64_t B, int top_k,

@@ -60,6 +60,8 @@ _SIGS = {
                                   c_void_p, c_void_p, c_void_p, c_void_p]),
     "lrc_layer_forward_generic": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int,
                                           c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "lrc_layer_forward_pairs": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_void_p]),
     "lrc_layer_last_launches": (c_int, [c_void_p]),
     "lrc_layer_forward_host": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int,
                                        c_void_p, c_void_p]),

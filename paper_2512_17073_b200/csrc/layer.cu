@@ -444,7 +444,9 @@ extern "C" int lrc_layer_last_launches(const lrc_layer* L) { return L ? L->last_
 
 static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int top_k, int top_n,
                                int renormalize, int compensate_shared, float* y, int32_t* topk_idx,
-                               float* topk_w, void* stream, bool allow_tiled) {
+                               float* topk_w, void* stream, bool allow_tiled,
+                               const int32_t* pairs_expert = nullptr, const float* pairs_w = nullptr,
+                               const uint8_t* pairs_comp = nullptr) {
   if (!L || !x || !y) return fail(LRC_ERR_INVALID, "forward: null argument");
   if (top_k < 0 || top_n < 0 || top_n > top_k)
     return fail(LRC_ERR_INVALID, "top_n must be <= top_k and both >= 0");
@@ -462,6 +464,7 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   PlanArgs plan = L->plan;
   plan.top_n = top_n;
   plan.compensate_shared = compensate_shared;
+  plan.comp_rows = pairs_comp;  // pairs mode: per-row flags, no implicit shared pairs
   int32_t* ti = topk_idx ? topk_idx : L->topk_idx;
   float* tw = topk_w ? topk_w : L->topk_w;
   RouteArgs ra{};
@@ -493,11 +496,13 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   // warm-up) overlaps the previous kernel's tail; it waits before touching x,
   // y, t or the plan
   ra.pdl = (!prof && L->pdl) ? 1 : 0;
+  ra.pairs_expert = pairs_expert;
+  ra.pairs_w = pairs_w;
   lrc_status s = launch_route(ra, st);
   if (s != LRC_OK) return s;
   ++launches;
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[1], st));
-  const int P = top_k + L->S;
+  const int P = top_k + (pairs_expert ? 0 : L->S);
   const int np_bound = static_cast<int>(B) * P;
   ExpertArgs a{};
   a.ne = L->E + L->S;
@@ -552,6 +557,13 @@ extern "C" lrc_status lrc_layer_forward(lrc_layer* L, const uint16_t* x, int64_t
                                         int32_t* topk_idx, float* topk_w, void* stream) {
   return forward_impl(L, x, B, top_k, top_n, renormalize, compensate_shared, y, topk_idx, topk_w,
                       stream, true);
+}
+
+extern "C" lrc_status lrc_layer_forward_pairs(lrc_layer* L, const uint16_t* x, int64_t B,
+                                              const int32_t* expert, const float* weight,
+                                              const uint8_t* comp, float* y, void* stream) {
+  if (!expert || !weight || !comp) return fail(LRC_ERR_INVALID, "forward_pairs: null routing");
+  return forward_impl(L, x, B, 1, 1, 0, 0, y, nullptr, nullptr, stream, true, expert, weight, comp);
 }
 
 extern "C" lrc_status lrc_layer_forward_generic(lrc_layer* L, const uint16_t* x, int64_t B,

@@ -35,6 +35,7 @@ struct PlanArgs {
   int* counts;              // [0] n_active, [1] n_comp
   ActiveRec* arec;          // [E+S] per active expert (layer forward only; null otherwise)
   const lrc_expert* experts;  // device table [E+S] (with arec)
+  const uint8_t* comp_rows;   // [B] pairs mode: per-row compensation flag (else top_n rule)
 };
 
 struct RouteArgs {
@@ -58,6 +59,10 @@ struct RouteArgs {
   float* y_zero;              // zero y rows
   int stamp;                  // LRC_ROUTE_STAMPS: per-CTA %globaltimer stamps (debug)
   int pdl;                    // launched as a programmatic dependent of the previous kernel
+  // pairs mode (expert-parallel receive side): routing is given, one expert per
+  // row (k = 1); the gate GEMV and softmax are skipped
+  const int32_t* pairs_expert;  // [B] or null
+  const float* pairs_w;         // [B]
 };
 
 // Row j of a quantized V (group size 64, BITS-bit LSB-first stream) dotted

@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
   }
   double* lg = reinterpret_cast<double*>(rsm);  // leader's layout: per token E weights + 64 scratch
   const int ldl = ra.E + 64;
-  for (int e = rank; e < ra.E; e += kCl) {
+  for (int e = rank; e < (ra.pairs_expert != nullptr ? 0 : ra.E); e += kCl) {
     const double* g = ra.gate_t + static_cast<int64_t>(e) * ra.d;
     double acc[kTT];
 #pragma unroll
@@ -526,17 +526,27 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
   RSTAMP(6);
   if (!leader) return;
   // ---- leader: softmax + top-k (warp per token), then the pair plan
-  if (warp < nb)
+  if (ra.pairs_expert != nullptr) {  // pairs mode: the routing is given (k = 1)
+    if (threadIdx.x < nb) {
+      const int32_t e = ra.pairs_expert[b0 + threadIdx.x];
+      const float w = ra.pairs_w[b0 + threadIdx.x];
+      s_tidx[threadIdx.x] = e;
+      s_tw[threadIdx.x] = w;
+      ra.topk_idx[b0 + threadIdx.x] = e;
+      ra.topk_w[b0 + threadIdx.x] = w;
+    }
+  } else if (warp < nb) {
     select_topk_warp(lg + warp * ldl, ra.E, ra.k, ra.renorm, b0 + warp, ra.probs, ra.topk_idx,
                      ra.topk_w, s_tidx + warp * ra.k, s_tw + warp * ra.k,
                      (ra.stamp && warp == 0 && blockIdx.y * gridDim.x + blockIdx.x < kStampCtas)
                          ? &g_route_stamps[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + 2]
                          : nullptr);
+  }
   RSTAMP(3);
   if (ra.plan.ticket == nullptr) return;
   wsync();
   if (ntiles == 1) {  // decode: the whole plan from shared memory, no ticket
-    if (ra.B * (ra.k + ra.plan.num_shared) <= 32) {
+    if (ra.B * (ra.k + (ra.plan.comp_rows ? 0 : ra.plan.num_shared)) <= 32) {
       if (warp == 0) build_plan_warp(ra.plan, s_tidx, s_tw, s_hc, s_et, static_cast<int>(ra.B), ra.k);
     } else {
       build_plan_block(ra.plan, s_tidx, s_tw, s_hc, s_et, static_cast<int>(ra.B), ra.k);
@@ -566,7 +576,7 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
 __device__ __noinline__ void build_plan_block(const PlanArgs& pa, const int32_t* tk_idx,
                                               const float* tk_w, const uint8_t* hc,
                                               const ExpertTiles* et, int B, int k) {
-  const int P = k + pa.num_shared;
+  const int P = k + (pa.comp_rows ? 0 : pa.num_shared);  // pairs mode: no implicit shared pairs
   const int NP = B * P;
   const int NE = pa.num_experts + pa.num_shared;
   __shared__ int s_cnt[LRC_MAX_EXPERTS];
@@ -646,7 +656,8 @@ __device__ __noinline__ void build_plan_block(const PlanArgs& pa, const int32_t*
       int comp = 0;
       if (valid) {
         const int j = p % P;
-        comp = (j < k) ? ((j < pa.top_n) && hc[e]) : (pa.compensate_shared && hc[e]);
+        comp = (j < k) ? ((pa.comp_rows != nullptr ? pa.comp_rows[p / P] != 0 : j < pa.top_n) && hc[e])
+                       : (pa.compensate_shared && hc[e]);
       }
       const unsigned m = __ballot_sync(0xffffffffu, comp);
       if (valid) {
@@ -688,7 +699,7 @@ __device__ __noinline__ void build_plan_warp(const PlanArgs& pa, const int32_t* 
                                              const float* tk_w, const uint8_t* hc,
                                              const ExpertTiles* et, int B, int k) {
   const int lane = threadIdx.x & 31;
-  const int P = k + pa.num_shared, NP = B * P;
+  const int P = k + (pa.comp_rows ? 0 : pa.num_shared), NP = B * P;
   const bool valid = lane < NP;
   int e = 0x7fffffff, j = 0;
   if (valid) {
@@ -715,7 +726,8 @@ __device__ __noinline__ void build_plan_warp(const PlanArgs& pa, const int32_t* 
     off += eq < e;
     nbelow += (eq < e) && ((sq & ((1u << q) - 1u)) == 0u);
   }
-  const bool comp = valid && ((j < k) ? (j < pa.top_n && hc[e] != 0) : (pa.compensate_shared && hc[e] != 0));
+  const bool row_comp = pa.comp_rows != nullptr ? (valid && pa.comp_rows[lane / P] != 0) : j < pa.top_n;
+  const bool comp = valid && ((j < k) ? (row_comp && hc[e] != 0) : (pa.compensate_shared && hc[e] != 0));
   const unsigned cm = __ballot_sync(0xffffffffu, comp);
   if (valid) {
     pa.pair_list[off + rk] = lane;

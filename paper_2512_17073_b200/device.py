@@ -180,6 +180,28 @@ class LRCMoELayer:
                       _lib.ptr(topk_w), _lib.stream_ptr()))
         return y, topk_idx, topk_w
 
+    def forward_pairs(self, x, expert, weight, comp, y=None):
+        """Given routing (expert-parallel receive side): row b of x (bf16 cuda)
+        goes to expert[b] (int32) with weight[b] (f32); the low-rank term iff
+        comp[b] (uint8).  Returns y (B, hidden) f32 = weight * E(x) per row."""
+        torch = _lib.device_required()
+        B = int(x.shape[0])
+        if y is None:
+            y = torch.empty((B, self.hidden), dtype=torch.float32, device="cuda")
+        if B == 0:
+            return y
+        self.ensure_capacity(B, 1)
+        ne = self.num_experts + self.num_shared
+        ex = expert.to(device="cuda", dtype=torch.int32).contiguous()
+        if int(ex.min()) < 0 or int(ex.max()) >= ne:
+            raise ValueError(f"forward_pairs: expert ids must be in [0, {ne})")
+        w = weight.to(device="cuda", dtype=torch.float32).contiguous()
+        c = comp.to(device="cuda", dtype=torch.uint8).contiguous()
+        _lib.check(_lib.lib().lrc_layer_forward_pairs(self._handle, _lib.ptr(x.contiguous()), B,
+                                                      _lib.ptr(ex), _lib.ptr(w), _lib.ptr(c),
+                                                      _lib.ptr(y), _lib.stream_ptr()))
+        return y
+
     def forward_host(self, x_host, y_host, top_k: int, top_n: int = 0, renormalize: bool = False,
                      compensate_shared: bool = True):
         """End-to-end call with HOST buffers (pinned torch CPU tensors): H2D of x,
@@ -219,13 +241,21 @@ class LRCMoELayer:
         or None for an expert absent from the store."""
         keep = _Keep()
         experts, missing = [], set()
+        absent = None  # one shared all-zero placeholder for every absent expert
         for eid, rec in enumerate(records):
             ex = _lib.LrcExpert()
             if rec is None:
                 missing.add(eid)
-                ex.w1 = _zero_qmat(ffn, hidden, keep)
-                ex.w3 = _zero_qmat(ffn, hidden, keep)
-                ex.w2 = _zero_qmat(hidden, ffn, keep)
+                if absent is None:
+                    absent = _lib.LrcExpert()
+                    absent.w1 = _zero_qmat(ffn, hidden, keep)
+                    absent.w3 = absent.w1
+                    absent.w2 = _zero_qmat(hidden, ffn, keep)
+                    if tiles and tiles_eligible(absent.w1, absent.w3, absent.w2):
+                        absent.up_tiles = build_tiles([absent.w1, absent.w3], keep).data_ptr()
+                        absent.down_tiles = build_tiles([absent.w2], keep).data_ptr()
+                experts.append(absent)
+                continue
             else:
                 for p in PROJ:
                     setattr(ex, p, _qm_to_device(rec[p].qm, keep))

@@ -1,0 +1,134 @@
+"""Expert-parallel MoE layer (north-star item 5).
+
+Experts are sharded across the ranks of a ``torch.distributed`` group: routed
+expert e lives on rank ``e * G // E``; shared experts are replicated and run on
+the token's own rank.  One step for a rank's local batch x (B, d):
+
+1. route locally (fp64 gate, stable top-k, top-n flags: ref/moe.py:165-193);
+2. dispatch: every (token, selected expert) pair is sent to the expert's owner
+   -- an all-to-all of the split sizes, then one all-to-all of the token rows
+   and one of the packed (expert, weight, compensated) metadata;
+3. the owner runs ``lrc_layer_forward_pairs`` on what it received: one launch
+   sequence over its local experts, U.(V.x) applied for the flagged pairs;
+4. combine: the weighted rows go back with the reverse all-to-all and are summed
+   per token (ref/moe.py:237-258), plus the local shared experts.
+
+Collectives are NCCL over NVLink/NVSwitch on the GPU path and gloo in the CPU
+tests (``route_fn`` / ``compute_fn`` let the tests inject the oracle; the
+defaults are the CUDA library and fail loudly without it).
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+
+
+def owner_of(expert, num_experts: int, world: int):
+    """Rank owning routed expert ``expert`` (tensor or int): floor(e * G / E)."""
+    return (expert * world) // num_experts
+
+
+class ExpertParallelLayer:
+    """One MoE layer sharded over ``group``; see the module docstring."""
+
+    def __init__(self, group, num_experts: int, num_shared: int, top_k: int, top_n: int,
+                 route_fn, compute_fn, compensate_shared: bool = True):
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.E, self.S, self.k, self.n = num_experts, num_shared, top_k, top_n
+        self.route_fn, self.compute_fn = route_fn, compute_fn
+        self.compensate_shared = compensate_shared
+
+    def local_experts(self):
+        return [e for e in range(self.E) if owner_of(e, self.E, self.world) == self.rank]
+
+    # ---------------------------------------------------------------- step --
+    def forward(self, x):
+        """x (B, d) on this rank's device -> y (B, d) float32 (sum over the
+        token's experts, as ref/moe.py:forward in mode "compensated")."""
+        import torch
+        import torch.distributed as dist
+
+        B, d = int(x.shape[0]), int(x.shape[1])
+        dev = x.device
+        idx, w = self.route_fn(x)                      # (B, k) int, (B, k) float
+        idx = idx.to(dev, torch.int64)
+        w = w.to(dev, torch.float32)
+        k = idx.shape[1]
+        token = torch.arange(B, device=dev).repeat_interleave(k)
+        expert = idx.reshape(-1)
+        weight = w.reshape(-1)
+        comp = (torch.arange(k, device=dev) < self.n).repeat(B).to(torch.int64)
+        dest = owner_of(expert, self.E, self.world)
+        order = torch.argsort(dest, stable=True)
+        token, expert, weight, comp, dest = token[order], expert[order], weight[order], comp[order], dest[order]
+        send = torch.bincount(dest, minlength=self.world).to(torch.int64)
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=self.group)
+        send_l, recv_l = send.tolist(), recv.tolist()
+        nrecv = int(sum(recv_l))
+        # token rows + packed metadata (expert id, weight bits, comp flag)
+        x_send = x[token].contiguous()
+        meta_send = torch.stack([expert.to(torch.int32), weight.view(torch.int32),
+                                 comp.to(torch.int32)], dim=1).contiguous()
+        x_recv = torch.empty((nrecv, d), dtype=x.dtype, device=dev)
+        meta_recv = torch.empty((nrecv, 3), dtype=torch.int32, device=dev)
+        dist.all_to_all_single(x_recv, x_send, recv_l, send_l, group=self.group)
+        dist.all_to_all_single(meta_recv, meta_send, recv_l, send_l, group=self.group)
+        y_rows = self.compute_fn(x_recv, meta_recv[:, 0].contiguous(),
+                                 meta_recv[:, 1].contiguous().view(torch.float32),
+                                 meta_recv[:, 2].contiguous().to(torch.uint8))
+        y_rows = y_rows.to(torch.float32).contiguous()
+        y_back = torch.empty((token.numel(), d), dtype=torch.float32, device=dev)
+        dist.all_to_all_single(y_back, y_rows, send_l, recv_l, group=self.group)
+        y = torch.zeros((B, d), dtype=torch.float32, device=dev)
+        y.index_add_(0, token, y_back)
+        if self.S:  # shared experts: replicated, computed on the token's own rank
+            xs = x.repeat(self.S, 1)
+            ex = torch.arange(self.E, self.E + self.S, device=dev).repeat_interleave(B).to(torch.int32)
+            ws = torch.ones(B * self.S, dtype=torch.float32, device=dev)
+            cs = torch.full((B * self.S,), int(self.compensate_shared), dtype=torch.uint8, device=dev)
+            ys = self.compute_fn(xs, ex, ws, cs).to(torch.float32)
+            y += ys.reshape(self.S, B, d).sum(0)
+        return y
+
+
+def cuda_route_fn(dl, top_k: int, top_n: int, renormalize: bool = False):
+    """Routing of a rank's local tokens on the GPU (lrc_route, bit-exact fp64)."""
+    torch = _lib.device_required()
+
+    def route(x):
+        B = int(x.shape[0])
+        idx = torch.empty((B, top_k), dtype=torch.int32, device="cuda")
+        w = torch.empty((B, top_k), dtype=torch.float32, device="cuda")
+        _lib.check(_lib.lib().lrc_route(_lib.ptr(dl.gate_t), _lib.ptr(x.contiguous()), _lib.DTYPE_BF16, B,
+                                        dl.hidden, dl.num_experts, top_k, top_n, int(bool(renormalize)),
+                                        ctypes.c_void_p(0), _lib.ptr(idx), _lib.ptr(w), _lib.stream_ptr()))
+        return idx, w
+
+    return route
+
+
+def from_device_layer(group, dl, top_k: int, top_n: int, renormalize: bool = False,
+                      compensate_shared: bool = True) -> ExpertParallelLayer:
+    """EP layer over a rank-local ``LRCMoELayer`` that holds (at least) the
+    experts this rank owns plus the shared experts (absent experts may be
+    None records: they share one placeholder)."""
+    return ExpertParallelLayer(group, dl.num_experts, dl.num_shared, top_k, top_n,
+                               cuda_route_fn(dl, top_k, top_n, renormalize),
+                               lambda xr, e, w, c: dl.forward_pairs(xr, e, w, c),
+                               compensate_shared)
+
+
+def owned_records(records, num_experts: int, world: int, rank: int):
+    """Records list with the experts of other ranks replaced by None (shared
+    experts, at index >= num_experts, are kept on every rank)."""
+    return [r if (i >= num_experts or owner_of(i, num_experts, world) == rank) else None
+            for i, r in enumerate(records)]
+
+
+__all__ = ["ExpertParallelLayer", "owner_of", "from_device_layer", "owned_records", "cuda_route_fn"]
