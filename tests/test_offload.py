@@ -1,0 +1,52 @@
+"""Offload engine (config C3): experts fetched on demand from pinned host memory
+into an LRU set of GPU slots give the same layer outputs as the resident layer,
+with hits, misses and evictions all exercised."""
+import pytest
+import torch
+
+from paper_2512_17073_b200 import offload
+from paper_2512_17073_b200.synth import SynthLayer
+
+
+@pytest.mark.gpu
+def test_offload_matches_resident_layers():
+    hidden, ffn, E = 512, 1024, 8
+    layers = [SynthLayer(hidden, ffn, E, top_k=2, rank=16, seed=20 + l, max_tokens=8) for l in range(2)]
+    host = [offload.host_experts_from_synth(sl) for sl in layers]
+    # 8 slots for 2 layers x 8 experts: a step needs up to B*k <= 8, so evictions occur
+    eng = offload.OffloadEngine([sl.gate for sl in layers], host, hidden, ffn, top_k=2, top_n=1,
+                                n_slots=8, max_tokens=8)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    worst = 0.0
+    for step in range(6):
+        B = 1 + step % 4
+        x = torch.randn((B, hidden), device="cuda", generator=gen).to(torch.bfloat16)
+        y = eng.forward(x)
+        ref = x
+        for sl in layers:
+            ref = sl.layer.forward(ref, 2, 1)[0].to(torch.bfloat16)
+        torch.cuda.synchronize()
+        err = float((y.float() - ref.float()).norm() / ref.float().norm())
+        worst = max(worst, err)
+    assert worst < 1e-2, worst  # bf16 chaining of two layers; single-layer check below
+    assert eng.stats["misses"] > 0 and eng.stats["hits"] > 0
+
+
+@pytest.mark.gpu
+def test_offload_single_layer_exact():
+    hidden, ffn, E = 512, 1024, 8
+    sl = SynthLayer(hidden, ffn, E, top_k=2, rank=16, seed=31, max_tokens=8)
+    eng = offload.OffloadEngine([sl.gate], [offload.host_experts_from_synth(sl)], hidden, ffn,
+                                top_k=2, top_n=1, n_slots=2, max_tokens=8)
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    for step in range(8):
+        x = torch.randn((1, hidden), device="cuda", generator=gen).to(torch.bfloat16)
+        y = eng.forward_layer(0, x)
+        ref = sl.layer.forward(x, 2, 1)[0]
+        torch.cuda.synchronize()
+        err = float((y - ref).norm() / ref.norm())
+        assert err < 1e-5, (step, err)
+    # 2 slots, top-2 routing over 8 experts: evictions must have happened
+    assert eng.stats["misses"] >= 3
+    per = sum(b.numel() for b in eng.host[0][0].bufs.values())
+    assert eng.stats["bytes"] >= eng.stats["misses"] * per * 0.9

@@ -1,0 +1,93 @@
+"""Config C3 measurement: Mixtral-8x7B-shaped decode through L layers with every
+expert (INT2 T2 tiles + rank-32 INT3 LR tiles + V factors) in pinned host
+memory, fetched on demand by the offload engine.  Reports decode tokens/s,
+bytes over the host link per token, achieved H2D GB/s and its fraction of the
+measured pinned H2D copy bandwidth (the C3 roofline is host-link bound).
+
+    python tools/offload_bench.py [--layers 8] [--tokens 16] [--slots 2]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2512_17073_b200 import offload  # noqa: E402
+from paper_2512_17073_b200.synth import SynthLayer  # noqa: E402
+
+
+def h2d_peak(nbytes=1 << 30, reps=5):
+    src = torch.empty((nbytes,), dtype=torch.uint8).pin_memory()
+    dst = torch.empty((nbytes,), dtype=torch.uint8, device="cuda")
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        dst.copy_(src, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    return nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--tokens", type=int, default=16)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--hidden", type=int, default=4096)
+    ap.add_argument("--ffn", type=int, default=14336)
+    ap.add_argument("--repeats", type=int, default=3)
+    args = ap.parse_args()
+    t0 = time.time()
+    gates, host = [], []
+    for l in range(args.layers):
+        sl = SynthLayer(args.hidden, args.ffn, 8, top_k=2, rank=32, seed=100 + l, max_tokens=8)
+        gates.append(sl.gate)
+        host.append(offload.host_experts_from_synth(sl))
+        del sl
+        torch.cuda.empty_cache()
+    build_s = time.time() - t0
+    peak = h2d_peak()
+    eng = offload.OffloadEngine(gates, host, args.hidden, args.ffn, top_k=2, top_n=1,
+                                n_slots=args.slots, max_tokens=8)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn((1, args.hidden), device="cuda", generator=gen).to(torch.bfloat16)
+    for _ in range(args.warmup):
+        eng.forward(x, normalize=True)
+    torch.cuda.synchronize()
+    runs = []
+    for _ in range(args.repeats):  # median of repeats (host-side variance is large)
+        for k in eng.stats:
+            eng.stats[k] = 0
+        t1 = time.perf_counter()
+        for _ in range(args.tokens):
+            x = eng.forward(x, normalize=True)
+        torch.cuda.synchronize()
+        runs.append((time.perf_counter() - t1, dict(eng.stats)))
+    runs.sort(key=lambda r: r[0])
+    dt, stats = runs[len(runs) // 2]
+    eng.stats = stats
+    per_tok = eng.stats["bytes"] / args.tokens
+    gbs = eng.stats["bytes"] / dt / 1e9
+    out = {
+        "metric": "offloaded decode tokens/s (C3: all experts in pinned host memory)",
+        "value": round(args.tokens / dt, 3), "unit": "tokens/s",
+        "config": {"layers": args.layers, "experts_per_layer": 8, "top_k": 2, "top_n": 1, "bits": 2,
+                   "rank": 32, "gpu_slots": args.slots, "batch": 1},
+        "host_bytes_per_token": int(per_tok), "h2d_achieved_gbs": round(gbs, 2),
+        "h2d_peak_gbs": round(peak, 2), "roofline_frac": round(gbs / peak, 4),
+        "stats": eng.stats, "ms_per_token": round(dt / args.tokens * 1e3, 3),
+        "runs_tok_s": [round(args.tokens / r[0], 2) for r in runs],
+        "pool_gb": round(sum(he.nbytes for lay in host for he in lay) / 1e9, 3),
+        "build_s": round(build_s, 1),
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
