@@ -135,6 +135,11 @@ lrc_status lrc_layer_create(const double* gate_t, int hidden, int ffn, int num_e
 void lrc_layer_destroy(lrc_layer* layer);
 /* Replace expert descriptors (offload engine: experts move between slots). */
 lrc_status lrc_layer_set_expert(lrc_layer* layer, int expert_id, const lrc_expert* e);
+/* Stream-ordered lrc_layer_set_expert: the device-side descriptor update is an
+ * async copy on `stream` (from a 64-entry pinned staging ring: at most 64
+ * updates may be in flight).  Later work on `stream` sees the new expert. */
+lrc_status lrc_layer_set_expert_async(lrc_layer* layer, int expert_id, const lrc_expert* e,
+                                      void* stream);
 
 /* ref/moe.py:217-259 forward(mode="compensated") for a batch of B tokens:
  * y[b] = sum_{e in top_k(b)} w_be * E_e(x_b) + sum_shared E_s(x_b), with the

@@ -56,6 +56,7 @@ _SIGS = {
                                  c_int, POINTER(c_void_p)]),
     "lrc_layer_destroy": (None, [c_void_p]),
     "lrc_layer_set_expert": (c_int, [c_void_p, c_int, POINTER(LrcExpert)]),
+    "lrc_layer_set_expert_async": (c_int, [c_void_p, c_int, POINTER(LrcExpert), c_void_p]),
     "lrc_layer_forward": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int,
                                   c_void_p, c_void_p, c_void_p, c_void_p]),
     "lrc_layer_forward_generic": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int,

@@ -234,6 +234,8 @@ struct lrc_layer {
   const double* gate_t = nullptr;
   std::vector<lrc_expert> host_experts;
   lrc_expert* d_experts = nullptr;
+  lrc_expert* h_stage = nullptr;  // pinned ring for stream-ordered descriptor updates
+  int stage_next = 0;
   // workspace
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -421,6 +423,7 @@ extern "C" lrc_status lrc_layer_create(const double* gate_t, int hidden, int ffn
 extern "C" void lrc_layer_destroy(lrc_layer* L) {
   if (!L) return;
   cudaFree(L->d_experts);
+  if (L->h_stage) cudaFreeHost(L->h_stage);
   cudaFree(L->ws);
   for (auto& e : L->ev)
     if (e) cudaEventDestroy(e);
@@ -436,6 +439,31 @@ extern "C" lrc_status lrc_layer_set_expert(lrc_layer* L, int expert_id, const lr
     return fail(LRC_ERR_UNSUPPORTED, "set_expert: rank above the layer's workspace rank");
   L->host_experts[expert_id] = *e;
   LRC_CUDA_TRY(cudaMemcpy(L->d_experts + expert_id, e, sizeof(lrc_expert), cudaMemcpyHostToDevice));
+  refresh_tiled(L);
+  return LRC_OK;
+}
+
+// Stream-ordered variant: the device descriptor is written by an async copy on
+// `stream` from a pinned staging ring (kStageRing entries per expert slot), so
+// it does not serialise against other streams (the offload engine's copies).
+// The host-side state (validation, tiled-path eligibility) updates immediately.
+extern "C" lrc_status lrc_layer_set_expert_async(lrc_layer* L, int expert_id, const lrc_expert* e,
+                                                 void* stream) {
+  constexpr int kStageRing = 64;
+  if (!L || !e || expert_id < 0 || expert_id >= L->E + L->S)
+    return fail(LRC_ERR_INVALID, "set_expert: bad id");
+  lrc_status s = validate_expert(*e, L->hidden, L->ffn);
+  if (s != LRC_OK) return s;
+  if (std::max({rank_of(e->u1), rank_of(e->u2), rank_of(e->u3)}) > L->maxr)
+    return fail(LRC_ERR_UNSUPPORTED, "set_expert: rank above the layer's workspace rank");
+  if (L->h_stage == nullptr)
+    LRC_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&L->h_stage), sizeof(lrc_expert) * kStageRing,
+                               cudaHostAllocDefault));
+  lrc_expert* slot = L->h_stage + (L->stage_next++ % kStageRing);
+  *slot = *e;
+  L->host_experts[expert_id] = *e;
+  LRC_CUDA_TRY(cudaMemcpyAsync(L->d_experts + expert_id, slot, sizeof(lrc_expert), cudaMemcpyHostToDevice,
+                               as_stream(stream)));
   refresh_tiled(L);
   return LRC_OK;
 }

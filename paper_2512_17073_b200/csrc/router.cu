@@ -351,7 +351,11 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const T* x = static_cast<const T*>(ra.x);
   RSTAMP(0);
-  griddep_launch_dependents_r();
+  // Dependents (the up kernel) are released only after this grid's own
+  // griddepcontrol.wait: a running up kernel then implies the previous layer is
+  // complete, so it may read x and build its activation operand before it waits
+  // for the routing.
+  if (!ra.pdl) griddep_launch_dependents_r();
   if (warp == kRThreads / 32) {  // warm-up warp: leader of a row-0 cluster only
     if (row == 0) {
       // arrive on the cluster barrier first (never waits): the logits handoff
@@ -363,7 +367,10 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
   }
   if (row > 0) {
     // ---- aux CTAs: speculative V.x rows (single tile) + zeroing of the outputs
-    if (ra.pdl) griddep_wait_r();  // x, y and t belong to the previous kernel until here
+    if (ra.pdl) {  // x, y and t belong to the previous kernel until here
+      griddep_wait_r();
+      griddep_launch_dependents_r();
+    }
     const int aux = (row - 1) * kCl + rank, naux = (gridDim.y - 1) * kCl;
     if (ra.y_zero != nullptr) {
       const int64_t n = static_cast<int64_t>(nb) * ra.d;
@@ -461,6 +468,7 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
       for (int l = threadIdx.x; l < (ra.d * 8 + 127) / 128; l += kRThreads)
         asm volatile("prefetch.global.L1 [%0];" ::"l"(ra.gate_t + static_cast<int64_t>(e) * ra.d + l * 16));
     griddep_wait_r();
+    griddep_launch_dependents_r();
   }
   double* lg = reinterpret_cast<double*>(rsm);  // leader's layout: per token E weights + 64 scratch
   const int ldl = ra.E + 64;

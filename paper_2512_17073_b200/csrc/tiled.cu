@@ -298,6 +298,7 @@ struct TiledParams {
   int nstage;
   int xs_stride;        // bf16 elements per x' row
   int xs_rows;          // x' rows held in shared memory (<= 8*NT)
+  int prebuilt;         // UP with B <= 8*NT: x' rows = tokens, built before the grid-dependency wait
   int debug;            // LRC_TILED_DEBUG: bit0 skip MMA core, bit1 skip epilogue math
 };
 
@@ -389,6 +390,78 @@ __device__ __forceinline__ bool pass_has_comp(uint32_t m, int pass, int tpp8) {
   return c;
 }
 
+
+// x' rows (x / m per 8-column slot, bf16, in the permuted B-fragment order) and
+// per-(group, row) sums (X, -128 X') for `nrows` rows over columns
+// [k0, k0 + 64 ng) of the chunk.  Row n reads x row rowsrc[n] (token, UP) or
+// a16 row rowsrc[n] (pair, DOWN); rowsrc == nullptr: row n is token n.  One
+// 16-byte load per thread-task, two tasks in flight per thread; the 8 lanes of
+// a (row, group) reduce its sums by shuffles (nthr is a multiple of 32).
+template <bool UP, int NT>
+__device__ __forceinline__ void build_xprime(const ExpertArgs& A, const TiledParams& P, uint16_t* xs,
+                                             float2* sums, const int* rowsrc, int nrows, int k0, int ng,
+                                             int t0, int nthr) {
+  constexpr int TPP = 8 * NT;
+      // one 16-byte x load per thread-task (8 columns), two tasks in flight per
+      // thread; the 8 lanes of a (token, group) reduce its sums by shuffles
+      const int ntask = nrows * ng * 8;
+      for (int base = 0; base < ntask; base += 2 * nthr) {
+        uint4 raw[2];
+        int tn[2], tg[2];
+        bool ok[2];
+        const int c8 = t0 & 7;  // == task & 7 (base is a multiple of 8)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int task = base + u * nthr + t0;
+          ok[u] = task < ntask;
+          const int ng8 = ok[u] ? (task >> 3) : 0;
+          tn[u] = ng8 / ng;
+          tg[u] = ng8 - tn[u] * ng;
+          raw[u] = make_uint4(0u, 0u, 0u, 0u);
+          if (ok[u]) {
+            const int src = rowsrc ? rowsrc[tn[u]] : tn[u];
+            const uint16_t* row = UP ? A.x + static_cast<int64_t>(src) * A.hidden
+                                     : A.a16 + static_cast<int64_t>(src) * A.ffn;
+            const int kk = k0 + tg[u] * 64 + c8 * 8;
+            if (kk + 8 <= P.K && (reinterpret_cast<uintptr_t>(row + kk) & 15) == 0) {
+              raw[u] = __ldg(reinterpret_cast<const uint4*>(row + kk));
+            } else {
+              uint16_t h[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) h[j] = (kk + j < P.K) ? row[kk + j] : 0;
+              raw[u] = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16),
+                                  h[4] | (uint32_t(h[5]) << 16), h[6] | (uint32_t(h[7]) << 16));
+            }
+          }
+        }
+        const float im = inv_mult(c8);  // slot j = c8 for columns c8*8 .. c8*8+7
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          float xsum = 0.f, xpsum = 0.f;
+          if (ok[u]) {
+            uint32_t* dst = reinterpret_cast<uint32_t*>(xs + tn[u] * P.xs_stride + tg[u] * 64);
+            const uint32_t w4[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
+            // column c8*8 + 2*tj + e -> 16-block c8/2, position tj*4 + (c8&1)*2 + e
+#pragma unroll
+            for (int tj = 0; tj < 4; ++tj) {
+              const float lo = bf2f(w4[tj] & 0xffff), hi = bf2f(w4[tj] >> 16);
+              xsum += lo + hi;
+              const float plo = lo * im, phi = hi * im;
+              xpsum += plo + phi;
+              dst[((c8 >> 1) * 16 + tj * 4 + (c8 & 1) * 2) >> 1] =
+                  static_cast<uint32_t>(f2bf(plo)) | (static_cast<uint32_t>(f2bf(phi)) << 16);
+            }
+          }
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) {
+            xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
+            xpsum += __shfl_xor_sync(0xffffffffu, xpsum, o);
+          }
+          if (ok[u] && c8 == 0) sums[tg[u] * TPP + tn[u]] = make_float2(xsum, -128.0f * xpsum);
+        }
+      }
+}
+
 struct ItemDesc {
   int ai, pass, chunk, tile, lr, gp0, gp1, pad;
 };
@@ -458,6 +531,14 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
   // wait), so its producer may start streaming W2 while the up kernel drains;
   // its consumers / epilogue wait before touching the up kernel's outputs.
   if (threadIdx.x == 0) TSTAMP(0);
+  if (UP && P.prebuilt) {
+    // the router releases this grid only after the previous layer finished,
+    // so x is final: build x' for all B tokens while the routing completes
+    uint16_t* xs0 = reinterpret_cast<uint16_t*>(smem + SM.xs);
+    float2* sums0 = reinterpret_cast<float2*>(smem + SM.sums);
+    build_xprime<UP, NT>(A, P, xs0, sums0, nullptr, P.xs_rows, 0, static_cast<int>(2 * P.GP), threadIdx.x,
+                         blockDim.x);
+  }
   if (UP) griddep_wait();
   griddep_launch_dependents();
   if (threadIdx.x == 0) TSTAMP(1);
@@ -775,66 +856,10 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
         }
         consumer_sync();
       }
-      const int k0 = gp0 * 128;
-      const int ng = (gp1 - gp0) * 2;
-      // only real token rows are built; empty columns read the shared zero row
-      // (their sums are never used: MMA columns are independent)
-      // one 16-byte x load per thread-task (8 columns), two tasks in flight per
-      // thread; the 8 lanes of a (token, group) reduce its sums by shuffles
-      const int ntask = pass_tok * ng * 8;
-      for (int base = 0; base < ntask; base += 2 * kNW * 32) {
-        uint4 raw[2];
-        int tn[2], tg[2];
-        bool ok[2];
-        const int c8 = ctid & 7;  // == task & 7 (base is a multiple of 8)
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int task = base + u * kNW * 32 + ctid;
-          ok[u] = task < ntask;
-          const int ng8 = ok[u] ? (task >> 3) : 0;
-          tn[u] = ng8 / ng;
-          tg[u] = ng8 - tn[u] * ng;
-          raw[u] = make_uint4(0u, 0u, 0u, 0u);
-          if (ok[u]) {
-            const uint16_t* row = UP ? A.x + static_cast<int64_t>(s_ctok[tn[u]]) * A.hidden
-                                     : A.a16 + static_cast<int64_t>(s_cpair[tn[u]]) * A.ffn;
-            const int kk = k0 + tg[u] * 64 + c8 * 8;
-            if (kk + 8 <= P.K && (reinterpret_cast<uintptr_t>(row + kk) & 15) == 0) {
-              raw[u] = __ldg(reinterpret_cast<const uint4*>(row + kk));
-            } else {
-              uint16_t h[8];
-#pragma unroll
-              for (int j = 0; j < 8; ++j) h[j] = (kk + j < P.K) ? row[kk + j] : 0;
-              raw[u] = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16),
-                                  h[4] | (uint32_t(h[5]) << 16), h[6] | (uint32_t(h[7]) << 16));
-            }
-          }
-        }
-        const float im = inv_mult(c8);  // slot j = c8 for columns c8*8 .. c8*8+7
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          float xsum = 0.f, xpsum = 0.f;
-          if (ok[u]) {
-            uint32_t* dst = reinterpret_cast<uint32_t*>(xs + tn[u] * P.xs_stride + tg[u] * 64);
-            const uint32_t w4[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
-            // column c8*8 + 2*tj + e -> 16-block c8/2, position tj*4 + (c8&1)*2 + e
-#pragma unroll
-            for (int tj = 0; tj < 4; ++tj) {
-              const float lo = bf2f(w4[tj] & 0xffff), hi = bf2f(w4[tj] >> 16);
-              xsum += lo + hi;
-              const float plo = lo * im, phi = hi * im;
-              xpsum += plo + phi;
-              dst[((c8 >> 1) * 16 + tj * 4 + (c8 & 1) * 2) >> 1] =
-                  static_cast<uint32_t>(f2bf(plo)) | (static_cast<uint32_t>(f2bf(phi)) << 16);
-            }
-          }
-#pragma unroll
-          for (int o = 1; o < 8; o <<= 1) {
-            xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
-            xpsum += __shfl_xor_sync(0xffffffffu, xpsum, o);
-          }
-          if (ok[u] && c8 == 0) sums[tg[u] * TPP + tn[u]] = make_float2(xsum, -128.0f * xpsum);
-        }
+      if (!P.prebuilt) {
+        // only real token rows are built; empty columns read the shared zero row
+        build_xprime<UP, NT>(A, P, xs, sums, UP ? s_ctok : s_cpair, pass_tok, gp0 * 128, (gp1 - gp0) * 2,
+                             ctid, kNW * 32);
       }
       consumer_sync();
     }
@@ -852,11 +877,18 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
     const int ngp = gp1 - gp0;
     const int nspan = (ngp + kSpanGP - 1) / kSpanGP;
     // B-fragment row of this lane per N-tile: token column nt*8+gid, or the zero row
+    // x' / sums row of a token column: its pass position, or (prebuilt) its token
     const uint16_t* xrow[NT];
+    int srow[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int n = nt * 8 + gid;
-      xrow[nt] = xs + (n < pass_tok ? n : P.xs_rows) * P.xs_stride + tid * 4;
+      xrow[nt] = xs + (n < pass_tok ? (P.prebuilt ? s_ctok[n] : n) : P.xs_rows) * P.xs_stride + tid * 4;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int col = nt * 8 + 2 * tid + c;
+        srow[nt][c] = col < pass_tok ? (P.prebuilt ? s_ctok[col] : col) : 0;
+      }
     }
     for (int sp = warp; sp < ((P.debug & 1) ? 0 : nspan); sp += kNW) {
       const int q0 = sp * kSpanGP, q1 = min(ngp, q0 + kSpanGP);
@@ -877,7 +909,8 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             // (X, -128X') of this lane's two token columns
-            xx[nt] = *reinterpret_cast<const float4*>(sums + gl * TPP + nt * 8 + 2 * tid);
+            const float2 s0 = sums[gl * TPP + srow[nt][0]], s1 = sums[gl * TPP + srow[nt][1]];
+            xx[nt] = make_float4(s0.x, s0.y, s1.x, s1.y);
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
               d[i][nt][0] = xx[nt].y;
@@ -1045,6 +1078,7 @@ static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, in
     if (P.nstage < 2) return fail(LRC_ERR_UNSUPPORTED, "tiled kernel: K too large for smem");
   }
   fits(nt);  // final x' row count for the chosen N-tiling
+  P.prebuilt = (UP && max_tok >= 1 && max_tok <= 8 * nt) ? 1 : 0;
   return (nt == 1) ? launch_one<UP, 1>(P, num_sms, st, pdl) : launch_one<UP, 2>(P, num_sms, st, pdl);
 }
 

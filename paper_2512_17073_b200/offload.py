@@ -12,7 +12,7 @@ Per layer step (decode, B <= 8 tokens):
    copy the expert's bytes host -> slot on the copy stream;
 3. point the layer's expert descriptors at the slots (``lrc_layer_set_expert``)
    and run the layer forward on the compute stream after the copies' events;
-All copies of a step are issued before the (blocking) descriptor updates, so
+All copies of a step are issued before the stream-ordered descriptor updates, so
 the host link runs back to back.  Temporal locality of routing across tokens is
 served by the LRU itself (a speculative next-layer prefetch was measured to
 regress -- it reorders the LRU onto slots still in use -- and was removed).
@@ -210,7 +210,8 @@ class OffloadEngine:
         slots = {e: self._fetch((layer, e), keys) for e in need}
         for e in need:
             d = self._desc(layer, e, slots[e])
-            _lib.check(_lib.lib().lrc_layer_set_expert(dl._handle, e, ctypes.byref(d)))
+            _lib.check(_lib.lib().lrc_layer_set_expert_async(dl._handle, e, ctypes.byref(d),
+                                                             _lib.stream_ptr()))
             dl._experts[e] = d  # a workspace re-create keeps the current slots
             torch.cuda.current_stream().wait_event(self.slot_ready[slots[e]])
         y, _, _ = dl.forward(x, self.k, self.n)
