@@ -297,7 +297,7 @@ static lrc_status validate_expert(const lrc_expert& e, int hidden, int ffn) {
 // compensators, quantized factors re-laid out as LR tiles (raw fp32 factors ->
 // generic path).  Also records the largest LR slot the kernels must stage.
 static void refresh_tiled(lrc_layer* L) {
-  bool ok = true;
+  bool ok = (L->hidden % 32) == 0;  // W2 streams as two 16-row-tiled halves
   L->lr_up_max = L->lr_down_max = 0;
   for (auto& e : L->host_experts) {
     ok = ok && e.up_tiles != nullptr && e.down_tiles != nullptr;

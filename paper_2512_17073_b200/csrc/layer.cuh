@@ -153,7 +153,7 @@ struct ExpertArgs {
 // (see fast.cu).  Offsets are per 16-row tile.
 struct LrLayout {
   int u1c, u3c, v2c, u1m, u3m, v2m, up_total;  // up: U1, U3 rows + V2^T rows
-  int u2c, u2m, down_total;                    // down: U2 rows
+  int u2c, u2bc, u2m, u2bm, down_total;        // down: U2 rows of the top / bottom row half
 };
 __host__ __device__ inline int pad16(int x) { return (x + 15) & ~15; }
 __host__ __device__ inline bool factor_present(const lrc_qmat& m) {
@@ -180,9 +180,13 @@ __host__ __device__ inline LrLayout lr_layout(const lrc_expert& e) {
   L.u3m = o; o += umeta(e.u3);
   L.v2m = o; o += factor_present(e.v2) ? pad16(r2 * 4) : 0;
   L.up_total = o;
+  // the down kernel streams W2 as two interleaved row halves (rows [0, H/2) and
+  // [H/2, H)), so a down LR tile holds the U2 rows of both halves' tile
   o = 0;
   L.u2c = o; o += codes(e.u2, r2);
+  L.u2bc = o; o += codes(e.u2, r2);
   L.u2m = o; o += umeta(e.u2);
+  L.u2bm = o; o += umeta(e.u2);
   L.down_total = o;
   return L;
 }

@@ -240,7 +240,7 @@ __device__ __noinline__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* x
 __device__ unsigned long long g_route_stamps[kStampCtas * 8];
 #define RSTAMP(k)                                                                     \
   do {                                                                                \
-    if (ra.stamp && threadIdx.x == 0) {                                               \
+    if ((ra.stamp & 1) && threadIdx.x == 0) {                                         \
       const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; \
       unsigned long long t_;                                                          \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
       // arrive on the cluster barrier first (never waits): the logits handoff
       // must not wait for this warp's cold instruction fetches
       asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-      if (rank == 0 && ra.plan.ticket != nullptr) warm_tail(ra, s_warm, s_hc, s_et);
+      if (rank == 0 && ra.plan.ticket != nullptr && !(ra.stamp & 2)) warm_tail(ra, s_warm, s_hc, s_et);
     }
     return;
   }
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
   } else if (warp < nb) {
     select_topk_warp(lg + warp * ldl, ra.E, ra.k, ra.renorm, b0 + warp, ra.probs, ra.topk_idx,
                      ra.topk_w, s_tidx + warp * ra.k, s_tw + warp * ra.k,
-                     (ra.stamp && warp == 0 && blockIdx.y * gridDim.x + blockIdx.x < kStampCtas)
+                     ((ra.stamp & 1) && warp == 0 && blockIdx.y * gridDim.x + blockIdx.x < kStampCtas)
                          ? &g_route_stamps[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + 2]
                          : nullptr);
   }
@@ -799,7 +799,9 @@ __device__ __noinline__ void warm_tail(const RouteArgs& ra, WarmScratch& ws, con
 int route_tiles(int64_t B) { return static_cast<int>((B + kTT - 1) / kTT); }
 
 lrc_status launch_route(const RouteArgs& ra_in, cudaStream_t st) {
-  static const int stamps = getenv("LRC_ROUTE_STAMPS") != nullptr;
+  // debug knobs: bit 0 = %globaltimer stamps, bit 1 = no tail warm-up warp
+  static const int stamps = (getenv("LRC_ROUTE_STAMPS") != nullptr ? 1 : 0) |
+                            (getenv("LRC_ROUTE_NOWARM") != nullptr ? 2 : 0);
   RouteArgs ra = ra_in;
   ra.stamp = stamps;
   // leader: logits scratch (kTT tokens x (E + 64) doubles); aux CTAs: the bf16

@@ -266,12 +266,14 @@ __global__ void build_lr_up_kernel(lrc_expert e, LrLayout L, uint8_t* __restrict
   }
 }
 
-__global__ void build_lr_down_kernel(lrc_expert e, LrLayout L, uint8_t* __restrict__ out) {
+__global__ void build_lr_down_kernel(lrc_expert e, LrLayout L, uint8_t* __restrict__ out, int half) {
   const int64_t t = blockIdx.x;
   uint8_t* base = out + t * L.down_total;
-  if (factor_present(e.u2)) {
+  if (factor_present(e.u2)) {  // tile t of the top half and of the bottom half
     fill_u_codes(base + L.u2c, e.u2, t * 16);
+    fill_u_codes(base + L.u2bc, e.u2, half + t * 16);
     fill_u_meta(base + L.u2m, e.u2, t * 16);
+    fill_u_meta(base + L.u2bm, e.u2, half + t * 16);
   }
 }
 
@@ -495,7 +497,9 @@ __device__ unsigned long long g_item_stamps[2][64][6];
 
 template <bool UP, int NT>
 __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constant__ TiledParams P) {
-  constexpr int NI = UP ? 2 : 1;
+  // two interleaved matrices per tile: w1|w3 (UP) or the two row halves of W2
+  // (DOWN: two independent accumulator chains, as for the up projection)
+  constexpr int NI = 2;
   constexpr int TPP = 8 * NT;  // tokens per pass
   constexpr int kEpi0 = kNW, kProd = kNW + kNEpi;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -711,8 +715,9 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
         const int pi = UP ? il : 2;
         const int r = EP.r[pi];
         const uint8_t* lr = st + P.stage_bytes;
-        const uint32_t* cw = reinterpret_cast<const uint32_t*>(lr + (UP ? (il ? EP.L.u3c : EP.L.u1c) : EP.L.u2c));
-        const uint8_t* meta = lr + (UP ? (il ? EP.L.u3m : EP.L.u1m) : EP.L.u2m);
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(
+            lr + (UP ? (il ? EP.L.u3c : EP.L.u1c) : (il ? EP.L.u2bc : EP.L.u2c)));
+        const uint8_t* meta = lr + (UP ? (il ? EP.L.u3m : EP.L.u1m) : (il ? EP.L.u2bm : EP.L.u2m));
         const int gsu = EP.ugs[pi];  // LR tile codes are 4-bit nibbles
         const int gpu = (r + gsu - 1) / gsu;
         const bool fast = (r % 8) == 0 && (gsu % 8) == 0;
@@ -771,8 +776,8 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
             actw[n * 16 + rr] = act;
             if (row < P.M) A.a16[static_cast<int64_t>(EP.epair[n]) * A.ffn + row] = f2bf(act);
           }
-        } else if (lane < 16 && row < P.M) {
-          atomicAdd(&A.y[static_cast<int64_t>(EP.etok[n]) * A.hidden + row], EP.ew[n] * v);
+        } else if (lane_on && row < P.M) {  // row half il of W2
+          atomicAdd(&A.y[static_cast<int64_t>(EP.etok[n]) * A.hidden + il * P.M + row], EP.ew[n] * v);
         }
       }
       __syncwarp();
@@ -1009,7 +1014,7 @@ void tiled_stamps_copy(uint64_t* host, int n) {
 
 template <bool UP, int NT>
 static lrc_status launch_one(const TiledParams& P, int num_sms, cudaStream_t st, bool pdl) {
-  constexpr int NI = UP ? 2 : 1;
+  constexpr int NI = 2;
   const SmemMap m = smem_map<NI, NT>(P);
   auto fn = tiled_kernel<UP, NT>;
   static int configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
@@ -1042,10 +1047,10 @@ static lrc_status launch_one(const TiledParams& P, int num_sms, cudaStream_t st,
 template <bool UP>
 static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, int lr_max,
                                cudaStream_t st, bool pdl) {
-  constexpr int NI = UP ? 2 : 1;
+  constexpr int NI = 2;  // w1|w3, or the two row halves of W2
   TiledParams P{};
   P.a = a;
-  P.M = UP ? a.ffn : a.hidden;
+  P.M = UP ? a.ffn : a.hidden / 2;  // rows per interleaved matrix
   P.K = UP ? a.hidden : a.ffn;
   P.GP = (P.K + 127) / 128;
   P.RT = (P.M + 15) / 16;
@@ -1140,7 +1145,7 @@ extern "C" lrc_status lrc_lr_tiles_bytes(const lrc_expert* e, int hidden, int ff
   if (s != LRC_OK) return s;
   const LrLayout L = lr_layout(*e);
   *up_bytes = static_cast<int64_t>(L.up_total) * ((ffn + 15) / 16);
-  *down_bytes = static_cast<int64_t>(L.down_total) * ((hidden + 15) / 16);
+  *down_bytes = static_cast<int64_t>(L.down_total) * ((hidden / 2 + 15) / 16);
   return LRC_OK;
 }
 
@@ -1156,7 +1161,7 @@ extern "C" lrc_status lrc_build_lr_tiles(const lrc_expert* e, int hidden, int ff
     LRC_CHECK_LAUNCH();
   }
   if (L.down_total > 0 && down_lr) {
-    build_lr_down_kernel<<<(hidden + 15) / 16, 256, 0, st>>>(*e, L, down_lr);
+    build_lr_down_kernel<<<(hidden / 2 + 15) / 16, 256, 0, st>>>(*e, L, down_lr, hidden / 2);
     LRC_CHECK_LAUNCH();
   }
   return LRC_OK;

@@ -95,6 +95,23 @@ def build_tiles(mats, keep: _Keep):
     return t
 
 
+def build_down_tiles(w2: _lib.LrcQmat, keep: _Keep):
+    """W2 tiles for the down kernel: the two row halves [0, H/2) and [H/2, H)
+    interleaved as the kernel's two matrices (two accumulator chains)."""
+    half = w2.rows // 2
+    groups = -(-w2.cols // w2.group_size)
+    views = []
+    for r0 in (0, half):
+        v = _lib.LrcQmat()
+        ctypes.memmove(ctypes.byref(v), ctypes.byref(w2), ctypes.sizeof(_lib.LrcQmat))
+        v.rows = half
+        v.packed = w2.packed + (r0 * w2.cols * w2.bits) // 8
+        v.scales = w2.scales + r0 * groups * 2
+        v.zeros = w2.zeros + r0 * groups * 2
+        views.append(v)
+    return build_tiles(views, keep)
+
+
 def build_lr_tiles(ex: _lib.LrcExpert, hidden: int, ffn: int, keep: _Keep) -> bool:
     """Low-rank factor tiles riding with the weight tiles (csrc/fast.cu); False if the
     factors cannot be tiled (raw fp32 factors -> generic kernels)."""
@@ -113,7 +130,8 @@ def build_lr_tiles(ex: _lib.LrcExpert, hidden: int, ffn: int, keep: _Keep) -> bo
 
 
 def tiles_eligible(*mats: _lib.LrcQmat) -> bool:
-    return all(m.bits == 2 and m.group_size == 64 and m.packed for m in mats)
+    """2-bit gs64 codes; W2 (rows = hidden) must split into 16-row-tiled halves."""
+    return all(m.bits == 2 and m.group_size == 64 and m.packed for m in mats) and mats[-1].rows % 32 == 0
 
 
 class LRCMoELayer:
@@ -253,7 +271,7 @@ class LRCMoELayer:
                     absent.w2 = _zero_qmat(hidden, ffn, keep)
                     if tiles and tiles_eligible(absent.w1, absent.w3, absent.w2):
                         absent.up_tiles = build_tiles([absent.w1, absent.w3], keep).data_ptr()
-                        absent.down_tiles = build_tiles([absent.w2], keep).data_ptr()
+                        absent.down_tiles = build_down_tiles(absent.w2, keep).data_ptr()
                 experts.append(absent)
                 continue
             else:
@@ -269,7 +287,7 @@ class LRCMoELayer:
                 ex.rank = rank
             if tiles and tiles_eligible(ex.w1, ex.w3, ex.w2):
                 ex.up_tiles = build_tiles([ex.w1, ex.w3], keep).data_ptr()
-                ex.down_tiles = build_tiles([ex.w2], keep).data_ptr()
+                ex.down_tiles = build_down_tiles(ex.w2, keep).data_ptr()
                 if ex.rank:
                     build_lr_tiles(ex, hidden, ffn, keep)
             experts.append(ex)

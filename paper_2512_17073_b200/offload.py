@@ -30,7 +30,7 @@ import collections
 import ctypes
 
 from . import _lib
-from .device import LRCMoELayer, _Keep, _zero_qmat, build_tiles
+from .device import LRCMoELayer, _Keep, _zero_qmat, build_down_tiles, build_tiles
 
 NAMES = ("up", "down", "up_lr", "down_lr", "v1p", "v1s", "v1z", "v3p", "v3s", "v3z")
 
@@ -65,7 +65,7 @@ def host_experts_from_synth(sl) -> list:
     out = []
     for e, ex in enumerate(sl.layer._experts):
         keep = _Keep()
-        dev = {"up": build_tiles([ex.w1, ex.w3], keep), "down": build_tiles([ex.w2], keep)}
+        dev = {"up": build_tiles([ex.w1, ex.w3], keep), "down": build_down_tiles(ex.w2, keep)}
         if ex.rank:
             dev["up_lr"], dev["down_lr"] = _lr_tiles(ex, sl.hidden, sl.ffn)
             for v in ("v1", "v3"):

@@ -17,7 +17,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .device import LRCMoELayer, _Keep, build_lr_tiles, build_tiles
+from .device import LRCMoELayer, _Keep, build_down_tiles, build_lr_tiles, build_tiles
 
 MIXTRAL = dict(hidden=4096, ffn=14336, num_experts=8, top_k=2)
 DEEPSEEK = dict(hidden=2048, ffn=11008, num_experts=64, top_k=8)
@@ -87,7 +87,7 @@ class SynthLayer:
                 ex.rank = rank
             if tiles and bits == 2:
                 ex.up_tiles = build_tiles([ex.w1, ex.w3], self.keep).data_ptr()
-                ex.down_tiles = build_tiles([ex.w2], self.keep).data_ptr()
+                ex.down_tiles = build_down_tiles(ex.w2, self.keep).data_ptr()
                 if ex.rank:
                     build_lr_tiles(ex, hidden, ffn, self.keep)
             experts.append(ex)
