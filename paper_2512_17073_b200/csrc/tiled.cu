@@ -319,7 +319,7 @@ __host__ __device__ inline SmemMap smem_map(const TiledParams& p) {
   SmemMap m;
   int o = p.nstage * (p.stage_bytes + p.lr_slot);
   m.xs = o;
-  o = align16(o + (p.xs_rows + 1) * p.xs_stride * 2);  // +1: shared zero row
+  o = align16(o + p.xs_rows * p.xs_stride * 2);
   m.sums = o;
   o = align16(o + p.SPC * kSpanGP * 2 * TPP * 8);
   m.red = o;
@@ -580,9 +580,6 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // the shared zero row read by MMA lanes whose token column is empty
-  for (int i = threadIdx.x; i < P.xs_stride / 2; i += blockDim.x)
-    reinterpret_cast<uint32_t*>(xs + P.xs_rows * P.xs_stride)[i] = 0u;
   __syncthreads();
   if (threadIdx.x == 0) TSTAMP(2);
   const int beg = s_range[0], end = s_range[1];
@@ -862,7 +859,8 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
         consumer_sync();
       }
       if (!P.prebuilt) {
-        // only real token rows are built; empty columns read the shared zero row
+        // only real token rows are built (empty MMA columns read row 0: their
+        // accumulators are never read -- MMA columns are independent)
         build_xprime<UP, NT>(A, P, xs, sums, UP ? s_ctok : s_cpair, pass_tok, gp0 * 128, (gp1 - gp0) * 2,
                              ctid, kNW * 32);
       }
@@ -881,14 +879,15 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
 
     const int ngp = gp1 - gp0;
     const int nspan = (ngp + kSpanGP - 1) / kSpanGP;
-    // B-fragment row of this lane per N-tile: token column nt*8+gid, or the zero row
+    // B-fragment row of this lane per N-tile: token column nt*8+gid (empty columns
+    // read row 0; their results are discarded)
     // x' / sums row of a token column: its pass position, or (prebuilt) its token
     const uint16_t* xrow[NT];
     int srow[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int n = nt * 8 + gid;
-      xrow[nt] = xs + (n < pass_tok ? (P.prebuilt ? s_ctok[n] : n) : P.xs_rows) * P.xs_stride + tid * 4;
+      xrow[nt] = xs + (n < pass_tok ? (P.prebuilt ? s_ctok[n] : n) : 0) * P.xs_stride + tid * 4;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int col = nt * 8 + 2 * tid + c;
