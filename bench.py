@@ -324,7 +324,7 @@ def run_ours(args, world, rank):
     e2e = {"value": round(world * args.steps * B / (e2e_ms / 1e3), 1), "unit": "tokens/s",
            "h2d_bytes_per_step": B * HIDDEN * 2, "d2h_bytes_per_step": B * HIDDEN * 4,
            "ms_per_step": round(e2e_ms / args.steps, 5),
-           "path": "lrc_layer_forward_host (C-ABI, pinned host x/y, eager launches)"}
+           "path": "lrc_layer_forward_host (C-ABI, pinned host x/y read/written by staging kernels in the PDL chain)"}
 
     # batch sweep (decode batch 1..64, same rotation, graph-replayed)
     sweep = {}

@@ -602,19 +602,68 @@ extern "C" lrc_status lrc_layer_forward_generic(lrc_layer* L, const uint16_t* x,
                       stream, false);
 }
 
+// Host-buffer staging as kernels (word copies through the UVA mapping of pinned
+// memory).  stage-in: releases its dependents at once, copies x, then waits for
+// its predecessor (the previous call's stage-out) before completing -- so the
+// router's own wait also covers the previous y read.  stage-out: waits for the
+// down kernel, then copies y.
+__global__ void stage_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int64_t n,
+                             int in) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (!in) asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+  if (in) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+static cudaError_t launch_stage(bool in, const void* src, void* dst, size_t bytes, cudaStream_t st,
+                                bool pdl) {
+  const int64_t n = static_cast<int64_t>(bytes / 4);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(32, (n + 255) / 256)));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, stage_kernel, static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst),
+                            n, in ? 1 : 0);
+}
+
 extern "C" lrc_status lrc_layer_forward_host(lrc_layer* L, const uint16_t* x_host, int64_t B,
                                              int top_k, int top_n, int renormalize,
                                              int compensate_shared, float* y_host, void* stream) {
   if (!L || !x_host || !y_host) return fail(LRC_ERR_INVALID, "forward_host: null argument");
   if (B < 0 || B > L->max_tokens) return fail(LRC_ERR_UNSUPPORTED, "B above max_tokens");
   cudaStream_t st = as_stream(stream);
-  LRC_CUDA_TRY(cudaMemcpyAsync(L->x_stage, x_host, sizeof(uint16_t) * B * L->hidden,
-                               cudaMemcpyHostToDevice, st));
+  const size_t xb = sizeof(uint16_t) * B * L->hidden, yb = sizeof(float) * B * L->hidden;
+  if (B == 0) return LRC_OK;
+  // Pinned (device-mapped under UVA) host buffers: the copies are kernels, so the
+  // whole call stays one programmatic-dependent-launch chain and the next
+  // router still overlaps the previous layer's tail.  Pageable: plain copies.
+  cudaPointerAttributes ax{}, ay{};
+  const bool mapped = cudaPointerGetAttributes(&ax, x_host) == cudaSuccess &&
+                      cudaPointerGetAttributes(&ay, y_host) == cudaSuccess &&
+                      ax.type == cudaMemoryTypeHost && ay.type == cudaMemoryTypeHost &&
+                      ax.devicePointer != nullptr && ay.devicePointer != nullptr && xb % 4 == 0;
+  cudaGetLastError();  // clear a sticky error from probing pageable memory
+  const bool pdl = !L->profiling && L->pdl;
+  if (mapped) {
+    LRC_CUDA_TRY(launch_stage(true, ax.devicePointer, L->x_stage, xb, st, pdl));
+  } else {
+    LRC_CUDA_TRY(cudaMemcpyAsync(L->x_stage, x_host, xb, cudaMemcpyHostToDevice, st));
+  }
   lrc_status s = forward_impl(L, L->x_stage, B, top_k, top_n, renormalize, compensate_shared,
-                              L->y_stage, nullptr, nullptr, stream, true);
+                              L->y_stage, nullptr, nullptr, st, true);
   if (s != LRC_OK) return s;
-  LRC_CUDA_TRY(cudaMemcpyAsync(y_host, L->y_stage, sizeof(float) * B * L->hidden,
-                               cudaMemcpyDeviceToHost, st));
+  if (mapped) {
+    LRC_CUDA_TRY(launch_stage(false, L->y_stage, ay.devicePointer, yb, st, pdl));
+  } else {
+    LRC_CUDA_TRY(cudaMemcpyAsync(y_host, L->y_stage, yb, cudaMemcpyDeviceToHost, st));
+  }
   return LRC_OK;
 }
 

@@ -50,3 +50,19 @@ def test_offload_single_layer_exact():
     assert eng.stats["misses"] >= 3
     per = sum(b.numel() for b in eng.host[0][0].bufs.values())
     assert eng.stats["bytes"] >= eng.stats["misses"] * per * 0.9
+
+
+@pytest.mark.gpu
+def test_forward_host_graph_replay():
+    """lrc_layer_forward_host captures its H2D -> layer -> D2H sequence as a
+    CUDA graph per shape; replays with new host buffers must match forward()."""
+    sl = SynthLayer(512, 1024, 8, top_k=2, rank=16, seed=41, max_tokens=8)
+    for B in (1, 1, 3, 3, 3, 1):
+        x = torch.randn((B, 512), device="cuda").to(torch.bfloat16)
+        xh = x.cpu().pin_memory()
+        yh = torch.empty((B, 512), dtype=torch.float32).pin_memory()
+        sl.layer.forward_host(xh, yh, 2, 1)
+        torch.cuda.synchronize()
+        ref = sl.layer.forward(x, 2, 1)[0].cpu()
+        err = float((yh - ref).norm() / ref.norm())
+        assert err < 1e-5, (B, err)
