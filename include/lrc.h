@@ -177,6 +177,12 @@ lrc_status lrc_layer_forward_host(lrc_layer* layer, const uint16_t* x_host, int6
  * around each phase; lrc_layer_phase_ms waits for the last forward and writes
  * {route, lr_down, up, down} durations in milliseconds. */
 lrc_status lrc_layer_set_profiling(lrc_layer* layer, int enabled);
+/* Batches of B >= min_tokens tokens run the tcgen05 grouped dequant-GEMM
+ * (prefill) path when the layer is eligible (2-bit gs=64 weights, hidden and
+ * ffn multiples of 64); min_tokens <= 0 disables it.  Default 256 (env
+ * LRC_PREFILL_MIN). */
+lrc_status lrc_layer_set_prefill_min(lrc_layer* layer, int64_t min_tokens);
+int lrc_layer_prefill_eligible(const lrc_layer* layer);
 lrc_status lrc_layer_phase_ms(lrc_layer* layer, float* ms4);
 /* Debug: %globaltimer (ns) stamps, 8 per CTA, of the last launch of the router
  * (which = 0; enabled by LRC_ROUTE_STAMPS=1 in the environment) or of the

@@ -230,6 +230,11 @@ struct lrc_layer {
   int hidden = 0, ffn = 0, E = 0, S = 0, max_tokens = 0, k_max = 0, maxr = 0;
   int num_sms = 148;
   bool tiled = false;
+  bool prefill_ok = false;  // tcgen05 prefill GEMM eligible (2-bit gs64 reference-layout weights)
+  int64_t prefill_min = [] {
+    const char* v = getenv("LRC_PREFILL_MIN");
+    return v ? static_cast<int64_t>(atoll(v)) : static_cast<int64_t>(256);
+  }();
   int last_launches = 0;
   const double* gate_t = nullptr;
   std::vector<lrc_expert> host_experts;
@@ -311,6 +316,8 @@ static void refresh_tiled(lrc_layer* L) {
     L->lr_down_max = std::max(L->lr_down_max, lay.down_total);
   }
   L->tiled = ok;
+  L->prefill_ok = prefill_eligible(L->host_experts.data(), static_cast<int>(L->host_experts.size()),
+                                   L->hidden, L->ffn);
 }
 
 static lrc_status alloc_workspace(lrc_layer* L) {
@@ -468,6 +475,14 @@ extern "C" lrc_status lrc_layer_set_expert_async(lrc_layer* L, int expert_id, co
   return LRC_OK;
 }
 
+extern "C" lrc_status lrc_layer_set_prefill_min(lrc_layer* L, int64_t min_tokens) {
+  if (!L) return fail(LRC_ERR_INVALID, "set_prefill_min: null layer");
+  L->prefill_min = min_tokens;
+  return LRC_OK;
+}
+
+extern "C" int lrc_layer_prefill_eligible(const lrc_layer* L) { return L && L->prefill_ok ? 1 : 0; }
+
 extern "C" int lrc_layer_last_launches(const lrc_layer* L) { return L ? L->last_launches : 0; }
 
 static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int top_k, int top_n,
@@ -550,7 +565,11 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
     ++launches;
   }
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[2], st));
-  if (allow_tiled && L->tiled) {
+  if (allow_tiled && L->prefill_ok && L->prefill_min > 0 && B >= L->prefill_min) {
+    // large batches: tcgen05 grouped dequant-GEMM (up, V2.a, down)
+    if ((s = launch_prefill(a, np_bound, st, &launches)) != LRC_OK) return s;
+    if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));  // phases: up+mid+down lumped into [2]
+  } else if (allow_tiled && L->tiled) {
     const int tok_bound = static_cast<int>(std::min<int64_t>(B, L->max_tokens));
     // programmatic dependent launch: the next kernel's CTAs are scheduled as SMs
     // free up and block in griddepcontrol.wait (no PDL while timing phases)

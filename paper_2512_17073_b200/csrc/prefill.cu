@@ -1,0 +1,410 @@
+// tcgen05 grouped dequant-GEMM for prefill and large batches (SURVEY 8(a) K3,
+// config C4).  Semantics: ref/moe.py:217-259 forward(mode="compensated") with
+// ref/lowrank.py:153-165 applying U.(V.x) for each token's top-n experts only.
+//
+// One CTA computes a [128-row x 256-pair] tile of TWO weight matrices that
+// share the B operand, over K in 64-column slabs (one 128-byte swizzle row):
+//   up   : W1 and W3 rows [m0, m0+128) x the expert's token rows of x
+//          -> SwiGLU in the epilogue -> bf16 activations a16[pair][ffn];
+//   down : W2 rows [m0, m0+128) and [m0+128, m0+256) x the pairs' a16 rows
+//          -> y[token] += w_pair * (.) with fp32 reductions.
+// Roles (288 threads, one CTA per SM: 193 KB smem, all 512 TMEM columns):
+//   warps 0-7  producers: thread t dequantizes row t&127 of matrix t>>7 (c*s+z
+//              in fp32, rounded once to bf16; codes and metadata prefetched two
+//              slabs ahead) straight into SWIZZLE_128B smem, and gathers its
+//              share of the B rows with cp.async one slab ahead (zero-filled
+//              past the expert's pairs); after the K loop, the epilogue.
+//   warp 8     one thread issues tcgen05.mma (M=128, N=256, K=16) into the two
+//              fp32 TMEM accumulators and commits each stage back to the
+//              producers (3-stage mbarrier ring).
+// The low-rank term is K augmentation: extra slabs whose A rows hold the U
+// factors (up: U1 in columns [0, R), U3 in [R, 2R); down: U2) and whose B rows
+// hold the pair's V.x vectors t (zero for uncompensated pairs), so U.(V.x)
+// lands in the same accumulator and Q(W)+UV^T is never formed.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "layer.cuh"
+#include "umma.cuh"
+
+namespace lrc {
+namespace {
+
+constexpr int kTM = 128;  // rows per accumulator
+constexpr int kTN = 256;  // pairs per tile (MMA N)
+constexpr int kKS = 64;   // K slab
+constexpr int kStages = 3;
+constexpr int kSlabA = kTM * 128;
+constexpr int kSlabB = kTN * 128;
+constexpr int kStageBytes = 2 * kSlabA + kSlabB;  // 64 KB
+constexpr int kProd = 256;
+constexpr int kThreads = kProd + 32;
+constexpr int kMmaWarp = kProd / 32;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024;
+constexpr uint32_t kIdesc = umma::idesc_bf16(kTM, kTN);
+
+struct PrefillArgs {
+  ExpertArgs a;
+  int down;      // 0: up, 1: down
+  int M, K;      // weight rows, main reduction length
+  int lr_slabs;  // K-augmentation slabs (0: layer without compensators)
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__device__ __forceinline__ uint64_t f32x2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint32_t bf16x2_of(uint64_t v) {  // round both halves to bf16
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return pack_bf16(lo, hi);
+}
+
+// Codes and group metadata of one row for one 64-column slab (reference
+// layout: row-major LSB-first 2-bit stream, one fp16 scale/zero per group).
+// Metadata stays raw until use so a prefetch never waits on its load.
+struct RowSlab {
+  uint4 c;
+  uint32_t sz;  // scale | zero << 16 (fp16 bits)
+};
+
+__device__ __forceinline__ RowSlab load_row(const lrc_qmat& W, int row, int M, int K, int k0) {
+  RowSlab r{make_uint4(0, 0, 0, 0), 0u};
+  if (row < M) {
+    const int64_t e0 = static_cast<int64_t>(row) * K + k0;
+    r.c = __ldg(reinterpret_cast<const uint4*>(W.packed + (e0 >> 2)));
+    const int64_t g = static_cast<int64_t>(row) * (K / kKS) + k0 / kKS;
+    r.sz = static_cast<uint32_t>(__ldg(W.scales + g)) | (static_cast<uint32_t>(__ldg(W.zeros + g)) << 16);
+  }
+  return r;
+}
+
+// Dequantize a row slab into its SWIZZLE_128B row.  Code i of a 16-bit field
+// is masked in place: (v & 3 << 2i) | 0x4B000000 is the float 2^23 + c*2^2i;
+// one FADD2 removes 2^23 and one FFMA2 with s*2^-2i (exact power-of-two
+// rescale) and z gives c*s + z with the same single rounding as fmaf(c, s, z).
+__device__ __forceinline__ void store_row(uint8_t* slab, int r, const RowSlab& v) {
+  const float s = h2f(static_cast<uint16_t>(v.sz & 0xFFFF)), z = h2f(static_cast<uint16_t>(v.sz >> 16));
+  uint64_t sp[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sp[j] = f32x2(s * exp2f(-4.0f * j), s * exp2f(-4.0f * j - 2.0f));
+  const uint64_t zz = f32x2(z, z), mm = f32x2(-8388608.0f, -8388608.0f);
+  const uint32_t w[4] = {v.c.x, v.c.y, v.c.z, v.c.w};
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch) {
+    const uint32_t b = (ch & 1) ? (w[ch >> 1] >> 16) : w[ch >> 1];
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float f0 = __uint_as_float(0x4B000000u | (b & (3u << (4 * j))));
+      const float f1 = __uint_as_float(0x4B000000u | (b & (12u << (4 * j))));
+      uint64_t t;
+      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f32x2(f0, f1)), "l"(mm));
+      asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(t), "l"(sp[j]), "l"(zz));
+      o[j] = bf16x2_of(t);
+    }
+    *reinterpret_cast<uint4*>(slab + umma::sw128_chunk(r, ch)) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+__device__ __forceinline__ int64_t t_index(const ExpertArgs& a, int p, int proj) {
+  return ((static_cast<int64_t>(a.plan.pair_token[p]) * a.ne + a.plan.pair_expert[p]) * 3 + proj) * a.maxr;
+}
+
+// A row of a K-augmentation slab: U(row, col - c0) for col in [c0, c0 + rank)
+__device__ void store_u_row(uint8_t* slab, int r, const lrc_qmat& U, int row, int gcol0, int c0) {
+  const bool pres = qmat_present(U) && row < U.rows;
+#pragma unroll 1
+  for (int j = 0; j < 8; ++j) {
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int col = gcol0 + 8 * j + q - c0;
+      v[q] = (pres && col >= 0 && col < U.cols) ? qmat_elem(U, row, col) : 0.0f;
+    }
+    *reinterpret_cast<uint4*>(slab + umma::sw128_chunk(r, j)) =
+        make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[kStages], empty[kStages], done;
+  __shared__ uint32_t tmem_base;
+  __shared__ const uint16_t* s_src[kTN];
+  __shared__ int s_pair[kTN];
+  const ExpertArgs& a = P.a;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // blockIdx.y -> (active expert, block of kTN of its pairs); the grid is an
+  // upper bound, surplus CTAs leave at once (uniformly)
+  int yb = blockIdx.y, ai = -1;
+  const int na = a.plan.counts[0];
+  for (int i = 0; i < na; ++i) {
+    const int nt = (a.plan.active_cnt[i] + kTN - 1) / kTN;
+    if (yb < nt) {
+      ai = i;
+      break;
+    }
+    yb -= nt;
+  }
+  if (ai < 0) return;
+  const int e = a.plan.active[ai];
+  const lrc_expert& E = a.experts[e];
+  const int off = a.plan.active_off[ai] + yb * kTN;
+  const int nvalid = min(kTN, a.plan.active_cnt[ai] - yb * kTN);
+  const int m0 = blockIdx.x * (P.down ? 2 * kTM : kTM);
+
+  int any_comp = 0;
+  for (int n = tid; n < kTN; n += kThreads) {
+    int p = -1;
+    const uint16_t* src = nullptr;
+    if (n < nvalid) {
+      p = a.plan.pair_list[off + n];
+      src = P.down ? a.a16 + static_cast<int64_t>(p) * a.ffn
+                   : a.x + static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden;
+      any_comp |= a.plan.pair_comp[p] >= 0;
+    }
+    s_pair[n] = p;
+    s_src[n] = src;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      umma::bar_init(&full[i], kProd);
+      umma::bar_init(&empty[i], 1);
+    }
+    umma::bar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) umma::tmem_alloc<2 * kTN>(&tmem_base);
+  umma::fence_before_sync();
+  const int lr_on = __syncthreads_or(any_comp) && P.lr_slabs > 0;
+  umma::fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  const int main_slabs = P.K / kKS;
+  const int nslab = main_slabs + (lr_on ? P.lr_slabs : 0);
+
+  if (warp < kMmaWarp) {
+    // ------------------------------------------------------------ producers
+    const int mat = tid >> 7, rl = tid & (kTM - 1);  // A row rl of A1 (mat 0) / A3 (mat 1)
+    const lrc_qmat& W = P.down ? E.w2 : (mat ? E.w3 : E.w1);
+    const int row = m0 + (P.down ? mat * kTM : 0) + rl;
+    const int bc = tid & 7, bn0 = tid >> 3;  // B gather: 8 lanes per 128-byte row
+    auto issue_b = [&](int s) {
+      const uint32_t bb = umma::smem_u32(sm + (s % kStages) * kStageBytes + 2 * kSlabA);
+      const int k0 = s * kKS + bc * 8;
+#pragma unroll
+      for (int i = 0; i < kTN / (kProd / 8); ++i) {
+        const int n = bn0 + (kProd / 8) * i;
+        const uint16_t* src = s_src[n];
+        umma::cp_async16(bb + umma::sw128_chunk(n, bc), src ? src + k0 : a.x, src ? 16u : 0u);
+      }
+      umma::cp_async_commit();
+    };
+    issue_b(0);
+    RowSlab c0 = load_row(W, row, P.M, P.K, 0);
+    RowSlab c1 = main_slabs > 1 ? load_row(W, row, P.M, P.K, kKS) : RowSlab{};
+    for (int s = 0; s < nslab; ++s) {
+      const int stage = s % kStages;
+      uint8_t* As = sm + stage * kStageBytes + mat * kSlabA;
+      uint8_t* Bs = sm + stage * kStageBytes + 2 * kSlabA;
+      const int sn = s + 1;
+      if (sn < main_slabs) {  // next slab's B rows (cp.async), one slab ahead
+        if (sn >= kStages) umma::bar_wait(&empty[sn % kStages], ((sn / kStages) - 1) & 1);
+        issue_b(sn);
+      }
+      RowSlab c2{};
+      if (s + 2 < main_slabs) c2 = load_row(W, row, P.M, P.K, (s + 2) * kKS);  // codes two ahead
+      if (s < main_slabs) {
+        store_row(As, rl, c0);
+        if (sn < main_slabs)
+          umma::cp_async_wait<1>();
+        else
+          umma::cp_async_wait<0>();
+      } else {
+        // K augmentation slab: columns [g0, g0 + 64) of [t1 | t3] (up) or t2 (down)
+        if (s >= kStages) umma::bar_wait(&empty[stage], ((s / kStages) - 1) & 1);
+        const int g0 = (s - main_slabs) * kKS, R = a.maxr;
+        if (P.down)
+          store_u_row(As, rl, E.u2, row, g0, 0);
+        else
+          store_u_row(As, rl, mat ? E.u3 : E.u1, row, g0, mat ? R : 0);
+        const int n = tid;  // one B row per producer thread
+        const int p = s_pair[n];
+        const bool comp = p >= 0 && a.plan.pair_comp[p] >= 0;
+#pragma unroll 1
+        for (int j = 0; j < 8; ++j) {
+          float v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int col = g0 + 8 * j + q;
+            float t = 0.0f;
+            if (comp) {
+              if (P.down) {
+                if (col < R) t = a.t[t_index(a, p, 2) + col];
+              } else if (col < R) {
+                t = a.t[t_index(a, p, 0) + col];
+              } else if (col < 2 * R) {
+                t = a.t[t_index(a, p, 1) + col - R];
+              }
+            }
+            v[q] = t;
+          }
+          *reinterpret_cast<uint4*>(Bs + umma::sw128_chunk(n, j)) = make_uint4(
+              pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+        }
+      }
+      umma::fence_proxy_async();  // generic smem writes (and landed cp.async) -> tensor core
+      umma::bar_arrive(&full[stage]);
+      c0 = c1;
+      c1 = c2;
+    }
+  } else if (lane == 0) {
+    // ------------------------------------------------------------ MMA issue
+    for (int s = 0; s < nslab; ++s) {
+      const int stage = s % kStages;
+      umma::bar_wait(&full[stage], (s / kStages) & 1);
+      umma::fence_after_sync();
+      const uint32_t a1 = umma::smem_u32(sm + stage * kStageBytes), a3 = a1 + kSlabA, b = a3 + kSlabA;
+#pragma unroll
+      for (int kk = 0; kk < kKS / 16; ++kk) {
+        const uint32_t acc = (s | kk) != 0 ? 1u : 0u;
+        const uint64_t db = umma::sdesc(b + 32 * kk);
+        umma::mma_bf16(tmem, umma::sdesc(a1 + 32 * kk), db, kIdesc, acc);
+        umma::mma_bf16(tmem + kTN, umma::sdesc(a3 + 32 * kk), db, kIdesc, acc);
+      }
+      umma::commit(&empty[stage]);
+    }
+    umma::commit(&done);
+  }
+
+  if (warp < kMmaWarp) {
+    // ------------------------------------------------------------ epilogue
+    // warp w reads TMEM lanes 32(w&3).. (rows) for pair columns [128(w>>2), +128)
+    umma::bar_wait(&done, 0);
+    umma::fence_after_sync();
+    const int q = warp & 3, half = warp >> 2;
+    const uint32_t lbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const int ra = m0 + q * 32 + lane, rb = m0 + kTM + q * 32 + lane;
+    const int cend = min(nvalid, (half + 1) * (kTN / 2));
+    for (int c0 = half * (kTN / 2); c0 < cend; c0 += 32) {
+      float h1[32], h3[32];
+      umma::tmem_ld32(lbase + c0, h1);
+      umma::tmem_ld32(lbase + kTN + c0, h3);
+      if (!P.down) {
+        if (ra < P.M) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int n = c0 + j;
+            if (n < nvalid) {
+              const float g = h1[j];
+              a.a16[static_cast<int64_t>(s_pair[n]) * a.ffn + ra] =
+                  f2bf(__fdividef(g, 1.0f + __expf(-g)) * h3[j]);
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = c0 + j;
+          if (n < nvalid) {
+            const int p = s_pair[n];
+            const float w = a.plan.pair_w[p];
+            float* yr = a.y + static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden;
+            if (ra < P.M) atomicAdd(yr + ra, w * h1[j]);
+            if (rb < P.M) atomicAdd(yr + rb, w * h3[j]);
+          }
+        }
+      }
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == kMmaWarp) umma::tmem_dealloc<2 * kTN>(tmem);
+}
+
+// t[b][e][2][j] = V2(e)[j, :] . a16_p for the compensated pairs (bf16 activations)
+__global__ void __launch_bounds__(256) lr_mid16_kernel(ExpertArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = blockIdx.x * 8 + warp;
+  const int slot = task / a.maxr;
+  if (slot >= a.plan.counts[1]) return;
+  const int j = task - slot * a.maxr;
+  const int p = a.plan.comp_list[slot];
+  const lrc_expert& E = a.experts[a.plan.pair_expert[p]];
+  const lrc_qmat& V = E.v2;
+  float acc = 0.0f;
+  if (qmat_present(V) && j < V.rows) {
+    const uint16_t* ap = a.a16 + static_cast<int64_t>(p) * a.ffn;
+    const bool g64 = V.dense == nullptr && V.group_size == 64 && ((V.cols * V.bits) % 32) == 0;
+    float av[1];
+    if (g64 && V.bits == 3) {
+      vrow_dot_tokens<3, 1>(V, j, ap, a.ffn, 1, av);
+      acc = av[0];
+    } else if (g64 && V.bits == 2) {
+      vrow_dot_tokens<2, 1>(V, j, ap, a.ffn, 1, av);
+      acc = av[0];
+    } else if (g64 && V.bits == 4) {
+      vrow_dot_tokens<4, 1>(V, j, ap, a.ffn, 1, av);
+      acc = av[0];
+    } else {
+      for (int k = lane; k < V.cols; k += 32) acc = fmaf(qmat_elem(V, j, k), bf2f(ap[k]), acc);
+      acc = warp_sum(acc);
+    }
+  }
+  if (lane == 0) a.t[t_index(a, p, 2) + j] = acc;
+}
+
+}  // namespace
+
+bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn) {
+  if (hidden % kKS != 0 || ffn % kKS != 0) return false;
+  for (int i = 0; i < n; ++i) {
+    const lrc_qmat* ws[3] = {&experts[i].w1, &experts[i].w3, &experts[i].w2};
+    for (auto w : ws)
+      if (w->dense != nullptr || w->packed == nullptr || w->bits != 2 || w->group_size != kKS ||
+          (reinterpret_cast<uintptr_t>(w->packed) & 15) != 0)
+        return false;
+  }
+  return true;
+}
+
+lrc_status launch_prefill(const ExpertArgs& a, int np_bound, cudaStream_t st, int* launches) {
+  static bool attr = false;
+  if (!attr) {
+    LRC_CUDA_TRY(cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    attr = true;
+  }
+  PrefillArgs P{};
+  P.a = a;
+  const int ytiles = (np_bound + kTN - 1) / kTN + a.ne;  // >= sum over experts of ceil(cnt / kTN)
+  P.down = 0;
+  P.M = a.ffn;
+  P.K = a.hidden;
+  P.lr_slabs = a.maxr ? (2 * a.maxr + kKS - 1) / kKS : 0;
+  prefill_kernel<<<dim3((a.ffn + kTM - 1) / kTM, ytiles), kThreads, kSmemBytes, st>>>(P);
+  LRC_CHECK_LAUNCH();
+  ++*launches;
+  if (a.maxr) {
+    lr_mid16_kernel<<<(np_bound * a.maxr + 7) / 8, 256, 0, st>>>(a);
+    LRC_CHECK_LAUNCH();
+    ++*launches;
+  }
+  P.down = 1;
+  P.M = a.hidden;
+  P.K = a.ffn;
+  P.lr_slabs = a.maxr ? (a.maxr + kKS - 1) / kKS : 0;
+  prefill_kernel<<<dim3((a.hidden + 2 * kTM - 1) / (2 * kTM), ytiles), kThreads, kSmemBytes, st>>>(P);
+  LRC_CHECK_LAUNCH();
+  ++*launches;
+  return LRC_OK;
+}
+
+}  // namespace lrc

@@ -149,6 +149,7 @@ class LRCMoELayer:
         self.gate_t = keep.add(torch.from_numpy(np.ascontiguousarray(np.asarray(gate, np.float64).T)).cuda())
         self.max_tokens, self.top_k = max_tokens, top_k
         self._handle = None
+        self._prefill_min = None  # None: the library default (LRC_PREFILL_MIN or 256)
         self._create()
 
     def _create(self):
@@ -161,6 +162,18 @@ class LRCMoELayer:
                                         self.num_experts, self.num_shared, arr,
                                         self.max_tokens, max(self.top_k, 1), ctypes.byref(h)))
         self._handle = h
+        if self._prefill_min is not None:
+            _lib.check(lib.lrc_layer_set_prefill_min(h, int(self._prefill_min)))
+
+    def set_prefill_min(self, min_tokens: int):
+        """Batches of >= min_tokens run the tcgen05 grouped-GEMM prefill path
+        (when eligible); <= 0 disables it."""
+        self._prefill_min = int(min_tokens)
+        _lib.check(_lib.lib().lrc_layer_set_prefill_min(self._handle, self._prefill_min))
+
+    @property
+    def prefill_eligible(self) -> bool:
+        return bool(_lib.lib().lrc_layer_prefill_eligible(self._handle))
 
     def __del__(self):
         try:
