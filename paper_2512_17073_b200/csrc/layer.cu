@@ -317,7 +317,7 @@ static void refresh_tiled(lrc_layer* L) {
   }
   L->tiled = ok;
   L->prefill_ok = prefill_eligible(L->host_experts.data(), static_cast<int>(L->host_experts.size()),
-                                   L->hidden, L->ffn);
+                                   L->hidden, L->ffn, L->maxr);
 }
 
 static lrc_status alloc_workspace(lrc_layer* L) {
@@ -560,13 +560,14 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   a.a16 = L->a16;
   a.y = y;
   a.max_pairs = L->max_pairs;
-  if (!spec && L->maxr) {  // exact V.x for the compensated pairs only
+  const bool prefill = allow_tiled && L->prefill_ok && L->prefill_min > 0 && B >= L->prefill_min;
+  if (!spec && L->maxr && !prefill) {  // exact V.x for the compensated pairs only
     if ((s = launch_lr_down(a, np_bound, st)) != LRC_OK) return s;
     ++launches;
   }
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[2], st));
-  if (allow_tiled && L->prefill_ok && L->prefill_min > 0 && B >= L->prefill_min) {
-    // large batches: tcgen05 grouped dequant-GEMM (up, V2.a, down)
+  if (prefill) {
+    // large batches: tcgen05 grouped dequant-GEMMs (V1|V3.x, up, V2.a, down)
     if ((s = launch_prefill(a, np_bound, st, &launches)) != LRC_OK) return s;
     if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));  // phases: up+mid+down lumped into [2]
   } else if (allow_tiled && L->tiled) {

@@ -204,7 +204,7 @@ lrc_status launch_down_tiled(const ExpertArgs& a, int num_sms, int max_tokens_pe
                              int lr_down_max, cudaStream_t st, bool pdl);
 
 // tcgen05 prefill GEMM (prefill.cu)
-bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn);
+bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn, int maxr);
 lrc_status launch_prefill(const ExpertArgs& a, int np_bound, cudaStream_t st, int* launches);
 
 }  // namespace lrc

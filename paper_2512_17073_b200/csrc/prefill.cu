@@ -43,9 +43,16 @@ constexpr int kMmaWarp = kProd / 32;
 constexpr int kSmemBytes = kStages * kStageBytes + 1024;
 constexpr uint32_t kIdesc = umma::idesc_bf16(kTM, kTN);
 
+enum Mode : int {
+  kUp = 0,      // A = W1 | W3 rows, B = x rows       -> SwiGLU -> a16
+  kDown = 1,    // A = W2 row halves, B = a16 rows    -> y += w * (.)
+  kVxUp = 2,    // A = V1 | V3 rows, B = x rows       -> t[.][0|1] (compensated pairs)
+  kVxDown = 3,  // A = V2 rows,      B = a16 rows     -> t[.][2]
+};
+
 struct PrefillArgs {
   ExpertArgs a;
-  int down;      // 0: up, 1: down
+  int mode;
   int M, K;      // weight rows, main reduction length
   int lr_slabs;  // K-augmentation slabs (0: layer without compensators)
 };
@@ -71,16 +78,17 @@ __device__ __forceinline__ uint32_t bf16x2_of(uint64_t v) {  // round both halve
 // Metadata stays raw until use so a prefetch never waits on its load.
 struct RowSlab {
   uint4 c;
-  uint32_t sz;  // scale | zero << 16 (fp16 bits)
+  uint32_t s, z;  // fp16 bits
 };
 
 __device__ __forceinline__ RowSlab load_row(const lrc_qmat& W, int row, int M, int K, int k0) {
-  RowSlab r{make_uint4(0, 0, 0, 0), 0u};
+  RowSlab r{make_uint4(0, 0, 0, 0), 0u, 0u};
   if (row < M) {
     const int64_t e0 = static_cast<int64_t>(row) * K + k0;
     r.c = __ldg(reinterpret_cast<const uint4*>(W.packed + (e0 >> 2)));
     const int64_t g = static_cast<int64_t>(row) * (K / kKS) + k0 / kKS;
-    r.sz = static_cast<uint32_t>(__ldg(W.scales + g)) | (static_cast<uint32_t>(__ldg(W.zeros + g)) << 16);
+    r.s = __ldg(W.scales + g);
+    r.z = __ldg(W.zeros + g);
   }
   return r;
 }
@@ -90,7 +98,7 @@ __device__ __forceinline__ RowSlab load_row(const lrc_qmat& W, int row, int M, i
 // one FADD2 removes 2^23 and one FFMA2 with s*2^-2i (exact power-of-two
 // rescale) and z gives c*s + z with the same single rounding as fmaf(c, s, z).
 __device__ __forceinline__ void store_row(uint8_t* slab, int r, const RowSlab& v) {
-  const float s = h2f(static_cast<uint16_t>(v.sz & 0xFFFF)), z = h2f(static_cast<uint16_t>(v.sz >> 16));
+  const float s = h2f(static_cast<uint16_t>(v.s)), z = h2f(static_cast<uint16_t>(v.z));
   uint64_t sp[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) sp[j] = f32x2(s * exp2f(-4.0f * j), s * exp2f(-4.0f * j - 2.0f));
@@ -117,9 +125,42 @@ __device__ __forceinline__ int64_t t_index(const ExpertArgs& a, int p, int proj)
   return ((static_cast<int64_t>(a.plan.pair_token[p]) * a.ne + a.plan.pair_expert[p]) * 3 + proj) * a.maxr;
 }
 
-// A row of a K-augmentation slab: U(row, col - c0) for col in [c0, c0 + rank)
-__device__ void store_u_row(uint8_t* slab, int r, const lrc_qmat& U, int row, int gcol0, int c0) {
-  const bool pres = qmat_present(U) && row < U.rows;
+template <int BITS>
+__device__ __forceinline__ void store_q_row_g64(uint8_t* slab, int r, const lrc_qmat& U, int row, int gcol0) {
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(U.packed);
+  const int64_t bit0 = (static_cast<int64_t>(row) * U.cols + gcol0) * BITS;  // multiple of 64*BITS: word aligned
+  const int64_t g = static_cast<int64_t>(row) * (U.cols / kKS) + gcol0 / kKS;
+  const float s = h2f(U.scales[g]), z = h2f(U.zeros[g]);
+  uint32_t w[2 * BITS + 1];
+#pragma unroll
+  for (int i = 0; i < 2 * BITS; ++i) w[i] = __ldg(words + (bit0 >> 5) + i);
+  w[2 * BITS] = 0u;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int b = (8 * j + q) * BITS;
+      v[q] = fmaf(static_cast<float>(__funnelshift_r(w[b >> 5], w[(b >> 5) + 1], b & 31) & ((1u << BITS) - 1u)),
+                  s, z);
+    }
+    *reinterpret_cast<uint4*>(slab + umma::sw128_chunk(r, j)) =
+        make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+  }
+}
+
+// Columns [gcol0, gcol0 + 64) of row `row` of a quantized (or dense) matrix,
+// shifted right by c0 (element col - c0; zero outside [0, cols) and for absent
+// rows) -> one SWIZZLE_128B row.  For the low-rank factors: U rows of the
+// K-augmentation slabs, V rows of the V.x GEMMs.
+__device__ void store_q_row(uint8_t* slab, int r, const lrc_qmat& U, int row, int gcol0, int c0) {
+  const bool pres = qmat_present(U) && row >= 0 && row < U.rows;
+  if (pres && c0 == 0 && U.dense == nullptr && U.group_size == kKS && (U.cols % kKS) == 0 &&
+      gcol0 + kKS <= U.cols) {
+    if (U.bits == 3) return store_q_row_g64<3>(slab, r, U, row, gcol0);
+    if (U.bits == 2) return store_q_row_g64<2>(slab, r, U, row, gcol0);
+    if (U.bits == 4) return store_q_row_g64<4>(slab, r, U, row, gcol0);
+  }
 #pragma unroll 1
   for (int j = 0; j < 8; ++j) {
     float v[8];
@@ -138,10 +179,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[kStages], empty[kStages], done;
   __shared__ uint32_t tmem_base;
-  __shared__ const uint16_t* s_src[kTN];
   __shared__ int s_pair[kTN];
   const ExpertArgs& a = P.a;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool b_act = P.mode == kDown || P.mode == kVxDown;  // B rows from a16 (else x)
+  const bool vx = P.mode >= kVxUp;
 
   // blockIdx.y -> (active expert, block of kTN of its pairs); the grid is an
   // upper bound, surplus CTAs leave at once (uniformly)
@@ -160,20 +202,16 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
   const lrc_expert& E = a.experts[e];
   const int off = a.plan.active_off[ai] + yb * kTN;
   const int nvalid = min(kTN, a.plan.active_cnt[ai] - yb * kTN);
-  const int m0 = blockIdx.x * (P.down ? 2 * kTM : kTM);
+  const int m0 = blockIdx.x * (P.mode == kDown ? 2 * kTM : kTM);
 
   int any_comp = 0;
   for (int n = tid; n < kTN; n += kThreads) {
     int p = -1;
-    const uint16_t* src = nullptr;
     if (n < nvalid) {
       p = a.plan.pair_list[off + n];
-      src = P.down ? a.a16 + static_cast<int64_t>(p) * a.ffn
-                   : a.x + static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden;
       any_comp |= a.plan.pair_comp[p] >= 0;
     }
     s_pair[n] = p;
-    s_src[n] = src;
   }
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -185,32 +223,59 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
   }
   if (warp == kMmaWarp) umma::tmem_alloc<2 * kTN>(&tmem_base);
   umma::fence_before_sync();
-  const int lr_on = __syncthreads_or(any_comp) && P.lr_slabs > 0;
+  any_comp = __syncthreads_or(any_comp);
   umma::fence_after_sync();
+  if (vx && !any_comp) {  // no compensated pair in this tile: nothing to compute
+    if (warp == kMmaWarp) umma::tmem_dealloc<2 * kTN>(tmem_base);
+    return;
+  }
   const uint32_t tmem = tmem_base;
   const int main_slabs = P.K / kKS;
-  const int nslab = main_slabs + (lr_on ? P.lr_slabs : 0);
+  const int nslab = main_slabs + ((any_comp && !vx) ? P.lr_slabs : 0);
 
   if (warp < kMmaWarp) {
     // ------------------------------------------------------------ producers
     const int mat = tid >> 7, rl = tid & (kTM - 1);  // A row rl of A1 (mat 0) / A3 (mat 1)
-    const lrc_qmat& W = P.down ? E.w2 : (mat ? E.w3 : E.w1);
-    const int row = m0 + (P.down ? mat * kTM : 0) + rl;
-    const int bc = tid & 7, bn0 = tid >> 3;  // B gather: 8 lanes per 128-byte row
-    auto issue_b = [&](int s) {
-      const uint32_t bb = umma::smem_u32(sm + (s % kStages) * kStageBytes + 2 * kSlabA);
-      const int k0 = s * kKS + bc * 8;
+    const lrc_qmat* Wp;
+    int row = m0 + rl;
+    switch (P.mode) {
+      case kUp: Wp = mat ? &E.w3 : &E.w1; break;
+      case kDown: Wp = &E.w2; row += mat * kTM; break;
+      case kVxUp: Wp = mat ? &E.v3 : &E.v1; break;
+      default: Wp = &E.v2; if (mat) row = -1; break;  // A3 unused (zero)
+    }
+    const lrc_qmat& W = *Wp;
+    // B gather: 8 lanes per 128-byte row, rows bn0 + 32 i; per-thread sources fixed for the tile
+    const int bc = tid & 7, bn0 = tid >> 3;
+    constexpr int kBRows = kTN / (kProd / 8);
+    const uint16_t* bsrc[kBRows];
+    uint32_t bmask = 0;
 #pragma unroll
-      for (int i = 0; i < kTN / (kProd / 8); ++i) {
-        const int n = bn0 + (kProd / 8) * i;
-        const uint16_t* src = s_src[n];
-        umma::cp_async16(bb + umma::sw128_chunk(n, bc), src ? src + k0 : a.x, src ? 16u : 0u);
+    for (int i = 0; i < kBRows; ++i) {
+      const int p = s_pair[bn0 + (kProd / 8) * i];
+      bsrc[i] = a.x + bc * 8;
+      if (p >= 0) {
+        bsrc[i] = (b_act ? a.a16 + static_cast<int64_t>(p) * a.ffn
+                         : a.x + static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden) + bc * 8;
+        bmask |= 1u << i;
       }
+    }
+    const uint32_t bdst0 = umma::smem_u32(sm + 2 * kSlabA) + umma::sw128_chunk(bn0, bc);
+    auto issue_b = [&](int s) {
+      const uint32_t bb = bdst0 + (s % kStages) * kStageBytes;
+      const int k0 = s * kKS;
+#pragma unroll
+      for (int i = 0; i < kBRows; ++i)
+        umma::cp_async16(bb + i * (kProd / 8) * 128, bsrc[i] + ((bmask >> i) & 1 ? k0 : 0),
+                         (bmask >> i) & 1 ? 16u : 0u);
       umma::cp_async_commit();
     };
     issue_b(0);
-    RowSlab c0 = load_row(W, row, P.M, P.K, 0);
-    RowSlab c1 = main_slabs > 1 ? load_row(W, row, P.M, P.K, kKS) : RowSlab{};
+    RowSlab c0{}, c1{};
+    if (!vx) {
+      c0 = load_row(W, row, P.M, P.K, 0);
+      if (main_slabs > 1) c1 = load_row(W, row, P.M, P.K, kKS);
+    }
     for (int s = 0; s < nslab; ++s) {
       const int stage = s % kStages;
       uint8_t* As = sm + stage * kStageBytes + mat * kSlabA;
@@ -221,9 +286,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
         issue_b(sn);
       }
       RowSlab c2{};
-      if (s + 2 < main_slabs) c2 = load_row(W, row, P.M, P.K, (s + 2) * kKS);  // codes two ahead
+      if (!vx && s + 2 < main_slabs) c2 = load_row(W, row, P.M, P.K, (s + 2) * kKS);  // codes two ahead
       if (s < main_slabs) {
-        store_row(As, rl, c0);
+        if (vx)
+          store_q_row(As, rl, W, row < P.M ? row : -1, s * kKS, 0);
+        else
+          store_row(As, rl, c0);
         if (sn < main_slabs)
           umma::cp_async_wait<1>();
         else
@@ -232,10 +300,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
         // K augmentation slab: columns [g0, g0 + 64) of [t1 | t3] (up) or t2 (down)
         if (s >= kStages) umma::bar_wait(&empty[stage], ((s / kStages) - 1) & 1);
         const int g0 = (s - main_slabs) * kKS, R = a.maxr;
-        if (P.down)
-          store_u_row(As, rl, E.u2, row, g0, 0);
+        if (P.mode == kDown)
+          store_q_row(As, rl, E.u2, row, g0, 0);
         else
-          store_u_row(As, rl, mat ? E.u3 : E.u1, row, g0, mat ? R : 0);
+          store_q_row(As, rl, mat ? E.u3 : E.u1, row, g0, mat ? R : 0);
         const int n = tid;  // one B row per producer thread
         const int p = s_pair[n];
         const bool comp = p >= 0 && a.plan.pair_comp[p] >= 0;
@@ -247,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
             const int col = g0 + 8 * j + q;
             float t = 0.0f;
             if (comp) {
-              if (P.down) {
+              if (P.mode == kDown) {
                 if (col < R) t = a.t[t_index(a, p, 2) + col];
               } else if (col < R) {
                 t = a.t[t_index(a, p, 0) + col];
@@ -298,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
       float h1[32], h3[32];
       umma::tmem_ld32(lbase + c0, h1);
       umma::tmem_ld32(lbase + kTN + c0, h3);
-      if (!P.down) {
+      if (P.mode == kUp) {
         if (ra < P.M) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -310,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
             }
           }
         }
-      } else {
+      } else if (P.mode == kDown) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int n = c0 + j;
@@ -322,6 +390,22 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
             if (rb < P.M) atomicAdd(yr + rb, w * h3[j]);
           }
         }
+      } else if (ra < a.maxr) {  // V.x rows -> t of the compensated pairs
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = c0 + j;
+          if (n < nvalid) {
+            const int p = s_pair[n];
+            if (a.plan.pair_comp[p] >= 0) {
+              if (P.mode == kVxUp) {
+                a.t[t_index(a, p, 0) + ra] = h1[j];
+                a.t[t_index(a, p, 1) + ra] = h3[j];
+              } else {
+                a.t[t_index(a, p, 2) + ra] = h1[j];
+              }
+            }
+          }
+        }
       }
     }
   }
@@ -330,42 +414,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
   if (warp == kMmaWarp) umma::tmem_dealloc<2 * kTN>(tmem);
 }
 
-// t[b][e][2][j] = V2(e)[j, :] . a16_p for the compensated pairs (bf16 activations)
-__global__ void __launch_bounds__(256) lr_mid16_kernel(ExpertArgs a) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int task = blockIdx.x * 8 + warp;
-  const int slot = task / a.maxr;
-  if (slot >= a.plan.counts[1]) return;
-  const int j = task - slot * a.maxr;
-  const int p = a.plan.comp_list[slot];
-  const lrc_expert& E = a.experts[a.plan.pair_expert[p]];
-  const lrc_qmat& V = E.v2;
-  float acc = 0.0f;
-  if (qmat_present(V) && j < V.rows) {
-    const uint16_t* ap = a.a16 + static_cast<int64_t>(p) * a.ffn;
-    const bool g64 = V.dense == nullptr && V.group_size == 64 && ((V.cols * V.bits) % 32) == 0;
-    float av[1];
-    if (g64 && V.bits == 3) {
-      vrow_dot_tokens<3, 1>(V, j, ap, a.ffn, 1, av);
-      acc = av[0];
-    } else if (g64 && V.bits == 2) {
-      vrow_dot_tokens<2, 1>(V, j, ap, a.ffn, 1, av);
-      acc = av[0];
-    } else if (g64 && V.bits == 4) {
-      vrow_dot_tokens<4, 1>(V, j, ap, a.ffn, 1, av);
-      acc = av[0];
-    } else {
-      for (int k = lane; k < V.cols; k += 32) acc = fmaf(qmat_elem(V, j, k), bf2f(ap[k]), acc);
-      acc = warp_sum(acc);
-    }
-  }
-  if (lane == 0) a.t[t_index(a, p, 2) + j] = acc;
-}
-
 }  // namespace
 
-bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn) {
-  if (hidden % kKS != 0 || ffn % kKS != 0) return false;
+bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn, int maxr) {
+  if (hidden % kKS != 0 || ffn % kKS != 0 || maxr > kTM) return false;
   for (int i = 0; i < n; ++i) {
     const lrc_qmat* ws[3] = {&experts[i].w1, &experts[i].w3, &experts[i].w2};
     for (auto w : ws)
@@ -385,26 +437,23 @@ lrc_status launch_prefill(const ExpertArgs& a, int np_bound, cudaStream_t st, in
   PrefillArgs P{};
   P.a = a;
   const int ytiles = (np_bound + kTN - 1) / kTN + a.ne;  // >= sum over experts of ceil(cnt / kTN)
-  P.down = 0;
-  P.M = a.ffn;
-  P.K = a.hidden;
-  P.lr_slabs = a.maxr ? (2 * a.maxr + kKS - 1) / kKS : 0;
-  prefill_kernel<<<dim3((a.ffn + kTM - 1) / kTM, ytiles), kThreads, kSmemBytes, st>>>(P);
-  LRC_CHECK_LAUNCH();
-  ++*launches;
-  if (a.maxr) {
-    lr_mid16_kernel<<<(np_bound * a.maxr + 7) / 8, 256, 0, st>>>(a);
+  auto launch = [&](int mode, int M, int K, int lr_slabs, int mtiles) -> lrc_status {
+    P.mode = mode;
+    P.M = M;
+    P.K = K;
+    P.lr_slabs = lr_slabs;
+    prefill_kernel<<<dim3(mtiles, ytiles), kThreads, kSmemBytes, st>>>(P);
     LRC_CHECK_LAUNCH();
     ++*launches;
-  }
-  P.down = 1;
-  P.M = a.hidden;
-  P.K = a.ffn;
-  P.lr_slabs = a.maxr ? (a.maxr + kKS - 1) / kKS : 0;
-  prefill_kernel<<<dim3((a.hidden + 2 * kTM - 1) / (2 * kTM), ytiles), kThreads, kSmemBytes, st>>>(P);
-  LRC_CHECK_LAUNCH();
-  ++*launches;
-  return LRC_OK;
+    return LRC_OK;
+  };
+  lrc_status s;
+  const int R = a.maxr;
+  if (R && (s = launch(kVxUp, R, a.hidden, 0, 1)) != LRC_OK) return s;
+  if ((s = launch(kUp, a.ffn, a.hidden, R ? (2 * R + kKS - 1) / kKS : 0, (a.ffn + kTM - 1) / kTM)) != LRC_OK)
+    return s;
+  if (R && (s = launch(kVxDown, R, a.ffn, 0, 1)) != LRC_OK) return s;
+  return launch(kDown, a.hidden, a.ffn, R ? (R + kKS - 1) / kKS : 0, (a.hidden + 2 * kTM - 1) / (2 * kTM));
 }
 
 }  // namespace lrc
