@@ -104,14 +104,18 @@ __device__ __forceinline__ void store_row(uint8_t* slab, int r, const RowSlab& v
   for (int j = 0; j < 4; ++j) sp[j] = f32x2(s * exp2f(-4.0f * j), s * exp2f(-4.0f * j - 2.0f));
   const uint64_t zz = f32x2(z, z), mm = f32x2(-8388608.0f, -8388608.0f);
   const uint32_t w[4] = {v.c.x, v.c.y, v.c.z, v.c.w};
+  uint32_t magic;  // in a register so (b & mask) | magic is ONE lop3 (one immediate per lop3)
+  asm("mov.b32 %0, 0x4B000000;" : "=r"(magic));
 #pragma unroll
   for (int ch = 0; ch < 8; ++ch) {
     const uint32_t b = (ch & 1) ? (w[ch >> 1] >> 16) : w[ch >> 1];
     uint32_t o[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float f0 = __uint_as_float(0x4B000000u | (b & (3u << (4 * j))));
-      const float f1 = __uint_as_float(0x4B000000u | (b & (12u << (4 * j))));
+      uint32_t u0, u1;
+      asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(u0) : "r"(b), "r"(3u << (4 * j)), "r"(magic));
+      asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(u1) : "r"(b), "r"(12u << (4 * j)), "r"(magic));
+      const float f0 = __uint_as_float(u0), f1 = __uint_as_float(u1);
       uint64_t t;
       asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f32x2(f0, f1)), "l"(mm));
       asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(t), "l"(sp[j]), "l"(zz));

@@ -65,12 +65,15 @@ __device__ __forceinline__ void bar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void bar_arrive_cpasync(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting thread is parked (not
+// spinning through issue slots the producers need) until the phase completes
+// or ~1 ms passes
 __device__ __forceinline__ bool bar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
-      "{.reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.b32 %0, 1, 0, P;}"
+      "{.reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3; selp.b32 %0, 1, 0, P;}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
       : "memory");
   return ok != 0;
 }
@@ -86,7 +89,7 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
   const uint64_t t0 = globaltimer();
   for (uint32_t spin = 1;; ++spin) {
     if (bar_try_wait(bar, parity)) return;
-    if ((spin & 0xFFFF) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+    if ((spin & 0xFF) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
   }
 }
 
