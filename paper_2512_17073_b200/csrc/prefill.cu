@@ -2,21 +2,26 @@
 // config C4).  Semantics: ref/moe.py:217-259 forward(mode="compensated") with
 // ref/lowrank.py:153-165 applying U.(V.x) for each token's top-n experts only.
 //
-// One CTA computes a [128-row x 256-pair] tile of TWO weight matrices that
-// share the B operand, over K in 64-column slabs (one 128-byte swizzle row):
-//   up   : W1 and W3 rows [m0, m0+128) x the expert's token rows of x
+// A CTA PAIR (cluster of 2, tcgen05 cta_group::2) computes a [256-row x
+// 256-pair] tile of TWO weight matrices that share the B operand, over K in
+// 64-column slabs (one 128-byte swizzle row); CTA r holds rows [128r, 128r+128)
+// of both A operands and pairs [128r, 128r+128) of B, and its TMEM receives its
+// 128 rows x all 256 pairs of both accumulators:
+//   up   : W1 and W3 rows [m0, m0+256) x the expert's token rows of x
 //          -> SwiGLU in the epilogue -> bf16 activations a16[pair][ffn];
-//   down : W2 rows [m0, m0+128) and [m0+128, m0+256) x the pairs' a16 rows
+//   down : W2 rows [m0, m0+256) and [m0+256, m0+512) x the pairs' a16 rows
 //          -> y[token] += w_pair * (.) with fp32 reductions.
-// Roles (288 threads, one CTA per SM: 193 KB smem, all 512 TMEM columns):
+// Roles per CTA (288 threads, one CTA per SM: 193 KB smem, 512 TMEM columns):
 //   warps 0-7  producers: thread t dequantizes row t&127 of matrix t>>7 (c*s+z
 //              in fp32, rounded once to bf16; codes and metadata prefetched two
-//              slabs ahead) straight into SWIZZLE_128B smem, and gathers its
-//              share of the B rows with cp.async one slab ahead (zero-filled
-//              past the expert's pairs); after the K loop, the epilogue.
-//   warp 8     one thread issues tcgen05.mma (M=128, N=256, K=16) into the two
-//              fp32 TMEM accumulators and commits each stage back to the
-//              producers (3-stage mbarrier ring).
+//              slabs ahead) straight into SWIZZLE_128B smem, gathers its share
+//              of the CTA's 128 B rows with cp.async two slabs ahead (zero-filled
+//              past the expert's pairs) and release-arrives on the LEADER's
+//              stage barrier; after the K loop, the epilogue from its own TMEM.
+//   warp 8     (leader CTA) one thread issues tcgen05.mma.cta_group::2
+//              (M=256, N=256, K=16) into the two fp32 accumulators and commits
+//              each stage back to both CTAs (multicast; 4-stage ring).
+// The pair halves each SM's share of the B operand (gather and smem reads).
 // The low-rank term is K augmentation: extra slabs whose A rows hold the U
 // factors (up: U1 in columns [0, R), U3 in [R, 2R); down: U2) and whose B rows
 // hold the pair's V.x vectors t (zero for uncompensated pairs), so U.(V.x)
@@ -30,18 +35,19 @@
 namespace lrc {
 namespace {
 
-constexpr int kTM = 128;  // rows per accumulator
+constexpr int kTM = 128;  // rows per accumulator per CTA (256 per pair)
 constexpr int kTN = 256;  // pairs per tile (MMA N)
+constexpr int kBN = 128;  // B rows per CTA
 constexpr int kKS = 64;   // K slab
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr int kSlabA = kTM * 128;
-constexpr int kSlabB = kTN * 128;
-constexpr int kStageBytes = 2 * kSlabA + kSlabB;  // 64 KB
+constexpr int kSlabB = kBN * 128;
+constexpr int kStageBytes = 2 * kSlabA + kSlabB;  // 48 KB
 constexpr int kProd = 256;
 constexpr int kThreads = kProd + 32;
 constexpr int kMmaWarp = kProd / 32;
 constexpr int kSmemBytes = kStages * kStageBytes + 1024;
-constexpr uint32_t kIdesc = umma::idesc_bf16(kTM, kTN);
+constexpr uint32_t kIdesc = umma::idesc_bf16(2 * kTM, kTN);
 
 enum Mode : int {
   kUp = 0,      // A = W1 | W3 rows, B = x rows       -> SwiGLU -> a16
@@ -81,14 +87,25 @@ struct RowSlab {
   uint32_t s, z;  // fp16 bits
 };
 
-__device__ __forceinline__ RowSlab load_row(const lrc_qmat& W, int row, int M, int K, int k0) {
+// The matrix pointers live in registers (QPtr), not behind the expert-table
+// reference, so a prefetch is one dependent-free load.
+struct QPtr {
+  const uint8_t* packed;
+  const uint16_t* scales;
+  const uint16_t* zeros;
+};
+
+__device__ __forceinline__ RowSlab load_row(const QPtr& W, int row, int M, int K, int k0) {
   RowSlab r{make_uint4(0, 0, 0, 0), 0u, 0u};
   if (row < M) {
     const int64_t e0 = static_cast<int64_t>(row) * K + k0;
-    r.c = __ldg(reinterpret_cast<const uint4*>(W.packed + (e0 >> 2)));
+    // volatile: issued where written (two slabs ahead), never sunk to the use
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.c.x), "=r"(r.c.y), "=r"(r.c.z), "=r"(r.c.w)
+                 : "l"(W.packed + (e0 >> 2)));
     const int64_t g = static_cast<int64_t>(row) * (K / kKS) + k0 / kKS;
-    r.s = __ldg(W.scales + g);
-    r.z = __ldg(W.zeros + g);
+    asm volatile("ld.global.nc.u16 %0, [%1];" : "=r"(r.s) : "l"(W.scales + g));
+    asm volatile("ld.global.nc.u16 %0, [%1];" : "=r"(r.z) : "l"(W.zeros + g));
   }
   return r;
 }
@@ -97,7 +114,7 @@ __device__ __forceinline__ RowSlab load_row(const lrc_qmat& W, int row, int M, i
 // is masked in place: (v & 3 << 2i) | 0x4B000000 is the float 2^23 + c*2^2i;
 // one FADD2 removes 2^23 and one FFMA2 with s*2^-2i (exact power-of-two
 // rescale) and z gives c*s + z with the same single rounding as fmaf(c, s, z).
-__device__ __forceinline__ void store_row(uint8_t* slab, int r, const RowSlab& v) {
+__device__ __forceinline__ void store_row(uint32_t slab, int r, const RowSlab& v) {
   const float s = h2f(static_cast<uint16_t>(v.s)), z = h2f(static_cast<uint16_t>(v.z));
   uint64_t sp[4];
 #pragma unroll
@@ -121,7 +138,7 @@ __device__ __forceinline__ void store_row(uint8_t* slab, int r, const RowSlab& v
       asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(t), "l"(sp[j]), "l"(zz));
       o[j] = bf16x2_of(t);
     }
-    *reinterpret_cast<uint4*>(slab + umma::sw128_chunk(r, ch)) = make_uint4(o[0], o[1], o[2], o[3]);
+    umma::sts128(slab + umma::sw128_chunk(r, ch), o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -130,7 +147,7 @@ __device__ __forceinline__ int64_t t_index(const ExpertArgs& a, int p, int proj)
 }
 
 template <int BITS>
-__device__ __forceinline__ void store_q_row_g64(uint8_t* slab, int r, const lrc_qmat& U, int row, int gcol0) {
+__device__ __forceinline__ void store_q_row_g64(uint32_t slab, int r, const lrc_qmat& U, int row, int gcol0) {
   const uint32_t* words = reinterpret_cast<const uint32_t*>(U.packed);
   const int64_t bit0 = (static_cast<int64_t>(row) * U.cols + gcol0) * BITS;  // multiple of 64*BITS: word aligned
   const int64_t g = static_cast<int64_t>(row) * (U.cols / kKS) + gcol0 / kKS;
@@ -148,8 +165,8 @@ __device__ __forceinline__ void store_q_row_g64(uint8_t* slab, int r, const lrc_
       v[q] = fmaf(static_cast<float>(__funnelshift_r(w[b >> 5], w[(b >> 5) + 1], b & 31) & ((1u << BITS) - 1u)),
                   s, z);
     }
-    *reinterpret_cast<uint4*>(slab + umma::sw128_chunk(r, j)) =
-        make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+    umma::sts128(slab + umma::sw128_chunk(r, j), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                 pack_bf16(v[6], v[7]));
   }
 }
 
@@ -157,7 +174,7 @@ __device__ __forceinline__ void store_q_row_g64(uint8_t* slab, int r, const lrc_
 // shifted right by c0 (element col - c0; zero outside [0, cols) and for absent
 // rows) -> one SWIZZLE_128B row.  For the low-rank factors: U rows of the
 // K-augmentation slabs, V rows of the V.x GEMMs.
-__device__ void store_q_row(uint8_t* slab, int r, const lrc_qmat& U, int row, int gcol0, int c0) {
+__device__ void store_q_row(uint32_t slab, int r, const lrc_qmat& U, int row, int gcol0, int c0) {
   const bool pres = qmat_present(U) && row >= 0 && row < U.rows;
   if (pres && c0 == 0 && U.dense == nullptr && U.group_size == kKS && (U.cols % kKS) == 0 &&
       gcol0 + kKS <= U.cols) {
@@ -173,8 +190,8 @@ __device__ void store_q_row(uint8_t* slab, int r, const lrc_qmat& U, int row, in
       const int col = gcol0 + 8 * j + q - c0;
       v[q] = (pres && col >= 0 && col < U.cols) ? qmat_elem(U, row, col) : 0.0f;
     }
-    *reinterpret_cast<uint4*>(slab + umma::sw128_chunk(r, j)) =
-        make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+    umma::sts128(slab + umma::sw128_chunk(r, j), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                 pack_bf16(v[6], v[7]));
   }
 }
 
@@ -186,11 +203,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
   __shared__ int s_pair[kTN];
   const ExpertArgs& a = P.a;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = static_cast<int>(umma::cluster_rank());
   const bool b_act = P.mode == kDown || P.mode == kVxDown;  // B rows from a16 (else x)
   const bool vx = P.mode >= kVxUp;
 
-  // blockIdx.y -> (active expert, block of kTN of its pairs); the grid is an
-  // upper bound, surplus CTAs leave at once (uniformly)
+  // blockIdx.y -> (active expert, block of kTN of its pairs), identical in both
+  // CTAs of the pair; the grid is an upper bound, surplus pairs leave at once
   int yb = blockIdx.y, ai = -1;
   const int na = a.plan.counts[0];
   for (int i = 0; i < na; ++i) {
@@ -206,7 +224,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
   const lrc_expert& E = a.experts[e];
   const int off = a.plan.active_off[ai] + yb * kTN;
   const int nvalid = min(kTN, a.plan.active_cnt[ai] - yb * kTN);
-  const int m0 = blockIdx.x * (P.mode == kDown ? 2 * kTM : kTM);
+  // rows of this CTA's A1 / A3 operands (row of TMEM lane l = base + l)
+  const int tile = blockIdx.x >> 1;
+  const int a1base = tile * (P.mode == kDown ? 4 * kTM : 2 * kTM) + rank * kTM;
+  const int a3base = a1base + (P.mode == kDown ? 2 * kTM : 0);
 
   int any_comp = 0;
   for (int n = tid; n < kTN; n += kThreads) {
@@ -219,21 +240,24 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
   }
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
-      umma::bar_init(&full[i], kProd);
+      // leader: its producers + the peer's forwarder; peer: its producers
+      umma::bar_init(&full[i], rank == 0 ? kProd + 1 : kProd);
       umma::bar_init(&empty[i], 1);
     }
     umma::bar_init(&done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kMmaWarp) umma::tmem_alloc<2 * kTN>(&tmem_base);
+  if (warp == kMmaWarp) umma::tmem_alloc2<2 * kTN>(&tmem_base);
   umma::fence_before_sync();
-  any_comp = __syncthreads_or(any_comp);
+  any_comp = __syncthreads_or(any_comp);  // over all 256 pairs: the same in both CTAs
+  umma::cluster_sync();                   // barriers initialised, TMEM allocated in both CTAs
   umma::fence_after_sync();
+  const uint32_t tmem = tmem_base;
   if (vx && !any_comp) {  // no compensated pair in this tile: nothing to compute
-    if (warp == kMmaWarp) umma::tmem_dealloc<2 * kTN>(tmem_base);
+    umma::fence_before_sync();
+    if (warp == kMmaWarp) umma::tmem_dealloc2<2 * kTN>(tmem);
     return;
   }
-  const uint32_t tmem = tmem_base;
   const int main_slabs = P.K / kKS;
   const int nslab = main_slabs + ((any_comp && !vx) ? P.lr_slabs : 0);
 
@@ -241,22 +265,25 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
     // ------------------------------------------------------------ producers
     const int mat = tid >> 7, rl = tid & (kTM - 1);  // A row rl of A1 (mat 0) / A3 (mat 1)
     const lrc_qmat* Wp;
-    int row = m0 + rl;
+    const int row = (mat ? a3base : a1base) + rl;
     switch (P.mode) {
       case kUp: Wp = mat ? &E.w3 : &E.w1; break;
-      case kDown: Wp = &E.w2; row += mat * kTM; break;
+      case kDown: Wp = &E.w2; break;
       case kVxUp: Wp = mat ? &E.v3 : &E.v1; break;
-      default: Wp = &E.v2; if (mat) row = -1; break;  // A3 unused (zero)
+      default: Wp = mat ? nullptr : &E.v2; break;  // A3 unused (zero)
     }
-    const lrc_qmat& W = *Wp;
-    // B gather: 8 lanes per 128-byte row, rows bn0 + 32 i; per-thread sources fixed for the tile
+    const lrc_qmat& W = Wp ? *Wp : E.v2;
+    const QPtr Wq{W.packed, W.scales, W.zeros};
+    const int qrow = (Wp && row < P.M) ? row : -1;  // quantized-factor row (vx) or -1 = zero
+    // B gather: this CTA's pairs [128 rank, +128): 8 lanes per 128-byte row,
+    // rows bn0 + 32 i; per-thread sources fixed for the tile
     const int bc = tid & 7, bn0 = tid >> 3;
-    constexpr int kBRows = kTN / (kProd / 8);
+    constexpr int kBRows = kBN / (kProd / 8);
     const uint16_t* bsrc[kBRows];
     uint32_t bmask = 0;
 #pragma unroll
     for (int i = 0; i < kBRows; ++i) {
-      const int p = s_pair[bn0 + (kProd / 8) * i];
+      const int p = s_pair[rank * kBN + bn0 + (kProd / 8) * i];
       bsrc[i] = a.x + bc * 8;
       if (p >= 0) {
         bsrc[i] = (b_act ? a.a16 + static_cast<int64_t>(p) * a.ffn
@@ -274,30 +301,21 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
                          (bmask >> i) & 1 ? 16u : 0u);
       umma::cp_async_commit();
     };
-    issue_b(0);
-    RowSlab c0{}, c1{};
-    if (!vx) {
-      c0 = load_row(W, row, P.M, P.K, 0);
-      if (main_slabs > 1) c1 = load_row(W, row, P.M, P.K, kKS);
-    }
-    for (int s = 0; s < nslab; ++s) {
+    // One slab: dequantize A (codes prefetched two slabs earlier), wait for
+    // this slab's B rows, publish the stage to the leader; then start the B
+    // gather two slabs ahead and the codes two slabs ahead.  Unrolled by three
+    // below so the prefetch registers rotate by name (no copies waiting on loads).
+    auto step = [&](int s, const RowSlab& cur, RowSlab& dst) {
       const int stage = s % kStages;
-      uint8_t* As = sm + stage * kStageBytes + mat * kSlabA;
-      uint8_t* Bs = sm + stage * kStageBytes + 2 * kSlabA;
-      const int sn = s + 1;
-      if (sn < main_slabs) {  // next slab's B rows (cp.async), one slab ahead
-        if (sn >= kStages) umma::bar_wait(&empty[sn % kStages], ((sn / kStages) - 1) & 1);
-        issue_b(sn);
-      }
-      RowSlab c2{};
-      if (!vx && s + 2 < main_slabs) c2 = load_row(W, row, P.M, P.K, (s + 2) * kKS);  // codes two ahead
+      const uint32_t As = umma::smem_u32(sm) + stage * kStageBytes + mat * kSlabA;
+      const uint32_t Bs = umma::smem_u32(sm) + stage * kStageBytes + 2 * kSlabA;
       if (s < main_slabs) {
         if (vx)
-          store_q_row(As, rl, W, row < P.M ? row : -1, s * kKS, 0);
+          store_q_row(As, rl, W, qrow, s * kKS, 0);
         else
-          store_row(As, rl, c0);
-        if (sn < main_slabs)
-          umma::cp_async_wait<1>();
+          store_row(As, rl, cur);
+        if (s + 1 < main_slabs)
+          umma::cp_async_wait<1>();  // B(s) landed; B(s+1) may be in flight
         else
           umma::cp_async_wait<0>();
       } else {
@@ -308,63 +326,90 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
           store_q_row(As, rl, E.u2, row, g0, 0);
         else
           store_q_row(As, rl, mat ? E.u3 : E.u1, row, g0, mat ? R : 0);
-        const int n = tid;  // one B row per producer thread
-        const int p = s_pair[n];
-        const bool comp = p >= 0 && a.plan.pair_comp[p] >= 0;
+        if (tid < kBN) {  // one B row per thread
+          const int n = tid;
+          const int p = s_pair[rank * kBN + n];
+          const bool comp = p >= 0 && a.plan.pair_comp[p] >= 0;
 #pragma unroll 1
-        for (int j = 0; j < 8; ++j) {
-          float v[8];
+          for (int j = 0; j < 8; ++j) {
+            float v[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int col = g0 + 8 * j + q;
-            float t = 0.0f;
-            if (comp) {
-              if (P.mode == kDown) {
-                if (col < R) t = a.t[t_index(a, p, 2) + col];
-              } else if (col < R) {
-                t = a.t[t_index(a, p, 0) + col];
-              } else if (col < 2 * R) {
-                t = a.t[t_index(a, p, 1) + col - R];
+            for (int q = 0; q < 8; ++q) {
+              const int col = g0 + 8 * j + q;
+              float t = 0.0f;
+              if (comp) {
+                if (P.mode == kDown) {
+                  if (col < R) t = a.t[t_index(a, p, 2) + col];
+                } else if (col < R) {
+                  t = a.t[t_index(a, p, 0) + col];
+                } else if (col < 2 * R) {
+                  t = a.t[t_index(a, p, 1) + col - R];
+                }
               }
+              v[q] = t;
             }
-            v[q] = t;
+            umma::sts128(Bs + umma::sw128_chunk(n, j), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                         pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
           }
-          *reinterpret_cast<uint4*>(Bs + umma::sw128_chunk(n, j)) = make_uint4(
-              pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
         }
       }
       umma::fence_proxy_async();  // generic smem writes (and landed cp.async) -> tensor core
-      umma::bar_arrive(&full[stage]);
-      c0 = c1;
-      c1 = c2;
+      umma::bar_arrive(&full[stage]);  // CTA scope: never waits on the prefetches in flight
+      const int sb = s + 2;
+      if (sb < main_slabs) {
+        if (sb >= kStages) umma::bar_wait_cluster(&empty[sb % kStages], ((sb / kStages) - 1) & 1);
+        issue_b(sb);
+      }
+      if (!vx && s + 2 < main_slabs) dst = load_row(Wq, row, P.M, P.K, (s + 2) * kKS);
+    };
+    issue_b(0);
+    if (main_slabs > 1) issue_b(1);
+    RowSlab r0{}, r1{}, r2{};
+    if (!vx) {
+      r0 = load_row(Wq, row, P.M, P.K, 0);
+      if (main_slabs > 1) r1 = load_row(Wq, row, P.M, P.K, kKS);
     }
-  } else if (lane == 0) {
-    // ------------------------------------------------------------ MMA issue
+    for (int s = 0; s < nslab; s += 3) {
+      step(s, r0, r2);
+      if (s + 1 < nslab) step(s + 1, r1, r0);
+      if (s + 2 < nslab) step(s + 2, r2, r1);
+    }
+  } else if (rank == 0 && lane == 0) {
+    // ------------------------------------------------------------ MMA issue (leader)
     for (int s = 0; s < nslab; ++s) {
       const int stage = s % kStages;
-      umma::bar_wait(&full[stage], (s / kStages) & 1);
+      umma::bar_wait_cluster(&full[stage], (s / kStages) & 1);
       umma::fence_after_sync();
       const uint32_t a1 = umma::smem_u32(sm + stage * kStageBytes), a3 = a1 + kSlabA, b = a3 + kSlabA;
 #pragma unroll
       for (int kk = 0; kk < kKS / 16; ++kk) {
         const uint32_t acc = (s | kk) != 0 ? 1u : 0u;
         const uint64_t db = umma::sdesc(b + 32 * kk);
-        umma::mma_bf16(tmem, umma::sdesc(a1 + 32 * kk), db, kIdesc, acc);
-        umma::mma_bf16(tmem + kTN, umma::sdesc(a3 + 32 * kk), db, kIdesc, acc);
+        umma::mma2_bf16(tmem, umma::sdesc(a1 + 32 * kk), db, kIdesc, acc);
+        umma::mma2_bf16(tmem + kTN, umma::sdesc(a3 + 32 * kk), db, kIdesc, acc);
       }
-      umma::commit(&empty[stage]);
+      umma::commit2(&empty[stage]);
     }
-    umma::commit(&done);
+    umma::commit2(&done);
+  } else if (rank == 1 && lane == 0) {
+    // ------------------------------------------------------------ forwarder (peer)
+    // one cluster-scope release per stage: the peer's stage is complete ->
+    // arrive on the leader's barrier (cumulative over the acquired arrivals)
+    for (int s = 0; s < nslab; ++s) {
+      const int stage = s % kStages;
+      umma::bar_wait(&full[stage], (s / kStages) & 1);
+      umma::bar_arrive_cta(&full[stage], 0);
+    }
   }
 
   if (warp < kMmaWarp) {
     // ------------------------------------------------------------ epilogue
     // warp w reads TMEM lanes 32(w&3).. (rows) for pair columns [128(w>>2), +128)
-    umma::bar_wait(&done, 0);
+    umma::bar_wait_cluster(&done, 0);
     umma::fence_after_sync();
     const int q = warp & 3, half = warp >> 2;
     const uint32_t lbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const int ra = m0 + q * 32 + lane, rb = m0 + kTM + q * 32 + lane;
+    const int ra = a1base + q * 32 + lane, rb = a3base + q * 32 + lane;
     const int cend = min(nvalid, (half + 1) * (kTN / 2));
     for (int c0 = half * (kTN / 2); c0 < cend; c0 += 32) {
       float h1[32], h3[32];
@@ -415,13 +460,14 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
   }
   umma::fence_before_sync();
   __syncthreads();
-  if (warp == kMmaWarp) umma::tmem_dealloc<2 * kTN>(tmem);
+  umma::cluster_sync();
+  if (warp == kMmaWarp) umma::tmem_dealloc2<2 * kTN>(tmem);
 }
 
 }  // namespace
 
 bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn, int maxr) {
-  if (hidden % kKS != 0 || ffn % kKS != 0 || maxr > kTM) return false;
+  if (hidden % kKS != 0 || ffn % kKS != 0 || maxr > 2 * kTM) return false;
   for (int i = 0; i < n; ++i) {
     const lrc_qmat* ws[3] = {&experts[i].w1, &experts[i].w3, &experts[i].w2};
     for (auto w : ws)
@@ -441,23 +487,33 @@ lrc_status launch_prefill(const ExpertArgs& a, int np_bound, cudaStream_t st, in
   PrefillArgs P{};
   P.a = a;
   const int ytiles = (np_bound + kTN - 1) / kTN + a.ne;  // >= sum over experts of ceil(cnt / kTN)
-  auto launch = [&](int mode, int M, int K, int lr_slabs, int mtiles) -> lrc_status {
+  auto launch = [&](int mode, int M, int K, int lr_slabs, int rows_per_pair) -> lrc_status {
     P.mode = mode;
     P.M = M;
     P.K = K;
     P.lr_slabs = lr_slabs;
-    prefill_kernel<<<dim3(mtiles, ytiles), kThreads, kSmemBytes, st>>>(P);
-    LRC_CHECK_LAUNCH();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * ((M + rows_per_pair - 1) / rows_per_pair), ytiles);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    LRC_CUDA_TRY(cudaLaunchKernelEx(&cfg, prefill_kernel, P));
     ++*launches;
     return LRC_OK;
   };
   lrc_status s;
   const int R = a.maxr;
-  if (R && (s = launch(kVxUp, R, a.hidden, 0, 1)) != LRC_OK) return s;
-  if ((s = launch(kUp, a.ffn, a.hidden, R ? (2 * R + kKS - 1) / kKS : 0, (a.ffn + kTM - 1) / kTM)) != LRC_OK)
-    return s;
-  if (R && (s = launch(kVxDown, R, a.ffn, 0, 1)) != LRC_OK) return s;
-  return launch(kDown, a.hidden, a.ffn, R ? (R + kKS - 1) / kKS : 0, (a.hidden + 2 * kTM - 1) / (2 * kTM));
+  if (R && (s = launch(kVxUp, R, a.hidden, 0, 2 * kTM)) != LRC_OK) return s;
+  if ((s = launch(kUp, a.ffn, a.hidden, R ? (2 * R + kKS - 1) / kKS : 0, 2 * kTM)) != LRC_OK) return s;
+  if (R && (s = launch(kVxDown, R, a.ffn, 0, 2 * kTM)) != LRC_OK) return s;
+  return launch(kDown, a.hidden, a.ffn, R ? (R + kKS - 1) / kKS : 0, 4 * kTM);
 }
 
 }  // namespace lrc

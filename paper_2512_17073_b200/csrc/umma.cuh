@@ -22,6 +22,11 @@ __device__ __forceinline__ uint32_t sw128_chunk(int r, int c) {
   return static_cast<uint32_t>(r) * 128u + ((static_cast<uint32_t>(c) ^ static_cast<uint32_t>(r & 7)) << 4);
 }
 
+__device__ __forceinline__ void sts128(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
 // Shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B
 // apart.  A K=16 step inside the 128-byte row advances the start by 32 B.
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
@@ -91,6 +96,65 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
     if (bar_try_wait(bar, parity)) return;
     if ((spin & 0xFF) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
   }
+}
+
+// ---- CTA pair (cluster of 2, cta_group::2) ---------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive (release at cluster scope) on the barrier at the same smem offset in CTA `rank`
+__device__ __forceinline__ void bar_arrive_cta(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ bool bar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{.reg .pred P; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2, %3; selp.b32 %0, 1, 0, "
+      "P;}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  if (bar_try_wait_cluster(bar, parity)) return;
+  const uint64_t t0 = globaltimer();
+  for (uint32_t spin = 1;; ++spin) {
+    if (bar_try_wait_cluster(bar, parity)) return;
+    if ((spin & 0xFF) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+  }
+}
+__device__ __forceinline__ void mma2_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+// arrive on `bar` in both CTAs of the pair once the leader's prior MMAs complete
+__device__ __forceinline__ void commit2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem) {  // whole warp, both CTAs
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(NCOLS));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_dealloc2(uint32_t tmem) {  // whole warp, both CTAs
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(NCOLS));
 }
 
 __device__ __forceinline__ void fence_proxy_async() {
