@@ -13,7 +13,7 @@
 //          -> y[token] += w_pair * (.) with fp32 reductions.
 // Roles per CTA (288 threads, one CTA per SM: 193 KB smem, 512 TMEM columns):
 //   warps 0-7  producers: thread t dequantizes row t&127 of matrix t>>7 (c*s+z
-//              in fp32, rounded once to bf16; codes and metadata prefetched two
+//              in fp32, rounded once to bf16; codes and metadata prefetched four
 //              slabs ahead) straight into SWIZZLE_128B smem, gathers its share
 //              of the CTA's 128 B rows with cp.async two slabs ahead (zero-filled
 //              past the expert's pairs) and release-arrives on the LEADER's
@@ -47,6 +47,7 @@ constexpr int kProd = 256;
 constexpr int kThreads = kProd + 32;
 constexpr int kMmaWarp = kProd / 32;
 constexpr int kSmemBytes = kStages * kStageBytes + 1024;
+constexpr int kPD = 4;  // code prefetch distance (slabs)
 constexpr uint32_t kIdesc = umma::idesc_bf16(2 * kTM, kTN);
 
 enum Mode : int {
@@ -174,7 +175,7 @@ __device__ __forceinline__ void store_q_row_g64(uint32_t slab, int r, const lrc_
 // shifted right by c0 (element col - c0; zero outside [0, cols) and for absent
 // rows) -> one SWIZZLE_128B row.  For the low-rank factors: U rows of the
 // K-augmentation slabs, V rows of the V.x GEMMs.
-__device__ void store_q_row(uint32_t slab, int r, const lrc_qmat& U, int row, int gcol0, int c0) {
+__device__ __noinline__ void store_q_row(uint32_t slab, int r, const lrc_qmat& U, int row, int gcol0, int c0) {
   const bool pres = qmat_present(U) && row >= 0 && row < U.rows;
   if (pres && c0 == 0 && U.dense == nullptr && U.group_size == kKS && (U.cols % kKS) == 0 &&
       gcol0 + kKS <= U.cols) {
@@ -301,10 +302,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
                          (bmask >> i) & 1 ? 16u : 0u);
       umma::cp_async_commit();
     };
-    // One slab: dequantize A (codes prefetched two slabs earlier), wait for
-    // this slab's B rows, publish the stage to the leader; then start the B
-    // gather two slabs ahead and the codes two slabs ahead.  Unrolled by three
-    // below so the prefetch registers rotate by name (no copies waiting on loads).
+    // One slab: dequantize A (codes prefetched kPD slabs earlier: scattered
+    // 16-byte row reads need a long lead under load), wait for this slab's B
+    // rows, publish the stage; then start the B gather two slabs ahead and the
+    // codes kPD slabs ahead.  Unrolled by kPD + 1 below so the prefetch
+    // registers rotate by name (no copies waiting on loads).
     auto step = [&](int s, const RowSlab& cur, RowSlab& dst) {
       const int stage = s % kStages;
       const uint32_t As = umma::smem_u32(sm) + stage * kStageBytes + mat * kSlabA;
@@ -360,19 +362,22 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
         if (sb >= kStages) umma::bar_wait_cluster(&empty[sb % kStages], ((sb / kStages) - 1) & 1);
         issue_b(sb);
       }
-      if (!vx && s + 2 < main_slabs) dst = load_row(Wq, row, P.M, P.K, (s + 2) * kKS);
+      if (!vx && s + kPD < main_slabs) dst = load_row(Wq, row, P.M, P.K, (s + kPD) * kKS);
     };
     issue_b(0);
     if (main_slabs > 1) issue_b(1);
-    RowSlab r0{}, r1{}, r2{};
+    RowSlab rs[kPD + 1];
+#pragma unroll
+    for (int i = 0; i <= kPD; ++i) rs[i] = RowSlab{};
     if (!vx) {
-      r0 = load_row(Wq, row, P.M, P.K, 0);
-      if (main_slabs > 1) r1 = load_row(Wq, row, P.M, P.K, kKS);
+#pragma unroll
+      for (int i = 0; i < kPD; ++i)
+        if (i < main_slabs) rs[i] = load_row(Wq, row, P.M, P.K, i * kKS);
     }
-    for (int s = 0; s < nslab; s += 3) {
-      step(s, r0, r2);
-      if (s + 1 < nslab) step(s + 1, r1, r0);
-      if (s + 2 < nslab) step(s + 2, r2, r1);
+    for (int s = 0; s < nslab; s += kPD + 1) {
+#pragma unroll
+      for (int i = 0; i <= kPD; ++i)
+        if (s + i < nslab) step(s + i, rs[i], rs[(i + kPD) % (kPD + 1)]);
     }
   } else if (rank == 0 && lane == 0) {
     // ------------------------------------------------------------ MMA issue (leader)

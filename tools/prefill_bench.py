@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--rank", type=int, default=32)
     ap.add_argument("--decode-too", action="store_true")
     ap.add_argument("--phases", action="store_true")
+    ap.add_argument("--n", type=int, nargs="*", default=[0, 1, 2], help="top_n values to run")
     args = ap.parse_args()
     d, ffn, E, k, r = 4096, 14336, 8, 2, args.rank
     peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
@@ -36,7 +37,7 @@ def main():
     paths = [("tcgen05", 1)] + ([("mma.sync", 0)] if args.decode_too else [])
     for name, pmin in paths:
         sl.layer.set_prefill_min(pmin)
-        for n in (0, 1, 2):
+        for n in args.n:
             for _ in range(2):
                 sl.layer.forward(x, top_k=k, top_n=n, y=y)
             torch.cuda.synchronize()
