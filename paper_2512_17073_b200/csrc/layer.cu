@@ -231,6 +231,9 @@ struct lrc_layer {
   int num_sms = 148;
   bool tiled = false;
   bool prefill_ok = false;  // tcgen05 prefill GEMM eligible (2-bit gs64 reference-layout weights)
+  uint16_t* lrp = nullptr;     // per-expert bf16 LR packs for the prefill path (built lazily)
+  std::vector<uint8_t> lrp_dirty;
+  uint16_t* tb = nullptr;      // prefill V.x rows [max_pairs][tb_width] bf16
   int64_t prefill_min = [] {
     const char* v = getenv("LRC_PREFILL_MIN");
     return v ? static_cast<int64_t>(atoll(v)) : static_cast<int64_t>(256);
@@ -344,6 +347,7 @@ static lrc_status alloc_workspace(lrc_layer* L) {
   size_t o_ys = take(size_t(L->max_tokens) * L->hidden * 4);
   size_t o_lg = take(size_t(L->max_tokens) * L->E * 8);
   size_t o_tt = take(size_t(route_tiles(L->max_tokens)) * 4 + 16);
+  size_t o_tb = take(size_t(NP) * prefill_tb_width(L->maxr) * 2 + 16);
   LRC_CUDA_TRY(cudaMalloc(&L->ws, off));
   LRC_CUDA_TRY(cudaMemset(L->ws, 0, off));
   L->ws_bytes = off;
@@ -374,6 +378,12 @@ static lrc_status alloc_workspace(lrc_layer* L) {
   L->y_stage = reinterpret_cast<float*>(base + o_ys);
   L->logits = reinterpret_cast<double*>(base + o_lg);
   L->tile_ticket = reinterpret_cast<int*>(base + o_tt);
+  L->tb = reinterpret_cast<uint16_t*>(base + o_tb);
+  if (L->maxr) {  // LR packs: built before the first prefill call (and after expert updates)
+    const size_t per = static_cast<size_t>(prefill_lr_pack_elems(L->hidden, L->ffn, L->maxr));
+    LRC_CUDA_TRY(cudaMalloc(&L->lrp, per * NE * 2));
+    L->lrp_dirty.assign(NE, 1);
+  }
   for (auto& e : L->ev) LRC_CUDA_TRY(cudaEventCreate(&e));
   std::vector<uint8_t> hc(NE);
   for (int e = 0; e < NE; ++e) hc[e] = has_comp(L->host_experts[e]) ? 1 : 0;
@@ -432,6 +442,7 @@ extern "C" void lrc_layer_destroy(lrc_layer* L) {
   cudaFree(L->d_experts);
   if (L->h_stage) cudaFreeHost(L->h_stage);
   cudaFree(L->ws);
+  cudaFree(L->lrp);
   for (auto& e : L->ev)
     if (e) cudaEventDestroy(e);
   delete L;
@@ -446,6 +457,7 @@ extern "C" lrc_status lrc_layer_set_expert(lrc_layer* L, int expert_id, const lr
     return fail(LRC_ERR_UNSUPPORTED, "set_expert: rank above the layer's workspace rank");
   L->host_experts[expert_id] = *e;
   LRC_CUDA_TRY(cudaMemcpy(L->d_experts + expert_id, e, sizeof(lrc_expert), cudaMemcpyHostToDevice));
+  if (!L->lrp_dirty.empty()) L->lrp_dirty[expert_id] = 1;
   refresh_tiled(L);
   return LRC_OK;
 }
@@ -471,6 +483,7 @@ extern "C" lrc_status lrc_layer_set_expert_async(lrc_layer* L, int expert_id, co
   L->host_experts[expert_id] = *e;
   LRC_CUDA_TRY(cudaMemcpyAsync(L->d_experts + expert_id, slot, sizeof(lrc_expert), cudaMemcpyHostToDevice,
                                as_stream(stream)));
+  if (!L->lrp_dirty.empty()) L->lrp_dirty[expert_id] = 1;
   refresh_tiled(L);
   return LRC_OK;
 }
@@ -568,7 +581,17 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[2], st));
   if (prefill) {
     // large batches: tcgen05 grouped dequant-GEMMs (V1|V3.x, up, V2.a, down)
-    if ((s = launch_prefill(a, np_bound, st, &launches)) != LRC_OK) return s;
+    if (L->maxr) {  // (re)build the bf16 LR packs of experts changed since the last prefill call
+      const size_t per = static_cast<size_t>(prefill_lr_pack_elems(L->hidden, L->ffn, L->maxr));
+      for (size_t i = 0; i < L->lrp_dirty.size(); ++i)
+        if (L->lrp_dirty[i]) {
+          if ((s = build_prefill_lr(L->host_experts[i], L->hidden, L->ffn, L->maxr, L->lrp + per * i, st)) !=
+              LRC_OK)
+            return s;
+          L->lrp_dirty[i] = 0;
+        }
+    }
+    if ((s = launch_prefill(a, np_bound, L->lrp, L->tb, st, &launches)) != LRC_OK) return s;
     if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));  // phases: up+mid+down lumped into [2]
   } else if (allow_tiled && L->tiled) {
     const int tok_bound = static_cast<int>(std::min<int64_t>(B, L->max_tokens));

@@ -205,6 +205,10 @@ lrc_status launch_down_tiled(const ExpertArgs& a, int num_sms, int max_tokens_pe
 
 // tcgen05 prefill GEMM (prefill.cu)
 bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn, int maxr);
-lrc_status launch_prefill(const ExpertArgs& a, int np_bound, cudaStream_t st, int* launches);
+int64_t prefill_lr_pack_elems(int hidden, int ffn, int maxr);  // bf16 elements per expert
+int prefill_tb_width(int maxr);
+lrc_status build_prefill_lr(const lrc_expert& e, int hidden, int ffn, int maxr, uint16_t* out, cudaStream_t st);
+lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp, uint16_t* tb, cudaStream_t st,
+                          int* launches);
 
 }  // namespace lrc

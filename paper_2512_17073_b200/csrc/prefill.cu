@@ -23,9 +23,14 @@
 //              each stage back to both CTAs (multicast; 4-stage ring).
 // The pair halves each SM's share of the B operand (gather and smem reads).
 // The low-rank term is K augmentation: extra slabs whose A rows hold the U
-// factors (up: U1 in columns [0, R), U3 in [R, 2R); down: U2) and whose B rows
-// hold the pair's V.x vectors t (zero for uncompensated pairs), so U.(V.x)
-// lands in the same accumulator and Q(W)+UV^T is never formed.
+// factors (up: [U1 | 0] for W1 rows, [0 | U3] for W3 rows; down: U2) and whose
+// B rows hold the pair's V.x vector (bf16 [t1 | t3] or t2, zero for
+// uncompensated pairs), so U.(V.x) lands in the same accumulator and
+// Q(W)+UV^T is never formed.  The V.x vectors come from the same engine run on
+// the V factors (modes kVxUp / kVxDown, one accumulator) for the tiles that
+// hold a compensated pair.  Factors are repacked once per expert into bf16
+// rows (the "LR pack", build_prefill_lr) so every low-rank slab is a plain
+// cp.async row copy issued two slabs ahead like B.
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -57,11 +62,39 @@ enum Mode : int {
   kVxDown = 3,  // A = V2 rows,      B = a16 rows     -> t[.][2]
 };
 
+// Per-expert LR pack (bf16, row-major), offsets in elements from the expert's
+// base = lrp + e * lrp_stride; R = layer max rank, WU = 64 ceil(2R/64),
+// WD = 64 ceil(R/64):
+//   u1x [ffn x WU]    [U1 | 0]        u3x [ffn x WU]   [0 | U3]
+//   u2x [hidden x WD] [U2 | 0]        vup [2R x hidden] [V1 ; V3]
+//   v2  [R x ffn]
+struct LrPack {
+  int64_t u1x, u3x, u2x, vup, v2, stride;
+  int WU, WD;
+};
+__host__ __device__ inline LrPack lr_pack_layout(int hidden, int ffn, int R) {
+  LrPack L{};
+  L.WU = 64 * ((2 * R + 63) / 64);
+  L.WD = 64 * ((R + 63) / 64);
+  int64_t o = 0;
+  L.u1x = o; o += static_cast<int64_t>(ffn) * L.WU;
+  L.u3x = o; o += static_cast<int64_t>(ffn) * L.WU;
+  L.u2x = o; o += static_cast<int64_t>(hidden) * L.WD;
+  L.vup = o; o += static_cast<int64_t>(2 * R) * hidden;
+  L.v2 = o;  o += static_cast<int64_t>(R) * ffn;
+  L.stride = (o + 63) & ~int64_t(63);
+  return L;
+}
+
 struct PrefillArgs {
   ExpertArgs a;
   int mode;
   int M, K;      // weight rows, main reduction length
   int lr_slabs;  // K-augmentation slabs (0: layer without compensators)
+  const uint16_t* lrp;  // LR packs [ne][stride]
+  LrPack L;
+  uint16_t* tb;  // [max_pairs][WT] bf16 V.x rows ([t1 | t3] after kVxUp, t2 after kVxDown)
+  int WT;
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -143,56 +176,32 @@ __device__ __forceinline__ void store_row(uint32_t slab, int r, const RowSlab& v
   }
 }
 
-__device__ __forceinline__ int64_t t_index(const ExpertArgs& a, int p, int proj) {
-  return ((static_cast<int64_t>(a.plan.pair_token[p]) * a.ne + a.plan.pair_expert[p]) * 3 + proj) * a.maxr;
-}
-
-template <int BITS>
-__device__ __forceinline__ void store_q_row_g64(uint32_t slab, int r, const lrc_qmat& U, int row, int gcol0) {
-  const uint32_t* words = reinterpret_cast<const uint32_t*>(U.packed);
-  const int64_t bit0 = (static_cast<int64_t>(row) * U.cols + gcol0) * BITS;  // multiple of 64*BITS: word aligned
-  const int64_t g = static_cast<int64_t>(row) * (U.cols / kKS) + gcol0 / kKS;
-  const float s = h2f(U.scales[g]), z = h2f(U.zeros[g]);
-  uint32_t w[2 * BITS + 1];
-#pragma unroll
-  for (int i = 0; i < 2 * BITS; ++i) w[i] = __ldg(words + (bit0 >> 5) + i);
-  w[2 * BITS] = 0u;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    float v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int b = (8 * j + q) * BITS;
-      v[q] = fmaf(static_cast<float>(__funnelshift_r(w[b >> 5], w[(b >> 5) + 1], b & 31) & ((1u << BITS) - 1u)),
-                  s, z);
+// LR pack builder: one thread per element (once per expert upload)
+__global__ void build_lr_pack_kernel(lrc_expert E, int hidden, int ffn, int R, LrPack L, uint16_t* out) {
+  const int64_t total = L.stride;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float v = 0.0f;
+    auto elem = [](const lrc_qmat& m, int64_t r, int64_t c) {
+      return (qmat_present(m) && r < m.rows && c < m.cols) ? qmat_elem(m, r, c) : 0.0f;
+    };
+    if (i < L.u3x) {
+      const int64_t r = i / L.WU, c = i % L.WU;
+      if (c < R) v = elem(E.u1, r, c);
+    } else if (i < L.u2x) {
+      const int64_t j = i - L.u3x, r = j / L.WU, c = j % L.WU;
+      if (c >= R && c < 2 * R) v = elem(E.u3, r, c - R);
+    } else if (i < L.vup) {
+      const int64_t j = i - L.u2x, r = j / L.WD, c = j % L.WD;
+      if (c < R) v = elem(E.u2, r, c);
+    } else if (i < L.v2) {
+      const int64_t j = i - L.vup, r = j / hidden, c = j % hidden;
+      v = r < R ? elem(E.v1, r, c) : elem(E.v3, r - R, c);
+    } else if (i < L.v2 + static_cast<int64_t>(R) * ffn) {
+      const int64_t j = i - L.v2, r = j / ffn, c = j % ffn;
+      v = elem(E.v2, r, c);
     }
-    umma::sts128(slab + umma::sw128_chunk(r, j), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                 pack_bf16(v[6], v[7]));
-  }
-}
-
-// Columns [gcol0, gcol0 + 64) of row `row` of a quantized (or dense) matrix,
-// shifted right by c0 (element col - c0; zero outside [0, cols) and for absent
-// rows) -> one SWIZZLE_128B row.  For the low-rank factors: U rows of the
-// K-augmentation slabs, V rows of the V.x GEMMs.
-__device__ __noinline__ void store_q_row(uint32_t slab, int r, const lrc_qmat& U, int row, int gcol0, int c0) {
-  const bool pres = qmat_present(U) && row >= 0 && row < U.rows;
-  if (pres && c0 == 0 && U.dense == nullptr && U.group_size == kKS && (U.cols % kKS) == 0 &&
-      gcol0 + kKS <= U.cols) {
-    if (U.bits == 3) return store_q_row_g64<3>(slab, r, U, row, gcol0);
-    if (U.bits == 2) return store_q_row_g64<2>(slab, r, U, row, gcol0);
-    if (U.bits == 4) return store_q_row_g64<4>(slab, r, U, row, gcol0);
-  }
-#pragma unroll 1
-  for (int j = 0; j < 8; ++j) {
-    float v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int col = gcol0 + 8 * j + q - c0;
-      v[q] = (pres && col >= 0 && col < U.cols) ? qmat_elem(U, row, col) : 0.0f;
-    }
-    umma::sts128(slab + umma::sw128_chunk(r, j), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
-                 pack_bf16(v[6], v[7]));
+    out[i] = f2bf(v);
   }
 }
 
@@ -261,111 +270,90 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
   }
   const int main_slabs = P.K / kKS;
   const int nslab = main_slabs + ((any_comp && !vx) ? P.lr_slabs : 0);
+  const uint16_t* pack = P.lrp ? P.lrp + static_cast<int64_t>(e) * P.L.stride : nullptr;
 
   if (warp < kMmaWarp) {
     // ------------------------------------------------------------ producers
     const int mat = tid >> 7, rl = tid & (kTM - 1);  // A row rl of A1 (mat 0) / A3 (mat 1)
-    const lrc_qmat* Wp;
     const int row = (mat ? a3base : a1base) + rl;
-    switch (P.mode) {
-      case kUp: Wp = mat ? &E.w3 : &E.w1; break;
-      case kDown: Wp = &E.w2; break;
-      case kVxUp: Wp = mat ? &E.v3 : &E.v1; break;
-      default: Wp = mat ? nullptr : &E.v2; break;  // A3 unused (zero)
-    }
-    const lrc_qmat& W = Wp ? *Wp : E.v2;
+    const lrc_qmat& W = P.mode == kDown ? E.w2 : (mat ? E.w3 : E.w1);
     const QPtr Wq{W.packed, W.scales, W.zeros};
-    const int qrow = (Wp && row < P.M) ? row : -1;  // quantized-factor row (vx) or -1 = zero
+    // copied A rows (bf16 from the LR pack): vx main slabs (V rows) and the
+    // K-augmentation slabs (U rows); null = zero row
+    const uint16_t* acopy_main = nullptr;  // row start, + 64 s
+    const uint16_t* acopy_lr = nullptr;    // row start, + 64 l
+    if (pack) {
+      if (P.mode == kVxUp && mat == 0 && row < P.M) acopy_main = pack + P.L.vup + static_cast<int64_t>(row) * a.hidden;
+      if (P.mode == kVxDown && mat == 0 && row < P.M) acopy_main = pack + P.L.v2 + static_cast<int64_t>(row) * a.ffn;
+      if (P.mode == kUp && row < P.M)
+        acopy_lr = pack + (mat ? P.L.u3x : P.L.u1x) + static_cast<int64_t>(row) * P.L.WU;
+      if (P.mode == kDown && row < P.M) acopy_lr = pack + P.L.u2x + static_cast<int64_t>(row) * P.L.WD;
+    }
     // B gather: this CTA's pairs [128 rank, +128): 8 lanes per 128-byte row,
     // rows bn0 + 32 i; per-thread sources fixed for the tile
     const int bc = tid & 7, bn0 = tid >> 3;
     constexpr int kBRows = kBN / (kProd / 8);
     const uint16_t* bsrc[kBRows];
+    const uint16_t* tsrc[kBRows];  // the pair's V.x row (K-augmentation slabs)
     uint32_t bmask = 0;
 #pragma unroll
     for (int i = 0; i < kBRows; ++i) {
       const int p = s_pair[rank * kBN + bn0 + (kProd / 8) * i];
       bsrc[i] = a.x + bc * 8;
+      tsrc[i] = a.x + bc * 8;
       if (p >= 0) {
         bsrc[i] = (b_act ? a.a16 + static_cast<int64_t>(p) * a.ffn
                          : a.x + static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden) + bc * 8;
+        if (P.tb) tsrc[i] = P.tb + static_cast<int64_t>(p) * P.WT + bc * 8;
         bmask |= 1u << i;
       }
     }
-    const uint32_t bdst0 = umma::smem_u32(sm + 2 * kSlabA) + umma::sw128_chunk(bn0, bc);
-    auto issue_b = [&](int s) {
-      const uint32_t bb = bdst0 + (s % kStages) * kStageBytes;
-      const int k0 = s * kKS;
+    const uint32_t sbase = umma::smem_u32(sm);
+    const uint32_t bdst0 = sbase + 2 * kSlabA + umma::sw128_chunk(bn0, bc);
+    const uint32_t adst0 = sbase + mat * kSlabA + rl * 128;  // + swizzled chunk offset per copy
+    // cp.async group of slab s: its B rows and, for copied slabs, this thread's A row
+    auto issue = [&](int s) {
+      const uint32_t st = (s % kStages) * kStageBytes;
+      const bool lr = s >= main_slabs;
+      const int k0 = (lr ? s - main_slabs : s) * kKS;
 #pragma unroll
-      for (int i = 0; i < kBRows; ++i)
-        umma::cp_async16(bb + i * (kProd / 8) * 128, bsrc[i] + ((bmask >> i) & 1 ? k0 : 0),
-                         (bmask >> i) & 1 ? 16u : 0u);
+      for (int i = 0; i < kBRows; ++i) {
+        const bool ok = (bmask >> i) & 1;
+        umma::cp_async16(bdst0 + st + i * (kProd / 8) * 128, (lr ? tsrc[i] : bsrc[i]) + (ok ? k0 : 0),
+                         ok ? 16u : 0u);
+      }
+      const uint16_t* ar = lr ? acopy_lr : (vx ? acopy_main : nullptr);
+      if (lr || (vx && mat == 0)) {  // (vx: A3 unused)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          umma::cp_async16(adst0 + st + ((static_cast<uint32_t>(c) ^ static_cast<uint32_t>(rl & 7)) << 4),
+                           ar ? ar + k0 + 8 * c : a.x, ar ? 16u : 0u);
+      }
       umma::cp_async_commit();
     };
     // One slab: dequantize A (codes prefetched kPD slabs earlier: scattered
-    // 16-byte row reads need a long lead under load), wait for this slab's B
-    // rows, publish the stage; then start the B gather two slabs ahead and the
-    // codes kPD slabs ahead.  Unrolled by kPD + 1 below so the prefetch
-    // registers rotate by name (no copies waiting on loads).
+    // 16-byte row reads need a long lead under load) unless it was copied, wait
+    // for the slab's cp.async group, publish the stage; then start the copies
+    // two slabs ahead and the codes kPD slabs ahead.  Unrolled by kPD + 1 below
+    // so the prefetch registers rotate by name (no copies waiting on loads).
     auto step = [&](int s, const RowSlab& cur, RowSlab& dst) {
       const int stage = s % kStages;
-      const uint32_t As = umma::smem_u32(sm) + stage * kStageBytes + mat * kSlabA;
-      const uint32_t Bs = umma::smem_u32(sm) + stage * kStageBytes + 2 * kSlabA;
-      if (s < main_slabs) {
-        if (vx)
-          store_q_row(As, rl, W, qrow, s * kKS, 0);
-        else
-          store_row(As, rl, cur);
-        if (s + 1 < main_slabs)
-          umma::cp_async_wait<1>();  // B(s) landed; B(s+1) may be in flight
-        else
-          umma::cp_async_wait<0>();
-      } else {
-        // K augmentation slab: columns [g0, g0 + 64) of [t1 | t3] (up) or t2 (down)
-        if (s >= kStages) umma::bar_wait(&empty[stage], ((s / kStages) - 1) & 1);
-        const int g0 = (s - main_slabs) * kKS, R = a.maxr;
-        if (P.mode == kDown)
-          store_q_row(As, rl, E.u2, row, g0, 0);
-        else
-          store_q_row(As, rl, mat ? E.u3 : E.u1, row, g0, mat ? R : 0);
-        if (tid < kBN) {  // one B row per thread
-          const int n = tid;
-          const int p = s_pair[rank * kBN + n];
-          const bool comp = p >= 0 && a.plan.pair_comp[p] >= 0;
-#pragma unroll 1
-          for (int j = 0; j < 8; ++j) {
-            float v[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const int col = g0 + 8 * j + q;
-              float t = 0.0f;
-              if (comp) {
-                if (P.mode == kDown) {
-                  if (col < R) t = a.t[t_index(a, p, 2) + col];
-                } else if (col < R) {
-                  t = a.t[t_index(a, p, 0) + col];
-                } else if (col < 2 * R) {
-                  t = a.t[t_index(a, p, 1) + col - R];
-                }
-              }
-              v[q] = t;
-            }
-            umma::sts128(Bs + umma::sw128_chunk(n, j), pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
-                         pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
-          }
-        }
-      }
+      if (s < main_slabs && !vx) store_row(sbase + stage * kStageBytes + mat * kSlabA, rl, cur);
+      if (s + 1 < nslab)
+        umma::cp_async_wait<1>();  // slab s landed; slab s+1 may be in flight
+      else
+        umma::cp_async_wait<0>();
       umma::fence_proxy_async();  // generic smem writes (and landed cp.async) -> tensor core
       umma::bar_arrive(&full[stage]);  // CTA scope: never waits on the prefetches in flight
       const int sb = s + 2;
-      if (sb < main_slabs) {
+      if (sb < nslab) {
         if (sb >= kStages) umma::bar_wait_cluster(&empty[sb % kStages], ((sb / kStages) - 1) & 1);
-        issue_b(sb);
+        issue(sb);
       }
       if (!vx && s + kPD < main_slabs) dst = load_row(Wq, row, P.M, P.K, (s + kPD) * kKS);
     };
-    issue_b(0);
-    if (main_slabs > 1) issue_b(1);
+    issue(0);
+    if (nslab > 1) issue(1);
     RowSlab rs[kPD + 1];
 #pragma unroll
     for (int i = 0; i <= kPD; ++i) rs[i] = RowSlab{};
@@ -391,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
         const uint32_t acc = (s | kk) != 0 ? 1u : 0u;
         const uint64_t db = umma::sdesc(b + 32 * kk);
         umma::mma2_bf16(tmem, umma::sdesc(a1 + 32 * kk), db, kIdesc, acc);
-        umma::mma2_bf16(tmem + kTN, umma::sdesc(a3 + 32 * kk), db, kIdesc, acc);
+        if (!vx) umma::mma2_bf16(tmem + kTN, umma::sdesc(a3 + 32 * kk), db, kIdesc, acc);
       }
       umma::commit2(&empty[stage]);
     }
@@ -419,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
     for (int c0 = half * (kTN / 2); c0 < cend; c0 += 32) {
       float h1[32], h3[32];
       umma::tmem_ld32(lbase + c0, h1);
-      umma::tmem_ld32(lbase + kTN + c0, h3);
+      if (!vx) umma::tmem_ld32(lbase + kTN + c0, h3);
       if (P.mode == kUp) {
         if (ra < P.M) {
 #pragma unroll
@@ -444,20 +432,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
             if (rb < P.M) atomicAdd(yr + rb, w * h3[j]);
           }
         }
-      } else if (ra < a.maxr) {  // V.x rows -> t of the compensated pairs
+      } else if (ra < P.WT) {  // V.x rows -> the pair's bf16 t row (zero when uncompensated)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int n = c0 + j;
           if (n < nvalid) {
             const int p = s_pair[n];
-            if (a.plan.pair_comp[p] >= 0) {
-              if (P.mode == kVxUp) {
-                a.t[t_index(a, p, 0) + ra] = h1[j];
-                a.t[t_index(a, p, 1) + ra] = h3[j];
-              } else {
-                a.t[t_index(a, p, 2) + ra] = h1[j];
-              }
-            }
+            P.tb[static_cast<int64_t>(p) * P.WT + ra] = a.plan.pair_comp[p] >= 0 ? f2bf(h1[j]) : 0;
           }
         }
       }
@@ -472,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
 }  // namespace
 
 bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn, int maxr) {
-  if (hidden % kKS != 0 || ffn % kKS != 0 || maxr > 2 * kTM) return false;
+  if (hidden % kKS != 0 || ffn % kKS != 0 || maxr > kTM) return false;
   for (int i = 0; i < n; ++i) {
     const lrc_qmat* ws[3] = {&experts[i].w1, &experts[i].w3, &experts[i].w2};
     for (auto w : ws)
@@ -483,7 +464,25 @@ bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn, int
   return true;
 }
 
-lrc_status launch_prefill(const ExpertArgs& a, int np_bound, cudaStream_t st, int* launches) {
+int64_t prefill_lr_pack_elems(int hidden, int ffn, int maxr) {
+  return maxr ? lr_pack_layout(hidden, ffn, maxr).stride : 0;
+}
+int prefill_tb_width(int maxr) {
+  if (!maxr) return 0;
+  const LrPack L = lr_pack_layout(64, 64, maxr);
+  return L.WU > L.WD ? L.WU : L.WD;
+}
+
+lrc_status build_prefill_lr(const lrc_expert& e, int hidden, int ffn, int maxr, uint16_t* out, cudaStream_t st) {
+  if (!maxr) return LRC_OK;
+  const LrPack L = lr_pack_layout(hidden, ffn, maxr);
+  build_lr_pack_kernel<<<592, 256, 0, st>>>(e, hidden, ffn, maxr, L, out);
+  LRC_CHECK_LAUNCH();
+  return LRC_OK;
+}
+
+lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp, uint16_t* tb, cudaStream_t st,
+                          int* launches) {
   static bool attr = false;
   if (!attr) {
     LRC_CUDA_TRY(cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
@@ -491,6 +490,13 @@ lrc_status launch_prefill(const ExpertArgs& a, int np_bound, cudaStream_t st, in
   }
   PrefillArgs P{};
   P.a = a;
+  const int R = lrp ? a.maxr : 0;
+  if (R) {
+    P.lrp = lrp;
+    P.L = lr_pack_layout(a.hidden, a.ffn, R);
+    P.tb = tb;
+    P.WT = prefill_tb_width(R);
+  }
   const int ytiles = (np_bound + kTN - 1) / kTN + a.ne;  // >= sum over experts of ceil(cnt / kTN)
   auto launch = [&](int mode, int M, int K, int lr_slabs, int rows_per_pair) -> lrc_status {
     P.mode = mode;
@@ -514,11 +520,10 @@ lrc_status launch_prefill(const ExpertArgs& a, int np_bound, cudaStream_t st, in
     return LRC_OK;
   };
   lrc_status s;
-  const int R = a.maxr;
-  if (R && (s = launch(kVxUp, R, a.hidden, 0, 2 * kTM)) != LRC_OK) return s;
-  if ((s = launch(kUp, a.ffn, a.hidden, R ? (2 * R + kKS - 1) / kKS : 0, 2 * kTM)) != LRC_OK) return s;
+  if (R && (s = launch(kVxUp, 2 * R, a.hidden, 0, 2 * kTM)) != LRC_OK) return s;
+  if ((s = launch(kUp, a.ffn, a.hidden, R ? P.L.WU / kKS : 0, 2 * kTM)) != LRC_OK) return s;
   if (R && (s = launch(kVxDown, R, a.ffn, 0, 2 * kTM)) != LRC_OK) return s;
-  return launch(kDown, a.hidden, a.ffn, R ? (R + kKS - 1) / kKS : 0, 4 * kTM);
+  return launch(kDown, a.hidden, a.ffn, R ? P.L.WD / kKS : 0, 4 * kTM);
 }
 
 }  // namespace lrc
