@@ -234,6 +234,9 @@ struct lrc_layer {
   uint16_t* lrp = nullptr;     // per-expert bf16 LR packs for the prefill path (built lazily)
   std::vector<uint8_t> lrp_dirty;
   uint16_t* tb = nullptr;      // prefill V.x rows [max_pairs][tb_width] bf16
+  int* plan_blk = nullptr;     // parallel plan: per-chunk histograms
+  uint32_t* plan_cmask = nullptr;
+  int* plan_ticket = nullptr;
   int64_t prefill_min = [] {
     const char* v = getenv("LRC_PREFILL_MIN");
     return v ? static_cast<int64_t>(atoll(v)) : static_cast<int64_t>(256);
@@ -348,6 +351,9 @@ static lrc_status alloc_workspace(lrc_layer* L) {
   size_t o_lg = take(size_t(L->max_tokens) * L->E * 8);
   size_t o_tt = take(size_t(route_tiles(L->max_tokens)) * 4 + 16);
   size_t o_tb = take(size_t(NP) * prefill_tb_width(L->maxr) * 2 + 16);
+  size_t o_pb = take(size_t(plan_parallel_blocks(NP) + 1) * (NE + 1) * 4);
+  size_t o_pcm = take(size_t(NE) * 4 + 16);
+  size_t o_ptk = take(16);
   LRC_CUDA_TRY(cudaMalloc(&L->ws, off));
   LRC_CUDA_TRY(cudaMemset(L->ws, 0, off));
   L->ws_bytes = off;
@@ -379,6 +385,9 @@ static lrc_status alloc_workspace(lrc_layer* L) {
   L->logits = reinterpret_cast<double*>(base + o_lg);
   L->tile_ticket = reinterpret_cast<int*>(base + o_tt);
   L->tb = reinterpret_cast<uint16_t*>(base + o_tb);
+  L->plan_blk = reinterpret_cast<int*>(base + o_pb);
+  L->plan_cmask = reinterpret_cast<uint32_t*>(base + o_pcm);
+  L->plan_ticket = reinterpret_cast<int*>(base + o_ptk);
   if (L->maxr) {  // LR packs: built before the first prefill call (and after expert updates)
     const size_t per = static_cast<size_t>(prefill_lr_pack_elems(L->hidden, L->ffn, L->maxr));
     LRC_CUDA_TRY(cudaMalloc(&L->lrp, per * NE * 2));
@@ -554,12 +563,22 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   ra.pdl = (!prof && L->pdl) ? 1 : 0;
   ra.pairs_expert = pairs_expert;
   ra.pairs_w = pairs_w;
+  const int P = top_k + (pairs_expert ? 0 : L->S);
+  const int np_bound = static_cast<int>(B) * P;
+  // large batches: routing only, then the parallel plan (the single-CTA serial
+  // plan would take ~1 us per 32 pairs)
+  const bool big_plan = np_bound > kSerialPlanMaxPairs;
+  if (big_plan) ra.plan.ticket = nullptr;
   lrc_status s = launch_route(ra, st);
   if (s != LRC_OK) return s;
   ++launches;
+  if (big_plan) {
+    if ((s = launch_plan_parallel(plan, ti, tw, static_cast<int>(B), top_k, L->plan_blk, L->plan_cmask,
+                                  L->plan_ticket, st)) != LRC_OK)
+      return s;
+    launches += 2;
+  }
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[1], st));
-  const int P = top_k + (pairs_expert ? 0 : L->S);
-  const int np_bound = static_cast<int>(B) * P;
   ExpertArgs a{};
   a.ne = L->E + L->S;
   a.experts = L->d_experts;

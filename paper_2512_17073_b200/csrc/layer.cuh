@@ -133,6 +133,11 @@ __device__ void vrow_dot_tokens(const lrc_qmat& V, int j, const uint16_t* __rest
 }
 
 int route_tiles(int64_t B);
+// large-batch plan (router in routing-only mode, then a parallel counting sort)
+constexpr int kSerialPlanMaxPairs = 2048;
+int plan_parallel_blocks(int64_t np);
+lrc_status launch_plan_parallel(const PlanArgs& pa, const int32_t* tk_idx, const float* tk_w, int B, int k,
+                                int* blk, uint32_t* cmask, int* ticket, cudaStream_t st);
 lrc_status launch_route(const RouteArgs& ra, cudaStream_t st);
 
 // Arguments of the expert phases.

@@ -798,6 +798,175 @@ __device__ __noinline__ void warm_tail(const RouteArgs& ra, WarmScratch& ws, con
 
 int route_tiles(int64_t B) { return static_cast<int>((B + kTT - 1) / kTT); }
 
+// ---------------------------------------------- large-batch parallel plan ---
+// Same output as build_plan_block (pairs grouped by expert, ascending pair id
+// inside each expert; compensated slots in pair order), as a counting sort over
+// 1024-pair chunks: per-chunk histograms, then a stable scatter whose offsets
+// are the chunk prefix sums; the last chunk writes the active lists and
+// records.  Replaces the serial single-CTA plan when B * P is large.
+constexpr int kPlanChunk = 1024;
+
+__device__ __forceinline__ void plan_pair(const PlanArgs& pa, const int32_t* tk_idx, const float* tk_w, int k,
+                                          int P, int p, int& e, float& w, bool& comp) {
+  const int b = p / P, j = p - b * P;
+  if (j < k) {
+    e = tk_idx[b * k + j];
+    w = tk_w[b * k + j];
+  } else {
+    e = pa.num_experts + (j - k);
+    w = 1.0f;
+  }
+  comp = (j < k) ? ((pa.comp_rows != nullptr ? pa.comp_rows[b] != 0 : j < pa.top_n) && pa.has_comp[e])
+                 : (pa.compensate_shared && pa.has_comp[e]);
+}
+
+__global__ void __launch_bounds__(kPlanChunk) plan_count_kernel(const PlanArgs pa, const int32_t* tk_idx,
+                                                                const float* tk_w, int B, int k, int* blk) {
+  const int P = k + (pa.comp_rows ? 0 : pa.num_shared), NP = B * P, NE = pa.num_experts + pa.num_shared;
+  __shared__ int cnt[LRC_MAX_EXPERTS + 1];
+  for (int e = threadIdx.x; e <= NE; e += blockDim.x) cnt[e] = 0;
+  __syncthreads();
+  const int p = blockIdx.x * kPlanChunk + threadIdx.x;
+  if (p < NP) {
+    int e;
+    float w;
+    bool comp;
+    plan_pair(pa, tk_idx, tk_w, k, P, p, e, w, comp);
+    pa.pair_expert[p] = e;
+    pa.pair_w[p] = w;
+    pa.pair_token[p] = p / P;
+    atomicAdd(&cnt[e], 1);
+    if (comp) atomicAdd(&cnt[NE], 1);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e <= NE; e += blockDim.x) blk[blockIdx.x * (NE + 1) + e] = cnt[e];
+}
+
+__global__ void __launch_bounds__(kPlanChunk) plan_scatter_kernel(const PlanArgs pa, const int32_t* tk_idx,
+                                                                  const float* tk_w, int B, int k, const int* blk,
+                                                                  uint32_t* cmask, int* ticket) {
+  const int P = k + (pa.comp_rows ? 0 : pa.num_shared), NP = B * P, NE = pa.num_experts + pa.num_shared;
+  const int nblk = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ int total[LRC_MAX_EXPERTS + 1];
+  __shared__ int start[LRC_MAX_EXPERTS + 1];
+  __shared__ int base[LRC_MAX_EXPERTS + 1];
+  __shared__ int wcnt[kPlanChunk / 32][LRC_MAX_EXPERTS + 1];
+  __shared__ int s_last, s_na;
+  __shared__ int s_act[LRC_MAX_EXPERTS];
+  for (int e = threadIdx.x; e <= NE; e += blockDim.x) {
+    int before = 0, all = 0;
+    for (int b = 0; b < nblk; ++b) {
+      const int c = blk[b * (NE + 1) + e];
+      all += c;
+      before += b < static_cast<int>(blockIdx.x) ? c : 0;
+    }
+    total[e] = all;
+    base[e] = before;
+  }
+  for (int e = lane; e <= NE; e += 32) wcnt[warp][e] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < NE; ++e) {
+      start[e] = acc;
+      acc += total[e];
+    }
+    start[NE] = 0;  // compensated slots start at 0
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e <= NE; e += blockDim.x) base[e] += start[e];
+  // per-warp histograms (ranks inside the warp from match_any)
+  const int p = blockIdx.x * kPlanChunk + threadIdx.x;
+  const bool valid = p < NP;
+  int e = -1 - lane;
+  float w = 0.0f;
+  bool comp = false;
+  if (valid) plan_pair(pa, tk_idx, tk_w, k, P, p, e, w, comp);
+  const unsigned lt = (1u << lane) - 1u;
+  const unsigned same = __match_any_sync(0xffffffffu, e);
+  const unsigned cm = __ballot_sync(0xffffffffu, comp);
+  if (valid && (same & lt) == 0) wcnt[warp][e] = __popc(same);
+  if (lane == 0) wcnt[warp][NE] = __popc(cm);
+  __syncthreads();
+  for (int x = threadIdx.x; x <= NE; x += blockDim.x) {  // exclusive scan over warps
+    int acc = 0;
+    for (int w2 = 0; w2 < kPlanChunk / 32; ++w2) {
+      const int c = wcnt[w2][x];
+      wcnt[w2][x] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  if (valid) {
+    const int pos = base[e] + wcnt[warp][e] + __popc(same & lt);
+    pa.pair_list[pos] = p;
+    const int slot = comp ? base[NE] + wcnt[warp][NE] + __popc(cm & lt) : -1;
+    pa.pair_comp[p] = slot;
+    if (comp) {
+      pa.comp_list[slot] = p;
+      atomicOr(&cmask[e], 1u << min((pos - start[e]) >> 3, 31));
+    }
+  }
+  // the last chunk publishes the active lists and per-expert records
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1) == nblk - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    int na = 0;
+    for (int x = 0; x < NE; ++x)
+      if (total[x] > 0) {
+        pa.active[na] = x;
+        pa.active_off[na] = start[x];
+        pa.active_cnt[na] = total[x];
+        s_act[na++] = x;
+      }
+    pa.counts[0] = na;
+    pa.counts[1] = total[NE];
+    s_na = na;
+    *ticket = 0;
+  }
+  __syncthreads();
+  if (pa.arec != nullptr) {
+    for (int a = threadIdx.x; a < s_na; a += blockDim.x) {
+      const int x = s_act[a];
+      const lrc_expert& X = pa.experts[x];
+      const LrLayout L = lr_layout(X);
+      ActiveRec R;
+      R.up_tiles = X.up_tiles;
+      R.down_tiles = X.down_tiles;
+      R.up_lr_tiles = X.up_lr_tiles;
+      R.down_lr_tiles = X.down_lr_tiles;
+      R.e = x;
+      R.off = start[x];
+      R.cnt = total[x];
+      R.cmask = *reinterpret_cast<volatile uint32_t*>(&cmask[x]);
+      R.up_lr_bytes = L.up_total;
+      R.down_lr_bytes = L.down_total;
+      R.pad[0] = R.pad[1] = 0;
+      pa.arec[a] = R;
+    }
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < NE; x += blockDim.x) cmask[x] = 0;
+}
+
+int plan_parallel_blocks(int64_t np) { return static_cast<int>((np + kPlanChunk - 1) / kPlanChunk); }
+
+lrc_status launch_plan_parallel(const PlanArgs& pa, const int32_t* tk_idx, const float* tk_w, int B, int k,
+                                int* blk, uint32_t* cmask, int* ticket, cudaStream_t st) {
+  const int P = k + (pa.comp_rows ? 0 : pa.num_shared);
+  const int nblk = plan_parallel_blocks(static_cast<int64_t>(B) * P);
+  if (nblk == 0) return LRC_OK;
+  plan_count_kernel<<<nblk, kPlanChunk, 0, st>>>(pa, tk_idx, tk_w, B, k, blk);
+  LRC_CHECK_LAUNCH();
+  plan_scatter_kernel<<<nblk, kPlanChunk, 0, st>>>(pa, tk_idx, tk_w, B, k, blk, cmask, ticket);
+  LRC_CHECK_LAUNCH();
+  return LRC_OK;
+}
+
 lrc_status launch_route(const RouteArgs& ra_in, cudaStream_t st) {
   // debug knobs: bit 0 = %globaltimer stamps, bit 1 = no tail warm-up warp
   static const int stamps = (getenv("LRC_ROUTE_STAMPS") != nullptr ? 1 : 0) |

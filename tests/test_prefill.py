@@ -146,3 +146,27 @@ def test_prefill_skewed_routing(torch):
     assert np.array_equal(ip, idd.cpu().numpy())
     yp, yd = yp.double().cpu().numpy(), yd.double().cpu().numpy()
     assert max(rel_l2(yp[t], yd[t]) for t in range(B)) <= TOL_Y
+
+
+@pytest.mark.parametrize("prefill", [False, True])
+def test_parallel_plan_matches_serial_plan(torch, prefill):
+    """B * (k + S) > 2048 pairs builds the pair plan with the parallel counting
+    sort; the same tokens in two halves use the serial plan.  Same routing and
+    the same per-token outputs (decode tiled path and prefill path), with
+    compensated shared experts (S = 1)."""
+    from paper_2512_17073_b200.synth import SynthLayer
+
+    B = 1100  # 3300 pairs
+    sl = SynthLayer(512, 1024, 8, top_k=2, num_shared=1, rank=16, seed=9, max_tokens=B)
+    sl.layer.set_prefill_min(1 if prefill else 0)
+    xs = torch.randn((B, 512), device="cuda").to(torch.bfloat16)
+    yb, ib, _ = sl.layer.forward(xs, top_k=2, top_n=1)
+    yb, ib = yb.double().cpu().numpy(), ib.cpu().numpy()
+    h = B // 2
+    y1, i1, _ = sl.layer.forward(xs[:h].contiguous(), top_k=2, top_n=1)
+    y1, i1 = y1.double().cpu().numpy(), i1.cpu().numpy()
+    y2, i2, _ = sl.layer.forward(xs[h:].contiguous(), top_k=2, top_n=1)
+    y2, i2 = y2.double().cpu().numpy(), i2.cpu().numpy()
+    assert np.array_equal(ib, np.concatenate([i1, i2]))
+    ys = np.concatenate([y1, y2])
+    assert max(rel_l2(yb[t], ys[t]) for t in range(B)) <= 1e-3
