@@ -332,6 +332,11 @@ def run_ours(args, world, rank):
         for Bs in (1, 2, 4, 8, 16, 32, 64):
             sweep[str(Bs)] = sweep_point(layers, Bs, hbm, tf_sust)
 
+    # C4 prefill: 16,384 tokens through one layer, tcgen05 path
+    prefill = None
+    if args.prefill and rank == 0:
+        prefill = prefill_point(tf_burst, tf_sust)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_ours(layers[0], B)
@@ -354,6 +359,7 @@ def run_ours(args, world, rank):
         "e2e": e2e,
         "clocks": clk.summary(),
         "sweep": sweep,
+        "prefill": prefill,
         "cpu_baseline": cpu,
     }
     if rank == 0:
@@ -400,6 +406,39 @@ def sweep_point(layers, B, hbm, tf_sust, steps=200):
     return {"tokens_s": round(steps * B / (ms / 1e3), 1), "us_per_step": round(ms * 1e3 / steps, 2),
             "gbs": round(byts / (ms / 1e3) / 1e9, 1), "frac": round(roof / (ms / 1e3), 4),
             "d_sel_mean": round(float(np.mean([s[0] for s in stats])), 2)}
+
+
+def prefill_point(tf_burst, tf_sust, B=16384, iters=3):
+    """C4: one Mixtral-shaped layer over 16,384 tokens (2,048 x 8) on the tcgen05
+    grouped dequant-GEMM path, top_n 0/1/2; tensor-bound roofline at the
+    measured bf16 peak (sustained: each launch runs for milliseconds)."""
+    import torch
+
+    from paper_2512_17073_b200.synth import SynthLayer
+
+    sl = SynthLayer(HIDDEN, FFN, E, top_k=TOPK, bits=BITS, rank=RANK, seed=4242, max_tokens=B)
+    sl.layer.set_prefill_min(1)
+    x = torch.randn((B, HIDDEN), device="cuda").to(torch.bfloat16)
+    y = torch.empty((B, HIDDEN), device="cuda", dtype=torch.float32)
+    out = {"tokens": B, "path": "router + parallel plan + tcgen05 cta_group::2 dequant-GEMMs (V.x, up, V2.a, down)"}
+    for n in (0, 1, 2):
+        sl.layer.forward(x, TOPK, n, y=y)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            sl.layer.forward(x, TOPK, n, y=y)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        fl = B * layer_flops(HIDDEN, FFN, TOPK, n, RANK, E)
+        tf = fl / (ms / 1e3) / 1e12
+        out[f"n{n}"] = {"ms_per_layer": round(ms, 3), "tokens_s": round(B / (ms / 1e3), 1),
+                        "tflops": round(tf, 1), "frac_sustained": round(tf / tf_sust, 4),
+                        "frac_burst": round(tf / tf_burst, 4), "launches": sl.layer.last_launches()}
+    del sl
+    torch.cuda.empty_cache()
+    return out
 
 
 # --------------------------------------------------------- CPU baselines ----
@@ -494,6 +533,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-sweep", dest="sweep", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefill", dest="prefill", action="store_false")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = 2000 if args.impl == "ours" else 5
