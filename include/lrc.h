@@ -179,7 +179,7 @@ lrc_status lrc_layer_forward_host(lrc_layer* layer, const uint16_t* x_host, int6
 lrc_status lrc_layer_set_profiling(lrc_layer* layer, int enabled);
 /* Batches of B >= min_tokens tokens run the tcgen05 grouped dequant-GEMM
  * (prefill) path when the layer is eligible (2-bit gs=64 weights, hidden and
- * ffn multiples of 64); min_tokens <= 0 disables it.  Default 256 (env
+ * ffn multiples of 64); min_tokens <= 0 disables it.  Default 128 (env
  * LRC_PREFILL_MIN). */
 lrc_status lrc_layer_set_prefill_min(lrc_layer* layer, int64_t min_tokens);
 int lrc_layer_prefill_eligible(const lrc_layer* layer);

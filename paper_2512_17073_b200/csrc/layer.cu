@@ -239,7 +239,7 @@ struct lrc_layer {
   int* plan_ticket = nullptr;
   int64_t prefill_min = [] {
     const char* v = getenv("LRC_PREFILL_MIN");
-    return v ? static_cast<int64_t>(atoll(v)) : static_cast<int64_t>(256);
+    return v ? static_cast<int64_t>(atoll(v)) : static_cast<int64_t>(128);
   }();
   int last_launches = 0;
   const double* gate_t = nullptr;

@@ -149,7 +149,7 @@ class LRCMoELayer:
         self.gate_t = keep.add(torch.from_numpy(np.ascontiguousarray(np.asarray(gate, np.float64).T)).cuda())
         self.max_tokens, self.top_k = max_tokens, top_k
         self._handle = None
-        self._prefill_min = None  # None: the library default (LRC_PREFILL_MIN or 256)
+        self._prefill_min = None  # None: the library default (LRC_PREFILL_MIN or 128)
         self._create()
 
     def _create(self):

@@ -90,7 +90,7 @@ def test_prefill_equals_decode_path(torch):
 @pytest.mark.parametrize("B", [256, 600])
 def test_mixtral_shape_prefill_vs_oracle(torch, B):
     """C2 dims (d=4096, ffn=14336, 8 experts top-2, INT2 + r32 top-1) at prefill
-    batch sizes; the default threshold routes B >= 256 to the tcgen05 path."""
+    batch sizes; the default threshold routes B >= 128 to the tcgen05 path."""
     from paper_2512_17073_b200.synth import SynthLayer
 
     sl = SynthLayer(4096, 14336, 8, top_k=2, rank=32, seed=11, max_tokens=B)
