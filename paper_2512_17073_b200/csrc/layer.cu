@@ -232,7 +232,8 @@ struct lrc_layer {
   bool tiled = false;
   bool prefill_ok = false;  // tcgen05 prefill GEMM eligible (2-bit gs64 reference-layout weights)
   uint16_t* lrp = nullptr;     // per-expert bf16 LR packs for the prefill path (built lazily)
-  std::vector<uint8_t> lrp_dirty;
+  uint8_t* ppk = nullptr;      // per-expert prefill packs of the weight codes (built lazily)
+  std::vector<uint8_t> lrp_dirty;  // per expert: packs stale (expert replaced)
   uint16_t* tb = nullptr;      // prefill V.x rows [max_pairs][tb_width] bf16
   int* plan_blk = nullptr;     // parallel plan: per-chunk histograms
   uint32_t* plan_cmask = nullptr;
@@ -388,10 +389,10 @@ static lrc_status alloc_workspace(lrc_layer* L) {
   L->plan_blk = reinterpret_cast<int*>(base + o_pb);
   L->plan_cmask = reinterpret_cast<uint32_t*>(base + o_pcm);
   L->plan_ticket = reinterpret_cast<int*>(base + o_ptk);
-  if (L->maxr) {  // LR packs: built before the first prefill call (and after expert updates)
+  L->lrp_dirty.assign(NE, 1);  // packs: built before the first prefill call (and after expert updates)
+  if (L->maxr) {
     const size_t per = static_cast<size_t>(prefill_lr_pack_elems(L->hidden, L->ffn, L->maxr));
     LRC_CUDA_TRY(cudaMalloc(&L->lrp, per * NE * 2));
-    L->lrp_dirty.assign(NE, 1);
   }
   for (auto& e : L->ev) LRC_CUDA_TRY(cudaEventCreate(&e));
   std::vector<uint8_t> hc(NE);
@@ -452,6 +453,7 @@ extern "C" void lrc_layer_destroy(lrc_layer* L) {
   if (L->h_stage) cudaFreeHost(L->h_stage);
   cudaFree(L->ws);
   cudaFree(L->lrp);
+  cudaFree(L->ppk);
   for (auto& e : L->ev)
     if (e) cudaEventDestroy(e);
   delete L;
@@ -600,17 +602,21 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[2], st));
   if (prefill) {
     // large batches: tcgen05 grouped dequant-GEMMs (V1|V3.x, up, V2.a, down)
-    if (L->maxr) {  // (re)build the bf16 LR packs of experts changed since the last prefill call
-      const size_t per = static_cast<size_t>(prefill_lr_pack_elems(L->hidden, L->ffn, L->maxr));
-      for (size_t i = 0; i < L->lrp_dirty.size(); ++i)
-        if (L->lrp_dirty[i]) {
-          if ((s = build_prefill_lr(L->host_experts[i], L->hidden, L->ffn, L->maxr, L->lrp + per * i, st)) !=
-              LRC_OK)
-            return s;
-          L->lrp_dirty[i] = 0;
-        }
-    }
-    if ((s = launch_prefill(a, np_bound, L->lrp, L->tb, st, &launches)) != LRC_OK) return s;
+    // (re)build the packs of experts changed since the last prefill call: the
+    // weight codes as contiguous per-slab blocks, the LR factors as bf16 rows
+    const size_t pb = static_cast<size_t>(prefill_pack_bytes(L->hidden, L->ffn));
+    if (L->ppk == nullptr) LRC_CUDA_TRY(cudaMalloc(&L->ppk, pb * L->lrp_dirty.size()));
+    const size_t per = static_cast<size_t>(prefill_lr_pack_elems(L->hidden, L->ffn, L->maxr));
+    for (size_t i = 0; i < L->lrp_dirty.size(); ++i)
+      if (L->lrp_dirty[i]) {
+        if ((s = build_prefill_pack(L->host_experts[i], L->hidden, L->ffn, L->ppk + pb * i, st)) != LRC_OK)
+          return s;
+        if (L->maxr &&
+            (s = build_prefill_lr(L->host_experts[i], L->hidden, L->ffn, L->maxr, L->lrp + per * i, st)) != LRC_OK)
+          return s;
+        L->lrp_dirty[i] = 0;
+      }
+    if ((s = launch_prefill(a, np_bound, L->lrp, L->tb, L->ppk, st, &launches)) != LRC_OK) return s;
     if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));  // phases: up+mid+down lumped into [2]
   } else if (allow_tiled && L->tiled) {
     const int tok_bound = static_cast<int>(std::min<int64_t>(B, L->max_tokens));

@@ -213,7 +213,9 @@ bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn, int
 int64_t prefill_lr_pack_elems(int hidden, int ffn, int maxr);  // bf16 elements per expert
 int prefill_tb_width(int maxr);
 lrc_status build_prefill_lr(const lrc_expert& e, int hidden, int ffn, int maxr, uint16_t* out, cudaStream_t st);
-lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp, uint16_t* tb, cudaStream_t st,
-                          int* launches);
+int64_t prefill_pack_bytes(int hidden, int ffn);  // per expert
+lrc_status build_prefill_pack(const lrc_expert& e, int hidden, int ffn, uint8_t* out, cudaStream_t st);
+lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp, uint16_t* tb,
+                          const uint8_t* ppk, cudaStream_t st, int* launches);
 
 }  // namespace lrc

@@ -51,8 +51,9 @@ constexpr int kStageBytes = 2 * kSlabA + kSlabB;  // 48 KB
 constexpr int kProd = 256;
 constexpr int kThreads = kProd + 32;
 constexpr int kMmaWarp = kProd / 32;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024;
-constexpr int kPD = 4;  // code prefetch distance (slabs)
+constexpr int kCB = 2560;  // prefill-pack block: 128 rows x (16 B codes) + 128 x (fp16 scale, fp16 zero)
+constexpr int kCR = 6;     // code ring depth (slabs), filled by cp.async.bulk
+constexpr int kSmemBytes = kStages * kStageBytes + kCR * 2 * kCB + 1024;
 constexpr uint32_t kIdesc = umma::idesc_bf16(2 * kTM, kTN);
 
 enum Mode : int {
@@ -86,6 +87,25 @@ __host__ __device__ inline LrPack lr_pack_layout(int hidden, int ffn, int R) {
   return L;
 }
 
+// Prefill pack: the reference codes + metadata of each weight matrix re-laid
+// out (same bytes) as blocks of [128 rows][16 B codes] + [128 rows][scale |
+// zero << 16], one block per (128-row block, 64-column slab), blocks ordered
+// row-block-major, so one slab of one CTA's A rows is ONE contiguous 2,560-byte
+// bulk copy.  Rows past the matrix are zero.
+struct PPack {
+  int64_t w1, w3, w2, stride;  // byte offsets in an expert's pack
+};
+__host__ __device__ inline PPack ppack_layout(int hidden, int ffn) {
+  const int64_t up = static_cast<int64_t>((ffn + 127) / 128) * (hidden / 64);
+  const int64_t dn = static_cast<int64_t>((hidden + 127) / 128) * (ffn / 64);
+  PPack L;
+  L.w1 = 0;
+  L.w3 = up * kCB;
+  L.w2 = 2 * up * kCB;
+  L.stride = (2 * up + dn) * kCB;
+  return L;
+}
+
 struct PrefillArgs {
   ExpertArgs a;
   int mode;
@@ -95,6 +115,8 @@ struct PrefillArgs {
   LrPack L;
   uint16_t* tb;  // [max_pairs][WT] bf16 V.x rows ([t1 | t3] after kVxUp, t2 after kVxDown)
   int WT;
+  const uint8_t* ppk;  // prefill packs [ne][PL.stride]
+  PPack PL;
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -113,35 +135,36 @@ __device__ __forceinline__ uint32_t bf16x2_of(uint64_t v) {  // round both halve
   return pack_bf16(lo, hi);
 }
 
-// Codes and group metadata of one row for one 64-column slab (reference
-// layout: row-major LSB-first 2-bit stream, one fp16 scale/zero per group).
-// Metadata stays raw until use so a prefetch never waits on its load.
+// One row of one 64-column slab: 16 B of 2-bit codes (LSB first) and the
+// group's fp16 scale / zero bits.
 struct RowSlab {
   uint4 c;
-  uint32_t s, z;  // fp16 bits
+  uint32_t s, z;
 };
 
-// The matrix pointers live in registers (QPtr), not behind the expert-table
-// reference, so a prefetch is one dependent-free load.
-struct QPtr {
-  const uint8_t* packed;
-  const uint16_t* scales;
-  const uint16_t* zeros;
-};
-
-__device__ __forceinline__ RowSlab load_row(const QPtr& W, int row, int M, int K, int k0) {
-  RowSlab r{make_uint4(0, 0, 0, 0), 0u, 0u};
-  if (row < M) {
-    const int64_t e0 = static_cast<int64_t>(row) * K + k0;
-    // volatile: issued where written (two slabs ahead), never sunk to the use
-    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.c.x), "=r"(r.c.y), "=r"(r.c.z), "=r"(r.c.w)
-                 : "l"(W.packed + (e0 >> 2)));
-    const int64_t g = static_cast<int64_t>(row) * (K / kKS) + k0 / kKS;
-    asm volatile("ld.global.nc.u16 %0, [%1];" : "=r"(r.s) : "l"(W.scales + g));
-    asm volatile("ld.global.nc.u16 %0, [%1];" : "=r"(r.z) : "l"(W.zeros + g));
+__global__ void build_ppack_kernel(lrc_expert E, int hidden, int ffn, PPack L, uint8_t* out) {
+  const int64_t up = static_cast<int64_t>((ffn + 127) / 128) * (hidden / 64);
+  const int64_t nblk = L.stride / kCB;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nblk * 128;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t blk = i >> 7;
+    const int r = static_cast<int>(i & 127);
+    const lrc_qmat& W = blk < up ? E.w1 : (blk < 2 * up ? E.w3 : E.w2);
+    const int64_t b = blk < 2 * up ? blk % up : blk - 2 * up;
+    const int K = blk < 2 * up ? hidden : ffn, M = blk < 2 * up ? ffn : hidden;
+    const int nslab = K / 64;
+    const int row = static_cast<int>(b / nslab) * 128 + r, s = static_cast<int>(b % nslab);
+    uint4 c = make_uint4(0, 0, 0, 0);
+    uint32_t sz = 0;
+    if (row < M) {
+      c = *reinterpret_cast<const uint4*>(W.packed + ((static_cast<int64_t>(row) * K + s * 64) >> 2));
+      const int64_t g = static_cast<int64_t>(row) * nslab + s;
+      sz = static_cast<uint32_t>(W.scales[g]) | (static_cast<uint32_t>(W.zeros[g]) << 16);
+    }
+    uint8_t* o = out + blk * kCB;
+    *reinterpret_cast<uint4*>(o + 16 * r) = c;
+    *reinterpret_cast<uint32_t*>(o + 2048 + 4 * r) = sz;
   }
-  return r;
 }
 
 // Dequantize a row slab into its SWIZZLE_128B row.  Code i of a 16-bit field
@@ -208,7 +231,7 @@ __global__ void build_lr_pack_kernel(lrc_expert E, int hidden, int ffn, int R, L
 __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[kStages], empty[kStages], done;
+  __shared__ uint64_t full[kStages], empty[kStages], done, rfull[kCR], rempty[kCR];
   __shared__ uint32_t tmem_base;
   __shared__ int s_pair[kTN];
   const ExpertArgs& a = P.a;
@@ -231,7 +254,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
   }
   if (ai < 0) return;
   const int e = a.plan.active[ai];
-  const lrc_expert& E = a.experts[e];
   const int off = a.plan.active_off[ai] + yb * kTN;
   const int nvalid = min(kTN, a.plan.active_cnt[ai] - yb * kTN);
   // rows of this CTA's A1 / A3 operands (row of TMEM lane l = base + l)
@@ -255,6 +277,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
       umma::bar_init(&empty[i], 1);
     }
     umma::bar_init(&done, 1);
+    for (int i = 0; i < kCR; ++i) {
+      umma::bar_init(&rfull[i], 1);
+      umma::bar_init(&rempty[i], kProd);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) umma::tmem_alloc2<2 * kTN>(&tmem_base);
@@ -276,8 +302,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
     // ------------------------------------------------------------ producers
     const int mat = tid >> 7, rl = tid & (kTM - 1);  // A row rl of A1 (mat 0) / A3 (mat 1)
     const int row = (mat ? a3base : a1base) + rl;
-    const lrc_qmat& W = P.mode == kDown ? E.w2 : (mat ? E.w3 : E.w1);
-    const QPtr Wq{W.packed, W.scales, W.zeros};
     // copied A rows (bf16 from the LR pack): vx main slabs (V rows) and the
     // K-augmentation slabs (U rows); null = zero row
     const uint16_t* acopy_main = nullptr;  // row start, + 64 s
@@ -331,41 +355,40 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
       }
       umma::cp_async_commit();
     };
-    // One slab: dequantize A (codes prefetched kPD slabs earlier: scattered
-    // 16-byte row reads need a long lead under load) unless it was copied, wait
-    // for the slab's cp.async group, publish the stage; then start the copies
-    // two slabs ahead and the codes kPD slabs ahead.  Unrolled by kPD + 1 below
-    // so the prefetch registers rotate by name (no copies waiting on loads).
-    auto step = [&](int s, const RowSlab& cur, RowSlab& dst) {
+    // One slab: dequantize A from the code ring (filled kCR slabs ahead by
+    // the bulk-copy loader) unless the slab is copied, wait for the slab's
+    // cp.async group, publish the stage; then start the copies two slabs ahead.
+    const uint32_t ring = sbase + kStages * kStageBytes + mat * kCB;
+    issue(0);
+    if (nslab > 1) issue(1);
+    for (int s = 0; s < nslab; ++s) {
       const int stage = s % kStages;
-      if (s < main_slabs && !vx) store_row(sbase + stage * kStageBytes + mat * kSlabA, rl, cur);
+      if (s < main_slabs && !vx) {
+        const int slot = s % kCR;
+        umma::bar_wait(&rfull[slot], (s / kCR) & 1);
+        RowSlab v;
+        const uint32_t blk = ring + slot * 2 * kCB;
+        uint32_t sz;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.c.x), "=r"(v.c.y), "=r"(v.c.z), "=r"(v.c.w)
+                     : "r"(blk + 16 * rl));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sz) : "r"(blk + 2048 + 4 * rl));
+        umma::bar_arrive(&rempty[slot]);
+        v.s = sz & 0xFFFFu;
+        v.z = sz >> 16;
+        store_row(sbase + stage * kStageBytes + mat * kSlabA, rl, v);
+      }
       if (s + 1 < nslab)
         umma::cp_async_wait<1>();  // slab s landed; slab s+1 may be in flight
       else
         umma::cp_async_wait<0>();
       umma::fence_proxy_async();  // generic smem writes (and landed cp.async) -> tensor core
-      umma::bar_arrive(&full[stage]);  // CTA scope: never waits on the prefetches in flight
+      umma::bar_arrive(&full[stage]);
       const int sb = s + 2;
       if (sb < nslab) {
         if (sb >= kStages) umma::bar_wait_cluster(&empty[sb % kStages], ((sb / kStages) - 1) & 1);
         issue(sb);
       }
-      if (!vx && s + kPD < main_slabs) dst = load_row(Wq, row, P.M, P.K, (s + kPD) * kKS);
-    };
-    issue(0);
-    if (nslab > 1) issue(1);
-    RowSlab rs[kPD + 1];
-#pragma unroll
-    for (int i = 0; i <= kPD; ++i) rs[i] = RowSlab{};
-    if (!vx) {
-#pragma unroll
-      for (int i = 0; i < kPD; ++i)
-        if (i < main_slabs) rs[i] = load_row(Wq, row, P.M, P.K, i * kKS);
-    }
-    for (int s = 0; s < nslab; s += kPD + 1) {
-#pragma unroll
-      for (int i = 0; i <= kPD; ++i)
-        if (s + i < nslab) step(s + i, rs[i], rs[(i + kPD) % (kPD + 1)]);
     }
   } else if (rank == 0 && lane == 0) {
     // ------------------------------------------------------------ MMA issue (leader)
@@ -384,6 +407,40 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
       umma::commit2(&empty[stage]);
     }
     umma::commit2(&done);
+  } else if (lane == 1) {
+    // ------------------------------------------------------------ code loader
+    // one 2,560-byte bulk copy per A matrix per slab from the prefill pack into
+    // the code ring, kCR slabs ahead of the dequantizing producers
+    if (!vx && P.ppk) {
+      const uint8_t* pk = P.ppk + static_cast<int64_t>(e) * P.PL.stride;
+      const int nblkM = (P.M + kTM - 1) / kTM;
+      const bool v1 = a1base < P.M, v3 = a3base < P.M;
+      const uint8_t* s1 = pk + (P.mode == kDown ? P.PL.w2 : P.PL.w1) +
+                          static_cast<int64_t>(min(a1base / kTM, nblkM - 1)) * main_slabs * kCB;
+      const uint8_t* s3 = pk + (P.mode == kDown ? P.PL.w2 : P.PL.w3) +
+                          static_cast<int64_t>(min(a3base / kTM, nblkM - 1)) * main_slabs * kCB;
+      const uint32_t ring0 = umma::smem_u32(sm) + kStages * kStageBytes;
+      for (int s = 0; s < main_slabs; ++s) {
+        const int slot = s % kCR;
+        if (s >= kCR) umma::bar_wait(&rempty[slot], ((s / kCR) - 1) & 1);
+        const uint32_t bar = umma::smem_u32(&rfull[slot]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((v1 ? kCB : 0) + (v3 ? kCB : 0))
+                     : "memory");
+        const uint32_t dst = ring0 + slot * 2 * kCB;
+        if (v1)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+              "l"(s1 + static_cast<int64_t>(s) * kCB), "n"(kCB), "r"(bar)
+              : "memory");
+        if (v3)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  dst + kCB),
+              "l"(s3 + static_cast<int64_t>(s) * kCB), "n"(kCB), "r"(bar)
+              : "memory");
+      }
+    }
   } else if (rank == 1 && lane == 0) {
     // ------------------------------------------------------------ forwarder (peer)
     // one cluster-scope release per stage: the peer's stage is complete ->
@@ -481,8 +538,16 @@ lrc_status build_prefill_lr(const lrc_expert& e, int hidden, int ffn, int maxr, 
   return LRC_OK;
 }
 
-lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp, uint16_t* tb, cudaStream_t st,
-                          int* launches) {
+int64_t prefill_pack_bytes(int hidden, int ffn) { return ppack_layout(hidden, ffn).stride; }
+
+lrc_status build_prefill_pack(const lrc_expert& e, int hidden, int ffn, uint8_t* out, cudaStream_t st) {
+  build_ppack_kernel<<<592, 256, 0, st>>>(e, hidden, ffn, ppack_layout(hidden, ffn), out);
+  LRC_CHECK_LAUNCH();
+  return LRC_OK;
+}
+
+lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp, uint16_t* tb,
+                          const uint8_t* ppk, cudaStream_t st, int* launches) {
   static bool attr = false;
   if (!attr) {
     LRC_CUDA_TRY(cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
@@ -490,6 +555,8 @@ lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp
   }
   PrefillArgs P{};
   P.a = a;
+  P.ppk = ppk;
+  P.PL = ppack_layout(a.hidden, a.ffn);
   const int R = lrp ? a.maxr : 0;
   if (R) {
     P.lrp = lrp;
