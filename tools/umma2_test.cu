@@ -54,7 +54,7 @@ __device__ bool wait_bar(uint64_t* bar, uint32_t parity) {
 }
 
 __global__ void __cluster_dims__(2, 1, 1) umma2_kernel(const __nv_bfloat16* A, const __nv_bfloat16* B, float* D,
-                                                       int* status) {
+                                                       int* status, long long* timing) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* sa = sm;               // 2 slabs x 16 KB (this CTA's 128 rows of A)
   uint8_t* sb = sm + 2 * MH * 128;  // 2 slabs x 16 KB (this CTA's 128 rows of B)
@@ -78,7 +78,7 @@ __global__ void __cluster_dims__(2, 1, 1) umma2_kernel(const __nv_bfloat16* A, c
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "n"(N));
+                 "n"(2 * N));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -116,7 +116,36 @@ __global__ void __cluster_dims__(2, 1, 1) umma2_kernel(const __nv_bfloat16* A, c
           : "memory");
     }
   }
-  if (!wait_bar(&done, 0)) {
+  bool ok_done = wait_bar(&done, 0);
+  if (ok_done && rank == 0 && tid == 0 && timing != nullptr) {
+    // throughput: ITERS x 8 back-to-back MMAs (M=256, N=256, K=16 each) on resident operands
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t idesc = idesc_bf16(M, N);
+    long long t0 = clock64();
+    for (int it = 0; it < 512; ++it) {
+      for (int ks = 0; ks < K / 16; ++ks) {
+        const int slab = ks / 4, kk = ks % 4;
+        const uint64_t da = sdesc(smem_u32(sa + slab * MH * 128) + kk * 32);
+        const uint64_t db = sdesc(smem_u32(sb + slab * NH * 128) + kk * 32);
+        asm volatile(
+            "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;}" ::"r"(tmem + 256),
+            "l"(da), "l"(db), "r"(idesc), "r"(1u));
+      }
+    }
+    const uint16_t mask = 3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(&done)),
+        "h"(mask)
+        : "memory");
+    wait_bar(&done, 1);
+    long long t1 = clock64();
+    timing[0] = t1 - t0;
+  }
+  if (ok_done && rank == 1 && tid == 0 && timing != nullptr) wait_bar(&done, 1);
+  __syncthreads();
+  if (!ok_done) {
     if (tid == 0) atomicExch(status, 2);
   } else {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -139,7 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) umma2_kernel(const __nv_bfloat16* A, c
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   cluster_sync();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(N));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * N));
   if (tid == 0) atomicAdd(status + 1, 1);
 }
 
@@ -168,8 +197,15 @@ int main() {
   cudaMemcpy(db, hb.data(), N * K * 2, cudaMemcpyHostToDevice);
   const int smem = 2 * MH * 128 + 2 * NH * 128 + 1024;
   cudaFuncSetAttribute(umma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  umma2_kernel<<<2, 128, smem>>>(da, db, dd, st);
+  long long* dt;
+  cudaMalloc(&dt, 8);
+  cudaMemset(dt, 0, 8);
+  umma2_kernel<<<2, 128, smem>>>(da, db, dd, st, dt);
   cudaError_t e = cudaDeviceSynchronize();
+  long long ht = 0;
+  cudaMemcpy(&ht, dt, 8, cudaMemcpyDeviceToHost);
+  printf("timing: 512 x 8 MMAs (M256 N256 K16, SS, cta_group::2): %lld cycles = %.1f cycles/MMA (ideal 128)\n", ht,
+         ht / 4096.0);
   int hs[2] = {0, 0};
   cudaMemcpy(hs, st, 8, cudaMemcpyDeviceToHost);
   std::vector<float> hd(M * N);
