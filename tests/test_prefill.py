@@ -170,3 +170,24 @@ def test_parallel_plan_matches_serial_plan(torch, prefill):
     assert np.array_equal(ib, np.concatenate([i1, i2]))
     ys = np.concatenate([y1, y2])
     assert max(rel_l2(yb[t], ys[t]) for t in range(B)) <= 1e-3
+
+
+def test_pairs_mode_prefill_matches_decode(torch):
+    """Expert-parallel receive side (lrc_layer_forward_pairs: routing given per
+    row, k = 1, per-row compensation flag) on the prefill path (B >= 128) vs the
+    decode kernels."""
+    from paper_2512_17073_b200.synth import SynthLayer
+
+    B = 400
+    sl = SynthLayer(512, 1024, 8, top_k=2, rank=16, seed=13, max_tokens=B)
+    g = torch.Generator(device="cpu").manual_seed(3)
+    xs = torch.randn((B, 512), device="cuda").to(torch.bfloat16)
+    ex = torch.randint(0, 8, (B,), generator=g, dtype=torch.int32)
+    w = torch.rand((B,), generator=g)
+    comp = (torch.rand((B,), generator=g) < 0.5).to(torch.uint8)
+    sl.layer.set_prefill_min(1)
+    yp = sl.layer.forward_pairs(xs, ex, w, comp).double().cpu().numpy()
+    sl.layer.set_prefill_min(0)
+    yd = sl.layer.forward_pairs(xs, ex, w, comp).double().cpu().numpy()
+    assert np.abs(yd).max() > 0
+    assert max(rel_l2(yp[t], yd[t]) for t in range(B)) <= TOL_Y
