@@ -104,6 +104,10 @@ class OffloadEngine:
         self.copy_stream = torch.cuda.Stream()
         self.keep = _Keep()
         self.stats = {"hits": 0, "misses": 0, "bytes": 0}
+        # routing read-back: pinned buffer + event polled by the host (a blocking
+        # pageable .cpu() sync showed 10-600 ms host stalls on the B200 boxes)
+        self._idx_host = torch.empty((max_tokens * max(top_k, 1),), dtype=torch.int32).pin_memory()
+        self._idx_ev = torch.cuda.Event()
         # shared placeholders for the descriptor fields the tiled path never reads
         self._zw13 = _zero_qmat(ffn, hidden, self.keep)
         self._zw2 = _zero_qmat(hidden, ffn, self.keep)
@@ -200,7 +204,13 @@ class OffloadEngine:
     def forward_layer(self, layer: int, x):
         """x (B, hidden) bf16 cuda -> y (B, hidden) f32 of layer ``layer``."""
         torch = _lib.device_required()
-        need = sorted(set(self.route(layer, x).cpu().reshape(-1).tolist()))
+        idx = self.route(layer, x).reshape(-1)
+        host = self._idx_host[:idx.numel()]
+        host.copy_(idx, non_blocking=True)
+        self._idx_ev.record(torch.cuda.current_stream())
+        while not self._idx_ev.query():  # poll (no blocking driver wait)
+            pass
+        need = sorted(set(host.tolist()))
         if need and (need[0] < 0 or need[-1] >= self.E):
             raise ValueError("offload: the router selected no valid expert (non-finite input?)")
         keys = {(layer, e) for e in need}
