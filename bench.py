@@ -336,6 +336,11 @@ def run_ours(args, world, rank):
     prefill = None
     if args.prefill and rank == 0:
         prefill = prefill_point(tf_burst, tf_sust)
+    # C3 offload (BASELINE configs[2], the north-star target): 32 layers, every
+    # expert in pinned host memory, fetched on demand
+    offl = None
+    if args.offload and rank == 0:
+        offl = offload_point()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -360,6 +365,7 @@ def run_ours(args, world, rank):
         "clocks": clk.summary(),
         "sweep": sweep,
         "prefill": prefill,
+        "offload": offl,
         "cpu_baseline": cpu,
     }
     if rank == 0:
@@ -437,6 +443,71 @@ def prefill_point(tf_burst, tf_sust, B=16384, iters=3):
                         "tflops": round(tf, 1), "frac_sustained": round(tf / tf_sust, 4),
                         "frac_burst": round(tf / tf_burst, 4), "launches": sl.layer.last_launches()}
     del sl
+    torch.cuda.empty_cache()
+    return out
+
+
+def offload_point(layers=32, tokens=8, repeats=5, slots=2):
+    """C3: Mixtral-8x7B 32-layer decode (B=1) with every expert (INT2 T2 tiles +
+    rank-32 LR tiles + V factors) in pinned host memory, fetched on demand by
+    the offload engine into `slots` GPU slots; host-link roofline = bytes moved
+    per token / the pinned H2D copy bandwidth measured here.  Median of repeats
+    (host-side launch stalls make single repeats noisy, see DESIGN 6b)."""
+    import time
+
+    import torch
+
+    from paper_2512_17073_b200 import offload
+    from paper_2512_17073_b200.synth import SynthLayer
+
+    t0 = time.time()
+    gates, host = [], []
+    for l in range(layers):
+        sl = SynthLayer(HIDDEN, FFN, E, top_k=TOPK, bits=BITS, rank=RANK, seed=900 + l, max_tokens=8)
+        gates.append(sl.gate)
+        host.append(offload.host_experts_from_synth(sl))
+        del sl
+        torch.cuda.empty_cache()
+    build_s = time.time() - t0
+    nb = 1 << 30
+    src = torch.empty((nb,), dtype=torch.uint8).pin_memory()
+    dst = torch.empty((nb,), dtype=torch.uint8, device="cuda")
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        dst.copy_(src, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    h2d = 5 * nb / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del src, dst
+    eng = offload.OffloadEngine(gates, host, HIDDEN, FFN, top_k=TOPK, top_n=TOPN, n_slots=slots, max_tokens=8)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn((1, HIDDEN), device="cuda", generator=gen).to(torch.bfloat16)
+    for _ in range(2):
+        x = eng.forward(x, normalize=True)
+    torch.cuda.synchronize()
+    runs = []
+    for _ in range(repeats):
+        for k in eng.stats:
+            eng.stats[k] = 0
+        t1 = time.perf_counter()
+        for _ in range(tokens):
+            x = eng.forward(x, normalize=True)
+        torch.cuda.synchronize()
+        runs.append((time.perf_counter() - t1, dict(eng.stats)))
+    order = sorted(runs, key=lambda r: r[0])
+    dt, stats = order[len(order) // 2]
+    gbs = stats["bytes"] / dt / 1e9
+    out = {"metric": "offloaded decode tokens/s (C3: 32 layers, all experts in pinned host memory)",
+           "value": round(tokens / dt, 3), "unit": "tokens/s", "layers": layers, "batch": 1, "gpu_slots": slots,
+           "host_bytes_per_token": int(stats["bytes"] / tokens), "h2d_achieved_gbs": round(gbs, 2),
+           "h2d_peak_gbs": round(h2d, 2), "roofline_frac": round(gbs / h2d, 4),
+           "runs_tok_s": [round(tokens / r[0], 2) for r in runs], "pool_gb": round(
+               sum(he.nbytes for lay in host for he in lay) / 1e9, 2), "build_s": round(build_s, 1),
+           "timing": "host wall clock around `tokens` decode steps + synchronize, median of repeats"}
+    del eng, host
     torch.cuda.empty_cache()
     return out
 
@@ -534,6 +605,7 @@ def main():
     ap.add_argument("--no-sweep", dest="sweep", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", dest="prefill", action="store_false")
+    ap.add_argument("--no-offload", dest="offload", action="store_false")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = 2000 if args.impl == "ours" else 5
