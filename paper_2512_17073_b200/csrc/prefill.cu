@@ -11,16 +11,21 @@
 //          -> SwiGLU in the epilogue -> bf16 activations a16[pair][ffn];
 //   down : W2 rows [m0, m0+256) and [m0+256, m0+512) x the pairs' a16 rows
 //          -> y[token] += w_pair * (.) with fp32 reductions.
-// Roles per CTA (288 threads, one CTA per SM: 193 KB smem, 512 TMEM columns):
+// Roles per CTA (288 threads, one CTA per SM: 223 KB smem, 512 TMEM columns):
 //   warps 0-7  producers: thread t dequantizes row t&127 of matrix t>>7 (c*s+z
-//              in fp32, rounded once to bf16; codes and metadata prefetched four
-//              slabs ahead) straight into SWIZZLE_128B smem, gathers its share
-//              of the CTA's 128 B rows with cp.async two slabs ahead (zero-filled
-//              past the expert's pairs) and release-arrives on the LEADER's
-//              stage barrier; after the K loop, the epilogue from its own TMEM.
-//   warp 8     (leader CTA) one thread issues tcgen05.mma.cta_group::2
-//              (M=256, N=256, K=16) into the two fp32 accumulators and commits
-//              each stage back to both CTAs (multicast; 4-stage ring).
+//              in fp32, rounded once to bf16) from the code ring straight into
+//              SWIZZLE_128B smem, gathers its share of the CTA's 128 B rows
+//              with cp.async two slabs ahead (zero-filled past the expert's
+//              pairs) and arrives on its CTA's stage barrier; after the K loop,
+//              the epilogue from its own TMEM.
+//   warp 8.1   loader: one cp.async.bulk per A matrix per slab copies the
+//              codes + fp16 scale/zero of the CTA's rows (prefill pack) into a
+//              6-deep code ring.
+//   warp 8.0   leader: issues tcgen05.mma.cta_group::2 (M=256, N=256, K=16)
+//              into the two fp32 accumulators and commits each stage back to
+//              both CTAs (multicast; 4-stage ring).  Peer: forwards each
+//              completed stage to the leader's barrier (one cluster-scope
+//              release per stage).
 // The pair halves each SM's share of the B operand (gather and smem reads).
 // The low-rank term is K augmentation: extra slabs whose A rows hold the U
 // factors (up: [U1 | 0] for W1 rows, [0 | U3] for W3 rows; down: U2) and whose
@@ -30,7 +35,8 @@
 // the V factors (modes kVxUp / kVxDown, one accumulator) for the tiles that
 // hold a compensated pair.  Factors are repacked once per expert into bf16
 // rows (the "LR pack", build_prefill_lr) so every low-rank slab is a plain
-// cp.async row copy issued two slabs ahead like B.
+// cp.async row copy issued two slabs ahead like B.  The up epilogue stages the
+// bf16 activations pair-major in the idle stage memory and writes 16-byte rows.
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -461,21 +467,27 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
     const uint32_t lbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const int ra = a1base + q * 32 + lane, rb = a3base + q * 32 + lane;
     const int cend = min(nvalid, (half + 1) * (kTN / 2));
+    // up: activations staged pair-major in the (now idle) stage memory, then
+    // written out as 16-byte rows (coalesced) instead of 2-byte scattered stores
+    uint16_t* stg = reinterpret_cast<uint16_t*>(sm);  // [kTN pairs][kTM rows] bf16
     for (int c0 = half * (kTN / 2); c0 < cend; c0 += 32) {
       float h1[32], h3[32];
-      umma::tmem_ld32(lbase + c0, h1);
-      if (!vx) umma::tmem_ld32(lbase + kTN + c0, h3);
-      if (P.mode == kUp) {
-        if (ra < P.M) {
+      {
+        uint32_t r1[32], r3[32];
+        umma::tmem_ld32_nowait(lbase + c0, r1);
+        if (!vx) umma::tmem_ld32_nowait(lbase + kTN + c0, r3);
+        umma::tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int n = c0 + j;
-            if (n < nvalid) {
-              const float g = h1[j];
-              a.a16[static_cast<int64_t>(s_pair[n]) * a.ffn + ra] =
-                  f2bf(__fdividef(g, 1.0f + __expf(-g)) * h3[j]);
-            }
-          }
+        for (int j = 0; j < 32; ++j) {
+          h1[j] = __uint_as_float(r1[j]);
+          h3[j] = vx ? 0.0f : __uint_as_float(r3[j]);
+        }
+      }
+      if (P.mode == kUp) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float g = h1[j];
+          stg[(c0 + j) * kTM + q * 32 + lane] = f2bf(__fdividef(g, 1.0f + __expf(-g)) * h3[j]);
         }
       } else if (P.mode == kDown) {
 #pragma unroll
@@ -497,6 +509,21 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
             const int p = s_pair[n];
             P.tb[static_cast<int64_t>(p) * P.WT + ra] = a.plan.pair_comp[p] >= 0 ? f2bf(h1[j]) : 0;
           }
+        }
+      }
+    }
+    if (P.mode == kUp) {
+      asm volatile("bar.sync 1, %0;" ::"n"(kProd) : "memory");  // producers only
+      const int r0 = a1base;  // this CTA's rows [r0, r0 + 128)
+      for (int i = tid; i < nvalid * (kTM / 8); i += kProd) {
+        const int n = i / (kTM / 8), c = i % (kTM / 8);
+        const int row = r0 + 8 * c;
+        uint16_t* dst = a.a16 + static_cast<int64_t>(s_pair[n]) * a.ffn + row;
+        const uint16_t* src = stg + n * kTM + 8 * c;
+        if (row + 8 <= P.M) {
+          *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+        } else {
+          for (int k = 0; k < 8 && row + k < P.M; ++k) dst[k] = src[k];
         }
       }
     }
