@@ -248,10 +248,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
 
   // blockIdx.y -> (active expert, block of kTN of its pairs), identical in both
   // CTAs of the pair; the grid is an upper bound, surplus pairs leave at once
-  int yb = blockIdx.y, ai = -1;
+  // (the per-expert pair counts are loaded in parallel: a scan over global
+  // loads would be one dependent L2 round trip per active expert)
+  __shared__ int s_cnt[LRC_MAX_EXPERTS];
   const int na = a.plan.counts[0];
+  for (int i = tid; i < na; i += kThreads) s_cnt[i] = a.plan.active_cnt[i];
+  __syncthreads();
+  int yb = blockIdx.y, ai = -1;
   for (int i = 0; i < na; ++i) {
-    const int nt = (a.plan.active_cnt[i] + kTN - 1) / kTN;
+    const int nt = (s_cnt[i] + kTN - 1) / kTN;
     if (yb < nt) {
       ai = i;
       break;
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
   if (ai < 0) return;
   const int e = a.plan.active[ai];
   const int off = a.plan.active_off[ai] + yb * kTN;
-  const int nvalid = min(kTN, a.plan.active_cnt[ai] - yb * kTN);
+  const int nvalid = min(kTN, s_cnt[ai] - yb * kTN);
   // rows of this CTA's A1 / A3 operands (row of TMEM lane l = base + l)
   const int tile = blockIdx.x >> 1;
   const int a1base = tile * (P.mode == kDown ? 4 * kTM : 2 * kTM) + rank * kTM;
