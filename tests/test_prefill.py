@@ -191,3 +191,27 @@ def test_pairs_mode_prefill_matches_decode(torch):
     yd = sl.layer.forward_pairs(xs, ex, w, comp).double().cpu().numpy()
     assert np.abs(yd).max() > 0
     assert max(rel_l2(yp[t], yd[t]) for t in range(B)) <= TOL_Y
+
+
+def test_deepseek_shape_prefill(torch):
+    """C5 shape (64 experts top-8, top-2 restore, d=2048, ffn=11008 = 43 x 256)
+    on the prefill path: many small per-expert tiles; vs the decode path and
+    the oracle."""
+    from paper_2512_17073_b200.synth import SynthLayer
+
+    B = 300
+    sl = SynthLayer(2048, 11008, 64, top_k=8, rank=32, seed=2, max_tokens=B)
+    assert sl.layer.prefill_eligible
+    xs = lrc.to_bf16(np.random.default_rng(5).standard_normal((B, 2048)))
+    xb = torch.from_numpy(xs).cuda().to(torch.bfloat16)
+    sl.layer.set_prefill_min(1)
+    yp, ip, _ = sl.layer.forward(xb, top_k=8, top_n=2)
+    sl.layer.set_prefill_min(0)
+    yd, idd, _ = sl.layer.forward(xb, top_k=8, top_n=2)
+    yp, yd, ip = yp.double().cpu().numpy(), yd.double().cpu().numpy(), ip.cpu().numpy()
+    assert np.array_equal(ip, idd.cpu().numpy())
+    assert max(rel_l2(yp[t], yd[t]) for t in range(B)) <= TOL_Y
+    st = bridge.synth_store(sl, sorted({int(e) for t in (0, B - 1) for e in ip[t]}))
+    for t in (0, B - 1):
+        yo = lrc.forward(xs[t], sl.gate, None, 8, 2, "compensated", st)
+        assert rel_l2(yp[t], yo) <= TOL_Y, rel_l2(yp[t], yo)
