@@ -146,7 +146,11 @@ lrc_status lrc_layer_set_expert_async(lrc_layer* layer, int expert_id, const lrc
  * low-rank term U.(V.x) applied inside the expert kernels for each token's
  * top_n experts only (never materialising Q(W)+UV).  top_n == 0 gives mode
  * "quantized".  x (B, hidden) bf16; y (B, hidden) f32.  topk_idx / topk_w
- * (B, top_k) may be NULL.  compensate_shared as ForwardConfig. */
+ * (B, top_k) may be NULL.  compensate_shared as ForwardConfig.
+ * Execution: B below the prefill threshold (default 128) runs the decode
+ * kernels (router + tiled up/down, 3 PDL-chained launches, graph-capturable);
+ * B at or above it runs the tcgen05 grouped dequant-GEMM path (router, parallel
+ * plan, V.x / up / V2.a / down GEMMs) when the layer is eligible. */
 lrc_status lrc_layer_forward(lrc_layer* layer, const uint16_t* x, int64_t B, int top_k,
                              int top_n, int renormalize, int compensate_shared, float* y,
                              int32_t* topk_idx, float* topk_w, void* stream);
