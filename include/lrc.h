@@ -186,6 +186,16 @@ lrc_status lrc_layer_set_profiling(lrc_layer* layer, int enabled);
  * ffn multiples of 64); min_tokens <= 0 disables it.  Default 128 (env
  * LRC_PREFILL_MIN). */
 lrc_status lrc_layer_set_prefill_min(lrc_layer* layer, int64_t min_tokens);
+/* GPU-driven expert paging (offload without a host round trip): every expert
+ * is one block in device-mapped pinned host memory (host_blocks: E+S pointers);
+ * offsets[10] = byte offsets in a block of the up tiles, down tiles, up LR
+ * tiles, down LR tiles, V1 packed/scales/zeros, V3 packed/scales/zeros (-1 =
+ * absent).  Each forward then copies the step's active experts into slots
+ * (slot a = the a-th active expert; n_slots must cover the distinct experts a
+ * step can select) inside the stream, repoints their descriptors, and runs the
+ * tiled decode kernels; no host synchronisation, graph-capturable. */
+lrc_status lrc_layer_set_pager(lrc_layer* layer, const void* const* host_blocks, const int64_t* offsets,
+                               int64_t block_bytes, uint8_t* slots, int n_slots, int64_t slot_bytes);
 int lrc_layer_prefill_eligible(const lrc_layer* layer);
 lrc_status lrc_layer_phase_ms(lrc_layer* layer, float* ms4);
 /* Debug: %globaltimer (ns) stamps, 8 per CTA, of the last launch of the router

@@ -223,6 +223,71 @@ lrc_status launch_lr_down(const ExpertArgs& a, int np_bound, cudaStream_t st) {
 
 }  // namespace lrc
 
+namespace lrc {
+// ------------------------------------------------- GPU-driven expert paging ---
+// Offload mode (north-star 4) without a host round trip: after the router's
+// plan, one launch copies every active expert's block from device-mapped
+// pinned host memory into slot a (a = its active index) with 16-byte loads
+// across all SMs, then repoints the expert's descriptor and its ActiveRec at
+// the slot.  Section order of a block (offsets in PagerArgs.off, -1 absent):
+// up tiles, down tiles, up LR tiles, down LR tiles, V1 packed/scales/zeros,
+// V3 packed/scales/zeros.
+struct PagerArgs {
+  const uint8_t* const* host;  // [E+S] device-visible block pointers
+  int64_t off[10];
+  int64_t bytes;               // block bytes (multiple of 16)
+  uint8_t* slots;
+  int64_t slot_bytes;
+  lrc_expert* experts;  // device table
+  PlanArgs plan;
+};
+
+__global__ void __launch_bounds__(256) pager_kernel(const PagerArgs g) {
+  const int a = blockIdx.y;
+  if (a >= g.plan.counts[0]) return;
+  const int e = g.plan.active[a];
+  const uint4* src = reinterpret_cast<const uint4*>(g.host[e]);
+  uint4* dst = reinterpret_cast<uint4*>(g.slots + static_cast<int64_t>(a) * g.slot_bytes);
+  const int64_t n = g.bytes / 16, stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {  // 4 loads in flight per thread (PCIe latency)
+    const uint4 v0 = src[i], v1 = src[i + stride], v2 = src[i + 2 * stride], v3 = src[i + 3 * stride];
+    dst[i] = v0;
+    dst[i + stride] = v1;
+    dst[i + 2 * stride] = v2;
+    dst[i + 3 * stride] = v3;
+  }
+  for (; i < n; i += stride) dst[i] = src[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint8_t* base = g.slots + static_cast<int64_t>(a) * g.slot_bytes;
+    auto at = [&](int k) -> const uint8_t* { return g.off[k] >= 0 ? base + g.off[k] : nullptr; };
+    lrc_expert d = g.experts[e];
+    d.up_tiles = at(0);
+    d.down_tiles = at(1);
+    d.up_lr_tiles = at(2);
+    d.down_lr_tiles = at(3);
+    if (g.off[4] >= 0) {
+      d.v1.packed = at(4);
+      d.v1.scales = reinterpret_cast<const uint16_t*>(at(5));
+      d.v1.zeros = reinterpret_cast<const uint16_t*>(at(6));
+    }
+    if (g.off[7] >= 0) {
+      d.v3.packed = at(7);
+      d.v3.scales = reinterpret_cast<const uint16_t*>(at(8));
+      d.v3.zeros = reinterpret_cast<const uint16_t*>(at(9));
+    }
+    g.experts[e] = d;
+    if (g.plan.arec != nullptr) {
+      ActiveRec& R = g.plan.arec[a];
+      R.up_tiles = d.up_tiles;
+      R.down_tiles = d.down_tiles;
+      R.up_lr_tiles = d.up_lr_tiles;
+      R.down_lr_tiles = d.down_lr_tiles;
+    }
+  }
+}
+}  // namespace lrc
+
 // =========================================================== layer object ===
 using namespace lrc;
 
@@ -235,6 +300,10 @@ struct lrc_layer {
   uint8_t* ppk = nullptr;      // per-expert prefill packs of the weight codes (built lazily)
   std::vector<uint8_t> lrp_dirty;  // per expert: packs stale (expert replaced)
   uint16_t* tb = nullptr;      // prefill V.x rows [max_pairs][tb_width] bf16
+  bool pager = false;          // GPU-driven expert paging (lrc_layer_set_pager)
+  PagerArgs pg{};
+  const uint8_t** pg_host = nullptr;  // device copy of the block pointers
+  int pg_slots = 0;
   int* plan_blk = nullptr;     // parallel plan: per-chunk histograms
   uint32_t* plan_cmask = nullptr;
   int* plan_ticket = nullptr;
@@ -453,6 +522,7 @@ extern "C" void lrc_layer_destroy(lrc_layer* L) {
   if (L->h_stage) cudaFreeHost(L->h_stage);
   cudaFree(L->ws);
   cudaFree(L->lrp);
+  cudaFree(L->pg_host);
   cudaFree(L->ppk);
   for (auto& e : L->ev)
     if (e) cudaEventDestroy(e);
@@ -496,6 +566,27 @@ extern "C" lrc_status lrc_layer_set_expert_async(lrc_layer* L, int expert_id, co
                                as_stream(stream)));
   if (!L->lrp_dirty.empty()) L->lrp_dirty[expert_id] = 1;
   refresh_tiled(L);
+  return LRC_OK;
+}
+
+extern "C" lrc_status lrc_layer_set_pager(lrc_layer* L, const void* const* host_blocks, const int64_t* offsets,
+                                          int64_t block_bytes, uint8_t* slots, int n_slots, int64_t slot_bytes) {
+  if (!L || !host_blocks || !offsets || !slots || n_slots <= 0 || block_bytes <= 0 || block_bytes % 16 ||
+      slot_bytes < block_bytes || slot_bytes % 16)
+    return fail(LRC_ERR_INVALID, "set_pager: bad arguments");
+  if (!L->tiled) return fail(LRC_ERR_UNSUPPORTED, "set_pager: needs the tiled decode layout");
+  const int NE = L->E + L->S;
+  if (L->pg_host == nullptr) LRC_CUDA_TRY(cudaMalloc(&L->pg_host, sizeof(uint8_t*) * NE));
+  LRC_CUDA_TRY(cudaMemcpy(L->pg_host, host_blocks, sizeof(uint8_t*) * NE, cudaMemcpyHostToDevice));
+  PagerArgs& g = L->pg;
+  g.host = L->pg_host;
+  for (int k = 0; k < 10; ++k) g.off[k] = offsets[k];
+  g.bytes = block_bytes;
+  g.slots = slots;
+  g.slot_bytes = slot_bytes;
+  g.experts = L->d_experts;
+  L->pg_slots = n_slots;
+  L->pager = true;
   return LRC_OK;
 }
 
@@ -551,7 +642,8 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   ra.plan = plan;
   // one prologue launch: gate GEMV + softmax/top-k + plan, zeroing of y and the
   // t2 accumulators, and (one token tile) the speculative low-rank V.x
-  const bool spec = L->maxr > 0 && B <= route_tiles(1) * 8 && route_tiles(B) == 1;
+  // (pager mode: the experts' V factors arrive after the router, so no speculative V.x)
+  const bool spec = !L->pager && L->maxr > 0 && B <= route_tiles(1) * 8 && route_tiles(B) == 1;
   ra.experts = L->d_experts;
   ra.t = L->t;
   ra.ne = L->E + L->S;
@@ -579,6 +671,13 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
                                   L->plan_ticket, st)) != LRC_OK)
       return s;
     launches += 2;
+  }
+  if (L->pager) {  // copy the active experts into their slots, repoint descriptors
+    PagerArgs g = L->pg;
+    g.plan = plan;
+    pager_kernel<<<dim3(static_cast<unsigned>(2 * L->num_sms), static_cast<unsigned>(L->pg_slots)), 256, 0, st>>>(g);
+    LRC_CHECK_LAUNCH();
+    ++launches;
   }
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[1], st));
   ExpertArgs a{};

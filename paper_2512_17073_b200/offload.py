@@ -242,3 +242,69 @@ class OffloadEngine:
                 y = y * torch.rsqrt(y.pow(2).mean(dim=-1, keepdim=True) + 1e-6)
             x = y.to(torch.bfloat16)
         return x
+
+
+class GpuPagerEngine(OffloadEngine):
+    """Offload with GPU-driven paging (``lrc_layer_set_pager``): every expert is
+    one block of device-mapped pinned host memory (sections in ``NAMES`` order
+    at fixed offsets); each layer forward copies its active experts into slots
+    inside the stream (SM loads over the host link) and repoints their
+    descriptors -- no host round trip per layer, so a token's whole layer chain
+    is asynchronous and graph-capturable.  No cross-token cache: slot a holds
+    the a-th active expert of the current step (the C3 "cache budget 0" case).
+    """
+
+    def __init__(self, gates, experts, hidden: int, ffn: int, top_k: int, top_n: int, max_tokens: int = 1):
+        torch = _lib.device_required()
+        self.hidden, self.ffn, self.k, self.n = hidden, ffn, top_k, top_n
+        self.E = len(experts[0])
+        self.host = experts
+        self.keep = _Keep()
+        n_slots = min(self.E, max_tokens * max(top_k, 1))
+        size = {n: max(int(he.bufs[n].numel()) for lay in experts for he in lay) for n in NAMES}
+        self.offsets, o = {}, 0
+        for n in NAMES:
+            self.offsets[n] = o if size[n] else -1
+            o += (size[n] + 255) // 256 * 256
+        self.block_bytes = max(o, 256)
+        self.slot_mem = self.keep.add(torch.zeros((n_slots, self.block_bytes), dtype=torch.uint8, device="cuda"))
+        self.slots = [{n: self.slot_mem[s, max(self.offsets[n], 0):max(self.offsets[n], 0) + max(size[n], 1)]
+                       for n in NAMES} for s in range(n_slots)]
+        # one pinned block per (layer, expert); UVA: the host pointer is device-visible
+        self.blocks = []
+        for lay in experts:
+            row = []
+            for he in lay:
+                blk = torch.zeros((self.block_bytes,), dtype=torch.uint8).pin_memory()
+                for n in NAMES:
+                    t = he.bufs[n]
+                    if t.numel():
+                        blk[self.offsets[n]:self.offsets[n] + t.numel()].copy_(t)
+                row.append(blk)
+            self.blocks.append(row)
+        self.stats = {"bytes": 0, "steps": 0}
+        self._zw13 = _zero_qmat(ffn, hidden, self.keep)
+        self._zw2 = _zero_qmat(hidden, ffn, self.keep)
+        self._zfac = {}
+        offs = (ctypes.c_int64 * 10)(*[self.offsets[n] for n in NAMES])
+        self.layers = []
+        for l, gate in enumerate(gates):
+            descs = [self._desc(l, e, 0) for e in range(self.E)]
+            dl = LRCMoELayer(gate, descs, hidden, ffn, self.E, 0, self.keep, max_tokens=max_tokens, top_k=top_k)
+            ptrs = (ctypes.c_void_p * self.E)(*[b.data_ptr() for b in self.blocks[l]])
+            _lib.check(_lib.lib().lrc_layer_set_pager(dl._handle, ptrs, offs, self.block_bytes,
+                                                      ctypes.c_void_p(self.slot_mem.data_ptr()), n_slots,
+                                                      self.block_bytes))
+            self.layers.append(dl)
+
+    def forward_layer(self, layer: int, x):
+        y, _, _ = self.layers[layer].forward(x, self.k, self.n)
+        self.stats["steps"] += 1
+        return y
+
+    def bytes_per_step(self, distinct_experts: int) -> int:
+        """Host-link bytes of one layer step that selects ``distinct_experts``."""
+        return distinct_experts * self.block_bytes
+
+
+__all__ = ["HostExpert", "OffloadEngine", "GpuPagerEngine", "host_experts_from_synth", "NAMES"]

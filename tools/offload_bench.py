@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--ffn", type=int, default=14336)
     ap.add_argument("--repeats", type=int, default=3)
+    ap.add_argument("--pager", action="store_true", help="GPU-driven paging (GpuPagerEngine)")
     args = ap.parse_args()
     t0 = time.time()
     gates, host = [], []
@@ -53,8 +54,11 @@ def main():
         torch.cuda.empty_cache()
     build_s = time.time() - t0
     peak = h2d_peak()
-    eng = offload.OffloadEngine(gates, host, args.hidden, args.ffn, top_k=2, top_n=1,
-                                n_slots=args.slots, max_tokens=8)
+    if args.pager:
+        eng = offload.GpuPagerEngine(gates, host, args.hidden, args.ffn, top_k=2, top_n=1, max_tokens=1)
+    else:
+        eng = offload.OffloadEngine(gates, host, args.hidden, args.ffn, top_k=2, top_n=1,
+                                    n_slots=args.slots, max_tokens=8)
     gen = torch.Generator(device="cuda").manual_seed(0)
     x = torch.randn((1, args.hidden), device="cuda", generator=gen).to(torch.bfloat16)
     for _ in range(args.warmup):
@@ -68,7 +72,10 @@ def main():
         for _ in range(args.tokens):
             x = eng.forward(x, normalize=True)
         torch.cuda.synchronize()
-        runs.append((time.perf_counter() - t1, dict(eng.stats)))
+        st = dict(eng.stats)
+        if args.pager:  # B=1, top-2: two distinct experts per layer step, whole blocks copied
+            st["bytes"] = args.tokens * args.layers * eng.bytes_per_step(2)
+        runs.append((time.perf_counter() - t1, st))
     runs.sort(key=lambda r: r[0])
     dt, stats = runs[len(runs) // 2]
     eng.stats = stats
@@ -78,7 +85,8 @@ def main():
         "metric": "offloaded decode tokens/s (C3: all experts in pinned host memory)",
         "value": round(args.tokens / dt, 3), "unit": "tokens/s",
         "config": {"layers": args.layers, "experts_per_layer": 8, "top_k": 2, "top_n": 1, "bits": 2,
-                   "rank": 32, "gpu_slots": args.slots, "batch": 1},
+                   "rank": 32, "gpu_slots": 2 if args.pager else args.slots, "batch": 1,
+                   "engine": "gpu pager (in-stream copies)" if args.pager else "host-driven LRU"},
         "host_bytes_per_token": int(per_tok), "h2d_achieved_gbs": round(gbs, 2),
         "h2d_peak_gbs": round(peak, 2), "roofline_frac": round(gbs / peak, 4),
         "stats": eng.stats, "ms_per_token": round(dt / args.tokens * 1e3, 3),
