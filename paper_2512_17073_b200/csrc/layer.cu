@@ -227,8 +227,8 @@ namespace lrc {
 // ------------------------------------------------- GPU-driven expert paging ---
 // Offload mode (north-star 4) without a host round trip: after the router's
 // plan, one launch copies every active expert's block from device-mapped
-// pinned host memory into slot a (a = its active index) with 16-byte loads
-// across all SMs, then repoints the expert's descriptor and its ActiveRec at
+// pinned host memory into slot a (a = its active index) with 16-byte
+// streaming loads across all SMs (8 in flight per thread), then repoints the expert's descriptor and its ActiveRec at
 // the slot.  Section order of a block (offsets in PagerArgs.off, -1 absent):
 // up tiles, down tiles, up LR tiles, down LR tiles, V1 packed/scales/zeros,
 // V3 packed/scales/zeros.
@@ -250,12 +250,12 @@ __global__ void __launch_bounds__(256) pager_kernel(const PagerArgs g) {
   uint4* dst = reinterpret_cast<uint4*>(g.slots + static_cast<int64_t>(a) * g.slot_bytes);
   const int64_t n = g.bytes / 16, stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < n; i += 4 * stride) {  // 4 loads in flight per thread (PCIe latency)
-    const uint4 v0 = src[i], v1 = src[i + stride], v2 = src[i + 2 * stride], v3 = src[i + 3 * stride];
-    dst[i] = v0;
-    dst[i + stride] = v1;
-    dst[i + 2 * stride] = v2;
-    dst[i + 3 * stride] = v3;
+  for (; i + 7 * stride < n; i += 8 * stride) {  // 8 loads in flight per thread (host-link latency)
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcs(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) __stcs(dst + i + u * stride, v[u]);
   }
   for (; i < n; i += stride) dst[i] = src[i];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
