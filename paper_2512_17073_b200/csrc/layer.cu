@@ -228,8 +228,9 @@ namespace lrc {
 // Offload mode (north-star 4) without a host round trip: after the router's
 // plan, one launch copies every active expert's block from device-mapped
 // pinned host memory into slot a (a = its active index) with 16-byte
-// streaming loads across all SMs (8 in flight per thread), then repoints the expert's descriptor and its ActiveRec at
-// the slot.  Section order of a block (offsets in PagerArgs.off, -1 absent):
+// streaming loads across all SMs (8 in flight per thread), then repoints the
+// expert's descriptor and its ActiveRec at the slot.  Section order of a block
+// (offsets in PagerArgs.off, -1 absent):
 // up tiles, down tiles, up LR tiles, down LR tiles, V1 packed/scales/zeros,
 // V3 packed/scales/zeros.
 struct PagerArgs {
