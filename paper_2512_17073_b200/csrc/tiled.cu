@@ -534,7 +534,20 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
   // plan is two launches old (complete before the up kernel passed its own
   // wait), so its producer may start streaming W2 while the up kernel drains;
   // its consumers / epilogue wait before touching the up kernel's outputs.
-  if (threadIdx.x == 0) TSTAMP(0);
+  if (threadIdx.x == 0) {
+    TSTAMP(0);
+    // the stage barriers do not depend on the plan: initialise them before the
+    // wait (the __syncthreads after the plan loads publishes them)
+    for (int s = 0; s < P.nstage; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kNW + 1);  // consumers + the item's epilogue warp (LR slot)
+    }
+    for (int r = 0; r < kNRed; ++r) {
+      mbar_init(&rfull[r], kNW);
+      mbar_init(&rempty[r], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (UP && P.prebuilt) {
     // the router releases this grid only after the previous layer finished,
     // so x is final: build x' for all B tokens while the routing completes
@@ -570,15 +583,6 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
     const int64_t total = acc;
     s_range[0] = static_cast<int>(total * blockIdx.x / gridDim.x);
     s_range[1] = static_cast<int>(total * (blockIdx.x + 1) / gridDim.x);
-    for (int s = 0; s < P.nstage; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kNW + 1);  // consumers + the item's epilogue warp (LR slot)
-    }
-    for (int r = 0; r < kNRed; ++r) {
-      mbar_init(&rfull[r], kNW);
-      mbar_init(&rempty[r], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (threadIdx.x == 0) TSTAMP(2);
