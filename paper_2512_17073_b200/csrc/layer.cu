@@ -775,8 +775,11 @@ extern "C" lrc_status lrc_layer_forward_generic(lrc_layer* L, const uint16_t* x,
 // its predecessor (the previous call's stage-out) before completing -- so the
 // router's own wait also covers the previous y read.  stage-out: waits for the
 // down kernel, then copies y.
-__global__ void stage_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int64_t n,
-                             int in) {
+// (16-byte words when both sides are 16-byte aligned and the size allows: the
+// host side is read/written over the host link, where transaction count, not
+// bytes, sets the latency of these small copies)
+template <typename W>
+__global__ void stage_kernel(const W* __restrict__ src, W* __restrict__ dst, int64_t n, int in) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (!in) asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -787,7 +790,9 @@ __global__ void stage_kernel(const uint32_t* __restrict__ src, uint32_t* __restr
 
 static cudaError_t launch_stage(bool in, const void* src, void* dst, size_t bytes, cudaStream_t st,
                                 bool pdl) {
-  const int64_t n = static_cast<int64_t>(bytes / 4);
+  const bool v16 = bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  const int64_t n = static_cast<int64_t>(bytes / (v16 ? 16 : 4));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(32, (n + 255) / 256)));
   cfg.blockDim = dim3(256);
@@ -797,8 +802,11 @@ static cudaError_t launch_stage(bool in, const void* src, void* dst, size_t byte
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, stage_kernel, static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst),
-                            n, in ? 1 : 0);
+  if (v16)
+    return cudaLaunchKernelEx(&cfg, stage_kernel<uint4>, static_cast<const uint4*>(src), static_cast<uint4*>(dst), n,
+                              in ? 1 : 0);
+  return cudaLaunchKernelEx(&cfg, stage_kernel<uint32_t>, static_cast<const uint32_t*>(src),
+                            static_cast<uint32_t*>(dst), n, in ? 1 : 0);
 }
 
 extern "C" lrc_status lrc_layer_forward_host(lrc_layer* L, const uint16_t* x_host, int64_t B,
