@@ -664,7 +664,8 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   // plan would take ~1 us per 32 pairs)
   const bool big_plan = np_bound > kSerialPlanMaxPairs;
   if (big_plan) ra.plan.ticket = nullptr;
-  lrc_status s = launch_route(ra, st);
+  static const bool no_bulk = getenv("LRC_NO_BULK_ROUTE") != nullptr;
+  lrc_status s = (big_plan && !no_bulk) ? launch_route_bulk(ra, st) : launch_route(ra, st);
   if (s != LRC_OK) return s;
   ++launches;
   if (big_plan) {

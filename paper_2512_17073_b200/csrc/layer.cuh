@@ -139,6 +139,7 @@ int plan_parallel_blocks(int64_t np);
 lrc_status launch_plan_parallel(const PlanArgs& pa, const int32_t* tk_idx, const float* tk_w, int B, int k,
                                 int* blk, uint32_t* cmask, int* ticket, cudaStream_t st);
 lrc_status launch_route(const RouteArgs& ra, cudaStream_t st);
+lrc_status launch_route_bulk(const RouteArgs& ra, cudaStream_t st);  // large batches, routing only
 
 // Arguments of the expert phases.
 struct ExpertArgs {

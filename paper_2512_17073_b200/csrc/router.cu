@@ -798,6 +798,154 @@ __device__ __noinline__ void warm_tail(const RouteArgs& ra, WarmScratch& ws, con
 
 int route_tiles(int64_t B) { return static_cast<int>((B + kTT - 1) / kTT); }
 
+// --------------------------------------------------- large-batch routing ---
+// The cluster router is latency-tuned for decode (one 8-CTA cluster per 8
+// tokens).  For large batches: a block per 32 tokens computes all their
+// logits as fp64 dot products (one (token, expert) pair per thread and pass;
+// x and gate chunks staged through padded shared memory), then the same
+// warp softmax + stable top-k as the leader (ref/moe.py:165-193); it also
+// zeroes the outputs the expert kernels accumulate into.  The pair plan then
+// comes from the parallel counting sort below.
+constexpr int kBT = 32;  // tokens per bulk-router block
+
+__host__ __device__ inline int bulk_chunk(int E) {  // d columns per staged chunk
+  int c = 8192 / (E > 0 ? E : 1);
+  c = c > 256 ? 256 : c;
+  return c < 16 ? 16 : (c & ~15);
+}
+static size_t bulk_smem(int E) {
+  const int c = bulk_chunk(E);
+  return (static_cast<size_t>(E) * (c + 1) + kBT * (c + 1) + kBT * (E + 64)) * sizeof(double) +
+         8 * 64 * (sizeof(int32_t) + sizeof(float));
+}
+
+template <typename T, int kMaxPJ>  // kMaxPJ >= ceil(kBT * E / 256) (token, expert) pairs per thread
+__global__ void __launch_bounds__(256) route_bulk_kernel(const __grid_constant__ RouteArgs ra) {
+  extern __shared__ __align__(16) double bsm[];
+  const int E = ra.E, d = ra.d, tid = threadIdx.x, warp = tid >> 5;
+  const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kBT;
+  const int64_t rem = ra.B - b0;
+  const int nb = rem < kBT ? static_cast<int>(rem) : kBT;
+  if (ra.y_zero != nullptr) {
+    float* yz = ra.y_zero + b0 * d;
+    const int64_t n = static_cast<int64_t>(nb) * d;
+    if ((d & 3) == 0 && (reinterpret_cast<uintptr_t>(ra.y_zero) & 15) == 0) {
+      for (int64_t i = tid; i < n / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(yz)[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    } else {
+      for (int64_t i = tid; i < n; i += blockDim.x) yz[i] = 0.0f;
+    }
+  }
+  if (ra.t2_zero != nullptr && ra.maxr > 0) {
+    const int n = nb * ra.ne * ra.maxr;
+    for (int i = tid; i < n; i += blockDim.x) {
+      const int t = i / (ra.ne * ra.maxr), r2 = i - t * ra.ne * ra.maxr;
+      const int e = r2 / ra.maxr, j = r2 - e * ra.maxr;
+      ra.t2_zero[(((b0 + t) * ra.ne + e) * 3 + 2) * ra.maxr + j] = 0.0f;
+    }
+  }
+  if (ra.pairs_expert != nullptr) {  // pairs mode: the routing is given (k = 1)
+    if (tid < nb) {
+      ra.topk_idx[b0 + tid] = ra.pairs_expert[b0 + tid];
+      ra.topk_w[b0 + tid] = ra.pairs_w[b0 + tid];
+    }
+    return;
+  }
+  const int C = bulk_chunk(E), ldg = C + 1;
+  double* gs = bsm;                        // [E][C + 1]
+  double* xs = gs + static_cast<size_t>(E) * ldg;  // [kBT][C + 1]
+  double* lg = xs + kBT * ldg;             // [kBT][E + 64]
+  int32_t* sidx = reinterpret_cast<int32_t*>(lg + kBT * (E + 64));
+  float* sw = reinterpret_cast<float*>(sidx + 8 * 64);
+  const T* x = static_cast<const T*>(ra.x);
+  const int npairs = kBT * E;
+  // four interleaved partial sums per (token, expert): independent fp64 FMA
+  // chains (a single chain is latency-bound); fixed, deterministic order
+  double acc[kMaxPJ][4];
+#pragma unroll
+  for (int j = 0; j < kMaxPJ; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[j][q] = 0.0;
+  for (int k0 = 0; k0 < d; k0 += C) {
+    const int cw = min(C, d - k0);
+    for (int i = tid; i < E * C; i += blockDim.x) {
+      const int e = i / C, c = i - e * C;
+      gs[e * ldg + c] = c < cw ? ra.gate_t[static_cast<int64_t>(e) * d + k0 + c] : 0.0;
+    }
+    for (int i = tid; i < kBT * C; i += blockDim.x) {
+      const int t = i / C, c = i - t * C;
+      xs[t * ldg + c] = (t < nb && c < cw) ? load_x(x, (b0 + t) * d + k0 + c) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kMaxPJ; ++j) {
+      const int pr = tid + j * 256;
+      if (pr < npairs) {
+        const int t = pr / E, e = pr - t * E;
+        const double* xr = xs + t * ldg;
+        const double* gr = gs + e * ldg;
+        double a0 = acc[j][0], a1 = acc[j][1], a2 = acc[j][2], a3 = acc[j][3];
+        int c = 0;
+        for (; c + 3 < cw; c += 4) {
+          a0 = fma(xr[c], gr[c], a0);
+          a1 = fma(xr[c + 1], gr[c + 1], a1);
+          a2 = fma(xr[c + 2], gr[c + 2], a2);
+          a3 = fma(xr[c + 3], gr[c + 3], a3);
+        }
+        for (; c < cw; ++c) a0 = fma(xr[c], gr[c], a0);
+        acc[j][0] = a0;
+        acc[j][1] = a1;
+        acc[j][2] = a2;
+        acc[j][3] = a3;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxPJ; ++j) {
+    const int pr = tid + j * 256;
+    if (pr < npairs) {
+      const int t = pr / E, e = pr - t * E;
+      lg[t * (E + 64) + e] = (acc[j][0] + acc[j][1]) + (acc[j][2] + acc[j][3]);
+    }
+  }
+  __syncthreads();
+  for (int t = warp; t < nb; t += blockDim.x / 32)
+    select_topk_warp(lg + t * (E + 64), E, ra.k, ra.renorm, b0 + t, ra.probs, ra.topk_idx, ra.topk_w,
+                     sidx + warp * 64, sw + warp * 64);
+}
+
+template <typename T>
+static lrc_status launch_route_bulk_t(const RouteArgs& ra, size_t smem, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>((ra.B + kBT - 1) / kBT);
+  const int pj = (kBT * ra.E + 255) / 256;
+  auto go = [&](auto kern) -> lrc_status {
+    static size_t configured = 0;  // per instantiation
+    if (configured < smem) {
+      LRC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      configured = smem;
+    }
+    kern<<<grid, 256, smem, st>>>(ra);
+    LRC_CHECK_LAUNCH();
+    return LRC_OK;
+  };
+  if (pj <= 1) return go(route_bulk_kernel<T, 1>);
+  if (pj <= 2) return go(route_bulk_kernel<T, 2>);
+  if (pj <= 8) return go(route_bulk_kernel<T, 8>);
+  return go(route_bulk_kernel<T, 32>);
+}
+
+lrc_status launch_route_bulk(const RouteArgs& ra, cudaStream_t st) {
+  if (ra.E > 256 || ra.k > 64) return fail(LRC_ERR_UNSUPPORTED, "bulk route: E <= 256, k <= 64");
+  const size_t smem = bulk_smem(ra.E);
+  switch (ra.x_dtype) {
+    case LRC_DTYPE_F64: return launch_route_bulk_t<double>(ra, smem, st);
+    case LRC_DTYPE_F32: return launch_route_bulk_t<float>(ra, smem, st);
+    case LRC_DTYPE_BF16: return launch_route_bulk_t<uint16_t>(ra, smem, st);
+    default: return fail(LRC_ERR_INVALID, "route: unknown x dtype");
+  }
+}
+
 // ---------------------------------------------- large-batch parallel plan ---
 // Same output as build_plan_block (pairs grouped by expert, ascending pair id
 // inside each expert; compensated slots in pair order), as a counting sort over

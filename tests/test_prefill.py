@@ -215,3 +215,19 @@ def test_deepseek_shape_prefill(torch):
     for t in (0, B - 1):
         yo = lrc.forward(xs[t], sl.gate, None, 8, 2, "compensated", st)
         assert rel_l2(yp[t], yo) <= TOL_Y, rel_l2(yp[t], yo)
+
+
+def test_bulk_router_indices_bit_exact(torch):
+    """Large batches route with the bulk router (routing only) + parallel plan:
+    every token's top-k indices bit-exact against the fp64 oracle router."""
+    from paper_2512_17073_b200.synth import SynthLayer
+
+    B = 3000  # 6000 pairs > the serial-plan limit
+    sl = SynthLayer(4096, 14336, 8, top_k=2, rank=32, seed=17, max_tokens=B)
+    xs = lrc.to_bf16(np.random.default_rng(17).standard_normal((B, 4096)))
+    _, idx, w = sl.layer.forward(torch.from_numpy(xs).cuda().to(torch.bfloat16), top_k=2, top_n=1)
+    idx, w = idx.cpu().numpy(), w.cpu().numpy()
+    for t in range(B):
+        wo, sel, _ = lrc.route(xs[t], sl.gate, 2, 1)
+        assert sel == list(idx[t]), (t, sel, idx[t])
+    assert np.all(np.isfinite(w)) and np.all(w > 0)
