@@ -900,7 +900,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
     }
     for (int sp = warp; sp < ((P.debug & 1) ? 0 : nspan); sp += kNW) {
       const int q0 = sp * kSpanGP, q1 = min(ngp, q0 + kSpanGP);
-#pragma unroll 2
+#pragma unroll 1
       for (int q = q0; q < q1; ++q) {
         const uint8_t* blk = st + q * NI * kBlk;
         uint4 cw[NI], mw[NI];
