@@ -1,0 +1,847 @@
+// Building blocks of the tensor-core decode core ("tcd"): 2-bit / 3-bit codes
+// decoded in registers into bf16 (128 + m*c, one LOP3 per two codes), stored
+// into TMEM with tcgen05.st, and consumed as the A operand of
+// tcgen05.mma.kind::f16 (M=128, N=8, K=16; A from TMEM, B = x/m in a
+// no-swizzle K-major shared-memory layout).
+//   part 1: correctness of the layouts / descriptors (variants printed)
+//   part 2: decode + st + MMA throughput per SM (codes from shared memory)
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/bin/tcd_test tools/tcd_test.cu
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+// no-swizzle K-major descriptor
+__device__ __forceinline__ uint64_t desc_ns(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  return d;
+}
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;}" ::"r"(d),
+      "r"(a), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{.reg .pred P; elect.sync _|P, 0xffffffff; selp.b32 %0, 1, 0, P;}" : "=r"(p));
+  return p != 0;
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n));
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (long spin = 0; !ok; ++spin) {
+    asm volatile(
+        "{.reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.b32 %0, 1, 0, P;}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (spin > (1L << 28)) __trap();
+  }
+}
+template <int N>
+__device__ __forceinline__ void tmem_st(uint32_t addr, const uint32_t (&r)[N]);
+template <>
+__device__ __forceinline__ void tmem_st<32>(uint32_t addr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---- decoders: 64 codes of one row-group -> 32 bf16x2 words (TMEM columns) ----
+// 2-bit (reference LSB-first row bytes): column 8w+q = (code 16w+q, code 16w+q+8), m = {1,4,16,1,4,16,1,4}[q]
+__device__ __forceinline__ void decode2(const uint4 c, uint32_t (&r)[32]) {
+  const uint32_t M = 0x43004300u;
+  const uint32_t w4[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t a = w4[w], b = a >> 6, d = a >> 12;
+    r[8 * w + 0] = (a & 0x00030003u) | M;
+    r[8 * w + 1] = (a & 0x000C000Cu) | M;
+    r[8 * w + 2] = (a & 0x00300030u) | M;
+    r[8 * w + 3] = (b & 0x00030003u) | M;
+    r[8 * w + 4] = (b & 0x000C000Cu) | M;
+    r[8 * w + 5] = (b & 0x00300030u) | M;
+    r[8 * w + 6] = (d & 0x00030003u) | M;
+    r[8 * w + 7] = (d & 0x000C000Cu) | M;
+  }
+}
+// 3-bit (repacked, 6 words per row-group): word w lo half = codes 10w+q at bit 3q (q<5),
+// hi half = codes 10w+5+q; bits 15/31 of words 0-2 -> codes 60/61, of words 3-5 -> 62/63.
+// column 5w+q: q=0:(w&7) m1, q=1:(w&0x38) m8, q=2:(w>>6&7) m1, q=3:(w>>6&0x38) m8, q=4:(w>>12&7) m1
+__device__ __forceinline__ void decode3(const uint32_t (&w6)[6], uint32_t (&r)[32]) {
+  const uint32_t M = 0x43004300u;
+#pragma unroll
+  for (int w = 0; w < 6; ++w) {
+    const uint32_t a = w6[w], b = a >> 6, d = a >> 12;
+    r[5 * w + 0] = (a & 0x00070007u) | M;
+    r[5 * w + 1] = (a & 0x00380038u) | M;
+    r[5 * w + 2] = (b & 0x00070007u) | M;
+    r[5 * w + 3] = (b & 0x00380038u) | M;
+    r[5 * w + 4] = (d & 0x00070007u) | M;
+  }
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    uint32_t t = ((w6[3 * s] >> 15) & 0x00010001u) | M;
+    t |= (w6[3 * s + 1] >> 14) & 0x00020002u;
+    t |= (w6[3 * s + 2] >> 13) & 0x00040004u;
+    r[30 + s] = t;
+  }
+}
+// host-side tables: for column j: (code a, code b, multiplier)
+static void table2(int* ca, int* cb, float* m) {
+  const float mm[8] = {1, 4, 16, 1, 4, 16, 1, 4};
+  for (int w = 0; w < 4; ++w)
+    for (int q = 0; q < 8; ++q) {
+      ca[8 * w + q] = 16 * w + q;
+      cb[8 * w + q] = 16 * w + q + 8;
+      m[8 * w + q] = mm[q];
+    }
+}
+static void table3(int* ca, int* cb, float* m) {
+  const float mm[5] = {1, 8, 1, 8, 1};
+  for (int w = 0; w < 6; ++w)
+    for (int q = 0; q < 5; ++q) {
+      ca[5 * w + q] = 10 * w + q;
+      cb[5 * w + q] = 10 * w + 5 + q;
+      m[5 * w + q] = mm[q];
+    }
+  ca[30] = 60; cb[30] = 61; m[30] = 1;
+  ca[31] = 62; cb[31] = 63; m[31] = 1;
+}
+static void repack3(const uint8_t* codes, uint32_t* w6) {  // 64 codes -> 6 words
+  const int qpos[5] = {0, 3, 6, 9, 12};
+  for (int w = 0; w < 6; ++w) {
+    uint32_t v = 0;
+    for (int q = 0; q < 5; ++q) {
+      v |= uint32_t(codes[10 * w + q]) << qpos[q];
+      v |= uint32_t(codes[10 * w + 5 + q]) << (16 + qpos[q]);
+    }
+    w6[w] = v;
+  }
+  for (int s = 0; s < 2; ++s)
+    for (int b = 0; b < 3; ++b) {
+      w6[3 * s + b] |= uint32_t((codes[60 + 2 * s] >> b) & 1) << 15;
+      w6[3 * s + b] |= uint32_t((codes[61 + 2 * s] >> b) & 1) << 31;
+    }
+}
+
+// ---------------------------------------------------------------- part 1 ----
+// A: 128 rows x 64 codes, B: 8 tokens x 64 (x'/m permuted), D = 128 x 8.
+// variant bits: 0 = swap LBO/SBO, 1 = swap bf16 halves order in the B operand
+__global__ void part1(const uint32_t* codes, int bits, const uint16_t* bop_std, const uint16_t* bop_swap,
+                      float* D, int variant) {
+  __shared__ __align__(1024) uint16_t sb[8 * 64];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint16_t* src = (variant & 2) ? bop_swap : bop_std;
+  for (int i = tid; i < 8 * 64; i += 128) sb[i] = src[i];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    bar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  uint32_t r[32];
+  if (bits == 2) {
+    const uint4 c = reinterpret_cast<const uint4*>(codes)[tid];
+    decode2(c, r);
+  } else {
+    uint32_t w6[6];
+    for (int i = 0; i < 6; ++i) w6[i] = codes[tid * 6 + i];
+    decode3(w6, r);
+  }
+  tmem_st<32>(tm + (static_cast<uint32_t>(warp * 32) << 16), r);
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0) {
+    const uint32_t lbo = (variant & 1) ? 1024 : 128, sbo = (variant & 1) ? 128 : 1024;
+    for (int s = 0; s < 4; ++s)
+      mma_ts(tm + 64, tm + 8 * s, desc_ns(smem_u32(sb) + s * 256, lbo, sbo), idesc_bf16(128, 8), s > 0);
+    commit(&bar);
+  }
+  bar_wait(&bar, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  uint32_t v[8];
+  tmem_ld8(tm + (static_cast<uint32_t>(warp * 32) << 16) + 64, v);
+  for (int n = 0; n < 8; ++n) D[tid * 8 + n] = __uint_as_float(v[n]);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm));
+}
+
+static uint16_t f2bf_host(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  return static_cast<uint16_t>((u + 0x7FFF + ((u >> 16) & 1)) >> 16);
+}
+
+static int run_part1(int bits) {
+  std::vector<uint8_t> code(128 * 64);
+  for (auto& c : code) c = rand() % (1 << bits);
+  std::vector<uint32_t> packed;
+  if (bits == 2) {
+    packed.assign(128 * 4, 0);
+    for (int r = 0; r < 128; ++r)
+      for (int k = 0; k < 64; ++k) packed[r * 4 + k / 16] |= uint32_t(code[r * 64 + k]) << (2 * (k % 16));
+  } else {
+    packed.assign(128 * 6, 0);
+    for (int r = 0; r < 128; ++r) repack3(&code[r * 64], &packed[r * 6]);
+  }
+  // x: small dyadic values (exact sums)
+  std::vector<float> x(8 * 64);
+  for (auto& v : x) v = float(rand() % 33 - 16) / 4.0f;
+  int ca[32], cb[32];
+  float m[32];
+  if (bits == 2) table2(ca, cb, m); else table3(ca, cb, m);
+  // B operand element (n, mma_k): mma_k = 2j -> x[ca[j]]/m, 2j+1 -> x[cb[j]]/m
+  // core-matrix layout: K-step s (16 mma_k) = 256 B: [core ko=0: 8 rows x 16 B][core ko=1]
+  std::vector<uint16_t> bstd(8 * 64), bswp(8 * 64);
+  for (int n = 0; n < 8; ++n)
+    for (int kk = 0; kk < 64; ++kk) {
+      const int j = kk / 2, odd = kk & 1;
+      const float v = (odd ? x[n * 64 + cb[j]] : x[n * 64 + ca[j]]) / m[j];
+      const float vs = (odd ? x[n * 64 + ca[j]] : x[n * 64 + cb[j]]) / m[j];
+      const int s = kk / 16, ko = (kk % 16) / 8, e = kk % 8;
+      const int idx = (s * 256 + ko * 128 + n * 16 + e * 2) / 2;
+      bstd[idx] = f2bf_host(v);
+      bswp[idx] = f2bf_host(vs);
+    }
+  uint32_t* dc;
+  uint16_t *db1, *db2;
+  float* dd;
+  cudaMalloc(&dc, packed.size() * 4);
+  cudaMalloc(&db1, 1024);
+  cudaMalloc(&db2, 1024);
+  cudaMalloc(&dd, 128 * 8 * 4);
+  cudaMemcpy(dc, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(db1, bstd.data(), 1024, cudaMemcpyHostToDevice);
+  cudaMemcpy(db2, bswp.data(), 1024, cudaMemcpyHostToDevice);
+  int good = -1;
+  for (int variant = 0; variant < 4; ++variant) {
+    part1<<<1, 128>>>(dc, bits, db1, db2, dd, variant);
+    cudaError_t e = cudaDeviceSynchronize();
+    std::vector<float> hd(128 * 8);
+    cudaMemcpy(hd.data(), dd, hd.size() * 4, cudaMemcpyDeviceToHost);
+    double maxerr = 0;
+    for (int r = 0; r < 128; ++r)
+      for (int n = 0; n < 8; ++n) {
+        double ref = 0, bias = 0;
+        for (int k = 0; k < 64; ++k) ref += double(code[r * 64 + k]) * x[n * 64 + k];
+        for (int j = 0; j < 32; ++j) bias += 128.0 * (x[n * 64 + ca[j]] + x[n * 64 + cb[j]]) / m[j];
+        maxerr = fmax(maxerr, fabs(hd[r * 8 + n] - bias - ref));
+      }
+    printf("bits %d variant %d (lbo/sbo %s, halves %s): %s max|err| %.4g\n", bits, variant,
+           (variant & 1) ? "swapped" : "128/1024", (variant & 2) ? "swapped" : "std", cudaGetErrorString(e),
+           maxerr);
+    if (e != cudaSuccess) return -1;
+    if (maxerr < 1e-3 && good < 0) good = variant;
+  }
+  cudaFree(dc); cudaFree(db1); cudaFree(db2); cudaFree(dd);
+  return good;
+}
+
+// ---------------------------------------------------------------- part 2 ----
+// Throughput: NDEC decode warps (2 per TMEM lane quarter, alternating groups),
+// one MMA thread.  Codes re-read from a static smem buffer of 16 (group, mat) units.
+// A ring of ASLOTS x 32 columns; D region per 8 groups (B = 1 block-diagonal).
+template <int BITS, int NDEC, int ASLOTS, bool EPI>
+__global__ void __launch_bounds__(NDEC * 32 + 32, 1) part2(int iters, long long* cyc, float* sink) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  constexpr int CB = BITS == 2 ? 16 : 24;  // code bytes per row-group
+  uint8_t* scodes = sm;                     // 16 units x 128 rows x CB
+  uint16_t* sbop = reinterpret_cast<uint16_t*>(sm + 16 * 128 * CB);  // 4 x 256 B
+  __shared__ uint64_t afull[ASLOTS], aempty[ASLOTS], dfull[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 16 * 128 * CB / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(scodes)[i] = i * 2654435761u;
+  for (int i = tid; i < 512; i += blockDim.x) sbop[i] = 0x3f80;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    for (int i = 0; i < ASLOTS; ++i) {
+      bar_init(&afull[i], 4);
+      bar_init(&aempty[i], 1);
+    }
+    bar_init(&dfull[0], 1);
+    bar_init(&dfull[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  const uint32_t dcol = ASLOTS * 32;  // D regions after the A ring (2 x 8 cols)
+  long long t0 = clock64();
+  if (warp < NDEC) {
+    const int q = warp & 3, h = warp >> 2;  // lane quarter, group parity (NDEC = 8) or 0
+    constexpr int H = NDEC / 4;
+    float acc = 0.f, sr = 1.f;
+    for (int u = h; u < iters; u += H) {  // unit u = (group, mat) in stream order
+      const int slot = u % ASLOTS;
+      const uint32_t ph = (u / ASLOTS) & 1;
+      if (u >= ASLOTS) bar_wait(&aempty[slot], ph ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t r[32];
+      const uint8_t* cp = scodes + (u & 15) * 128 * CB + (q * 32 + lane) * CB;
+      if (BITS == 2) {
+        decode2(*reinterpret_cast<const uint4*>(cp), r);
+      } else {
+        uint32_t w6[6];
+        const uint2* p2 = reinterpret_cast<const uint2*>(cp);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const uint2 v = p2[i];
+          w6[2 * i] = v.x;
+          w6[2 * i + 1] = v.y;
+        }
+        decode3(w6, r);
+      }
+      tmem_st<32>(tm + (static_cast<uint32_t>(q * 32) << 16) + slot * 32, r);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) bar_arrive(&afull[slot]);
+      sr += __uint_as_float(r[0] ^ r[31]);
+      if (EPI && (u & 15) == 16 - H + h && u >= 32) {  // region (16 units) done: epilogue of the previous one
+        const int reg = (u / 16 - 1);
+        bar_wait(&dfull[reg & 1], (reg >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint32_t v[8];
+        tmem_ld8(tm + (static_cast<uint32_t>(q * 32) << 16) + dcol + (reg & 1) * 8, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc = fmaf(__uint_as_float(v[j]), sr, acc);
+      }
+    }
+    if (acc == 12345.f) sink[tid] = acc;
+  } else if (lane == 0) {
+    for (int u = 0; u < iters; ++u) {
+      const int slot = u % ASLOTS;
+      bar_wait(&afull[slot], (u / ASLOTS) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int reg = u / 16;
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        mma_ts(tm + dcol + (reg & 1) * 8, tm + slot * 32 + 8 * s, desc_ns(smem_u32(sbop) + s * 256, 128, 1024),
+               idesc_bf16(128, 8), (u & 15) > 0 || s > 0);
+      commit(&aempty[slot]);
+      if ((u & 15) == 15) commit(&dfull[reg & 1]);
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (tid == 0) cyc[blockIdx.x] = t1 - t0;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+
+template <int BITS, int NDEC, int ASLOTS, bool EPI>
+static void run_part2(const char* name) {
+  const int iters = 16 * 2000, grid = 148;
+  long long* dcyc;
+  float* sink;
+  cudaMalloc(&dcyc, grid * 8);
+  cudaMalloc(&sink, 4096 * 4);
+  const int CB = BITS == 2 ? 16 : 24;
+  const int smem = 16 * 128 * CB + 1024 + 1024;
+  auto k = part2<BITS, NDEC, ASLOTS, EPI>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k<<<grid, NDEC * 32 + 32, smem>>>(iters, dcyc, sink);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  k<<<grid, NDEC * 32 + 32, smem>>>(iters, dcyc, sink);
+  cudaEventRecord(e1);
+  cudaError_t e = cudaDeviceSynchronize();
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  std::vector<long long> h(grid);
+  cudaMemcpy(h.data(), dcyc, grid * 8, cudaMemcpyDeviceToHost);
+  long long mx = 0;
+  for (auto v : h) mx = v > mx ? v : mx;
+  const double w = double(iters) * 128 * 64;
+  const double bytes_per_w = BITS / 8.0 + 4.0 / 64;  // codes + fp16 scale/zero
+  printf("%-28s %s  %.1f weights/clk/SM  -> %.2f TB/s equivalent (%.3f ms, %.0f GW/s/SM)\n", name,
+         cudaGetErrorString(e), w / mx, w * grid * bytes_per_w / (ms * 1e-3) / 1e12, ms, w / (ms * 1e-3) / 1e9);
+  cudaFree(dcyc);
+  cudaFree(sink);
+}
+
+
+// ---------------------------------------------------------------- part 3 ----
+// Back-to-back MMA issue rate: TS (A in TMEM) vs SS (A in smem, no swizzle), M=128, N variable.
+template <bool TS, int N, int NCOMMIT>
+__global__ void part3(int nmma, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3f803f80u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    bar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  if (tid == 0) {
+    const long long t0 = clock64();
+    uint32_t ph = 0;
+    for (int i = 0; i < nmma; ++i) {
+      // A: 8 slots x 8 columns (TS) / 8 x 4 KB (SS); B: 16 x N x 2 B per K step
+      const uint64_t db = desc_ns(smem_u32(sm + 32768) + (i & 7) * (32 * N), 128, 256);
+      if (TS) {
+        mma_ts(tm + 256, tm + (i & 7) * 8, db, idesc_bf16(128, N), i > 0);
+      } else {
+        const uint64_t da = desc_ns(smem_u32(sm) + (i & 7) * 4096, 128, 256);
+        asm volatile(
+            "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}" ::"r"(tm + 256),
+            "l"(da), "l"(db), "r"(idesc_bf16(128, N)), "r"(i > 0 ? 1u : 0u));
+      }
+      if (NCOMMIT > 0 && (i % (NCOMMIT > 0 ? NCOMMIT : 1)) == NCOMMIT - 1) {
+        commit(&bar);
+        bar_wait(&bar, ph);
+        ph ^= 1;
+      }
+    }
+    commit(&bar);
+    bar_wait(&bar, ph);
+    cyc[blockIdx.x] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+template <bool TS, int N, int NCOMMIT>
+static void run_part3(int grid) {
+  const int nmma = 4096;
+  long long* d;
+  cudaMalloc(&d, grid * 8);
+  auto k = part3<TS, N, NCOMMIT>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  k<<<grid, 128, 100 * 1024>>>(nmma, d);
+  k<<<grid, 128, 100 * 1024>>>(nmma, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h = 0;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("MMA %s M=128 N=%3d commit/%d grid %3d: %s %.1f cycles/MMA\n", TS ? "TS" : "SS", N, NCOMMIT, grid,
+         cudaGetErrorString(e), double(h) / nmma);
+  cudaFree(d);
+}
+
+// ---------------------------------------------------------------- part 4 ----
+// Same, TS only, with ND independent accumulators round-robin (accumulator
+// dependency vs issue floor), kind::f16 (K=16) or kind::f8f6f4 e4m3 (K=32).
+template <int N, int ND, bool F8>
+__global__ void part4(int nmma, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x38383838u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    bar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  const uint32_t id = F8 ? ((1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (8u << 24)) : idesc_bf16(128, N);
+  if (tid == 0) {
+    const long long t0 = clock64();
+    for (int i = 0; i < nmma; ++i) {
+      const uint64_t db = desc_ns(smem_u32(sm + 32768) + (i & 7) * (32 * N), 128, 256);
+      const uint32_t d = tm + 256 + (i % ND) * N;
+      if (F8)
+        asm volatile(
+            "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;}" ::"r"(d),
+            "r"(tm + (i & 7) * 8), "l"(db), "r"(id), "r"(i >= ND ? 1u : 0u));
+      else
+        mma_ts(d, tm + (i & 7) * 8, db, id, i >= ND);
+    }
+    commit(&bar);
+    bar_wait(&bar, 0);
+    cyc[blockIdx.x] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+template <int N, int ND, bool F8>
+static void run_part4() {
+  const int nmma = 4096;
+  long long* d;
+  cudaMalloc(&d, 8);
+  auto k = part4<N, ND, F8>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  k<<<1, 128, 100 * 1024>>>(nmma, d);
+  k<<<1, 128, 100 * 1024>>>(nmma, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h = 0;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("MMA TS %s N=%3d ND=%d: %s %.1f cycles/MMA\n", F8 ? "f8 K32" : "bf16 K16", N, ND, cudaGetErrorString(e),
+         double(h) / nmma);
+  cudaFree(d);
+}
+
+// ---------------------------------------------------------------- part 5 ----
+// Issue-overhead check: 8 MMAs per loop iteration, descriptors precomputed.
+template <int N, bool F8>
+__global__ void part5(int iters, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x38383838u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    bar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  const uint32_t id = F8 ? ((1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (8u << 24)) : idesc_bf16(128, N);
+  if (warp == 0) {
+    const uint64_t db0 = desc_ns(smem_u32(sm + 32768), 128, 256);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      {
+        if (elect_one()) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) mma_ts(tm + 256 + (j & 3) * N, tm + j * 8, db0 + j * 16, id, 1u);
+        }
+        __syncwarp();
+      }
+    }
+    if (elect_one()) {
+      commit(&bar);
+    }
+    __syncwarp();
+    bar_wait(&bar, 0);
+    if (tid == 0) cyc[blockIdx.x] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+template <int N, bool F8>
+static void run_part5() {
+  const int iters = 512;
+  long long* d;
+  cudaMalloc(&d, 8);
+  auto k = part5<N, F8>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  k<<<1, 128, 100 * 1024>>>(iters, d);
+  k<<<1, 128, 100 * 1024>>>(iters, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h = 0;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("unrolled MMA TS %s N=%3d: %s %.1f cycles/MMA\n", F8 ? "f8 K32" : "bf16 K16", N, cudaGetErrorString(e),
+         double(h) / (iters * 8));
+  cudaFree(d);
+}
+
+// ---------------------------------------------------------------- part 6 ----
+// 8-bit A operand from TMEM: kind::f8f6f4 (A e4m3 = 8 + c, B e4m3) and kind::i8
+// (A u8 = c, B s8).  2-bit codes, one row-group (64 codes) per thread, K = 32 per MMA.
+// TMEM column 4w+j byte b = code 16w + 4b + j  (reg j of word w = (w >> 2j) & 0x03030303).
+__host__ __device__ constexpr uint32_t idesc8(bool i8, int m, int n) {
+  return (i8 ? (2u << 4) | (1u << 10) : (1u << 4)) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+template <bool I8>
+__global__ void part6(const uint32_t* codes, const uint8_t* bop, float* D, int* Di) {
+  __shared__ __align__(1024) uint8_t sb[8 * 64];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 8 * 64; i += 128) sb[i] = bop[i];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    bar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  uint32_t r[16];
+  const uint4 c = reinterpret_cast<const uint4*>(codes)[tid];
+  const uint32_t w4[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+  for (int w = 0; w < 4; ++w)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r[4 * w + j] = ((w4[w] >> (2 * j)) & 0x03030303u) | (I8 ? 0u : 0x50505050u);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          tm + (static_cast<uint32_t>(warp * 32) << 16)),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      const uint64_t db = desc_ns(smem_u32(sb) + s * 256, 128, 1024);
+      if (I8)
+        asm volatile(
+            "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;}" ::"r"(tm + 64),
+            "r"(tm + 8 * s), "l"(db), "r"(idesc8(true, 128, 8)), "r"(s > 0 ? 1u : 0u));
+      else
+        asm volatile(
+            "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;}" ::"r"(tm + 64),
+            "r"(tm + 8 * s), "l"(db), "r"(idesc8(false, 128, 8)), "r"(s > 0 ? 1u : 0u));
+    }
+    commit(&bar);
+  }
+  bar_wait(&bar, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  uint32_t v[8];
+  tmem_ld8(tm + (static_cast<uint32_t>(warp * 32) << 16) + 64, v);
+  for (int n = 0; n < 8; ++n) {
+    D[tid * 8 + n] = __uint_as_float(v[n]);
+    Di[tid * 8 + n] = static_cast<int>(v[n]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm));
+}
+static uint8_t e4m3_int(int v) {  // exact small integers |v| <= 15
+  if (v == 0) return 0;
+  const int a = v < 0 ? -v : v;
+  int e = 0;
+  while ((a >> (e + 1)) != 0) ++e;  // a in [2^e, 2^(e+1))
+  const int mant = (a << 3 >> e) & 7;
+  return static_cast<uint8_t>((v < 0 ? 0x80 : 0) | ((e + 7) << 3) | mant);
+}
+template <bool I8>
+static void run_part6() {
+  std::vector<uint8_t> code(128 * 64);
+  for (auto& c : code) c = rand() % 4;
+  std::vector<uint32_t> packed(128 * 4, 0);
+  for (int r = 0; r < 128; ++r)
+    for (int k = 0; k < 64; ++k) packed[r * 4 + k / 16] |= uint32_t(code[r * 64 + k]) << (2 * (k % 16));
+  std::vector<int> x(8 * 64);
+  for (auto& v : x) v = rand() % 31 - 15;
+  std::vector<uint8_t> b(8 * 64);
+  for (int n = 0; n < 8; ++n)
+    for (int k = 0; k < 64; ++k) {
+      const int col = k / 4, byte = k % 4, w = col / 4, j = col % 4;
+      const int ci = 16 * w + 4 * byte + j;
+      const int s = k / 32, ko = (k % 32) / 16, e = k % 16;
+      b[s * 256 + ko * 128 + n * 16 + e] = I8 ? static_cast<uint8_t>(static_cast<int8_t>(x[n * 64 + ci]))
+                                              : e4m3_int(x[n * 64 + ci]);
+    }
+  uint32_t* dc;
+  uint8_t* db;
+  float* dd;
+  int* di;
+  cudaMalloc(&dc, 2048);
+  cudaMalloc(&db, 512);
+  cudaMalloc(&dd, 4096);
+  cudaMalloc(&di, 4096);
+  cudaMemcpy(dc, packed.data(), 2048, cudaMemcpyHostToDevice);
+  cudaMemcpy(db, b.data(), 512, cudaMemcpyHostToDevice);
+  part6<I8><<<1, 128>>>(dc, db, dd, di);
+  cudaError_t e = cudaDeviceSynchronize();
+  std::vector<float> hd(1024);
+  std::vector<int> hi(1024);
+  cudaMemcpy(hd.data(), dd, 4096, cudaMemcpyDeviceToHost);
+  cudaMemcpy(hi.data(), di, 4096, cudaMemcpyDeviceToHost);
+  double maxerr = 0;
+  for (int r = 0; r < 128; ++r)
+    for (int n = 0; n < 8; ++n) {
+      long ref = 0, sx = 0;
+      for (int k = 0; k < 64; ++k) {
+        ref += long(code[r * 64 + k]) * x[n * 64 + k];
+        sx += x[n * 64 + k];
+      }
+      const double got = I8 ? double(hi[r * 8 + n]) : double(hd[r * 8 + n]) - 8.0 * sx;
+      maxerr = fmax(maxerr, fabs(got - ref));
+    }
+  printf("part6 %s: %s max|err| %.4g\n", I8 ? "kind::i8 (u8 A, s8 B)" : "kind::f8f6f4 (e4m3 8+c)",
+         cudaGetErrorString(e), maxerr);
+}
+template <int N, bool I8>
+__global__ void part7(int iters, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    bar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  const uint32_t id = idesc8(I8, 128, N);
+  if (warp == 0) {
+    const uint64_t db0 = desc_ns(smem_u32(sm + 32768), 128, 256);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      if (elect_one()) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (I8)
+            asm volatile(
+                "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;}" ::"r"(tm + 256 + (j & 3) * N),
+                "r"(tm + j * 8), "l"(db0 + j * 16), "r"(id), "r"(1u));
+          else
+            asm volatile(
+                "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;}" ::"r"(tm + 256 + (j & 3) * N),
+                "r"(tm + j * 8), "l"(db0 + j * 16), "r"(id), "r"(1u));
+        }
+      }
+      __syncwarp();
+    }
+    if (elect_one()) commit(&bar);
+    __syncwarp();
+    bar_wait(&bar, 0);
+    if (tid == 0) cyc[blockIdx.x] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+template <int N, bool I8>
+static void run_part7() {
+  const int iters = 512;
+  long long* d;
+  cudaMalloc(&d, 8);
+  auto k = part7<N, I8>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  k<<<1, 128, 100 * 1024>>>(iters, d);
+  k<<<1, 128, 100 * 1024>>>(iters, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h = 0;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("unrolled MMA TS %s K32 N=%3d: %s %.1f cycles/MMA\n", I8 ? "i8" : "f8", N, cudaGetErrorString(e),
+         double(h) / (iters * 8));
+  cudaFree(d);
+}
+
+int main() {
+  setvbuf(stdout, NULL, _IONBF, 0);
+  srand(7);
+  int g2 = run_part1(2);
+  int g3 = run_part1(3);
+  printf("working variant: 2-bit %d, 3-bit %d\n", g2, g3);
+  run_part6<false>();
+  run_part6<true>();
+  run_part5<8, false>();
+  run_part5<16, false>();
+
+  run_part7<8, false>();
+  run_part7<32, false>();
+  run_part7<8, true>();
+  run_part7<32, true>();
+  run_part4<8, 1, false>();
+  run_part4<8, 2, false>();
+  run_part4<8, 4, false>();
+  run_part4<8, 8, false>();
+  run_part4<16, 8, false>();
+  run_part4<32, 8, false>();
+  run_part4<64, 4, false>();
+  run_part4<8, 1, true>();
+  run_part4<8, 8, true>();
+  run_part4<32, 8, true>();
+  run_part3<true, 8, 0>(1);
+  run_part3<true, 16, 0>(1);
+  run_part3<true, 64, 0>(1);
+  run_part3<true, 256, 0>(1);
+  run_part3<false, 8, 0>(1);
+  run_part3<false, 16, 0>(1);
+  run_part3<false, 256, 0>(1);
+  run_part3<true, 8, 4>(1);
+  run_part3<true, 8, 0>(148);
+  run_part2<2, 8, 8, false>("2-bit 8 dec warps, 8 slots");
+  run_part2<2, 8, 8, true>("2-bit 8 dec, 8 slots, epi");
+  run_part2<2, 4, 8, true>("2-bit 4 dec, 8 slots, epi");
+  run_part2<2, 8, 12, true>("2-bit 8 dec, 12 slots, epi");
+  run_part2<3, 8, 8, true>("3-bit 8 dec, 8 slots, epi");
+  return 0;
+}
