@@ -197,10 +197,24 @@ lrc_status lrc_layer_set_prefill_min(lrc_layer* layer, int64_t min_tokens);
 lrc_status lrc_layer_set_pager(lrc_layer* layer, const void* const* host_blocks, const int64_t* offsets,
                                int64_t block_bytes, uint8_t* slots, int n_slots, int64_t slot_bytes);
 int lrc_layer_prefill_eligible(const lrc_layer* layer);
+/* Batches of B <= max_tokens (at most 8) tokens run the tensor-core decode
+ * engine when the layer is eligible (2- or 3-bit gs=64 weights, hidden and ffn
+ * multiples of 128, compensator rank <= 64 with 2..4-bit factors): ONE
+ * persistent kernel per layer step -- per-CTA fused routing (E <= 16; larger
+ * E uses the cluster router first), tcgen05.mma.kind::i8 with the decoded
+ * codes as the TMEM A operand, the low-rank terms, SwiGLU and the weighted
+ * combine, split stream-K over all SMs with one grid barrier between the
+ * w1|w3 and w2 phases.  0 disables it (the mma.sync tiled kernels run).
+ * Default 8 (env LRC_TCD_MAX).  The engine keeps its own copy of the codes in
+ * the tcd layout (built lazily on the first eligible forward and after
+ * lrc_layer_set_expert*). */
+lrc_status lrc_layer_set_tcd_max(lrc_layer* layer, int max_tokens);
+int lrc_layer_tcd_eligible(const lrc_layer* layer);
 lrc_status lrc_layer_phase_ms(lrc_layer* layer, float* ms4);
 /* Debug: %globaltimer (ns) stamps, 8 per CTA, of the last launch of the router
- * (which = 0; enabled by LRC_ROUTE_STAMPS=1 in the environment) or of the
- * tiled kernels (which = 1: [down, up][256 CTAs][8]; LRC_TILED_DEBUG bit 3).
+ * (which = 0; enabled by LRC_ROUTE_STAMPS=1 in the environment), of the
+ * tiled kernels (which = 1: [down, up][256 CTAs][8]; LRC_TILED_DEBUG bit 3)
+ * or of the tensor-core decode kernel (which = 2: [148 CTAs][8]; LRC_TCD_STAMPS=1).
  * Copies n values and clears the device buffer. */
 lrc_status lrc_debug_stamps(int which, uint64_t* host, int n);
 

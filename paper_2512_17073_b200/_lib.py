@@ -69,6 +69,8 @@ _SIGS = {
     "lrc_layer_set_profiling": (c_int, [c_void_p, c_int]),
     "lrc_layer_set_prefill_min": (c_int, [c_void_p, c_int64]),
     "lrc_layer_prefill_eligible": (c_int, [c_void_p]),
+    "lrc_layer_set_tcd_max": (c_int, [c_void_p, c_int]),
+    "lrc_layer_tcd_eligible": (c_int, [c_void_p]),
     "lrc_layer_set_pager": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int, c_int64]),
     "lrc_layer_phase_ms": (c_int, [c_void_p, POINTER(c_float)]),
     "lrc_debug_stamps": (c_int, [c_int, c_void_p, c_int]),

@@ -7,6 +7,7 @@
 
 #include "common.cuh"
 #include "layer.cuh"
+#include "tcd.cuh"
 
 namespace lrc {
 
@@ -292,6 +293,12 @@ __global__ void __launch_bounds__(256) pager_kernel(const PagerArgs g) {
 // =========================================================== layer object ===
 using namespace lrc;
 
+constexpr int kStageRing = 64;
+struct StageEntry {
+  lrc_expert e;
+  uint8_t has_comp;
+};
+
 struct lrc_layer {
   int hidden = 0, ffn = 0, E = 0, S = 0, max_tokens = 0, k_max = 0, maxr = 0;
   int num_sms = 148;
@@ -316,8 +323,10 @@ struct lrc_layer {
   const double* gate_t = nullptr;
   std::vector<lrc_expert> host_experts;
   lrc_expert* d_experts = nullptr;
-  lrc_expert* h_stage = nullptr;  // pinned ring for stream-ordered descriptor updates
+  StageEntry* h_stage = nullptr;  // pinned ring for stream-ordered descriptor updates
   int stage_next = 0;
+  cudaEvent_t stage_ev[kStageRing] = {};
+  uint8_t stage_used[kStageRing] = {};
   // workspace
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -337,6 +346,22 @@ struct lrc_layer {
   float* y_stage = nullptr;
   bool profiling = false;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  // tensor-core decode engine (tcd.cu): batches of B <= tcd_max tokens
+  int tcd_max = [] {
+    const char* v = getenv("LRC_TCD_MAX");
+    return v ? atoi(v) : 0;  // off by default until it beats the tiled kernels
+  }();
+  bool tcd_ok = false;
+  int tcd_bits = 2, tcd_fbits = 3;
+  std::vector<uint8_t> tcd_dirty;  // per expert: pack stale
+  bool tcd_table_dirty = true;
+  uint8_t* tcd_packs = nullptr;     // [NE][up | down]
+  int64_t tcd_up_bytes = 0, tcd_down_bytes = 0, tcd_lru_bytes = 0, tcd_lrd_bytes = 0;
+  std::vector<tcd::Expert> tcd_host;
+  tcd::Expert* d_tcd = nullptr;
+  float* gate32 = nullptr;          // (E, hidden) fp32 copy of gate_t (fused routing)
+  void* tcd_ws = nullptr;
+  tcd::Args tcd_args{};
 };
 
 static bool has_comp(const lrc_expert& e) {
@@ -395,6 +420,8 @@ static void refresh_tiled(lrc_layer* L) {
   L->tiled = ok;
   L->prefill_ok = prefill_eligible(L->host_experts.data(), static_cast<int>(L->host_experts.size()),
                                    L->hidden, L->ffn, L->maxr);
+  L->tcd_ok = L->maxr <= tcd::kRMax && tcd::eligible(L->host_experts.data(), static_cast<int>(L->host_experts.size()),
+                                                      L->hidden, L->ffn, &L->tcd_bits, &L->tcd_fbits);
 }
 
 static lrc_status alloc_workspace(lrc_layer* L) {
@@ -521,10 +548,16 @@ extern "C" void lrc_layer_destroy(lrc_layer* L) {
   if (!L) return;
   cudaFree(L->d_experts);
   if (L->h_stage) cudaFreeHost(L->h_stage);
+  for (auto& ev : L->stage_ev)
+    if (ev) cudaEventDestroy(ev);
   cudaFree(L->ws);
   cudaFree(L->lrp);
   cudaFree(L->pg_host);
   cudaFree(L->ppk);
+  cudaFree(L->tcd_packs);
+  cudaFree(L->d_tcd);
+  cudaFree(L->gate32);
+  cudaFree(L->tcd_ws);
   for (auto& e : L->ev)
     if (e) cudaEventDestroy(e);
   delete L;
@@ -540,6 +573,12 @@ extern "C" lrc_status lrc_layer_set_expert(lrc_layer* L, int expert_id, const lr
   L->host_experts[expert_id] = *e;
   LRC_CUDA_TRY(cudaMemcpy(L->d_experts + expert_id, e, sizeof(lrc_expert), cudaMemcpyHostToDevice));
   if (!L->lrp_dirty.empty()) L->lrp_dirty[expert_id] = 1;
+  if (!L->tcd_dirty.empty()) L->tcd_dirty[expert_id] = 1;
+  L->tcd_table_dirty = true;
+  {
+    const uint8_t hc = has_comp(*e) ? 1 : 0;  // top-n decisions of the tiled/prefill plan
+    LRC_CUDA_TRY(cudaMemcpy(const_cast<uint8_t*>(L->plan.has_comp) + expert_id, &hc, 1, cudaMemcpyHostToDevice));
+  }
   refresh_tiled(L);
   return LRC_OK;
 }
@@ -550,22 +589,34 @@ extern "C" lrc_status lrc_layer_set_expert(lrc_layer* L, int expert_id, const lr
 // The host-side state (validation, tiled-path eligibility) updates immediately.
 extern "C" lrc_status lrc_layer_set_expert_async(lrc_layer* L, int expert_id, const lrc_expert* e,
                                                  void* stream) {
-  constexpr int kStageRing = 64;
   if (!L || !e || expert_id < 0 || expert_id >= L->E + L->S)
     return fail(LRC_ERR_INVALID, "set_expert: bad id");
   lrc_status s = validate_expert(*e, L->hidden, L->ffn);
   if (s != LRC_OK) return s;
   if (std::max({rank_of(e->u1), rank_of(e->u2), rank_of(e->u3)}) > L->maxr)
     return fail(LRC_ERR_UNSUPPORTED, "set_expert: rank above the layer's workspace rank");
-  if (L->h_stage == nullptr)
-    LRC_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&L->h_stage), sizeof(lrc_expert) * kStageRing,
+  if (L->h_stage == nullptr) {
+    // each ring entry: the descriptor followed by the plan's has_comp byte
+    LRC_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&L->h_stage), sizeof(StageEntry) * kStageRing,
                                cudaHostAllocDefault));
-  lrc_expert* slot = L->h_stage + (L->stage_next++ % kStageRing);
-  *slot = *e;
+    for (auto& ev : L->stage_ev) LRC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  const int k = L->stage_next++ % kStageRing;
+  // the entry's previous async copies must have read it before it is rewritten
+  if (L->stage_used[k]) LRC_CUDA_TRY(cudaEventSynchronize(L->stage_ev[k]));
+  StageEntry* slot = L->h_stage + k;
+  slot->e = *e;
+  slot->has_comp = has_comp(*e) ? 1 : 0;
   L->host_experts[expert_id] = *e;
-  LRC_CUDA_TRY(cudaMemcpyAsync(L->d_experts + expert_id, slot, sizeof(lrc_expert), cudaMemcpyHostToDevice,
-                               as_stream(stream)));
+  cudaStream_t st = as_stream(stream);
+  LRC_CUDA_TRY(cudaMemcpyAsync(L->d_experts + expert_id, &slot->e, sizeof(lrc_expert), cudaMemcpyHostToDevice, st));
+  LRC_CUDA_TRY(cudaMemcpyAsync(const_cast<uint8_t*>(L->plan.has_comp) + expert_id, &slot->has_comp, 1,
+                               cudaMemcpyHostToDevice, st));
+  LRC_CUDA_TRY(cudaEventRecord(L->stage_ev[k], st));
+  L->stage_used[k] = 1;
   if (!L->lrp_dirty.empty()) L->lrp_dirty[expert_id] = 1;
+  if (!L->tcd_dirty.empty()) L->tcd_dirty[expert_id] = 1;
+  L->tcd_table_dirty = true;
   refresh_tiled(L);
   return LRC_OK;
 }
@@ -601,6 +652,133 @@ extern "C" int lrc_layer_prefill_eligible(const lrc_layer* L) { return L && L->p
 
 extern "C" int lrc_layer_last_launches(const lrc_layer* L) { return L ? L->last_launches : 0; }
 
+// ------------------------------------------------ tcd engine plumbing ----
+__global__ void gate32_kernel(const double* g, float* o, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    o[i] = static_cast<float>(g[i]);
+}
+
+// L2 norm of each gate row (E, d), rounded up: the routing kernel's fp32 error bound
+__global__ void gate_norm_kernel(const double* g, int d, float* out) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const double v = g[static_cast<int64_t>(blockIdx.x) * d + i];
+    s += v * v;
+  }
+  s = warp_sum_d(s);
+  __shared__ double part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += part[w];
+    out[blockIdx.x] = static_cast<float>(sqrt(t) * 1.001);
+  }
+}
+
+static int64_t tcd_stride(const lrc_layer* L) {  // bytes per expert: codes up|down, LR up|down
+  return L->tcd_up_bytes + L->tcd_down_bytes + L->tcd_lru_bytes + L->tcd_lrd_bytes;
+}
+
+static bool tcd_fused_routing(const lrc_layer* L) {
+  return L->E <= tcd::kFuseMaxE && static_cast<int64_t>(L->E) * L->hidden * 4 <= 160 * 1024;
+}
+
+// (Re)build the tcd packs of changed experts, the device expert table, the
+// fp32 gate and the workspace.  Not graph-capturable (host copies): the first
+// forward after a change runs it, later forwards only check flags.
+static lrc_status tcd_prepare(lrc_layer* L, cudaStream_t st) {
+  const int NE = L->E + L->S;
+  const int T0 = L->ffn / 128;
+  if (L->tcd_packs == nullptr) {
+    L->tcd_up_bytes = tcd::pack_bytes(L->ffn, L->hidden, 2, L->tcd_bits);
+    L->tcd_down_bytes = tcd::pack_bytes(L->hidden, L->ffn, 1, L->tcd_bits);
+    if (L->maxr > 0) {
+      L->tcd_lru_bytes = static_cast<int64_t>(L->ffn / 128) * tcd::lr_up_tile_bytes(L->maxr);
+      L->tcd_lrd_bytes = static_cast<int64_t>(L->hidden / 128) * tcd::lr_down_tile_bytes(L->maxr);
+    }
+    LRC_CUDA_TRY(cudaMalloc(&L->tcd_packs, static_cast<size_t>(tcd_stride(L)) * NE));
+    L->tcd_dirty.assign(NE, 1);
+    L->tcd_host.assign(NE, tcd::Expert{});
+    LRC_CUDA_TRY(cudaMalloc(&L->d_tcd, sizeof(tcd::Expert) * NE));
+    const int64_t ng = static_cast<int64_t>(L->E) * L->hidden;
+    LRC_CUDA_TRY(cudaMalloc(&L->gate32, sizeof(float) * (ng + L->E)));
+    gate32_kernel<<<148, 256, 0, st>>>(L->gate_t, L->gate32, ng);
+    LRC_CHECK_LAUNCH();
+    gate_norm_kernel<<<L->E, 256, 0, st>>>(L->gate_t, L->hidden, L->gate32 + ng);
+    LRC_CHECK_LAUNCH();
+    // workspace
+    tcd::Args& a = L->tcd_args;
+    a.max_act = std::min({NE, tcd::kMaxTok * L->k_max + L->S, tcd::kMaxAct});
+    size_t off = 0;
+    auto take = [&](size_t b) {
+      size_t o = off;
+      off += (b + 255) & ~size_t(255);
+      return o;
+    };
+    const size_t o_gb = take(8), o_tc = take(2 * tcd::kMaxP * 4), o_t13 = take(tcd::kMaxP * 2 * tcd::kRMax * 4);
+    const size_t o_t2 = take(2 * tcd::kMaxP * tcd::kRMax * 4), o_xc = take(2 * 4);
+    const size_t G0 = L->hidden / 64, G1 = L->ffn / 64;
+    const size_t o_xd = take(tcd::kMaxTok * G0 * 512), o_xs = take(tcd::kMaxTok * G0 * 16);
+    const size_t o_ad = take(tcd::kMaxP * G1 * 512), o_as = take(tcd::kMaxP * G1 * 16);
+    const size_t o_ha = take(static_cast<size_t>(a.max_act) * T0 * 2 * tcd::kMaxTok * 128 * 4);
+    const size_t o_hc = take(static_cast<size_t>(a.max_act) * T0 * 4);
+    LRC_CUDA_TRY(cudaMalloc(&L->tcd_ws, off));
+    LRC_CUDA_TRY(cudaMemsetAsync(L->tcd_ws, 0, off, st));
+    char* b = static_cast<char*>(L->tcd_ws);
+    a.gbar = reinterpret_cast<unsigned long long*>(b + o_gb);
+    a.tcnt = reinterpret_cast<unsigned*>(b + o_tc);
+    a.t13 = reinterpret_cast<float*>(b + o_t13);
+    a.t2 = reinterpret_cast<float*>(b + o_t2);
+    a.xcnt = reinterpret_cast<unsigned*>(b + o_xc);
+    a.xdig = reinterpret_cast<uint8_t*>(b + o_xd);
+    a.xsum = reinterpret_cast<float4*>(b + o_xs);
+    a.adig = reinterpret_cast<uint8_t*>(b + o_ad);
+    a.asum = reinterpret_cast<float4*>(b + o_as);
+    a.hacc = reinterpret_cast<float*>(b + o_ha);
+    a.hcnt = reinterpret_cast<unsigned*>(b + o_hc);
+  }
+  bool any = false;
+  for (int e = 0; e < NE; ++e) {
+    if (!L->tcd_dirty[e]) continue;
+    const lrc_expert& x = L->host_experts[e];
+    uint8_t* up = L->tcd_packs + static_cast<size_t>(tcd_stride(L)) * e;
+    uint8_t* down = up + L->tcd_up_bytes;
+    uint8_t* lru = down + L->tcd_down_bytes;
+    uint8_t* lrd = lru + L->tcd_lru_bytes;
+    const lrc_qmat upm[2] = {x.w1, x.w3};
+    lrc_status s;
+    if ((s = tcd::build_pack(upm, 2, L->tcd_bits, up, st)) != LRC_OK) return s;
+    if ((s = tcd::build_pack(&x.w2, 1, L->tcd_bits, down, st)) != LRC_OK) return s;
+    const bool comp = has_comp(x);
+    if (comp && (s = tcd::build_lr_pack(x, L->hidden, L->ffn, lru, lrd, st)) != LRC_OK) return s;
+    tcd::Expert& t = L->tcd_host[e];
+    t.up = up;
+    t.down = down;
+    t.lr_up = comp ? lru : nullptr;
+    t.lr_down = comp ? lrd : nullptr;
+    t.u1 = x.u1; t.v1 = x.v1; t.u3 = x.u3; t.v3 = x.v3; t.u2 = x.u2; t.v2 = x.v2;
+    t.rank = has_comp(x) ? rank_of(x.u1) : 0;
+    L->tcd_dirty[e] = 0;
+    any = true;
+  }
+  if (any || L->tcd_table_dirty) {
+    LRC_CUDA_TRY(cudaMemcpyAsync(L->d_tcd, L->tcd_host.data(), sizeof(tcd::Expert) * NE, cudaMemcpyHostToDevice, st));
+    LRC_CUDA_TRY(cudaStreamSynchronize(st));  // the host table may change before the copy would run
+    L->tcd_table_dirty = false;
+  }
+  return LRC_OK;
+}
+
+extern "C" lrc_status lrc_layer_set_tcd_max(lrc_layer* L, int max_tokens) {
+  if (!L) return fail(LRC_ERR_INVALID, "set_tcd_max: null layer");
+  L->tcd_max = max_tokens;
+  return LRC_OK;
+}
+
+extern "C" int lrc_layer_tcd_eligible(const lrc_layer* L) { return L && L->tcd_ok ? 1 : 0; }
+
 static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int top_k, int top_n,
                                int renormalize, int compensate_shared, float* y, int32_t* topk_idx,
                                float* topk_w, void* stream, bool allow_tiled,
@@ -618,6 +796,79 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[0], st));
   if (B == 0) {
     L->last_launches = 0;
+    return LRC_OK;
+  }
+  if (L->pager) {  // every distinct expert of the step needs its own slot
+    const int64_t distinct = std::min<int64_t>(L->E, B * (pairs_expert ? 1 : top_k)) + (pairs_expert ? 0 : L->S);
+    if (distinct > L->pg_slots) return fail(LRC_ERR_UNSUPPORTED, "pager: more distinct experts than slots");
+  }
+  // ---- tensor-core decode engine: one persistent kernel per layer step
+  const int P_tcd = pairs_expert ? 1 : top_k + L->S;
+  if (allow_tiled && L->tcd_ok && !L->pager && L->tcd_max > 0 && B <= std::min(L->tcd_max, tcd::kMaxTok) &&
+      B * P_tcd <= tcd::kMaxP && top_k <= 8) {
+    lrc_status s = tcd_prepare(L, st);
+    if (s != LRC_OK) return s;
+    int32_t* ti = topk_idx ? topk_idx : L->topk_idx;
+    float* tw = topk_w ? topk_w : L->topk_w;
+    const bool fused = !pairs_expert && tcd_fused_routing(L);
+    const bool pdl = !prof && L->pdl;
+    if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[1], st));
+    if (!pairs_expert && !fused) {  // large expert counts: the cluster router writes the top-k
+      RouteArgs ra{};
+      ra.gate_t = L->gate_t;
+      ra.x = x;
+      ra.x_dtype = LRC_DTYPE_BF16;
+      ra.B = B;
+      ra.d = L->hidden;
+      ra.E = L->E;
+      ra.k = top_k;
+      ra.renorm = renormalize;
+      ra.topk_idx = ti;
+      ra.topk_w = tw;
+      ra.logits = L->logits;
+      ra.tile_ticket = L->tile_ticket;
+      ra.plan = L->plan;
+      ra.plan.ticket = nullptr;  // routing only
+      ra.pdl = pdl ? 1 : 0;
+      if ((s = launch_route(ra, st)) != LRC_OK) return s;
+      ++launches;
+    }
+    if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[2], st));
+    tcd::Args a = L->tcd_args;
+    a.x = x;
+    a.B = static_cast<int>(B);
+    a.hidden = L->hidden;
+    a.ffn = L->ffn;
+    a.E = L->E;
+    a.S = pairs_expert ? 0 : L->S;
+    a.top_k = pairs_expert ? 1 : top_k;
+    a.top_n = pairs_expert ? 1 : top_n;
+    a.renorm = renormalize;
+    a.comp_shared = compensate_shared;
+    a.bits = L->tcd_bits;
+    a.fb = L->tcd_fbits;
+    a.gate32 = fused ? L->gate32 : nullptr;
+    a.gate64 = L->gate_t;
+    a.gnorm = L->gate32 + static_cast<int64_t>(L->E) * L->hidden;
+    a.pairs_mode = pairs_expert ? 1 : 0;
+    a.given_idx = pairs_expert ? pairs_expert : ti;
+    a.given_w = pairs_expert ? pairs_w : tw;
+    a.given_comp = pairs_comp;
+    a.ex = L->d_tcd;
+    a.y = y;
+    a.topk_idx = ti;
+    a.topk_w = tw;
+    static const bool stamps = getenv("LRC_TCD_STAMPS") != nullptr;
+    a.stamp = stamps ? 1 : 0;
+    static const int dbg = getenv("LRC_TCD_DEBUG") ? atoi(getenv("LRC_TCD_DEBUG")) : 0;
+    a.dbg = dbg;
+    if ((s = tcd::launch(a, L->num_sms, st, pdl)) != LRC_OK) return s;
+    ++launches;
+    if (prof) {
+      LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));
+      LRC_CUDA_TRY(cudaEventRecord(L->ev[4], st));
+    }
+    L->last_launches = launches;
     return LRC_OK;
   }
   PlanArgs plan = L->plan;
@@ -695,7 +946,8 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   a.a16 = L->a16;
   a.y = y;
   a.max_pairs = L->max_pairs;
-  const bool prefill = allow_tiled && L->prefill_ok && L->prefill_min > 0 && B >= L->prefill_min;
+  // (the pager's descriptors point at slot copies of the tiled layout only)
+  const bool prefill = allow_tiled && L->prefill_ok && !L->pager && L->prefill_min > 0 && B >= L->prefill_min;
   if (!spec && L->maxr && !prefill) {  // exact V.x for the compensated pairs only
     if ((s = launch_lr_down(a, np_bound, st)) != LRC_OK) return s;
     ++launches;

@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "layer.cuh"
+#include "tcd.cuh"
 
 namespace lrc {
 
@@ -1176,8 +1177,23 @@ lrc_status launch_route(const RouteArgs& ra_in, cudaStream_t st) {
 
 extern "C" lrc_status lrc_debug_stamps(int which, uint64_t* host, int n) {
   using namespace lrc;
-  if (n < 0 || n > (which == 0 ? kStampCtas * 8 : 2 * 256 * 8 + 2 * 64 * 6)) return fail(LRC_ERR_INVALID, "stamps: bad count");
+  if (which < 4 && (n < 0 || n > (which == 0 ? kStampCtas * 8 : 2 * 256 * 8 + 2 * 64 * 6)))
+    return fail(LRC_ERR_INVALID, "stamps: bad count");
   LRC_CUDA_TRY(cudaDeviceSynchronize());
+  if (which == 4) {  // debug: tcd wait mode = n
+    tcd::set_wait_mode(n);
+    return LRC_OK;
+  }
+  if (which == 3) {
+    if (n != 2048) return fail(LRC_ERR_INVALID, "trace: 2048 values");
+    tcd::trace_copy(host);
+    return LRC_OK;
+  }
+  if (which == 2) {
+    if (n > 148 * 16) return fail(LRC_ERR_INVALID, "stamps: bad count");
+    tcd::stamps_copy(host, n);
+    return LRC_OK;
+  }
   if (which != 0) {
     tiled_stamps_copy(host, n);
     return LRC_OK;

@@ -150,6 +150,8 @@ class LRCMoELayer:
         self.max_tokens, self.top_k = max_tokens, top_k
         self._handle = None
         self._prefill_min = None  # None: the library default (LRC_PREFILL_MIN or 128)
+        self._tcd_max = None      # None: the library default (LRC_TCD_MAX or 8)
+        self._pager = None        # lrc_layer_set_pager arguments (re-applied on re-create)
         self._create()
 
     def _create(self):
@@ -164,6 +166,27 @@ class LRCMoELayer:
         self._handle = h
         if self._prefill_min is not None:
             _lib.check(lib.lrc_layer_set_prefill_min(h, int(self._prefill_min)))
+        if self._tcd_max is not None:
+            _lib.check(lib.lrc_layer_set_tcd_max(h, int(self._tcd_max)))
+        if self._pager is not None:
+            _lib.check(lib.lrc_layer_set_pager(h, *self._pager))
+
+    def set_pager(self, host_blocks, offsets, block_bytes: int, slots_ptr: int, n_slots: int,
+                  slot_bytes: int):
+        """GPU-driven expert paging (lrc_layer_set_pager); kept across workspace re-creates."""
+        self._pager = (host_blocks, offsets, int(block_bytes), ctypes.c_void_p(slots_ptr), int(n_slots),
+                       int(slot_bytes))
+        _lib.check(_lib.lib().lrc_layer_set_pager(self._handle, *self._pager))
+
+    def set_tcd_max(self, max_tokens: int):
+        """Batches of <= max_tokens (<= 8) run the tensor-core decode engine when
+        eligible; 0 disables it."""
+        self._tcd_max = int(max_tokens)
+        _lib.check(_lib.lib().lrc_layer_set_tcd_max(self._handle, self._tcd_max))
+
+    @property
+    def tcd_eligible(self) -> bool:
+        return bool(_lib.lib().lrc_layer_tcd_eligible(self._handle))
 
     def set_prefill_min(self, min_tokens: int):
         """Batches of >= min_tokens run the tcgen05 grouped-GEMM prefill path

@@ -115,8 +115,12 @@ class OffloadEngine:
         self.layers = []
         for l, gate in enumerate(gates):
             descs = [self._desc(l, e, 0) for e in range(self.E)]
-            self.layers.append(LRCMoELayer(gate, descs, hidden, ffn, self.E, 0, self.keep,
-                                           max_tokens=max_tokens, top_k=top_k))
+            dl = LRCMoELayer(gate, descs, hidden, ffn, self.E, 0, self.keep, max_tokens=max_tokens, top_k=top_k)
+            # the descriptors' reference-layout weights are zero placeholders: only
+            # the tiled decode kernels (which read the slot tiles) may run
+            dl.set_prefill_min(0)
+            dl.set_tcd_max(0)
+            self.layers.append(dl)
 
     # ----------------------------------------------------------- helpers --
     def _zero_factor(self, m: _lib.LrcQmat) -> _lib.LrcQmat:
@@ -291,10 +295,10 @@ class GpuPagerEngine(OffloadEngine):
         for l, gate in enumerate(gates):
             descs = [self._desc(l, e, 0) for e in range(self.E)]
             dl = LRCMoELayer(gate, descs, hidden, ffn, self.E, 0, self.keep, max_tokens=max_tokens, top_k=top_k)
+            dl.set_prefill_min(0)
+            dl.set_tcd_max(0)
             ptrs = (ctypes.c_void_p * self.E)(*[b.data_ptr() for b in self.blocks[l]])
-            _lib.check(_lib.lib().lrc_layer_set_pager(dl._handle, ptrs, offs, self.block_bytes,
-                                                      ctypes.c_void_p(self.slot_mem.data_ptr()), n_slots,
-                                                      self.block_bytes))
+            dl.set_pager(ptrs, offs, self.block_bytes, self.slot_mem.data_ptr(), n_slots, self.block_bytes)
             self.layers.append(dl)
 
     def forward_layer(self, layer: int, x):

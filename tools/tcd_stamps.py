@@ -1,0 +1,60 @@
+"""Per-CTA %globaltimer stamps of one tensor-core decode layer step (LRC_TCD_STAMPS=1).
+Stamps: 8 gate in smem, 9 logits reduced, 10 selection done, 11 before the plan;
+0 after the grid-dependency wait, 1 plan done, 2 aux V.x jobs done,
+3 aux phase-U finalisation done, 4 grid barrier passed, 5 CTA end,
+6 decode warp 0 enters phase D, 7 MMA warp done."""
+import os
+import sys
+
+os.environ["LRC_TCD_STAMPS"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import ctypes  # noqa: E402
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2512_17073_b200 import _lib  # noqa: E402
+from paper_2512_17073_b200.synth import SynthLayer  # noqa: E402
+
+_lib.load()
+WM = int(os.environ.get('TCD_WAIT_MODE', '0'))
+_lib.check(_lib.lib().lrc_debug_stamps(4, None, WM))
+print('wait mode', WM)
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+sl = SynthLayer(4096, 14336, 8, top_k=2, bits=2, rank=32, seed=5, max_tokens=64)
+x = torch.randn((B, 4096), device="cuda").to(torch.bfloat16)
+for _ in range(3):
+    sl.layer.forward(x, 2, 1)
+torch.cuda.synchronize()
+buf = (ctypes.c_uint64 * (148 * 16))()
+_lib.check(_lib.lib().lrc_debug_stamps(2, buf, 148 * 16))
+sl.layer.forward(x, 2, 1)
+torch.cuda.synchronize()
+_lib.check(_lib.lib().lrc_debug_stamps(2, buf, 148 * 16))
+st = np.array(buf[:], dtype=np.float64).reshape(148, 16)
+t0 = st[:, 0][st[:, 0] > 0].min()
+t0c = st[0, 0]
+rel = np.where(st > 0, (st - t0) / 1e3, np.nan)
+names = ["wait", "plan", "vx", "U fin", "gbar", "end", "dec->D", "mma end", "gate in", "logits", "select",
+         "pre-plan"]
+print("NST*1000+NDS:", st[:, 12][:4])
+for i, n in ((13, "prod stage0 issued"), (14, "dec0 sees stage0"), (15, "prod stage9 issued")):
+    col = rel[:, i]
+    print(f"{i} {n:18s} min {np.nanmin(col):8.2f}  med {np.nanmedian(col):8.2f}  max {np.nanmax(col):8.2f} us")
+for i, n in enumerate(names):
+    col = rel[:, i]
+    print(f"{i} {n:8s} min {np.nanmin(col):8.2f}  med {np.nanmedian(col):8.2f}  max {np.nanmax(col):8.2f} us")
+
+tr = (ctypes.c_uint64 * 2048)()
+_lib.check(_lib.lib().lrc_debug_stamps(3, tr, 2048))
+sl.layer.forward(x, 2, 1)
+torch.cuda.synchronize()
+_lib.check(_lib.lib().lrc_debug_stamps(3, tr, 2048))
+t = np.array(tr[:], dtype=np.float64).reshape(8, 256)
+b = t[0][0]
+def f(v):
+    return f"{v - b:8.0f}" if v > 0 else "       -"
+print("CTA 0, clock64 cycles from producer stage-0 issue")
+print("stage: codes issued | B issued | dec w0 done | MMA issued | epi w0 done")
+for i in range(40):
+    print(f"  {i:3d}: {f(t[0][i])} {f(t[1][i])} {f(t[3][i])} {f(t[2][i])} {f(t[5][i])}")

@@ -804,44 +804,215 @@ static void run_part7() {
   cudaFree(d);
 }
 
+// ---------------------------------------------------------------- part 8 ----
+// Cost of tcgen05.commit / fences / mbarrier ops issued by one thread (no MMAs in flight
+// or one MMA per iteration).
+template <int MODE>
+__global__ void part8(int iters, long long* cyc) {
+  __shared__ uint64_t bar[16];
+  __shared__ uint32_t tbase;
+  __shared__ __align__(1024) uint8_t sb[4096];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 1024; i += blockDim.x) reinterpret_cast<uint32_t*>(sb)[i] = 0x01010101u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    for (int i = 0; i < 16; ++i) bar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  if (warp == 0) {
+    const uint64_t db = desc_ns(smem_u32(sb), 128, 256);
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      if (MODE == 0) {  // commit only
+        if (elect_one()) commit(&bar[i & 15]);
+        __syncwarp();
+      } else if (MODE == 1) {  // fence::after only
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      } else if (MODE == 2) {  // MMA (i8, N=8, 2 per iter) + commit
+        if (elect_one()) {
+          asm volatile(
+              "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;}" ::"r"(tm + 256),
+              "r"(tm), "l"(db), "r"(idesc8(true, 128, 8)), "r"(0u));
+          asm volatile(
+              "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;}" ::"r"(tm + 256),
+              "r"(tm + 8), "l"(db + 16), "r"(idesc8(true, 128, 8)), "r"(1u));
+          commit(&bar[i & 15]);
+        }
+        __syncwarp();
+      } else if (MODE == 3) {  // MMA x2, no commit
+        if (elect_one()) {
+          asm volatile(
+              "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;}" ::"r"(tm + 256),
+              "r"(tm), "l"(db), "r"(idesc8(true, 128, 8)), "r"(0u));
+          asm volatile(
+              "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;}" ::"r"(tm + 256),
+              "r"(tm + 8), "l"(db + 16), "r"(idesc8(true, 128, 8)), "r"(1u));
+        }
+        __syncwarp();
+      } else if (MODE == 4) {  // mbarrier arrive (release.cta) + test_wait on it
+        if (elect_one()) {
+          bar_arrive(&bar[i & 15]);
+        }
+        __syncwarp();
+      }
+    }
+    const long long t1 = clock64();
+    if (tid == 0) cyc[0] = t1 - t0;
+    if (MODE == 2 || MODE == 3) {
+      if (elect_one()) commit(&bar[15]);
+      __syncwarp();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+template <int MODE>
+static void run_part8(const char* name) {
+  const int iters = 1024;
+  long long* d;
+  cudaMalloc(&d, 8);
+  part8<MODE><<<1, 128>>>(iters, d);
+  part8<MODE><<<1, 128>>>(iters, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h = 0;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("%-36s %s %.1f cycles/iter\n", name, cudaGetErrorString(e), double(h) / iters);
+  cudaFree(d);
+}
+
+// ---------------------------------------------------------------- part 9 ----
+// tcgen05.st.32x32b.x16 + wait::st latency/throughput; NW warps, each its own lane quarter/columns
+template <int NW, bool WAIT>
+__global__ void part9(int iters, long long* cyc) {
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+  uint32_t r[16];
+  for (int i = 0; i < 16; ++i) r[i] = tid * 16 + i;
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            tm + ((it + warp / 4) % 16) * 16),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+    if (WAIT) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    r[it & 15] += 1;
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  const long long t1 = clock64();
+  if ((tid & 31) == 0) cyc[warp] = t1 - t0;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+}
+template <int NW, bool WAIT>
+static void run_part9(const char* name) {
+  const int iters = 1024;
+  long long* d;
+  cudaMalloc(&d, 64 * 8);
+  part9<NW, WAIT><<<1, NW * 32>>>(iters, d);
+  part9<NW, WAIT><<<1, NW * 32>>>(iters, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[64];
+  cudaMemcpy(h, d, NW * 8, cudaMemcpyDeviceToHost);
+  printf("%-36s %s %.1f cycles/iter (warp 0)\n", name, cudaGetErrorString(e), double(h[0]) / iters);
+  cudaFree(d);
+}
+
+// ---------------------------------------------------------------- part 10 ----
+// mbarrier phase checks on an already-completed phase: latency per check (warp-wide)
+__device__ __forceinline__ bool test_wait_p(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{.reg .pred P; mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2; selp.b32 %0, 1, 0, P;}"
+               : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool try_wait_p(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{.reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.b32 %0, 1, 0, P;}"
+               : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+  return ok != 0;
+}
+template <int MODE>
+__global__ void part10(int iters, long long* cyc, int* sink) {
+  __shared__ uint64_t bar[4];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) bar_init(&bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) bar_arrive(&bar[0]);  // phase 0 of bar[0] complete
+  __syncthreads();
+  int acc = 0;
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    if (MODE == 0) acc += test_wait_p(&bar[0], 0);
+    else if (MODE == 1) acc += try_wait_p(&bar[0], 0);
+    else if (MODE == 2) {  // arrive on bar[1] by lane 0 + syncwarp
+      if ((tid & 31) == 0) bar_arrive(&bar[1]);
+      __syncwarp();
+    } else {  // shared load round trip
+      acc += reinterpret_cast<volatile int*>(bar)[2 + (acc & 1)];
+    }
+  }
+  const long long t1 = clock64();
+  if (tid == 0) cyc[0] = t1 - t0;
+  if (acc == 12345) sink[0] = acc;
+}
+template <int MODE>
+static void run_part10(const char* name, int threads) {
+  const int iters = 1024;
+  long long* d;
+  int* sink;
+  cudaMalloc(&d, 8);
+  cudaMalloc(&sink, 4);
+  part10<MODE><<<1, threads>>>(iters, d, sink);
+  part10<MODE><<<1, threads>>>(iters, d, sink);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h = 0;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("%-40s %s %.1f cycles/iter\n", name, cudaGetErrorString(e), double(h) / iters);
+  cudaFree(d);
+}
+
 int main() {
   setvbuf(stdout, NULL, _IONBF, 0);
   srand(7);
-  int g2 = run_part1(2);
-  int g3 = run_part1(3);
-  printf("working variant: 2-bit %d, 3-bit %d\n", g2, g3);
-  run_part6<false>();
-  run_part6<true>();
-  run_part5<8, false>();
-  run_part5<16, false>();
-
-  run_part7<8, false>();
-  run_part7<32, false>();
-  run_part7<8, true>();
-  run_part7<32, true>();
-  run_part4<8, 1, false>();
-  run_part4<8, 2, false>();
-  run_part4<8, 4, false>();
-  run_part4<8, 8, false>();
-  run_part4<16, 8, false>();
-  run_part4<32, 8, false>();
-  run_part4<64, 4, false>();
-  run_part4<8, 1, true>();
-  run_part4<8, 8, true>();
-  run_part4<32, 8, true>();
-  run_part3<true, 8, 0>(1);
-  run_part3<true, 16, 0>(1);
-  run_part3<true, 64, 0>(1);
-  run_part3<true, 256, 0>(1);
-  run_part3<false, 8, 0>(1);
-  run_part3<false, 16, 0>(1);
-  run_part3<false, 256, 0>(1);
-  run_part3<true, 8, 4>(1);
-  run_part3<true, 8, 0>(148);
-  run_part2<2, 8, 8, false>("2-bit 8 dec warps, 8 slots");
-  run_part2<2, 8, 8, true>("2-bit 8 dec, 8 slots, epi");
-  run_part2<2, 4, 8, true>("2-bit 4 dec, 8 slots, epi");
-  run_part2<2, 8, 12, true>("2-bit 8 dec, 12 slots, epi");
-  run_part2<3, 8, 8, true>("3-bit 8 dec, 8 slots, epi");
+  run_part10<0>("test_wait completed phase (1 warp)", 32);
+  run_part10<1>("try_wait completed phase (1 warp)", 32);
+  run_part10<0>("test_wait completed phase (15 warps)", 480);
+  run_part10<2>("lane0 arrive + syncwarp (1 warp)", 32);
+  run_part10<3>("volatile shared load (1 warp)", 32);
+  run_part9<1, true>("st x16 + wait, 1 warp");
+  run_part9<1, false>("st x16 no wait, 1 warp");
+  run_part9<8, true>("st x16 + wait, 8 warps");
+  run_part9<8, false>("st x16 no wait, 8 warps");
+  run_part8<0>("commit only");
+  run_part8<1>("fence::after_thread_sync only");
+  run_part8<2>("2 MMA i8 N8 + commit");
+  run_part8<3>("2 MMA i8 N8, no commit");
+  run_part8<4>("mbarrier arrive (elect)");
   return 0;
 }
