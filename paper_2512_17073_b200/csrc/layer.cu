@@ -349,7 +349,7 @@ struct lrc_layer {
   // tensor-core decode engine (tcd.cu): batches of B <= tcd_max tokens
   int tcd_max = [] {
     const char* v = getenv("LRC_TCD_MAX");
-    return v ? atoi(v) : 0;  // off by default until it beats the tiled kernels
+    return v ? atoi(v) : -1;  // -1: auto (on where the tiled kernels do not apply, e.g. 3-bit)
   }();
   bool tcd_ok = false;
   int tcd_bits = 2, tcd_fbits = 3;
@@ -804,7 +804,8 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   }
   // ---- tensor-core decode engine: one persistent kernel per layer step
   const int P_tcd = pairs_expert ? 1 : top_k + L->S;
-  if (allow_tiled && L->tcd_ok && !L->pager && L->tcd_max > 0 && B <= std::min(L->tcd_max, tcd::kMaxTok) &&
+  const int tcd_max = L->tcd_max >= 0 ? L->tcd_max : (L->tiled ? 0 : tcd::kMaxTok);
+  if (allow_tiled && L->tcd_ok && !L->pager && tcd_max > 0 && B <= std::min(tcd_max, tcd::kMaxTok) &&
       B * P_tcd <= tcd::kMaxP && top_k <= 8) {
     lrc_status s = tcd_prepare(L, st);
     if (s != LRC_OK) return s;

@@ -1180,6 +1180,11 @@ extern "C" lrc_status lrc_debug_stamps(int which, uint64_t* host, int n) {
   if (which < 4 && (n < 0 || n > (which == 0 ? kStampCtas * 8 : 2 * 256 * 8 + 2 * 64 * 6)))
     return fail(LRC_ERR_INVALID, "stamps: bad count");
   LRC_CUDA_TRY(cudaDeviceSynchronize());
+  if (which == 5) {
+    if (n != 192) return fail(LRC_ERR_INVALID, "wstat: 192 values");
+    tcd::wstat_copy(reinterpret_cast<unsigned long long*>(host));
+    return LRC_OK;
+  }
   if (which == 4) {  // debug: tcd wait mode = n
     tcd::set_wait_mode(n);
     return LRC_OK;

@@ -41,21 +41,26 @@
 namespace lrc {
 namespace tcd {
 
-constexpr int kThreads = 480;
-constexpr int kMmaWarp = 8, kProdWarp = 9, kHelpWarp = 10, kAux0 = 11;
-constexpr int kNAS = 2;   // A ring: stages x 8 units x 16 TMEM columns
+constexpr int kDec = 8;  // decode warps: 2 per TMEM lane quarter, each <= 4 units of a stage
+constexpr int kNEpi = 4;     // epilogue warps: one per lane quarter, every unit of a stage
+constexpr int kEpi0 = kDec;
+constexpr int kMmaWarp = kDec + kNEpi, kProdWarp = kMmaWarp + 1, kAux0 = kMmaWarp + 2;
+constexpr int kWarps = kAux0 + 4, kThreads = kWarps * 32;
+constexpr int kNAS = 3;   // A ring (max): stages x 8 units x 16 TMEM columns
 constexpr int kGPS = 4;   // groups per stage (2 when an expert has > 4 tokens)
-constexpr int kDCol = kNAS * 128;  // D ring after the A ring
+
 constexpr int kMaxNST = 8;
 constexpr int kMaxNDS = 4;
 constexpr int kMaxE = LRC_MAX_EXPERTS;
-constexpr int kTresBytes = 2 * 2 * kMaxTok * 128 * 4;
+constexpr int kMaxStages = 512;
+constexpr int kTresBytes = 2 * 2 * kMaxTok * 128 * 4;  // 2 slots x {w1, w3}
 
 __device__ uint64_t g_stamps[148 * 16];
 __device__ uint64_t g_trace[4][256];  // CTA 0: producer stage codes, producer stage B, MMA stage, decode-w0 stage
 __device__ __forceinline__ void trace(const Args& A, int w, int i) {
   if (A.stamp && blockIdx.x == 0 && i < 256) g_trace[w][i] = clock64();
 }
+__device__ unsigned long long g_wstat[24][8];  // CTA 0 per warp (see tools/tcd_stamps.py)  // CTA 0 per warp: wait cycles [full, dfull, bopf, tempty, afull(MMA), bopf(MMA), empty(prod), total]
 __device__ uint64_t g_trace2[4][256];  // CTA 0: -, epilogue-w0 stage, -, -
 __device__ __forceinline__ void trace2(const Args& A, int w, int i) {
   if (A.stamp && blockIdx.x == 0 && i < 256) g_trace2[w][i] = clock64();
@@ -108,7 +113,8 @@ __device__ __forceinline__ void wait(uint64_t* b, uint32_t parity) {
   if (try_wait(b, parity)) return;
   uint64_t t0 = 0;
   for (uint32_t spin = 1;; ++spin) {
-    if (try_wait_sleep(b, parity)) return;
+    if (try_wait(b, parity)) return;
+    __nanosleep(20);
     if ((spin & 0xFF) == 0) {
       const uint64_t t = umma::globaltimer();
       if (t0 == 0) t0 = t;
@@ -170,6 +176,26 @@ __device__ __forceinline__ void bulk_g2s_plain(uint32_t dst, const void* src, ui
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float4 ldsf4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ void red_add(float* p, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
@@ -223,16 +249,18 @@ __device__ __forceinline__ void decode3(const uint32_t (&w)[6], uint32_t (&r)[16
 // --------------------------------------------------------------- cursor ----
 // Walks this CTA's groups: phase U (w1|w3 units) then phase D (w2 units).
 struct Cur {
-  int lo0, hi0, lo1, hi1, H, F;
+  int lo0, hi0, lo1, hi1, H, F, gps, NST;
   int ph, G, T, NM, lo, hi;   // current phase parameters
   int L, ta, ttile, tg;       // linear group index and its (expert, tile, group)
-  int sg, ns, mat, stage, u, gps;
-  __device__ void init(const Plan& P, int hidden, int ffn) {
+  int sg, ns, mat, stage, u;
+  int slot, sphase;           // ring slot of the stage and its use parity
+  __device__ void init(const Plan& P, int hidden, int ffn, int nst = 1) {
     gps = P.gps;
+    NST = nst;
     lo0 = static_cast<int>(P.lo[0]); hi0 = static_cast<int>(P.hi[0]);
     lo1 = static_cast<int>(P.lo[1]); hi1 = static_cast<int>(P.hi[1]);
     H = hidden; F = ffn;
-    stage = 0; sg = 0; mat = 0; u = 0;
+    stage = 0; sg = 0; mat = 0; u = 0; slot = 0; sphase = 0;
     set_phase(0);
     norm();
   }
@@ -263,7 +291,16 @@ struct Cur {
   __device__ bool stage_last_group() const { return sg == ns - 1; }
   // from a stage start: does the stage end its tile segment?
   __device__ bool stage_seg_end() const { return tg + ns == G || L + ns == hi; }
-  __device__ void step() {
+  __device__ __forceinline__ void bump_stage() {
+    ++stage;
+    if (++slot == NST) {
+      slot = 0;
+      sphase ^= 1;
+    }
+    sg = 0;
+    norm();
+  }
+  __device__ __forceinline__ void step() {
     ++L;
     if (++tg == G) {
       tg = 0;
@@ -275,11 +312,7 @@ struct Cur {
   }
   __device__ void next_group() {
     step();
-    if (++sg == ns) {
-      ++stage;
-      sg = 0;
-      norm();
-    }
+    if (++sg == ns) bump_stage();
   }
   __device__ void next_unit() {
     ++u;
@@ -287,11 +320,17 @@ struct Cur {
     mat = 0;
     next_group();
   }
-  __device__ void next_stage() {  // from a stage start
-    for (int i = 0; i < ns; ++i) step();
-    ++stage;
-    sg = 0;
-    norm();
+  __device__ __forceinline__ void next_stage() {  // from a stage start (a stage never crosses a tile)
+    L += ns;
+    tg += ns;
+    if (tg == G) {
+      tg = 0;
+      if (++ttile == T) {
+        ttile = 0;
+        ++ta;
+      }
+    }
+    bump_stage();
   }
 };
 
@@ -356,13 +395,14 @@ __device__ __forceinline__ void digit_image(int bits, float v0, float v1, uint8_
 struct Shared {
   Plan P;
   uint64_t full[kMaxNST], bopf[kMaxNST], empty[kMaxNST];
-  uint64_t afull[kNAS], dfull[kMaxNDS];
+  uint64_t afull[kNAS], aempty[kNAS], dfull[kMaxNDS], dempty[kMaxNDS], xrdy;
+  int NAS, dcol;  // A ring depth, first D column
   uint64_t tfull[2], tempty[2], dready, gbarr;
   uint32_t tmem_base;
   int N, SB, NST, NDS, bop_off, xs_off, BG;
   uint8_t* ring;
   float* tres;
-  float red[15][40];
+  float red[kWarps][40];
   double lg64[kMaxTok][kFuseMaxE];
   float pw[kMaxTok][kMaxE];
   uint8_t pc[kMaxTok][kMaxE];
@@ -370,6 +410,13 @@ struct Shared {
   int last_flag;
   float t13s[2][2 * kRMax];
   float gred[4];
+  int nstage, nstage_u;       // this CTA's stages (phase U first)
+  // resident B operand (B == 1): the token's x images (phase U), then the
+  // activation images of this CTA's phase-D groups, loaded once per phase
+  int res, bimg_off, bsum_off;
+  uint64_t bimgf;
+  uint16_t doff[kMaxStages];  // per stage: image index of its first group in the resident buffer
+  int2 stab[kMaxStages];      // per stage: {g | tile << 16, a | ph << 8 | ns << 9 | seg_end << 12 | seg_ng << 16}
   float t2red[4][kRMax];
 };
 
@@ -412,7 +459,7 @@ __device__ __forceinline__ int warp_argmax(float v, int idx) {
 __device__ __noinline__ void route_fused(const Args& A, Shared& S, const float* gs) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = A.hidden, B = A.B;
-  const int wpt = max(1, 15 / B);
+  const int wpt = max(1, kWarps / B);
   const int t = warp / wpt, wi = warp % wpt;
   float acc[kFuseMaxE], xx = 0.f, xm = 0.f;
 #pragma unroll
@@ -525,7 +572,7 @@ __device__ __noinline__ void route_fallback(const Args& A, Shared& S) {
     __syncthreads();
     if (tid < A.E) {
       double sd = 0.0;
-      for (int w = 0; w < 15; ++w) sd += reinterpret_cast<double*>(&S.red[w][0])[tid];
+      for (int w = 0; w < kWarps; ++w) sd += reinterpret_cast<double*>(&S.red[w][0])[tid];
       S.lg64[t][tid] = sd;
     }
     __syncthreads();
@@ -588,7 +635,7 @@ __device__ __noinline__ void route_rest(const Args& A, Shared& S, bool fused) {
       __syncthreads();
       if (tid == 0) {
         float m = 0.f;
-        for (int w = 0; w < 15; ++w) m = fmaxf(m, S.red[w][0]);
+        for (int w = 0; w < kWarps; ++w) m = fmaxf(m, S.red[w][0]);
         S.P.xmax[t] = m;
       }
       __syncthreads();
@@ -676,13 +723,92 @@ __device__ __noinline__ void build_plan(const Args& A, Shared& S) {
     S.bop_off = P.gps * 2 * Geo<BITS>::UB;
     S.xs_off = S.bop_off + P.gps * S.BG;
     S.SB = S.xs_off + kMaxTok * P.gps * 16;
+    S.res = A.B == 1 ? 1 : 0;
+    int bimg_bytes = 0;
+    if (S.res) {
+      const int nimg = max(static_cast<int>(G0), static_cast<int>(P.hi[1] - P.lo[1]));
+      S.SB = S.bop_off;  // stages carry only codes + metadata
+      bimg_bytes = nimg * (512 + 16);
+    }
     uint32_t dyn;
     asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
-    S.NST = min(kMaxNST, static_cast<int>((dyn - kTresBytes) / S.SB));
+    S.NST = min(kMaxNST, static_cast<int>((dyn - kTresBytes - bimg_bytes) / S.SB));
+    if (S.res) {
+      S.bimg_off = S.NST * S.SB;
+      S.bsum_off = S.bimg_off + (bimg_bytes / (512 + 16)) * 512;
+    }
     // D ring after the A ring (256 columns): stages x 2 gps units x N columns;
     // NDS = 2 lets the epilogue trail the decode by one stage
-    S.NDS = 2 * P.gps * N <= 128 ? 2 : 1;
+    // TMEM: A ring (NAS x 128 columns) then the D ring (NDS x 2 gps x N columns)
+    const int dblk = 2 * P.gps * N;
+    S.NAS = 3 * 128 + dblk <= 512 ? 3 : 2;  // B == 1 (N = 8): 3 A stages + 2 D stages of 64 columns
+    S.dcol = S.NAS * 128;
+    S.NDS = max(1, min(kMaxNDS, (512 - S.dcol) / dblk));
   }
+}
+
+// ---- this CTA's stages (a stage = <= gps consecutive groups of one tile)
+struct Stg {
+  int g, tile, a, ph, ns, seg_end, seg_ng;
+};
+__device__ __forceinline__ Stg stg(const Shared& S, int s) {
+  const int2 r = S.stab[s];
+  Stg t;
+  t.g = r.x & 0xffff;
+  t.tile = r.x >> 16;
+  t.a = r.y & 0xff;
+  t.ph = (r.y >> 8) & 1;
+  t.ns = (r.y >> 9) & 7;
+  t.seg_end = (r.y >> 12) & 1;
+  t.seg_ng = r.y >> 16;
+  return t;
+}
+// warp 0: the span [lo, hi) of (expert, tile, group) of each phase -> tile parts
+// (one lane each) -> stages of <= gps groups
+__device__ __noinline__ void build_stages(const Args& A, Shared& S) {
+  const int lane = threadIdx.x & 31;
+  const Plan& P = S.P;
+  const int gps = P.gps;
+  int base = 0;
+  for (int ph = 0; ph < 2; ++ph) {
+    int gbase = 0;
+    const int G = ph == 0 ? A.hidden / 64 : A.ffn / 64, T = ph == 0 ? A.ffn / 128 : A.hidden / 128;
+    const int lo = static_cast<int>(P.lo[ph]), hi = static_cast<int>(P.hi[ph]);
+    if (hi > lo) {
+      const int t0 = lo / G, t1 = (hi - 1) / G;
+      for (int tp0 = t0; tp0 <= t1; tp0 += 32) {
+        const int tl = tp0 + lane;
+        int n = 0, g0 = 0, g1 = 0;
+        if (tl <= t1) {
+          g0 = tl == t0 ? lo % G : 0;
+          g1 = tl == t1 ? (hi - 1) % G + 1 : G;
+          n = (g1 - g0 + gps - 1) / gps;
+        }
+        int pre = n, gpre = g1 - g0;  // inclusive prefixes: stages, groups
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, pre, o), w = __shfl_up_sync(0xffffffffu, gpre, o);
+          if (lane >= o) {
+            pre += v;
+            gpre += w;
+          }
+        }
+        const int at = base + pre - n, gat = gbase + gpre - (g1 - g0);
+        for (int k = 0; k < n && at + k < kMaxStages; ++k) {
+          const int g = g0 + k * gps, ns = min(gps, g1 - g);
+          const int segend = g + ns == g1 ? 1 : 0;
+          S.stab[at + k] = make_int2(g | ((tl % T) << 16), (tl / T) | (ph << 8) | (ns << 9) | (segend << 12) |
+                                                             ((g1 - g0) << 16));
+          // resident-B image index: U = the group's K index; D = position in this CTA's D groups
+          S.doff[at + k] = static_cast<uint16_t>(ph == 0 ? g : gat + k * gps);
+        }
+        base += __shfl_sync(0xffffffffu, pre, 31);
+        gbase += __shfl_sync(0xffffffffu, gpre, 31);
+      }
+    }
+    if (ph == 0 && lane == 0) S.nstage_u = min(base, kMaxStages);
+  }
+  if (lane == 0) S.nstage = min(base, kMaxStages);
 }
 
 // ---- producer: per stage one cp.async.bulk of the codes + metadata (ring
@@ -692,61 +818,93 @@ __device__ __noinline__ void build_plan(const Args& A, Shared& S) {
 template <int BITS>
 __device__ __noinline__ void role_producer(const Args& A, Shared& S) {
   constexpr int UB = Geo<BITS>::UB;
-  const int NST = S.NST, SB = S.SB, BG = S.BG, G0 = A.hidden / 64, G1 = A.ffn / 64;
+  const int lane = threadIdx.x & 31;
+  const int NST = S.NST, SB = S.SB, BG = S.BG, G0 = A.hidden / 64, G1 = A.ffn / 64, nst = S.nstage;
   const Plan& P = S.P;
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   const uint32_t ring = smem_u32(S.ring);
-  const unsigned xtarget = static_cast<unsigned>(A.B) * G0;
-  Cur cc, cb;  // codes cursor, B-operand cursor (cb.stage < cc.stage)
-  cc.init(P, A.hidden, A.ffn);
-  cb.init(P, A.hidden, A.ffn);
+  int sc = 0, sb = 0;  // next stage for codes / for the B operand (sb < sc)
+  int cslot = 0, cph = 0, bslot = 0;
   bool xready = false, dready = false;
   uint64_t t0 = 0;
-  while (!cb.done()) {
+  while (sb < nst || sc < nst) {
     bool progress = false;
-    if (!cc.done()) {
-      const int slot = cc.stage % NST, m = cc.stage / NST;
-      if (m == 0 || try_wait(&S.empty[slot], (m - 1) & 1)) {
-        const uint8_t* base = P.act_pack[cc.a()][cc.ph];
-        const size_t off = (static_cast<size_t>(cc.tile()) * cc.G + cc.g()) * cc.NM * UB;
-        const uint32_t bytes = static_cast<uint32_t>(cc.ns * cc.NM * UB);
-        arrive_tx(&S.full[slot], bytes);
-        bulk_g2s(ring + slot * SB, base + off, bytes, &S.full[slot], pol);
-        trace(A, 0, cc.stage);
-        cc.next_stage();
+    // codes + metadata: one bulk copy (lane 0) once the ring slot is free
+    if (sc < nst && (sc < NST || try_wait(&S.empty[cslot], cph ^ 1))) {
+      if (lane == 0) {
+        const Stg t = stg(S, sc);
+        const int nm = 2 - t.ph, G = t.ph == 0 ? G0 : G1;
+        const size_t off = (static_cast<size_t>(t.tile) * G + t.g) * nm * UB;
+        const uint32_t bytes = static_cast<uint32_t>(t.ns * nm * UB);
+        arrive_tx(&S.full[cslot], bytes);
+        bulk_g2s(ring + cslot * SB, P.act_pack[t.a][t.ph] + off, bytes, &S.full[cslot], pol);
+        trace(A, 0, sc);
+      }
+      ++sc;
+      if (++cslot == NST) {
+        cslot = 0;
+        cph ^= 1;
+      }
+      progress = true;
+    }
+    if (S.res) {  // resident B operand: x images once (phase U), activation images once (phase D)
+      if (sb == 0 && (xready || (xready = try_wait(&S.xrdy, 0)))) {
+        if (lane == 0) {
+          const int G0b = A.hidden / 64;
+          arrive_tx(&S.bimgf, G0b * (512 + 16));
+          bulk_g2s_plain(ring + S.bimg_off, A.xdig, G0b * 512, &S.bimgf);
+          bulk_g2s_plain(ring + S.bsum_off, A.xsum, G0b * 16, &S.bimgf);
+        }
+        sb = 1;
+        progress = true;
+      } else if (sb == 1 && (dready || (dready = try_wait(&S.dready, 0)))) {
+        if (lane == 0) {
+          int bytes = 0;
+          for (int k = S.nstage_u; k < nst; ++k) bytes += stg(S, k).ns * (512 + 16);
+          arrive_tx(&S.bimgf, static_cast<uint32_t>(bytes));
+          for (int k = S.nstage_u; k < nst; ++k) {
+            const Stg t = stg(S, k);
+            const int p = P.act_p0[t.a], dof = S.doff[k];
+            bulk_g2s_plain(ring + S.bimg_off + dof * 512, A.adig + (static_cast<size_t>(p) * G1 + t.g) * 512,
+                           t.ns * 512, &S.bimgf);
+            bulk_g2s_plain(ring + S.bsum_off + dof * 16, A.asum + static_cast<size_t>(p) * G1 + t.g, t.ns * 16,
+                           &S.bimgf);
+          }
+        }
+        sb = nst;
         progress = true;
       }
-    }
-    if (cb.stage < cc.stage) {
-      if (cb.ph == 0 && !xready) xready = ld_acquire(&A.xcnt[P.par]) >= xtarget;
-      if (cb.ph == 1 && !dready) dready = try_wait(&S.dready, 0);
-      if (cb.ph == 0 ? xready : dready) {
-        const int slot = cb.stage % NST, a = cb.a(), na = P.act_n[a], p0 = P.act_p0[a];
-        const uint32_t st = ring + slot * SB;
-        const int ns = cb.ns;
-        arrive_tx(&S.bopf[slot], static_cast<uint32_t>(na * ns * (512 + 16)));
+      if (sc >= nst && sb >= nst) break;
+    } else if (sb < sc) {
+      // B operand (digit images + group sums): 16-byte cp.async by all lanes
+      // (LDGSTS: not queued behind the ring's bulk copies), completion tracked
+      // by one arrive.noinc per lane on the stage's bopf barrier
+      const Stg t = stg(S, sb);
+      if (t.ph == 0 && !xready) xready = try_wait(&S.xrdy, 0);
+      if (t.ph == 1 && !dready) dready = try_wait(&S.dready, 0);
+      if (t.ph == 0 ? xready : dready) {
+        const int na = P.act_n[t.a], p0 = P.act_p0[t.a], ns = t.ns;
+        const uint32_t st = ring + bslot * SB;
+        const int G = t.ph == 0 ? G0 : G1;
         for (int j = 0; j < na; ++j) {
           const int p = p0 + j;
-          const int row = cb.ph == 0 ? P.pair_tok[p] : p;  // image row: token (U) or pair (D)
-          const int G = cb.ph == 0 ? G0 : G1;
-          const uint8_t* img = (cb.ph == 0 ? A.xdig : A.adig) + (static_cast<size_t>(row) * G + cb.g()) * 512;
-          const float4* sm = (cb.ph == 0 ? A.xsum : A.asum) + static_cast<size_t>(row) * G + cb.g();
-          if (na == 1 && BG == 512) {  // one token, one-token stages: contiguous in both places
-            bulk_g2s_plain(st + S.bop_off, img, ns * 512, &S.bopf[slot]);
-          } else if (na == 1) {
-            for (int sg = 0; sg < ns; ++sg)
-              bulk_g2s_plain(st + S.bop_off + sg * BG, img + sg * 512, 512, &S.bopf[slot]);
-          } else {  // token j: K half s of group sg -> sg * BG + s * na * 256 + j * 256
-            for (int sg = 0; sg < ns; ++sg)
-              for (int hs = 0; hs < 2; ++hs)
-                bulk_g2s_plain(st + S.bop_off + sg * BG + hs * na * 256 + j * 256, img + sg * 512 + hs * 256, 256,
-                               &S.bopf[slot]);
+          const int row = t.ph == 0 ? P.pair_tok[p] : p;  // image row: token (U) or pair (D)
+          const uint8_t* img = (t.ph == 0 ? A.xdig : A.adig) + (static_cast<size_t>(row) * G + t.g) * 512;
+          const float4* sm = (t.ph == 0 ? A.xsum : A.asum) + static_cast<size_t>(row) * G + t.g;
+          // group sg, K half hs, 16-byte chunk c (16 per half) -> sg * BG + hs * na * 256 + j * 256 + 16 c
+          for (int k = lane; k < ns * 32; k += 32) {
+            const int sg = k >> 5, hs = (k >> 4) & 1, cidx = k & 15;
+            umma::cp_async16(st + S.bop_off + sg * BG + hs * na * 256 + j * 256 + cidx * 16,
+                             img + sg * 512 + hs * 256 + cidx * 16, 16);
           }
-          bulk_g2s_plain(st + S.xs_off + j * P.gps * 16, sm, ns * 16, &S.bopf[slot]);
+          if (lane < ns) umma::cp_async16(st + S.xs_off + (j * P.gps + lane) * 16, sm + lane, 16);
         }
-        trace(A, 1, cb.stage);
-        cb.next_stage();
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&S.bopf[bslot]))
+                     : "memory");
+        if (lane == 0) trace(A, 1, sb);
+        ++sb;
+        if (++bslot == NST) bslot = 0;
         progress = true;
       }
     }
@@ -763,34 +921,45 @@ __device__ __noinline__ void role_producer(const Args& A, Shared& S) {
 // ---- MMA issuer: per stage, 2 x tcgen05.mma.kind::i8 (K = 32 each) per
 // (group, matrix) unit with N = 8 x the expert's tokens, one commit for the
 // stage's D block and one for its ring slot
+template <bool ONE>
 __device__ __noinline__ void role_mma(const Args& A, Shared& S, int bop_off) {
-  const int NST = S.NST, SB = S.SB, N = S.N, NDS = S.NDS, BG = S.BG;
-  const uint32_t tm = S.tmem_base;
+  // ONE (B == 1): one token per expert, N = 8, resident B operand, A ring 3, D ring 2
+  const int NST = S.NST, SB = S.SB, nst = S.nstage, nsu = S.nstage_u;
+  const int N = ONE ? 8 : S.N, NDS = ONE ? 2 : S.NDS, NAS = ONE ? 3 : S.NAS, BG = ONE ? 512 : S.BG;
+  const uint32_t tm = S.tmem_base, dcol = S.dcol;
   const uint32_t ring = smem_u32(S.ring);
-  Cur c;
-  c.init(S.P, A.hidden, A.ffn);
   const int dstride = 2 * S.P.gps * N;
-  while (!c.done()) {
-    const int slot = c.stage % NST, as = c.stage % kNAS, ds = c.stage % NDS;
-    wait(&S.bopf[slot], (c.stage / NST) & 1);
-    wait(&S.afull[as], (c.stage / kNAS) & 1);
+  int slot = 0, sph = 0, as = 0, aph = 0, ds = 0, dph = 0;
+  for (int s = 0; s < nst; ++s) {
+    const Stg t = stg(S, s);
+    if (!ONE) {
+      wait(&S.bopf[slot], sph);
+    } else {
+      if (s == 0) wait(&S.bimgf, 0);    // x images
+      if (s == nsu) wait(&S.bimgf, 1);  // activation images
+    }
+    wait(&S.afull[as], aph);
+    if (s >= NDS) wait(&S.dempty[ds], dph ^ 1);
     fence_after();
     if (elect_one()) {
-      const int na = S.P.act_n[c.a()], nu = c.ns * c.NM;
+      const int na = ONE ? 1 : S.P.act_n[t.a], nm = 2 - t.ph, nu = t.ns * nm;
       const uint32_t id = idesc_i8(na == 1 ? 8 : (8 * na + 15) / 16 * 16);
-      const uint32_t bop0 = ring + slot * SB + bop_off;
+      const uint32_t bop0 = ONE ? ring + S.bimg_off + S.doff[s] * 512 : ring + slot * SB + bop_off;
       for (int u = 0; u < nu; ++u) {
-        const uint32_t bop = bop0 + (u / c.NM) * BG;
-        const uint32_t d = tm + kDCol + ds * dstride + u * N, a = tm + as * 128 + u * 16;
+        const uint32_t bop = bop0 + (u >> (nm - 1)) * BG;
+        const uint32_t d = tm + dcol + ds * dstride + u * N, a = tm + as * 128 + u * 16;
         mma_i8(d, a, bdesc(bop), id, 0u);
         mma_i8(d, a + 8, bdesc(bop + na * 256), id, 1u);
       }
+      commit(&S.aempty[as]);
       commit(&S.dfull[ds]);
       commit(&S.empty[slot]);
-      trace(A, 2, c.stage);
+      trace(A, 2, s);
     }
     __syncwarp();
-    c.next_stage();
+    if (++slot == NST) { slot = 0; sph ^= 1; }
+    if (++as == NAS) { as = 0; aph ^= 1; }
+    if (++ds == NDS) { ds = 0; dph ^= 1; }
   }
 }
 
@@ -798,163 +967,189 @@ __device__ __noinline__ void role_mma(const Args& A, Shared& S, int bop_off) {
 // previous stage (NDS = 2) or of this stage (NDS = 1, N = 24).
 // Phase U: half h decodes matrix h (w1 / w3) of the stage's groups; phase D:
 // half h decodes the groups sg with sg % 2 == h.
-template <int BITS>
+template <int BITS, bool ONE>
 __device__ __noinline__ void role_decode(const Args& A, Shared& S) {
   constexpr int CB = Geo<BITS>::CB, UB = Geo<BITS>::UB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = warp >> 2, q = warp & 3, row = q * 32 + lane;
-  const int NST = S.NST, SB = S.SB, N = S.N, NDS = S.NDS, H = A.hidden;
-  const int lagst = NDS - 1;  // stages between a stage's decode and its epilogue
-  const Plan& P = S.P;
+  const int sub = warp >> 2, q = warp & 3, row = q * 32 + lane;  // units u = sub + 2 i of a stage
+  const int NST = S.NST, SB = S.SB, nst = S.nstage, NAS = ONE ? 3 : S.NAS;
   const uint32_t tl = S.tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+  const uint32_t ring = smem_u32(S.ring) + row * CB;
+  int slot = 0, sph = 0, as = 0, aph = 0;
+  for (int s = 0; s < nst; ++s) {
+    const Stg t = stg(S, s);
+    wait(&S.full[slot], sph);
+    if (s >= NAS) wait(&S.aempty[as], aph ^ 1);  // MMAs of stage s - NAS read this A block
+    fence_after();
+    const uint32_t st = ring + slot * SB;
+    const int nu = t.ns * (2 - t.ph);
+    uint32_t cw[4][6];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int u = sub + 2 * i;
+      if (u < nu) {
+        const uint32_t cp = st + u * UB;
+        if (BITS == 2) {
+          const uint4 v = lds128(cp);
+          cw[i][0] = v.x; cw[i][1] = v.y; cw[i][2] = v.z; cw[i][3] = v.w;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const uint2 v = lds64(cp + 8 * k);
+            cw[i][2 * k] = v.x;
+            cw[i][2 * k + 1] = v.y;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) arrive(&S.empty[slot]);  // codes read
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int u = sub + 2 * i;
+      if (u < nu) {
+        uint32_t r[16];
+        if (BITS == 2) {
+          decode2(make_uint4(cw[i][0], cw[i][1], cw[i][2], cw[i][3]), r);
+        } else {
+          uint32_t w[6] = {cw[i][0], cw[i][1], cw[i][2], cw[i][3], cw[i][4], cw[i][5]};
+          decode3(w, r);
+        }
+        st16(tl + as * 128 + u * 16, r);
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      arrive(&S.afull[as]);
+      if (warp == 0) trace(A, 3, s);
+    }
+    if (++slot == NST) { slot = 0; sph ^= 1; }
+    if (++as == NAS) { as = 0; aph ^= 1; }
+  }
+}
+
+// ---- epilogue warps (one per TMEM lane quarter; thread = tile row): every
+// unit of a stage -> per-group scale/zero and 2^-S, accumulated per matrix;
+// segment ends: w1|w3 results to the finalisers (phase U) or the weighted
+// combine into y (phase D)
+template <int BITS, bool ONE>
+__device__ __noinline__ void role_epilogue(const Args& A, Shared& S) {
+  constexpr int CB = Geo<BITS>::CB, UB = Geo<BITS>::UB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, row = q * 32 + lane;
+  const int NST = S.NST, SB = S.SB, nst = S.nstage, H = A.hidden;
+  const int N = ONE ? 8 : S.N, NDS = ONE ? 2 : S.NDS;
+  const Plan& P = S.P;
+  const uint32_t tl = S.tmem_base + (static_cast<uint32_t>(q * 32) << 16) + S.dcol;
   uint8_t* const ring = S.ring;
-  Cur lead, lag;
-  lead.init(P, A.hidden, A.ffn);
-  lag.init(P, A.hidden, A.ffn);
-  float acc[kMaxTok];
+  const uint32_t sring = smem_u32(S.ring);
+  const int dstride = 2 * P.gps * N;
+  const uint32_t bsum = sring + S.bsum_off;
+  float acc[2][kMaxTok];
 #pragma unroll
-  for (int j = 0; j < kMaxTok; ++j) acc[j] = 0.f;
-  int useg = 0;  // phase-U segments flushed (tile-result slot use counter)
-  while (!lag.done()) {
-    if (!lead.done() && lead.stage <= lag.stage + lagst) {
-      // -------- decode my units of stage lead.stage
-      const int slot = lead.stage % NST, as = lead.stage % kNAS;
-      wait(&S.full[slot], (lead.stage / NST) & 1);
-      fence_after();
-      const uint8_t* st = ring + static_cast<size_t>(slot) * SB;
-      const int nu = lead.ns * lead.NM;
-      // my <= 4 units: all code loads first, then decode + store
-      uint32_t cw[4][6];
+  for (int m = 0; m < 2; ++m)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int u = h + 2 * i;
-        if (u < nu) {
-          const uint8_t* cp = st + u * UB + row * CB;
-          if (BITS == 2) {
-            const uint4 v = *reinterpret_cast<const uint4*>(cp);
-            cw[i][0] = v.x; cw[i][1] = v.y; cw[i][2] = v.z; cw[i][3] = v.w;
-          } else {
+    for (int j = 0; j < kMaxTok; ++j) acc[m][j] = 0.f;
+  int useg = 0;
+  int slot = 0, sph = 0, ds = 0, dph = 0;
+  for (int s = 0; s < nst; ++s) {
+    const Stg t = stg(S, s);
+    const int nm = 2 - t.ph;
+    const uint8_t* st = ring + static_cast<size_t>(slot) * SB;
+    const int na = ONE ? 1 : P.act_n[t.a], p0 = P.act_p0[t.a];
+    const int nu = t.ns * nm;
+    wait(&S.dfull[ds], dph);
+    if (!ONE) wait(&S.bopf[slot], sph);
+    fence_after();
+    if (ONE) {
+      const uint32_t xs4 = bsum + S.doff[s] * 16;
+      const uint32_t meta = sring + slot * SB + 128 * CB + row * 4;
+      uint32_t D[8][4];
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              const uint2 v = *reinterpret_cast<const uint2*>(cp + 8 * k);
-              cw[i][2 * k] = v.x;
-              cw[i][2 * k + 1] = v.y;
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int u = h + 2 * i;
-        if (u < nu) {
-          uint32_t r[16];
-          if (BITS == 2) {
-            decode2(make_uint4(cw[i][0], cw[i][1], cw[i][2], cw[i][3]), r);
-          } else {
-            uint32_t w[6] = {cw[i][0], cw[i][1], cw[i][2], cw[i][3], cw[i][4], cw[i][5]};
-            decode3(w, r);
-          }
-          st16(tl + as * 128 + u * 16, r);
-        }
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      for (int u = 0; u < 8; ++u)
+        if (u < nu) ld4(tl + ds * dstride + u * N, D[u]);
+      ld_wait();
       fence_before();
       __syncwarp();
-      if (lane == 0) {
-        arrive(&S.afull[as]);
-        if (warp == 0) trace(A, 3, lead.stage);
-      }
-      lead.next_stage();
-      continue;
-    }
-    // -------- epilogue of stage lag.stage
-    Cur& c = lag;
-    const int slot = c.stage % NST, ds = c.stage % NDS;
-    const uint8_t* st = ring + static_cast<size_t>(slot) * SB;
-    const int a = c.a(), na = P.act_n[a], p0 = P.act_p0[a];
-    const int nu = c.ns * c.NM;
-    wait(&S.dfull[ds], (c.stage / NDS) & 1);
-    wait(&S.bopf[slot], (c.stage / NST) & 1);
-    fence_after();
-    const int dstride = 2 * P.gps * N;
-    const float4* xs4 = reinterpret_cast<const float4*>(st + S.xs_off);
-    if (na <= 2) {  // common case: all loads of my <= 4 units issued before one wait
-      uint32_t D[4][2][4];
+      if (lane == 0) arrive(&S.dempty[ds]);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-          if (h + 2 * i < nu && j < na) ld4(tl + kDCol + ds * dstride + (h + 2 * i) * N + 8 * j, D[i][j]);
-      ld_wait();
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int u = h + 2 * i;
+      for (int u = 0; u < 8; ++u) {
         if (u < nu) {
-          const int sg = u / c.NM;
-          const uint32_t sz = *reinterpret_cast<const uint32_t*>(st + u * UB + 128 * CB + row * 4);
-          const float s = h2f(static_cast<uint16_t>(sz & 0xffff)), z = h2f(static_cast<uint16_t>(sz >> 16));
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            if (j < na) {
-              const float4 xq = xs4[j * P.gps + sg];
-              const int v = (static_cast<int>(D[i][j][0]) << 14) + (static_cast<int>(D[i][j][1]) << 7) +
-                            static_cast<int>(D[i][j][2]);
-              acc[j] = fmaf(fmaf(s, static_cast<float>(v), z * xq.y), xq.x, acc[j]);
-            }
-          }
+          const int sg = u >> (nm - 1), mat = u & (nm - 1);
+          const uint32_t sz = lds32(meta + u * UB);
+          const float2 sf = __half22float2(*reinterpret_cast<const __half2*>(&sz));
+          const float4 xq = ldsf4(xs4 + sg * 16);
+          const int v = (static_cast<int>(D[u][0]) << 14) + (static_cast<int>(D[u][1]) << 7) + static_cast<int>(D[u][2]);
+          const float r = fmaf(sf.x, static_cast<float>(v), sf.y * xq.y) * xq.x;
+          if (mat) acc[1][0] += r;
+          else acc[0][0] += r;
         }
       }
     } else {
+      const float4* xs4 = reinterpret_cast<const float4*>(st + S.xs_off);
 #pragma unroll 1
-      for (int u = h; u < nu; u += 2) {
-        const int sg = u / c.NM;
+      for (int u = 0; u < nu; ++u) {
+        const int sg = u >> (nm - 1), mat = u & (nm - 1);
         uint32_t D[kMaxTok][4];
 #pragma unroll
         for (int j = 0; j < kMaxTok; ++j)
-          if (j < na) ld4(tl + kDCol + ds * dstride + u * N + 8 * j, D[j]);
+          if (j < na) ld4(tl + ds * dstride + u * N + 8 * j, D[j]);
         ld_wait();
         const uint32_t sz = *reinterpret_cast<const uint32_t*>(st + u * UB + 128 * CB + row * 4);
-        const float s = h2f(static_cast<uint16_t>(sz & 0xffff)), z = h2f(static_cast<uint16_t>(sz >> 16));
+        const float2 sf = __half22float2(*reinterpret_cast<const __half2*>(&sz));
 #pragma unroll
         for (int j = 0; j < kMaxTok; ++j) {
           if (j < na) {
             const float4 xq = xs4[j * P.gps + sg];
             const int v = (static_cast<int>(D[j][0]) << 14) + (static_cast<int>(D[j][1]) << 7) +
                           static_cast<int>(D[j][2]);
-            acc[j] = fmaf(fmaf(s, static_cast<float>(v), z * xq.y), xq.x, acc[j]);
+            const float r = fmaf(sf.x, static_cast<float>(v), sf.y * xq.y) * xq.x;
+            if (mat) acc[1][j] += r;
+            else acc[0][j] += r;
           }
         }
       }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) arrive(&S.dempty[ds]);
     }
-    fence_before();
-    if (lane == 0 && warp == 0) trace2(A, 1, c.stage);
-    if (c.stage_seg_end()) {  // segment end: flush this half's partial sums
-      if (c.ph == 0) {
+    __syncwarp();
+    if (lane == 0) arrive(&S.empty[slot]);  // metadata and sums read
+    if (lane == 0 && warp == kEpi0) trace2(A, 1, s);
+    if (t.seg_end) {  // segment end: flush
+      if (t.ph == 0) {
         const int ts = useg & 1;
         if (useg >= 2) wait(&S.tempty[ts], ((useg >> 1) - 1) & 1);
-        float* tr = S.tres + ts * (2 * kMaxTok * 128);
+        const uint32_t tr = smem_u32(S.tres) + ts * (2 * kMaxTok * 128) * 4;
 #pragma unroll
-        for (int j = 0; j < kMaxTok; ++j)
-          if (j < na) tr[(h * kMaxTok + j) * 128 + row] = acc[j];
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+          for (int j = 0; j < kMaxTok; ++j)
+            if (j < na)
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(tr + ((m * kMaxTok + j) * 128 + row) * 4), "f"(acc[m][j])
+                           : "memory");
         __syncwarp();
         if (lane == 0) arrive(&S.tfull[ts]);
         ++useg;
       } else {
-        const int rg = (c.tile()) * 128 + row;
+        const int rg = t.tile * 128 + row;
 #pragma unroll
         for (int j = 0; j < kMaxTok; ++j) {
           if (j < na) {
             const int p = p0 + j;
-            red_add(A.y + static_cast<size_t>(P.pair_tok[p]) * H + rg, acc[j] * P.pair_w[p]);
+            red_add(A.y + static_cast<size_t>(P.pair_tok[p]) * H + rg, acc[0][j] * P.pair_w[p]);
           }
         }
       }
 #pragma unroll
-      for (int j = 0; j < kMaxTok; ++j) acc[j] = 0.f;
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int j = 0; j < kMaxTok; ++j) acc[m][j] = 0.f;
     }
-    __syncwarp();
-    if (lane == 0) arrive(&S.empty[slot]);
-    c.next_stage();
+    if (++slot == NST) { slot = 0; sph ^= 1; }
+    if (++ds == NDS) { ds = 0; dph ^= 1; }
   }
 }
 
@@ -1069,24 +1264,19 @@ __device__ __noinline__ void finalize_up(const Args& A, Shared& S, int a, int ti
 
 // phase-U tile results -> (split tiles: accumulate, last contributor) finalise
 __device__ __noinline__ void aux_phase_u(const Args& A, Shared& S) {
-  Cur c;
-  c.init(S.P, A.hidden, A.ffn);
   const int f = threadIdx.x - kAux0 * 32, lane = f & 31;
   const Plan& P = S.P;
   const int G0 = A.hidden / 64, T0 = A.ffn / 128;
-  int useg = 0, seg_g0 = 0;
-  while (!c.done() && c.ph == 0) {
-    if (c.seg_start()) seg_g0 = c.g();
-    if (!c.seg_end()) {
-      c.next_group();
-      continue;
-    }
-    const int a = c.a(), tile = c.tile(), na = P.act_n[a];
-    const int ng = c.g() + 1 - seg_g0;
+  int useg = 0;
+  for (int s = 0; s < S.nstage_u; ++s) {
+    const Stg t = stg(S, s);
+    if (!t.seg_end) continue;
+    const int a = t.a, tile = t.tile, na = P.act_n[a];
+    const int ng = t.seg_ng;
     const int ts = useg & 1;
     wait(&S.tfull[ts], (useg >> 1) & 1);
     float h1[kMaxTok], h3[kMaxTok];
-    const float* tr = S.tres + ts * (2 * kMaxTok * 128);
+    const float* tr = S.tres + ts * (2 * kMaxTok * 128);  // [w1, w3][token][row]
 #pragma unroll
     for (int j = 0; j < kMaxTok; ++j) {
       h1[j] = j < na ? tr[j * 128 + f] : 0.f;
@@ -1127,37 +1317,32 @@ __device__ __noinline__ void aux_phase_u(const Args& A, Shared& S) {
       }
     }
     if (fin) finalize_up(A, S, a, tile, h1, h3);
-    c.next_group();
   }
 }
 
 // phase D: U2.t2 for the tiles whose group 0 this CTA owns
 __device__ __noinline__ void aux_phase_d(const Args& A, Shared& S) {
-  Cur c;
-  c.init(S.P, A.hidden, A.ffn);
-  while (!c.done() && c.ph == 0) c.next_group();
   const int f = threadIdx.x - kAux0 * 32;
   const Plan& P = S.P;
   const int par = P.par, H = A.hidden;
-  while (!c.done()) {
-    if (c.ph == 1 && c.g() == 0) {
-      const int a = c.a(), tile = c.tile(), na = P.act_n[a], p0 = P.act_p0[a];
-      const Expert& ex = A.ex[P.act_e[a]];
-      const int i = tile * 128 + f;
-      for (int j = 0; j < na; ++j) {
-        const int p = p0 + j;
-        if (P.pair_comp[p] < 0) continue;
-        const int rk = ex.rank, RB = lr_rb(rk);
-        for (int k = f; k < rk; k += 128) S.t13s[1][k] = __ldcg(A.t2 + (par * kMaxP + p) * kRMax + k);
-        named_sync(2, 128);
-        const uint8_t* lt = ex.lr_down + static_cast<size_t>(tile) * lr_down_tile_bytes(rk);
-        const uint32_t mz = reinterpret_cast<const uint32_t*>(lt + 128 * RB)[f];
-        const float d = nib_dot(lt + f * RB, rk, h2f(mz & 0xffff), h2f(mz >> 16), S.t13s[1]);
-        named_sync(2, 128);
-        red_add(A.y + static_cast<size_t>(P.pair_tok[p]) * H + i, d * P.pair_w[p]);
-      }
+  for (int s = S.nstage_u; s < S.nstage; ++s) {
+    const Stg st = stg(S, s);
+    if (st.g != 0) continue;
+    const int a = st.a, tile = st.tile, na = P.act_n[a], p0 = P.act_p0[a];
+    const Expert& ex = A.ex[P.act_e[a]];
+    const int i = tile * 128 + f;
+    for (int j = 0; j < na; ++j) {
+      const int p = p0 + j;
+      if (P.pair_comp[p] < 0) continue;
+      const int rk = ex.rank, RB = lr_rb(rk);
+      for (int k = f; k < rk; k += 128) S.t13s[1][k] = __ldcg(A.t2 + (par * kMaxP + p) * kRMax + k);
+      named_sync(2, 128);
+      const uint8_t* lt = ex.lr_down + static_cast<size_t>(tile) * lr_down_tile_bytes(rk);
+      const uint32_t mz = reinterpret_cast<const uint32_t*>(lt + 128 * RB)[f];
+      const float d = nib_dot(lt + f * RB, rk, h2f(mz & 0xffff), h2f(mz >> 16), S.t13s[1]);
+      named_sync(2, 128);
+      red_add(A.y + static_cast<size_t>(P.pair_tok[p]) * H + i, d * P.pair_w[p]);
     }
-    c.next_group();
   }
 }
 
@@ -1175,6 +1360,15 @@ __device__ __noinline__ void role_aux(const Args& A, Shared& S) {
     const size_t n = static_cast<size_t>(A.B) * A.hidden;
     const size_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
     for (size_t i = lo + f; i < hi; i += 128) A.y[i] = 0.f;
+  }
+  if (f == 0) {  // the grid's x digit images -> the producer may copy phase-U B operands
+    const unsigned xtarget = static_cast<unsigned>(A.B) * (A.hidden / 64);
+    const uint64_t t0 = umma::globaltimer();
+    while (ld_acquire(&A.xcnt[par]) < xtarget) {
+      __nanosleep(64);
+      if (umma::globaltimer() - t0 > 2000000000ull) __trap();
+    }
+    arrive(&S.xrdy);
   }
   vx_jobs(A, S);
   if (aw == 0) stamp(A, 2);
@@ -1209,16 +1403,22 @@ __global__ void __launch_bounds__(kThreads, 1) tcd_kernel(const __grid_constant_
   if (tid == 0) {
     for (int i = 0; i < kMaxNST; ++i) {
       bar_init(&S.full[i], 1);
-      bar_init(&S.bopf[i], 1);
-      bar_init(&S.empty[i], 9);
+      bar_init(&S.bopf[i], 32);
+      bar_init(&S.empty[i], kDec + kNEpi + 1);  // decode warps (codes), epilogue warps (meta, sums), MMA (B)
     }
-    for (int i = 0; i < kNAS; ++i) bar_init(&S.afull[i], 8);
+    for (int i = 0; i < kNAS; ++i) {
+      bar_init(&S.afull[i], kDec);
+      bar_init(&S.aempty[i], 1);
+    }
+    for (int i = 0; i < kMaxNDS; ++i) bar_init(&S.dempty[i], kNEpi);
     for (int i = 0; i < kMaxNDS; ++i) bar_init(&S.dfull[i], 1);
     for (int i = 0; i < 2; ++i) {
-      bar_init(&S.tfull[i], 8);
+      bar_init(&S.tfull[i], kNEpi);
       bar_init(&S.tempty[i], 4);
     }
     bar_init(&S.dready, 1);
+    bar_init(&S.xrdy, 1);
+    bar_init(&S.bimgf, 1);
     bar_init(&S.gbarr, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1254,7 +1454,7 @@ __global__ void __launch_bounds__(kThreads, 1) tcd_kernel(const __grid_constant_
   __syncthreads();
   {  // x digit images (phase-U B operand): (token, group) items spread over the grid's warps
     const int G0 = A.hidden / 64, n = A.B * G0, lane = tid & 31;
-    for (int it = blockIdx.x * 15 + warp; it < n; it += gridDim.x * 15) {
+    for (int it = blockIdx.x * kWarps + warp; it < n; it += gridDim.x * kWarps) {
       const int t = it / G0, g = it % G0;
       const uint32_t v2 = __ldg(reinterpret_cast<const unsigned int*>(A.x + static_cast<size_t>(t) * A.hidden + g * 64) + lane);
       digit_image(BITS, bf2f(v2 & 0xffff), bf2f(v2 >> 16), A.xdig + static_cast<size_t>(it) * 512, A.xsum + it, lane);
@@ -1272,21 +1472,26 @@ __global__ void __launch_bounds__(kThreads, 1) tcd_kernel(const __grid_constant_
   }
   route_rest(A, S, fused);
   if (warp == 0) stamp(A, 11);
-  if (warp == 0) build_plan<BITS>(A, S);
+  if (warp == 0) {
+    build_plan<BITS>(A, S);
+    __syncwarp();
+    build_stages(A, S);
+  }
   __syncthreads();
   if (warp == 0) stamp(A, 1);
 
   if (warp == kProdWarp) {
-    if (elect_one()) role_producer<BITS>(A, S);
-  } else if (A.dbg & (8192 | 16384) && warp >= 8 && !(warp == kMmaWarp && (A.dbg & 16384))) {
-    // isolation tests: only producer + decode (+ MMA)
-  } else if (warp == kHelpWarp) {
-    // (idle)
+    role_producer<BITS>(A, S);
   } else if (warp == kMmaWarp) {
-    role_mma(A, S, S.bop_off);
+    if (S.res) role_mma<true>(A, S, S.bop_off);
+    else role_mma<false>(A, S, S.bop_off);
     stamp(A, 7);
-  } else if (warp < 8) {
-    role_decode<BITS>(A, S);
+  } else if (warp < kDec) {
+    if (S.res) role_decode<BITS, true>(A, S);
+    else role_decode<BITS, false>(A, S);
+  } else if (warp < kEpi0 + kNEpi) {
+    if (S.res) role_epilogue<BITS, true>(A, S);
+    else role_epilogue<BITS, false>(A, S);
   } else {
     role_aux(A, S);
   }
@@ -1445,11 +1650,15 @@ bool eligible(const lrc_expert* experts, int n, int hidden, int ffn, int* bits, 
 
 template <int BITS>
 static lrc_status launch_t(const Args& a, int num_sms, cudaStream_t st, bool pdl) {
-  static int configured = 0;
-  const int smem = 227 * 1024 - 24 * 1024;  // dynamic: ring + tile results (static state ~20 KB)
-  if (!configured) {
+  static int smem = 0;
+  if (smem == 0) {  // dynamic shared memory: everything the static state leaves
+    cudaFuncAttributes fa{};
+    LRC_CUDA_TRY(cudaFuncGetAttributes(&fa, tcd_kernel<BITS>));
+    int dev = 0, optin = 0;
+    LRC_CUDA_TRY(cudaGetDevice(&dev));
+    LRC_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    smem = (optin - static_cast<int>(fa.sharedSizeBytes) - 1024) & ~1023;
     LRC_CUDA_TRY(cudaFuncSetAttribute(tcd_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = 1;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(num_sms);
@@ -1471,6 +1680,12 @@ lrc_status launch(const Args& a, int num_sms, cudaStream_t st, bool pdl) {
 }
 
 void set_wait_mode(int) {}
+void wstat_copy(unsigned long long* host) {
+  cudaMemcpyFromSymbol(host, g_wstat, sizeof(g_wstat));
+  void* dev = nullptr;
+  cudaGetSymbolAddress(&dev, g_wstat);
+  cudaMemset(dev, 0, sizeof(g_wstat));
+}
 void trace_copy(uint64_t* host) {
   cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace));
   cudaMemcpyFromSymbol(host + 1024, g_trace2, sizeof(g_trace2));

@@ -71,6 +71,7 @@ lrc_status launch(const Args& a, int num_sms, cudaStream_t st, bool pdl);
 void stamps_copy(uint64_t* host, int n);
 void trace_copy(uint64_t* host);  // [4][256]
 void set_wait_mode(int m);
+void wstat_copy(unsigned long long* host);  // [24][8]
 
 }  // namespace tcd
 }  // namespace lrc

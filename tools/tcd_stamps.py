@@ -45,6 +45,18 @@ for i, n in enumerate(names):
     col = rel[:, i]
     print(f"{i} {n:8s} min {np.nanmin(col):8.2f}  med {np.nanmedian(col):8.2f}  max {np.nanmax(col):8.2f} us")
 
+ws = (ctypes.c_uint64 * 192)()
+_lib.check(_lib.lib().lrc_debug_stamps(5, ws, 192))
+sl.layer.forward(x, 2, 1)
+torch.cuda.synchronize()
+_lib.check(_lib.lib().lrc_debug_stamps(5, ws, 192))
+w = np.array(ws[:], dtype=np.float64).reshape(24, 8)
+print("CTA 0 wait cycles: decode warps: full aempty | total;  epilogue warps: dfull bopf | total")
+for i in range(8):
+    print(f"  dec w{i}: {w[i][0]:9.0f} {w[i][1]:9.0f} | {w[i][7]:9.0f}")
+for i in range(8, 16):
+    print(f"  epi w{i}: {w[i][2]:9.0f} {w[i][3]:9.0f} | {w[i][7]:9.0f}")
+print(f"  mma w12: afull+dempty {w[16][4]:9.0f} bopf {w[16][5]:9.0f} | total {w[16][7]:9.0f}")
 tr = (ctypes.c_uint64 * 2048)()
 _lib.check(_lib.lib().lrc_debug_stamps(3, tr, 2048))
 sl.layer.forward(x, 2, 1)
@@ -55,6 +67,6 @@ b = t[0][0]
 def f(v):
     return f"{v - b:8.0f}" if v > 0 else "       -"
 print("CTA 0, clock64 cycles from producer stage-0 issue")
-print("stage: codes issued | B issued | dec w0 done | MMA issued | epi w0 done")
+print("stage: codes issued | B issued | dec w0 aempty seen | dec w0 done | MMA issued | epi dfull seen | epi done")
 for i in range(40):
-    print(f"  {i:3d}: {f(t[0][i])} {f(t[1][i])} {f(t[3][i])} {f(t[2][i])} {f(t[5][i])}")
+    print(f"  {i:3d}: {f(t[0][i])} {f(t[1][i])} {f(t[7][i])} {f(t[3][i])} {f(t[2][i])} {f(t[6][i])} {f(t[5][i])}")
