@@ -43,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(HERE, "_lib", "obj")
     os.makedirs(objdir, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include")]
-    cflags = [f for f in FLAGS if f != "-shared"]
+    cflags = [f for f in FLAGS if f != "-shared"] + os.environ.get("LRC_NVCC_EXTRA", "").split()
     procs = []
     objs = []
     for src in sources():

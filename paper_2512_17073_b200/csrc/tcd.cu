@@ -46,6 +46,11 @@ constexpr int kNEpi = 4;     // epilogue warps: one per lane quarter, every unit
 constexpr int kEpi0 = kDec;
 constexpr int kMmaWarp = kDec + kNEpi, kProdWarp = kMmaWarp + 1, kAux0 = kMmaWarp + 2;
 constexpr int kWarps = kAux0 + 4, kThreads = kWarps * 32;
+#ifndef TCD_ONE_NAS
+#define TCD_ONE_NAS 3
+#endif
+// B == 1 (N = 8, D block 64 columns): TMEM = kOneNAS x 128 A columns + kOneNDS x 64 D columns
+constexpr int kOneNAS = TCD_ONE_NAS, kOneNDS = (512 - 128 * kOneNAS) / 64 > 4 ? 4 : (512 - 128 * kOneNAS) / 64;
 constexpr int kNAS = 3;   // A ring (max): stages x 8 units x 16 TMEM columns
 constexpr int kGPS = 4;   // groups per stage (2 when an expert has > 4 tokens)
 
@@ -54,13 +59,13 @@ constexpr int kMaxNDS = 4;
 constexpr int kMaxE = LRC_MAX_EXPERTS;
 constexpr int kMaxStages = 512;
 constexpr int kTresBytes = 2 * 2 * kMaxTok * 128 * 4;  // 2 slots x {w1, w3}
+constexpr int kEaccBytes = 2 * kMaxTok * 128 * 4;     // epilogue segment sums (B > 1)
 
 __device__ uint64_t g_stamps[148 * 16];
 __device__ uint64_t g_trace[4][256];  // CTA 0: producer stage codes, producer stage B, MMA stage, decode-w0 stage
 __device__ __forceinline__ void trace(const Args& A, int w, int i) {
   if (A.stamp && blockIdx.x == 0 && i < 256) g_trace[w][i] = clock64();
 }
-__device__ unsigned long long g_wstat[24][8];  // CTA 0 per warp (see tools/tcd_stamps.py)  // CTA 0 per warp: wait cycles [full, dfull, bopf, tempty, afull(MMA), bopf(MMA), empty(prod), total]
 __device__ uint64_t g_trace2[4][256];  // CTA 0: -, epilogue-w0 stage, -, -
 __device__ __forceinline__ void trace2(const Args& A, int w, int i) {
   if (A.stamp && blockIdx.x == 0 && i < 256) g_trace2[w][i] = clock64();
@@ -109,12 +114,40 @@ __device__ __forceinline__ bool try_wait_sleep(uint64_t* b, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifndef TCD_WAIT
+#define TCD_WAIT 1
+#endif
+__device__ __forceinline__ bool try_wait_hw(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{.reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.b32 %0, 1, 0, P;}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void wait(uint64_t* b, uint32_t parity) {
   if (try_wait(b, parity)) return;
   uint64_t t0 = 0;
+#if TCD_WAIT == 2
+  uint32_t ns = 32;
+#endif
   for (uint32_t spin = 1;; ++spin) {
+#if TCD_WAIT == 1
+    if (try_wait_hw(b, parity)) return;
+#elif TCD_WAIT == 3
+    if (try_wait_sleep(b, parity)) return;
+#else
     if (try_wait(b, parity)) return;
+#endif
+#if TCD_WAIT == 0
+#ifndef TCD_SPIN
     __nanosleep(20);
+#endif
+#elif TCD_WAIT == 2
+    __nanosleep(ns);
+    ns = min(ns * 2, 512u);
+#endif
     if ((spin & 0xFF) == 0) {
       const uint64_t t = umma::globaltimer();
       if (t0 == 0) t0 = t;
@@ -122,6 +155,54 @@ __device__ __forceinline__ void wait(uint64_t* b, uint32_t parity) {
     }
   }
 }
+// debug (-DTCD_WSTAT and A.stamp): waits with the cycles spent accumulated per
+// warp (CTA 0 -> g_wstat; tools/tcd_stamps.py prints them)
+__device__ unsigned long long g_wstat[24][8];
+#ifdef TCD_WSTAT
+struct WStat {
+  long long t0, c[8];
+};
+__device__ __forceinline__ void wstat_init(const Args& A, WStat& w) {
+  if (A.stamp) {
+    w.t0 = clock64();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w.c[i] = 0;
+  }
+}
+template <int K>
+__device__ __forceinline__ void wait_s(const Args& A, WStat& w, uint64_t* b, uint32_t parity) {
+  if (!A.stamp) {
+    wait(b, parity);
+    return;
+  }
+  const long long t = clock64();
+  wait(b, parity);
+  w.c[K] += clock64() - t;
+}
+template <int K>
+__device__ __forceinline__ void wstat_add(const Args& A, WStat& w, long long v) {
+  if (A.stamp) w.c[K] += v;
+}
+__device__ __forceinline__ long long wstat_clock(const Args& A) { return A.stamp ? clock64() : 0; }
+__device__ __forceinline__ void wstat_done(const Args& A, WStat& w) {
+  if (A.stamp && blockIdx.x == 0 && (threadIdx.x & 31) == 0) {
+    w.c[7] = clock64() - w.t0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) g_wstat[threadIdx.x >> 5][i] = w.c[i];
+  }
+}
+#else
+struct WStat {};
+__device__ __forceinline__ void wstat_init(const Args&, WStat&) {}
+template <int K>
+__device__ __forceinline__ void wait_s(const Args&, WStat&, uint64_t* b, uint32_t parity) {
+  wait(b, parity);
+}
+template <int K>
+__device__ __forceinline__ void wstat_add(const Args&, WStat&, long long) {}
+__device__ __forceinline__ long long wstat_clock(const Args&) { return 0; }
+__device__ __forceinline__ void wstat_done(const Args&, WStat&) {}
+#endif
 __device__ __forceinline__ bool elect_one() {
   uint32_t p;
   asm volatile("{.reg .pred P; elect.sync _|P, 0xffffffff; selp.b32 %0, 1, 0, P;}" : "=r"(p));
@@ -162,6 +243,10 @@ __device__ __forceinline__ void ld4(uint32_t taddr, uint32_t (&r)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(taddr));
+}
+__device__ __forceinline__ void ld3(uint32_t taddr, uint32_t (&r)[3]) {  // columns c, c+1, c+2
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r[2]) : "r"(taddr + 2));
 }
 __device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
@@ -246,93 +331,6 @@ __device__ __forceinline__ void decode3(const uint32_t (&w)[6], uint32_t (&r)[16
   }
 }
 
-// --------------------------------------------------------------- cursor ----
-// Walks this CTA's groups: phase U (w1|w3 units) then phase D (w2 units).
-struct Cur {
-  int lo0, hi0, lo1, hi1, H, F, gps, NST;
-  int ph, G, T, NM, lo, hi;   // current phase parameters
-  int L, ta, ttile, tg;       // linear group index and its (expert, tile, group)
-  int sg, ns, mat, stage, u;
-  int slot, sphase;           // ring slot of the stage and its use parity
-  __device__ void init(const Plan& P, int hidden, int ffn, int nst = 1) {
-    gps = P.gps;
-    NST = nst;
-    lo0 = static_cast<int>(P.lo[0]); hi0 = static_cast<int>(P.hi[0]);
-    lo1 = static_cast<int>(P.lo[1]); hi1 = static_cast<int>(P.hi[1]);
-    H = hidden; F = ffn;
-    stage = 0; sg = 0; mat = 0; u = 0; slot = 0; sphase = 0;
-    set_phase(0);
-    norm();
-  }
-  __device__ __forceinline__ void set_phase(int p) {
-    ph = p;
-    if (p == 0) {
-      G = H / 64; T = F / 128; NM = 2; lo = lo0; hi = hi0;
-    } else {
-      G = F / 64; T = H / 128; NM = 1; lo = lo1; hi = hi1;
-    }
-    L = lo;
-    tg = L % G;
-    ttile = (L / G) % T;
-    ta = L / (G * T);
-  }
-  __device__ __forceinline__ void norm() {  // at a stage start: skip exhausted phases, size the stage
-    while (ph < 2 && L >= hi) {
-      if (ph == 0) set_phase(1); else ph = 2;
-    }
-    if (ph < 2) ns = min(gps, min(G - tg, hi - L));
-  }
-  __device__ bool done() const { return ph >= 2; }
-  __device__ int a() const { return ta; }
-  __device__ int tile() const { return ttile; }
-  __device__ int g() const { return tg; }
-  __device__ bool seg_end() const { return tg == G - 1 || L == hi - 1; }
-  __device__ bool seg_start() const { return tg == 0 || L == lo; }
-  __device__ bool stage_last_group() const { return sg == ns - 1; }
-  // from a stage start: does the stage end its tile segment?
-  __device__ bool stage_seg_end() const { return tg + ns == G || L + ns == hi; }
-  __device__ __forceinline__ void bump_stage() {
-    ++stage;
-    if (++slot == NST) {
-      slot = 0;
-      sphase ^= 1;
-    }
-    sg = 0;
-    norm();
-  }
-  __device__ __forceinline__ void step() {
-    ++L;
-    if (++tg == G) {
-      tg = 0;
-      if (++ttile == T) {
-        ttile = 0;
-        ++ta;
-      }
-    }
-  }
-  __device__ void next_group() {
-    step();
-    if (++sg == ns) bump_stage();
-  }
-  __device__ void next_unit() {
-    ++u;
-    if (++mat < NM) return;
-    mat = 0;
-    next_group();
-  }
-  __device__ __forceinline__ void next_stage() {  // from a stage start (a stage never crosses a tile)
-    L += ns;
-    tg += ns;
-    if (tg == G) {
-      tg = 0;
-      if (++ttile == T) {
-        ttile = 0;
-        ++ta;
-      }
-    }
-    bump_stage();
-  }
-};
 
 // ------------------------------------------------------- factor access ----
 // element (r, c) of a quantized factor (reference bitstream, fp16 meta)
@@ -402,6 +400,7 @@ struct Shared {
   int N, SB, NST, NDS, bop_off, xs_off, BG;
   uint8_t* ring;
   float* tres;
+  float* eacc;  // B > 1 epilogue segment sums [2][kMaxTok][128]
   float red[kWarps][40];
   double lg64[kMaxTok][kFuseMaxE];
   float pw[kMaxTok][kMaxE];
@@ -416,7 +415,7 @@ struct Shared {
   int res, bimg_off, bsum_off;
   uint64_t bimgf;
   uint16_t doff[kMaxStages];  // per stage: image index of its first group in the resident buffer
-  int2 stab[kMaxStages];      // per stage: {g | tile << 16, a | ph << 8 | ns << 9 | seg_end << 12 | seg_ng << 16}
+  int2 stab[kMaxStages];      // per stage: {g | tile << 16, a | ph << 8 | ns << 9 | seg_end << 13 | seg_ng << 16}
   float t2red[4][kRMax];
 };
 
@@ -732,7 +731,7 @@ __device__ __noinline__ void build_plan(const Args& A, Shared& S) {
     }
     uint32_t dyn;
     asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
-    S.NST = min(kMaxNST, static_cast<int>((dyn - kTresBytes - bimg_bytes) / S.SB));
+    S.NST = min(kMaxNST, static_cast<int>((dyn - kTresBytes - kEaccBytes - bimg_bytes) / S.SB));
     if (S.res) {
       S.bimg_off = S.NST * S.SB;
       S.bsum_off = S.bimg_off + (bimg_bytes / (512 + 16)) * 512;
@@ -741,7 +740,7 @@ __device__ __noinline__ void build_plan(const Args& A, Shared& S) {
     // NDS = 2 lets the epilogue trail the decode by one stage
     // TMEM: A ring (NAS x 128 columns) then the D ring (NDS x 2 gps x N columns)
     const int dblk = 2 * P.gps * N;
-    S.NAS = 3 * 128 + dblk <= 512 ? 3 : 2;  // B == 1 (N = 8): 3 A stages + 2 D stages of 64 columns
+    S.NAS = A.B == 1 ? kOneNAS : (3 * 128 + dblk <= 512 ? 3 : 2);
     S.dcol = S.NAS * 128;
     S.NDS = max(1, min(kMaxNDS, (512 - S.dcol) / dblk));
   }
@@ -758,8 +757,8 @@ __device__ __forceinline__ Stg stg(const Shared& S, int s) {
   t.tile = r.x >> 16;
   t.a = r.y & 0xff;
   t.ph = (r.y >> 8) & 1;
-  t.ns = (r.y >> 9) & 7;
-  t.seg_end = (r.y >> 12) & 1;
+  t.ns = (r.y >> 9) & 15;
+  t.seg_end = (r.y >> 13) & 1;
   t.seg_ng = r.y >> 16;
   return t;
 }
@@ -768,10 +767,12 @@ __device__ __forceinline__ Stg stg(const Shared& S, int s) {
 __device__ __noinline__ void build_stages(const Args& A, Shared& S) {
   const int lane = threadIdx.x & 31;
   const Plan& P = S.P;
-  const int gps = P.gps;
   int base = 0;
   for (int ph = 0; ph < 2; ++ph) {
     int gbase = 0;
+    // units per stage: phase U gps groups x (w1, w3); phase D gps groups of w2, or
+    // 2 gps with the resident B operand (B == 1: the stage carries 2 gps units either way)
+    const int gps = (ph == 1 && S.res) ? 2 * P.gps : P.gps;
     const int G = ph == 0 ? A.hidden / 64 : A.ffn / 64, T = ph == 0 ? A.ffn / 128 : A.hidden / 128;
     const int lo = static_cast<int>(P.lo[ph]), hi = static_cast<int>(P.hi[ph]);
     if (hi > lo) {
@@ -797,7 +798,7 @@ __device__ __noinline__ void build_stages(const Args& A, Shared& S) {
         for (int k = 0; k < n && at + k < kMaxStages; ++k) {
           const int g = g0 + k * gps, ns = min(gps, g1 - g);
           const int segend = g + ns == g1 ? 1 : 0;
-          S.stab[at + k] = make_int2(g | ((tl % T) << 16), (tl / T) | (ph << 8) | (ns << 9) | (segend << 12) |
+          S.stab[at + k] = make_int2(g | ((tl % T) << 16), (tl / T) | (ph << 8) | (ns << 9) | (segend << 13) |
                                                              ((g1 - g0) << 16));
           // resident-B image index: U = the group's K index; D = position in this CTA's D groups
           S.doff[at + k] = static_cast<uint16_t>(ph == 0 ? g : gat + k * gps);
@@ -921,45 +922,121 @@ __device__ __noinline__ void role_producer(const Args& A, Shared& S) {
 // ---- MMA issuer: per stage, 2 x tcgen05.mma.kind::i8 (K = 32 each) per
 // (group, matrix) unit with N = 8 x the expert's tokens, one commit for the
 // stage's D block and one for its ring slot
+// 8 units x 2 MMAs of a full B == 1 stage; unit u: D columns 8u (N = 8), A
+// columns 16u, B image (u >> SH) (512 bytes = 32 descriptor address units),
+// second K half 256 bytes on
+template <int SH>
+__device__ __forceinline__ void mma_stage8(uint32_t d0, uint32_t a0, uint64_t b0, uint32_t id) {
+  const uint32_t blo = static_cast<uint32_t>(b0), bhi = static_cast<uint32_t>(b0 >> 32);
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const uint32_t bl = blo + (u >> SH) * 32;
+    asm volatile(
+        "{.reg .b64 bd0, bd1; mov.b64 bd0, {%2, %4}; mov.b64 bd1, {%3, %4};\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], bd0, %5, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%6], bd1, %5, 1;}" ::"r"(d0 + u * 8),
+        "r"(a0 + u * 16), "r"(bl), "r"(bl + 16), "r"(bhi), "r"(id), "r"(a0 + u * 16 + 8));
+  }
+}
+
 template <bool ONE>
 __device__ __noinline__ void role_mma(const Args& A, Shared& S, int bop_off) {
   // ONE (B == 1): one token per expert, N = 8, resident B operand, A ring 3, D ring 2
   const int NST = S.NST, SB = S.SB, nst = S.nstage, nsu = S.nstage_u;
-  const int N = ONE ? 8 : S.N, NDS = ONE ? 2 : S.NDS, NAS = ONE ? 3 : S.NAS, BG = ONE ? 512 : S.BG;
+  const int N = ONE ? 8 : S.N, NDS = ONE ? kOneNDS : S.NDS, NAS = ONE ? kOneNAS : S.NAS, BG = ONE ? 512 : S.BG;
   const uint32_t tm = S.tmem_base, dcol = S.dcol;
   const uint32_t ring = smem_u32(S.ring);
   const int dstride = 2 * S.P.gps * N;
   int slot = 0, sph = 0, as = 0, aph = 0, ds = 0, dph = 0;
+  WStat ws;
+  wstat_init(A, ws);
   for (int s = 0; s < nst; ++s) {
     const Stg t = stg(S, s);
     if (!ONE) {
       wait(&S.bopf[slot], sph);
     } else {
-      if (s == 0) wait(&S.bimgf, 0);    // x images
-      if (s == nsu) wait(&S.bimgf, 1);  // activation images
+      if (s == 0) wait_s<6>(A, ws, &S.bimgf, 0);    // x images
+      if (s == nsu) wait_s<6>(A, ws, &S.bimgf, 1);  // activation images
     }
-    wait(&S.afull[as], aph);
-    if (s >= NDS) wait(&S.dempty[ds], dph ^ 1);
+    wait_s<4>(A, ws, &S.afull[as], aph);
+    if (s >= NDS) wait_s<5>(A, ws, &S.dempty[ds], dph ^ 1);
     fence_after();
+    const long long tm0 = wstat_clock(A);
     if (elect_one()) {
       const int na = ONE ? 1 : S.P.act_n[t.a], nm = 2 - t.ph, nu = t.ns * nm;
       const uint32_t id = idesc_i8(na == 1 ? 8 : (8 * na + 15) / 16 * 16);
       const uint32_t bop0 = ONE ? ring + S.bimg_off + S.doff[s] * 512 : ring + slot * SB + bop_off;
+      if (ONE && nu == 8) {
+        // full B == 1 stage, fully unrolled: descriptors are the stage bases plus constants
+        const uint32_t d0 = tm + dcol + ds * (8 * 8), a0 = tm + as * 128;
+        const uint64_t b0 = bdesc(bop0);
+        if (t.ph == 0) mma_stage8<1>(d0, a0, b0, id);
+        else mma_stage8<0>(d0, a0, b0, id);
+      } else
       for (int u = 0; u < nu; ++u) {
         const uint32_t bop = bop0 + (u >> (nm - 1)) * BG;
         const uint32_t d = tm + dcol + ds * dstride + u * N, a = tm + as * 128 + u * 16;
         mma_i8(d, a, bdesc(bop), id, 0u);
         mma_i8(d, a + 8, bdesc(bop + na * 256), id, 1u);
       }
+      wstat_add<2>(A, ws, wstat_clock(A) - tm0);
       commit(&S.aempty[as]);
       commit(&S.dfull[ds]);
       commit(&S.empty[slot]);
+      wstat_add<3>(A, ws, wstat_clock(A) - tm0);
       trace(A, 2, s);
+      if (A.dbg & 32) {  // debug: MMA completion latency seen by the issuer
+        wait(&S.dfull[ds], dph);
+        trace(A, 1, s);
+      }
     }
     __syncwarp();
     if (++slot == NST) { slot = 0; sph ^= 1; }
     if (++as == NAS) { as = 0; aph ^= 1; }
     if (++ds == NDS) { ds = 0; dph ^= 1; }
+  }
+  wstat_done(A, ws);
+}
+
+// one decode warp's units u = sub + 2 i (i < 4) of a stage: codes (shared) ->
+// 8-bit A operand (TMEM); the ring slot's codes are released after the loads
+template <int BITS, bool FULL>
+__device__ __forceinline__ void dec_units(uint32_t st, uint32_t ta, int sub, int nu, int lane, uint64_t* empty) {
+  constexpr int UB = Geo<BITS>::UB;
+  uint32_t cw[4][6];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int u = sub + 2 * i;
+    if (FULL || u < nu) {
+      const uint32_t cp = st + u * UB;
+      if (BITS == 2) {
+        const uint4 v = lds128(cp);
+        cw[i][0] = v.x; cw[i][1] = v.y; cw[i][2] = v.z; cw[i][3] = v.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const uint2 v = lds64(cp + 8 * k);
+          cw[i][2 * k] = v.x;
+          cw[i][2 * k + 1] = v.y;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) arrive(empty);  // codes read
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int u = sub + 2 * i;
+    if (FULL || u < nu) {
+      uint32_t r[16];
+      if (BITS == 2) {
+        decode2(make_uint4(cw[i][0], cw[i][1], cw[i][2], cw[i][3]), r);
+      } else {
+        uint32_t w[6] = {cw[i][0], cw[i][1], cw[i][2], cw[i][3], cw[i][4], cw[i][5]};
+        decode3(w, r);
+      }
+      st16(ta + u * 16, r);
+    }
   }
 }
 
@@ -972,52 +1049,24 @@ __device__ __noinline__ void role_decode(const Args& A, Shared& S) {
   constexpr int CB = Geo<BITS>::CB, UB = Geo<BITS>::UB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = warp >> 2, q = warp & 3, row = q * 32 + lane;  // units u = sub + 2 i of a stage
-  const int NST = S.NST, SB = S.SB, nst = S.nstage, NAS = ONE ? 3 : S.NAS;
+  const int NST = S.NST, SB = S.SB, nst = S.nstage, NAS = ONE ? kOneNAS : S.NAS;
   const uint32_t tl = S.tmem_base + (static_cast<uint32_t>(q * 32) << 16);
   const uint32_t ring = smem_u32(S.ring) + row * CB;
   int slot = 0, sph = 0, as = 0, aph = 0;
+  WStat ws;
+  wstat_init(A, ws);
   for (int s = 0; s < nst; ++s) {
     const Stg t = stg(S, s);
-    wait(&S.full[slot], sph);
-    if (s >= NAS) wait(&S.aempty[as], aph ^ 1);  // MMAs of stage s - NAS read this A block
+    wait_s<0>(A, ws, &S.full[slot], sph);
+    if (s >= NAS) wait_s<1>(A, ws, &S.aempty[as], aph ^ 1);  // MMAs of stage s - NAS read this A block
     fence_after();
+    if (lane == 0 && warp == 0) trace2(A, 3, s);
     const uint32_t st = ring + slot * SB;
     const int nu = t.ns * (2 - t.ph);
-    uint32_t cw[4][6];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int u = sub + 2 * i;
-      if (u < nu) {
-        const uint32_t cp = st + u * UB;
-        if (BITS == 2) {
-          const uint4 v = lds128(cp);
-          cw[i][0] = v.x; cw[i][1] = v.y; cw[i][2] = v.z; cw[i][3] = v.w;
-        } else {
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            const uint2 v = lds64(cp + 8 * k);
-            cw[i][2 * k] = v.x;
-            cw[i][2 * k + 1] = v.y;
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) arrive(&S.empty[slot]);  // codes read
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int u = sub + 2 * i;
-      if (u < nu) {
-        uint32_t r[16];
-        if (BITS == 2) {
-          decode2(make_uint4(cw[i][0], cw[i][1], cw[i][2], cw[i][3]), r);
-        } else {
-          uint32_t w[6] = {cw[i][0], cw[i][1], cw[i][2], cw[i][3], cw[i][4], cw[i][5]};
-          decode3(w, r);
-        }
-        st16(tl + as * 128 + u * 16, r);
-      }
-    }
+    // full stage (the common case): no per-unit predicates, so the loads and
+    // the decode chains of the four units interleave
+    if (nu == 8) dec_units<BITS, true>(st, tl + as * 128, sub, nu, lane, &S.empty[slot]);
+    else dec_units<BITS, false>(st, tl + as * 128, sub, nu, lane, &S.empty[slot]);
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     fence_before();
     __syncwarp();
@@ -1027,6 +1076,101 @@ __device__ __noinline__ void role_decode(const Args& A, Shared& S) {
     }
     if (++slot == NST) { slot = 0; sph ^= 1; }
     if (++as == NAS) { as = 0; aph ^= 1; }
+  }
+  wstat_done(A, ws);
+}
+
+// B == 1 epilogue of one stage (N = 8: unit u's D block = columns 8u..8u+2,
+// the x digits' dot products): TMEM loads, then the group metadata and x
+// sums while they are in flight, then per unit s * dot + z * sum(x) scaled
+// by 2^-S.  Phase U: unit u = (group u / 2, matrix u % 2); phase D: group u.
+template <int UB, bool FULL, int PH>
+__device__ __forceinline__ void epi_one(uint32_t td, uint32_t meta, uint32_t xs4, int nu, int lane, uint64_t* dempty,
+                                        float& acc0, float& acc1) {
+  uint32_t D[8][3];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (FULL || u < nu) ld3(td + u * 8, D[u]);
+  ld_wait();
+  fence_before();
+  __syncwarp();
+  if (lane == 0) arrive(dempty);
+  uint32_t sz[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (FULL || u < nu) sz[u] = lds32(meta + u * UB);
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    if (FULL || u < nu) {
+      const uint2 xv = lds64(xs4 + (PH == 0 ? u >> 1 : u) * 16);
+      const float2 sf = __half22float2(*reinterpret_cast<const __half2*>(&sz[u]));
+      const int v = (static_cast<int>(D[u][0]) << 14) + (static_cast<int>(D[u][1]) << 7) + static_cast<int>(D[u][2]);
+      const float r = fmaf(sf.x, static_cast<float>(v), sf.y * __uint_as_float(xv.y)) * __uint_as_float(xv.x);
+      if (PH == 0 && (u & 1)) acc1 += r;
+      else acc0 += r;
+    }
+  }
+}
+
+// B > 1 epilogue of one stage: NA (>= na) tokens per unit, UC units per chunk
+// (stage sums in registers, segment sums in shared memory: eacc + (m kMaxTok + j) 512)
+template <int UB, int NA, int UC>
+__device__ __forceinline__ void epi_multi(uint32_t td, int N, uint32_t meta, uint32_t xs, int gps, int nu, int sh,
+                                          int na, uint32_t eacc, bool fresh) {
+  float rs[2][NA];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int j = 0; j < NA; ++j) rs[m][j] = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < nu; c += UC) {
+    uint32_t D[UC][NA][3];
+#pragma unroll
+    for (int i = 0; i < UC; ++i)
+#pragma unroll
+      for (int j = 0; j < NA; ++j)
+        if (c + i < nu && j < na) ld3(td + (c + i) * N + 8 * j, D[i][j]);
+    uint32_t sz[UC];
+#pragma unroll
+    for (int i = 0; i < UC; ++i)
+      if (c + i < nu) sz[i] = lds32(meta + (c + i) * UB);
+    ld_wait();
+#pragma unroll
+    for (int i = 0; i < UC; ++i) {
+      if (c + i < nu) {
+        const float2 sf = __half22float2(*reinterpret_cast<const __half2*>(&sz[i]));
+        const bool mat = ((c + i) & sh) != 0;
+        const int sg = (c + i) >> sh;
+#pragma unroll
+        for (int j = 0; j < NA; ++j) {
+          if (j < na) {
+            const uint2 xv = lds64(xs + (j * gps + sg) * 16);
+            const float2 xq = make_float2(__uint_as_float(xv.x), __uint_as_float(xv.y));
+            const int v = (static_cast<int>(D[i][j][0]) << 14) + (static_cast<int>(D[i][j][1]) << 7) +
+                          static_cast<int>(D[i][j][2]);
+            const float r = fmaf(sf.x, static_cast<float>(v), sf.y * xq.y) * xq.x;
+            // both sums updated (selects): a branch here is merged by the compiler
+            // into rs[mat][j], a dynamic index that moves rs to local memory
+            rs[0][j] += mat ? 0.f : r;
+            rs[1][j] += mat ? r : 0.f;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    if (m <= sh) {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) {
+        if (j < na) {
+          const uint32_t a = eacc + (m * kMaxTok + j) * 512;
+          float v = rs[m][j];
+          if (!fresh) v += __uint_as_float(lds32(a));
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+        }
+      }
+    }
   }
 }
 
@@ -1040,77 +1184,54 @@ __device__ __noinline__ void role_epilogue(const Args& A, Shared& S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, row = q * 32 + lane;
   const int NST = S.NST, SB = S.SB, nst = S.nstage, H = A.hidden;
-  const int N = ONE ? 8 : S.N, NDS = ONE ? 2 : S.NDS;
+  const int N = ONE ? 8 : S.N, NDS = ONE ? kOneNDS : S.NDS;
   const Plan& P = S.P;
   const uint32_t tl = S.tmem_base + (static_cast<uint32_t>(q * 32) << 16) + S.dcol;
   uint8_t* const ring = S.ring;
   const uint32_t sring = smem_u32(S.ring);
   const int dstride = 2 * P.gps * N;
   const uint32_t bsum = sring + S.bsum_off;
-  float acc[2][kMaxTok];
-#pragma unroll
-  for (int m = 0; m < 2; ++m)
-#pragma unroll
-    for (int j = 0; j < kMaxTok; ++j) acc[m][j] = 0.f;
+  float acc0 = 0.f, acc1 = 0.f;  // B == 1: this row's w1 (or w2) and w3 sums of the segment
+  const uint32_t eacc = smem_u32(S.eacc) + row * 4;  // B > 1: [2][kMaxTok][128] segment sums
+  bool fresh = true;
   int useg = 0;
   int slot = 0, sph = 0, ds = 0, dph = 0;
+  WStat ws;
+  wstat_init(A, ws);
   for (int s = 0; s < nst; ++s) {
     const Stg t = stg(S, s);
     const int nm = 2 - t.ph;
     const uint8_t* st = ring + static_cast<size_t>(slot) * SB;
     const int na = ONE ? 1 : P.act_n[t.a], p0 = P.act_p0[t.a];
     const int nu = t.ns * nm;
-    wait(&S.dfull[ds], dph);
+    wait_s<2>(A, ws, &S.dfull[ds], dph);
     if (!ONE) wait(&S.bopf[slot], sph);
     fence_after();
+    if (lane == 0 && warp == kEpi0) trace2(A, 2, s);
     if (ONE) {
       const uint32_t xs4 = bsum + S.doff[s] * 16;
       const uint32_t meta = sring + slot * SB + 128 * CB + row * 4;
-      uint32_t D[8][4];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (u < nu) ld4(tl + ds * dstride + u * N, D[u]);
-      ld_wait();
-      fence_before();
-      __syncwarp();
-      if (lane == 0) arrive(&S.dempty[ds]);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (u < nu) {
-          const int sg = u >> (nm - 1), mat = u & (nm - 1);
-          const uint32_t sz = lds32(meta + u * UB);
-          const float2 sf = __half22float2(*reinterpret_cast<const __half2*>(&sz));
-          const float4 xq = ldsf4(xs4 + sg * 16);
-          const int v = (static_cast<int>(D[u][0]) << 14) + (static_cast<int>(D[u][1]) << 7) + static_cast<int>(D[u][2]);
-          const float r = fmaf(sf.x, static_cast<float>(v), sf.y * xq.y) * xq.x;
-          if (mat) acc[1][0] += r;
-          else acc[0][0] += r;
-        }
+      const uint32_t td = tl + ds * dstride;
+      if (nu == 8) {
+        if (t.ph == 0) epi_one<UB, true, 0>(td, meta, xs4, nu, lane, &S.dempty[ds], acc0, acc1);
+        else epi_one<UB, true, 1>(td, meta, xs4, nu, lane, &S.dempty[ds], acc0, acc1);
+      } else {
+        if (t.ph == 0) epi_one<UB, false, 0>(td, meta, xs4, nu, lane, &S.dempty[ds], acc0, acc1);
+        else epi_one<UB, false, 1>(td, meta, xs4, nu, lane, &S.dempty[ds], acc0, acc1);
       }
     } else {
-      const float4* xs4 = reinterpret_cast<const float4*>(st + S.xs_off);
-#pragma unroll 1
-      for (int u = 0; u < nu; ++u) {
-        const int sg = u >> (nm - 1), mat = u & (nm - 1);
-        uint32_t D[kMaxTok][4];
-#pragma unroll
-        for (int j = 0; j < kMaxTok; ++j)
-          if (j < na) ld4(tl + ds * dstride + u * N + 8 * j, D[j]);
-        ld_wait();
-        const uint32_t sz = *reinterpret_cast<const uint32_t*>(st + u * UB + 128 * CB + row * 4);
-        const float2 sf = __half22float2(*reinterpret_cast<const __half2*>(&sz));
-#pragma unroll
-        for (int j = 0; j < kMaxTok; ++j) {
-          if (j < na) {
-            const float4 xq = xs4[j * P.gps + sg];
-            const int v = (static_cast<int>(D[j][0]) << 14) + (static_cast<int>(D[j][1]) << 7) +
-                          static_cast<int>(D[j][2]);
-            const float r = fmaf(sf.x, static_cast<float>(v), sf.y * xq.y) * xq.x;
-            if (mat) acc[1][j] += r;
-            else acc[0][j] += r;
-          }
-        }
-      }
+      // several tokens per expert: D block of unit u, token j = columns u N + 8 j;
+      // units in chunks whose TMEM loads are all in flight together
+      const uint32_t td = tl + ds * dstride, meta = sring + slot * SB + 128 * CB + row * 4;
+      const uint32_t xs = sring + slot * SB + S.xs_off;
+      const int sh = nm - 1;
+      // reloaded per stage (volatile): keeps the compiler from hoisting every
+      // instance's gps / N derived offsets out of the stage loop (register spills)
+      const int gps = static_cast<int>(lds32(smem_u32(&S.P.gps))), N = static_cast<int>(lds32(smem_u32(&S.N)));
+      if (na == 1) epi_multi<UB, 1, 2>(td, N, meta, xs, gps, nu, sh, na, eacc, fresh);
+      else if (na == 2) epi_multi<UB, 2, 1>(td, N, meta, xs, gps, nu, sh, na, eacc, fresh);
+      else if (na <= 4) epi_multi<UB, 4, 1>(td, N, meta, xs, gps, nu, sh, na, eacc, fresh);
+      else epi_multi<UB, 8, 1>(td, N, meta, xs, gps, nu, sh, na, eacc, fresh);
       fence_before();
       __syncwarp();
       if (lane == 0) arrive(&S.dempty[ds]);
@@ -1118,18 +1239,22 @@ __device__ __noinline__ void role_epilogue(const Args& A, Shared& S) {
     __syncwarp();
     if (lane == 0) arrive(&S.empty[slot]);  // metadata and sums read
     if (lane == 0 && warp == kEpi0) trace2(A, 1, s);
+    fresh = false;
     if (t.seg_end) {  // segment end: flush
+      fresh = true;
       if (t.ph == 0) {
         const int ts = useg & 1;
-        if (useg >= 2) wait(&S.tempty[ts], ((useg >> 1) - 1) & 1);
+        if (useg >= 2) wait_s<3>(A, ws, &S.tempty[ts], ((useg >> 1) - 1) & 1);
         const uint32_t tr = smem_u32(S.tres) + ts * (2 * kMaxTok * 128) * 4;
 #pragma unroll
         for (int m = 0; m < 2; ++m)
 #pragma unroll
           for (int j = 0; j < kMaxTok; ++j)
-            if (j < na)
-              asm volatile("st.shared.f32 [%0], %1;" ::"r"(tr + ((m * kMaxTok + j) * 128 + row) * 4), "f"(acc[m][j])
+            if (j < na) {
+              const float v = ONE ? (m == 0 ? acc0 : acc1) : __uint_as_float(lds32(eacc + (m * kMaxTok + j) * 512));
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(tr + ((m * kMaxTok + j) * 128 + row) * 4), "f"(v)
                            : "memory");
+            }
         __syncwarp();
         if (lane == 0) arrive(&S.tfull[ts]);
         ++useg;
@@ -1139,18 +1264,17 @@ __device__ __noinline__ void role_epilogue(const Args& A, Shared& S) {
         for (int j = 0; j < kMaxTok; ++j) {
           if (j < na) {
             const int p = p0 + j;
-            red_add(A.y + static_cast<size_t>(P.pair_tok[p]) * H + rg, acc[0][j] * P.pair_w[p]);
+            const float v = ONE ? acc0 : __uint_as_float(lds32(eacc + j * 512));
+            red_add(A.y + static_cast<size_t>(P.pair_tok[p]) * H + rg, v * P.pair_w[p]);
           }
         }
       }
-#pragma unroll
-      for (int m = 0; m < 2; ++m)
-#pragma unroll
-        for (int j = 0; j < kMaxTok; ++j) acc[m][j] = 0.f;
+      acc0 = acc1 = 0.f;
     }
     if (++slot == NST) { slot = 0; sph ^= 1; }
     if (++ds == NDS) { ds = 0; dph ^= 1; }
   }
+  wstat_done(A, ws);
 }
 
 // ---- aux warps (128 threads = tile rows)
@@ -1449,6 +1573,7 @@ __global__ void __launch_bounds__(kThreads, 1) tcd_kernel(const __grid_constant_
     uint32_t dyn;
     asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
     S.tres = reinterpret_cast<float*>(smem + dyn - kTresBytes);
+    S.eacc = reinterpret_cast<float*>(smem + dyn - kTresBytes - kEaccBytes);
   }
   for (int i = tid; i < kMaxE; i += kThreads) S.mark[i] = 0u;
   __syncthreads();

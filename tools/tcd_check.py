@@ -41,8 +41,9 @@ def compare(name, sl, B, k, n, seed=0):
     return rel(y1, y2), same_idx
 
 
-def timing(B=1, layers=8, steps=400, tcd=True):
-    sls = [SynthLayer(4096, 14336, 8, top_k=2, bits=2, rank=32, seed=100 * l, max_tokens=64) for l in range(layers)]
+def timing(B=1, layers=8, steps=400, tcd=True, bits=2):
+    sls = [SynthLayer(4096, 14336, 8, top_k=2, bits=bits, rank=32, seed=100 * l, max_tokens=64, tiles=(bits == 2))
+           for l in range(layers)]
     xs = [torch.randn((B, 4096), device="cuda").to(torch.bfloat16) for _ in range(2 * layers)]
     ys = [torch.empty((B, 4096), dtype=torch.float32, device="cuda") for _ in range(layers)]
     idx = [torch.empty((B, 2), dtype=torch.int32, device="cuda") for _ in range(layers)]
@@ -54,7 +55,8 @@ def timing(B=1, layers=8, steps=400, tcd=True):
 
         def step(i):
             l = i % layers
-            sls[l].layer.forward(xs[i % (2 * layers)], 2, 1, y=ys[l], topk_idx=idx[l], topk_w=wts[l])
+            sls[l].layer.forward(xs[i % (2 * layers)], 2, 1, y=ys[l], topk_idx=idx[l], topk_w=wts[l],
+                                 generic=(bits != 2 and mode != "tcd"))
 
         for i in range(2 * layers):
             step(i)
@@ -79,7 +81,8 @@ def timing(B=1, layers=8, steps=400, tcd=True):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         out[mode] = ms * 1e3 / steps
-        print(f"timing {mode}: B={B} {out[mode]:.2f} us/step  {steps * B / (ms / 1e3):.0f} tok/s", flush=True)
+        name = mode if bits == 2 or mode == "tcd" else "generic"
+        print(f"timing {name}: {bits}-bit B={B} {out[mode]:.2f} us/step  {steps * B / (ms / 1e3):.0f} tok/s", flush=True)
     return out
 
 
@@ -107,7 +110,11 @@ def main():
         del sl
     torch.cuda.empty_cache()
     timing(B=1)
-    if not quick:
+    if "--timing3" in sys.argv:
+        timing(B=8, steps=200)
+        timing(B=1, bits=3, steps=200)
+        timing(B=8, bits=3, steps=100)
+    elif not quick:
         timing(B=8, steps=200)
 
 

@@ -51,12 +51,12 @@ sl.layer.forward(x, 2, 1)
 torch.cuda.synchronize()
 _lib.check(_lib.lib().lrc_debug_stamps(5, ws, 192))
 w = np.array(ws[:], dtype=np.float64).reshape(24, 8)
-print("CTA 0 wait cycles: decode warps: full aempty | total;  epilogue warps: dfull bopf | total")
+print("CTA 0 wait cycles: decode warps: full aempty | total;  epilogue warps: dfull tempty | total")
 for i in range(8):
     print(f"  dec w{i}: {w[i][0]:9.0f} {w[i][1]:9.0f} | {w[i][7]:9.0f}")
-for i in range(8, 16):
+for i in range(8, 12):
     print(f"  epi w{i}: {w[i][2]:9.0f} {w[i][3]:9.0f} | {w[i][7]:9.0f}")
-print(f"  mma w12: afull+dempty {w[16][4]:9.0f} bopf {w[16][5]:9.0f} | total {w[16][7]:9.0f}")
+print(f"  mma w12: afull {w[12][4]:9.0f} dempty {w[12][5]:9.0f} images {w[12][6]:9.0f} | issue {w[12][2]:9.0f} +commits {w[12][3]:9.0f} | total {w[12][7]:9.0f}")
 tr = (ctypes.c_uint64 * 2048)()
 _lib.check(_lib.lib().lrc_debug_stamps(3, tr, 2048))
 sl.layer.forward(x, 2, 1)
@@ -67,6 +67,6 @@ b = t[0][0]
 def f(v):
     return f"{v - b:8.0f}" if v > 0 else "       -"
 print("CTA 0, clock64 cycles from producer stage-0 issue")
-print("stage: codes issued | B issued | dec w0 aempty seen | dec w0 done | MMA issued | epi dfull seen | epi done")
+print("stage: codes issued | B issued | dec w0 aempty seen | dec w0 done | MMA issued | epi dfull seen | epi D loaded | epi done")
 for i in range(40):
-    print(f"  {i:3d}: {f(t[0][i])} {f(t[1][i])} {f(t[7][i])} {f(t[3][i])} {f(t[2][i])} {f(t[6][i])} {f(t[5][i])}")
+    print(f"  {i:3d}: {f(t[0][i])} {f(t[1][i])} {f(t[7][i])} {f(t[3][i])} {f(t[2][i])} {f(t[6][i])} {f(t[4][i])} {f(t[5][i])}")

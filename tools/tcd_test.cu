@@ -997,9 +997,220 @@ static void run_part10(const char* name, int threads) {
   cudaFree(d);
 }
 
+
+// ---------------------------------------------------------------- part 11 ----
+// MMA throughput (i8 K32 N=8, A from TMEM, unrolled) while other warps load
+// the TMEM ports: NST warps doing tcgen05.st x16 (+wait) to other columns,
+// NLD warps doing tcgen05.ld x4 (+wait) from the D area.
+template <int NST, int NLD, bool SS>
+__global__ void part11(int iters, long long* cyc, int* sink) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  __shared__ volatile int stop;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    bar_init(&bar, 1);
+    stop = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  const uint32_t id = idesc8(true, 128, 8);
+  if (warp == 0) {
+    const uint64_t db0 = desc_ns(smem_u32(sm + 32768), 128, 256);
+    const uint64_t da0 = desc_ns(smem_u32(sm), 128, 256);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      if (elect_one()) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (SS)
+            asm volatile(
+                "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;}" ::"r"(tm + 256 + (j & 3) * 8),
+                "l"(da0 + j * 128), "l"(db0 + j * 16), "r"(id), "r"(1u));
+          else
+            asm volatile(
+                "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;}" ::"r"(tm + 256 + (j & 3) * 8),
+                "r"(tm + j * 8), "l"(db0 + j * 16), "r"(id), "r"(1u));
+        }
+      }
+      __syncwarp();
+    }
+    if (elect_one()) commit(&bar);
+    __syncwarp();
+    bar_wait(&bar, 0);
+    if (tid == 0) {
+      cyc[0] = clock64() - t0;
+      stop = 1;
+    }
+  } else if (warp <= NST) {
+    const uint32_t tl = tm + (static_cast<uint32_t>(((warp - 1) & 3) * 32) << 16) + 128 + ((warp - 1) >> 2) * 64;
+    uint32_t r[16];
+    for (int i = 0; i < 16; ++i) r[i] = tid * 16 + i;
+    long long n = 0;
+    while (!stop) {
+#pragma unroll 1
+      for (int k = 0; k < 4; ++k) {
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+                tl + k * 16),
+            "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+            "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      n += 4;
+      r[n & 15] += 1;
+    }
+    if ((tid & 31) == 0) sink[warp] = static_cast<int>(n);
+  } else if (warp <= NST + NLD) {
+    const uint32_t tl = tm + (static_cast<uint32_t>(((warp - 1 - NST) & 3) * 32) << 16) + 384;
+    long long n = 0;
+    uint32_t acc = 0;
+    const long long tl0 = clock64();
+    while (!stop) {
+      uint32_t d[8][4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(d[u][0]), "=r"(d[u][1]), "=r"(d[u][2]), "=r"(d[u][3]) : "r"(tl + u * 8));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += d[u][0] + d[u][1];
+      n += 8;
+    }
+    if ((tid & 31) == 0) sink[warp] = static_cast<int>((clock64() - tl0) / (n / 8)) + (acc == 12345 ? 1 : 0);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+template <int NST, int NLD, bool SS>
+static void run_part11() {
+  const int iters = 512;
+  long long* d;
+  int* sink;
+  cudaMalloc(&d, 8);
+  cudaMalloc(&sink, 64 * 4);
+  auto k = part11<NST, NLD, SS>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  const int thr = 32 * (1 + NST + NLD);
+  k<<<1, thr, 100 * 1024>>>(iters, d, sink);
+  k<<<1, thr, 100 * 1024>>>(iters, d, sink);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h = 0;
+  int hs[64];
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(hs, sink, 64 * 4, cudaMemcpyDeviceToHost);
+  printf("part11 %s MMA i8 N8 K32 with %d st-warps, %d ld-warps: %s %.1f cycles/MMA  (st per warp %d, ld 8x4+wait %d cycles)\n",
+         SS ? "SS" : "TS", NST, NLD, cudaGetErrorString(e), double(h) / (iters * 8), NST ? hs[1] : 0,
+         NLD ? hs[1 + NST] : 0);
+  cudaFree(d);
+  cudaFree(sink);
+}
+
+// ---------------------------------------------------------------- part 12 ----
+// One decode stage's MMAs in isolation: NU units x 2 MMAs (i8 K32 N8, A from
+// TMEM, D per unit), one commit, wait: latency per stage
+template <int NU>
+__global__ void part12(int iters, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    bar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  const uint32_t id = idesc8(true, 128, 8);
+  if (warp == 0) {
+    const uint32_t b0 = smem_u32(sm + 32768);
+    long long tot = 0;
+    for (int it = 0; it < iters; ++it) {
+      const long long t0 = clock64();
+      if (elect_one()) {
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+          const uint32_t d = tm + 384 + u * 8, a = tm + (it % 3) * 128 + u * 16;
+          const uint64_t bd = desc_ns(b0 + (u >> 1) * 512, 128, 256);
+          asm volatile(
+              "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;}" ::"r"(d), "r"(a), "l"(bd), "r"(id), "r"(0u));
+          asm volatile(
+              "{.reg .pred p; setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;}" ::"r"(d), "r"(a + 8), "l"(bd + 16), "r"(id), "r"(1u));
+        }
+        commit(&bar);
+      }
+      __syncwarp();
+      bar_wait(&bar, it & 1);
+      tot += clock64() - t0;
+    }
+    if (tid == 0) cyc[0] = tot;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+template <int NU>
+static void run_part12() {
+  const int iters = 256;
+  long long* d;
+  cudaMalloc(&d, 8);
+  auto k = part12<NU>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  k<<<1, 128, 100 * 1024>>>(iters, d);
+  k<<<1, 128, 100 * 1024>>>(iters, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h = 0;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("part12 stage of %d units (%d MMAs) + commit + wait: %s %.1f cycles/stage\n", NU, 2 * NU,
+         cudaGetErrorString(e), double(h) / iters);
+  cudaFree(d);
+}
+
 int main() {
   setvbuf(stdout, NULL, _IONBF, 0);
   srand(7);
+  if (getenv("PART12")) {
+    run_part12<1>();
+    run_part12<2>();
+    run_part12<4>();
+    run_part12<8>();
+    return 0;
+  }
+  if (getenv("PART11")) {
+    run_part11<0, 0, false>();
+    run_part11<1, 0, false>();
+    run_part11<4, 0, false>();
+    run_part11<8, 0, false>();
+    run_part11<0, 4, false>();
+    run_part11<8, 4, false>();
+    run_part11<0, 0, true>();
+    run_part11<8, 0, true>();
+    run_part11<8, 4, true>();
+    return 0;
+  }
   run_part10<0>("test_wait completed phase (1 warp)", 32);
   run_part10<1>("try_wait completed phase (1 warp)", 32);
   run_part10<0>("test_wait completed phase (15 warps)", 480);
