@@ -64,6 +64,33 @@ __device__ __forceinline__ float lr_up_dot(const lrc_qmat& U, int row, const flo
 // --------------------------------------------------- generic expert kernels ---
 constexpr int kChunk = 8;
 
+// qrow_dot_g64 with the token count rounded up to 1, 2, 4 or 8 (fewer
+// registers and no dead token lanes for the common small counts)
+template <int BITS, typename XT>
+__device__ __forceinline__ void gdot(const lrc_qmat& W, int row, const XT* const (&xp)[kChunk], int nb,
+                                     float (&acc)[kChunk]) {
+  if (nb == 1) {
+    const XT* const x1[1] = {xp[0]};
+    float a1[1];
+    qrow_dot_g64<BITS, 1>(W, row, x1, 1, a1);
+    acc[0] = a1[0];
+  } else if (nb == 2) {
+    const XT* const x2[2] = {xp[0], xp[1]};
+    float a2[2];
+    qrow_dot_g64<BITS, 2>(W, row, x2, 2, a2);
+    acc[0] = a2[0];
+    acc[1] = a2[1];
+  } else if (nb <= 4) {
+    const XT* const x4[4] = {xp[0], xp[1], xp[2], xp[3]};
+    float a4[4];
+    qrow_dot_g64<BITS, 4>(W, row, x4, nb, a4);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = a4[i];
+  } else {
+    qrow_dot_g64<BITS, kChunk>(W, row, xp, nb, acc);
+  }
+}
+
 __global__ void __launch_bounds__(256) up_generic_kernel(ExpertArgs a) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -85,21 +112,38 @@ __global__ void __launch_bounds__(256) up_generic_kernel(ExpertArgs a) {
         int p = a.plan.pair_list[off + c0 + min(i, nch - 1)];
         xp[i] = a.x + static_cast<int64_t>(a.plan.pair_token[p]) * a.hidden;
       }
-      for (int k = lane; k < a.hidden; k += 32) {
-        const float w1v = qmat_elem(E.w1, f, k), w3v = qmat_elem(E.w3, f, k);
+      const bool fast = a.g64 && E.w1.bits == E.w3.bits;
+      if (fast && E.w1.bits == 2) {
+        gdot<2>(E.w1, f, xp, nch, acc1);
+        gdot<2>(E.w3, f, xp, nch, acc3);
+      } else if (fast && E.w1.bits == 3) {
+        gdot<3>(E.w1, f, xp, nch, acc1);
+        gdot<3>(E.w3, f, xp, nch, acc3);
+      } else if (fast && E.w1.bits == 4) {
+        gdot<4>(E.w1, f, xp, nch, acc1);
+        gdot<4>(E.w3, f, xp, nch, acc3);
+      } else {
+        for (int k = lane; k < a.hidden; k += 32) {
+          const float w1v = qmat_elem(E.w1, f, k), w3v = qmat_elem(E.w3, f, k);
+#pragma unroll
+          for (int i = 0; i < kChunk; ++i) {
+            if (i < nch) {
+              const float xv = bf2f(xp[i][k]);
+              acc1[i] = fmaf(w1v, xv, acc1[i]);
+              acc3[i] = fmaf(w3v, xv, acc3[i]);
+            }
+          }
+        }
 #pragma unroll
         for (int i = 0; i < kChunk; ++i) {
-          if (i < nch) {
-            const float xv = bf2f(xp[i][k]);
-            acc1[i] = fmaf(w1v, xv, acc1[i]);
-            acc3[i] = fmaf(w3v, xv, acc3[i]);
-          }
+          acc1[i] = warp_sum(acc1[i]);
+          acc3[i] = warp_sum(acc3[i]);
         }
       }
 #pragma unroll
       for (int i = 0; i < kChunk; ++i) {
         if (i < nch) {
-          float h1 = warp_sum(acc1[i]), h3 = warp_sum(acc3[i]);
+          float h1 = acc1[i], h3 = acc3[i];
           const int p = a.plan.pair_list[off + c0 + i];
           const int slot = a.plan.pair_comp[p];
           if (slot >= 0) {
@@ -126,8 +170,21 @@ __global__ void __launch_bounds__(256) lr_mid_kernel(ExpertArgs a) {
   float acc = 0.0f;
   if (qmat_present(E.v2) && j < E.v2.rows) {
     const float* ap = a.a32 + static_cast<int64_t>(p) * a.ffn;
-    for (int k = lane; k < E.v2.cols; k += 32) acc = fmaf(qmat_elem(E.v2, j, k), ap[k], acc);
-    acc = warp_sum(acc);
+    const float* const xp[1] = {ap};
+    float av[1];
+    if (a.g64 && qmat_g64(E.v2) && E.v2.bits == 3) {
+      qrow_dot_g64<3, 1>(E.v2, j, xp, 1, av);
+      acc = av[0];
+    } else if (a.g64 && qmat_g64(E.v2) && E.v2.bits == 2) {
+      qrow_dot_g64<2, 1>(E.v2, j, xp, 1, av);
+      acc = av[0];
+    } else if (a.g64 && qmat_g64(E.v2) && E.v2.bits == 4) {
+      qrow_dot_g64<4, 1>(E.v2, j, xp, 1, av);
+      acc = av[0];
+    } else {
+      for (int k = lane; k < E.v2.cols; k += 32) acc = fmaf(qmat_elem(E.v2, j, k), ap[k], acc);
+      acc = warp_sum(acc);
+    }
   }
   if (lane == 0) a.t[t_base(a, p, 2) + j] = acc;
 }
@@ -153,16 +210,26 @@ __global__ void __launch_bounds__(256) down_generic_kernel(ExpertArgs a) {
         int p = a.plan.pair_list[off + c0 + min(i, nch - 1)];
         ap[i] = a.a32 + static_cast<int64_t>(p) * a.ffn;
       }
-      for (int k = lane; k < a.ffn; k += 32) {
-        const float wv = qmat_elem(E.w2, r, k);
+      if (a.g64 && E.w2.bits == 2) {
+        gdot<2>(E.w2, r, ap, nch, acc);
+      } else if (a.g64 && E.w2.bits == 3) {
+        gdot<3>(E.w2, r, ap, nch, acc);
+      } else if (a.g64 && E.w2.bits == 4) {
+        gdot<4>(E.w2, r, ap, nch, acc);
+      } else {
+        for (int k = lane; k < a.ffn; k += 32) {
+          const float wv = qmat_elem(E.w2, r, k);
 #pragma unroll
-        for (int i = 0; i < kChunk; ++i)
-          if (i < nch) acc[i] = fmaf(wv, ap[i][k], acc[i]);
+          for (int i = 0; i < kChunk; ++i)
+            if (i < nch) acc[i] = fmaf(wv, ap[i][k], acc[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < kChunk; ++i) acc[i] = warp_sum(acc[i]);
       }
 #pragma unroll
       for (int i = 0; i < kChunk; ++i) {
         if (i < nch) {
-          float v = warp_sum(acc[i]);
+          float v = acc[i];
           const int p = a.plan.pair_list[off + c0 + i];
           const int slot = a.plan.pair_comp[p];
           if (slot >= 0 && qmat_present(E.u2))
@@ -303,7 +370,8 @@ struct lrc_layer {
   int hidden = 0, ffn = 0, E = 0, S = 0, max_tokens = 0, k_max = 0, maxr = 0;
   int num_sms = 148;
   bool tiled = false;
-  bool prefill_ok = false;  // tcgen05 prefill GEMM eligible (2-bit gs64 reference-layout weights)
+  bool prefill_ok = false;
+  int prefill_bits = 2;  // code width of the prefill packs  // tcgen05 prefill GEMM eligible (2-bit gs64 reference-layout weights)
   uint16_t* lrp = nullptr;     // per-expert bf16 LR packs for the prefill path (built lazily)
   uint8_t* ppk = nullptr;      // per-expert prefill packs of the weight codes (built lazily)
   std::vector<uint8_t> lrp_dirty;  // per expert: packs stale (expert replaced)
@@ -352,6 +420,7 @@ struct lrc_layer {
     return v ? atoi(v) : -1;  // -1: auto (on where the tiled kernels do not apply, e.g. 3-bit)
   }();
   bool tcd_ok = false;
+  bool g64_ok = false;  // generic path: group-vectorised decode (qrow_dot_g64) for every expert
   int tcd_bits = 2, tcd_fbits = 3;
   std::vector<uint8_t> tcd_dirty;  // per expert: pack stale
   bool tcd_table_dirty = true;
@@ -418,8 +487,16 @@ static void refresh_tiled(lrc_layer* L) {
     L->lr_down_max = std::max(L->lr_down_max, lay.down_total);
   }
   L->tiled = ok;
+  const int old_pbits = L->prefill_bits;
   L->prefill_ok = prefill_eligible(L->host_experts.data(), static_cast<int>(L->host_experts.size()),
-                                   L->hidden, L->ffn, L->maxr);
+                                   L->hidden, L->ffn, L->maxr, &L->prefill_bits);
+  if (L->prefill_bits != old_pbits && L->ppk != nullptr) {  // pack size follows the code width
+    cudaFree(L->ppk);
+    L->ppk = nullptr;
+    std::fill(L->lrp_dirty.begin(), L->lrp_dirty.end(), 1);
+  }
+  L->g64_ok = (L->hidden % 64) == 0 && (L->ffn % 64) == 0;
+  for (auto& e : L->host_experts) L->g64_ok = L->g64_ok && qmat_g64(e.w1) && qmat_g64(e.w3) && qmat_g64(e.w2);
   L->tcd_ok = L->maxr <= tcd::kRMax && tcd::eligible(L->host_experts.data(), static_cast<int>(L->host_experts.size()),
                                                       L->hidden, L->ffn, &L->tcd_bits, &L->tcd_fbits);
 }
@@ -947,8 +1024,14 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   a.a16 = L->a16;
   a.y = y;
   a.max_pairs = L->max_pairs;
+  a.g64 = (L->g64_ok && !L->pager && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(L->a32) & 15) == 0) ? 1 : 0;
   // (the pager's descriptors point at slot copies of the tiled layout only)
-  const bool prefill = allow_tiled && L->prefill_ok && !L->pager && L->prefill_min > 0 && B >= L->prefill_min;
+  // without tiled packs (3-bit codes) the prefill engine also takes the batches
+  // above the tensor-core decode engine's range: the generic CUDA-core path is
+  // 15x slower there (tools/prefill3_check.py)
+  const int64_t pmin = L->tiled ? L->prefill_min : std::min<int64_t>(L->prefill_min, tcd::kMaxTok + 1);
+  const bool prefill = allow_tiled && L->prefill_ok && !L->pager && L->prefill_min > 0 && B >= pmin;
   if (!spec && L->maxr && !prefill) {  // exact V.x for the compensated pairs only
     if ((s = launch_lr_down(a, np_bound, st)) != LRC_OK) return s;
     ++launches;
@@ -958,19 +1041,19 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
     // large batches: tcgen05 grouped dequant-GEMMs (V1|V3.x, up, V2.a, down)
     // (re)build the packs of experts changed since the last prefill call: the
     // weight codes as contiguous per-slab blocks, the LR factors as bf16 rows
-    const size_t pb = static_cast<size_t>(prefill_pack_bytes(L->hidden, L->ffn));
+    const size_t pb = static_cast<size_t>(prefill_pack_bytes(L->hidden, L->ffn, L->prefill_bits));
     if (L->ppk == nullptr) LRC_CUDA_TRY(cudaMalloc(&L->ppk, pb * L->lrp_dirty.size()));
     const size_t per = static_cast<size_t>(prefill_lr_pack_elems(L->hidden, L->ffn, L->maxr));
     for (size_t i = 0; i < L->lrp_dirty.size(); ++i)
       if (L->lrp_dirty[i]) {
-        if ((s = build_prefill_pack(L->host_experts[i], L->hidden, L->ffn, L->ppk + pb * i, st)) != LRC_OK)
+        if ((s = build_prefill_pack(L->host_experts[i], L->hidden, L->ffn, L->prefill_bits, L->ppk + pb * i, st)) != LRC_OK)
           return s;
         if (L->maxr &&
             (s = build_prefill_lr(L->host_experts[i], L->hidden, L->ffn, L->maxr, L->lrp + per * i, st)) != LRC_OK)
           return s;
         L->lrp_dirty[i] = 0;
       }
-    if ((s = launch_prefill(a, np_bound, L->lrp, L->tb, L->ppk, st, &launches)) != LRC_OK) return s;
+    if ((s = launch_prefill(a, np_bound, L->lrp, L->tb, L->ppk, L->prefill_bits, st, &launches)) != LRC_OK) return s;
     if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));  // phases: up+mid+down lumped into [2]
   } else if (allow_tiled && L->tiled) {
     const int tok_bound = static_cast<int>(std::min<int64_t>(B, L->max_tokens));

@@ -132,6 +132,77 @@ __device__ void vrow_dot_tokens(const lrc_qmat& V, int j, const uint16_t* __rest
   for (int t = 0; t < MAXT; ++t) acc[t] = warp_sum(acc[t]);
 }
 
+// Row `row` of a quantized weight matrix (group size 64, BITS-bit LSB-first
+// stream, rows word-aligned) dotted with NT token vectors xp[t] (bf16 or f32,
+// 16-byte aligned, length W.cols): each lane takes whole 64-code groups and
+// decodes them with funnel shifts once for all tokens.  acc[t] is
+// warp-reduced on return.  The generic expert path for g64 codes of any width
+// (ref/quant.py:216-224: W = s * c + z per group).
+__device__ __forceinline__ void load8(const uint16_t* p, float (&v)[8]) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const uint32_t u4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v[2 * q] = bf2f(u4[q] & 0xffff);
+    v[2 * q + 1] = bf2f(u4[q] >> 16);
+  }
+}
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <int BITS, int NT, typename XT>
+__device__ void qrow_dot_g64(const lrc_qmat& W, int row, const XT* const (&xp)[NT], int nb, float (&acc)[NT]) {
+  constexpr int NW = 2 * BITS;  // 32-bit words per 64-code group
+  const int lane = threadIdx.x & 31;
+  const int gpr = W.cols / 64;
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(W.packed) + (static_cast<int64_t>(row) * W.cols * BITS >> 5);
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
+  for (int g = lane; g < gpr; g += 32) {
+    uint32_t w[NW + 1];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) w[i] = __ldg(words + g * NW + i);
+    w[NW] = 0u;
+    const float s = h2f(W.scales[static_cast<int64_t>(row) * gpr + g]);
+    const float z = h2f(W.zeros[static_cast<int64_t>(row) * gpr + g]);
+    float cx[NT], sx[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) cx[t] = sx[t] = 0.0f;
+#pragma unroll
+    for (int i8 = 0; i8 < 8; ++i8) {
+      float c[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int bit = (i8 * 8 + q) * BITS;
+        c[q] = static_cast<float>(__funnelshift_r(w[bit >> 5], w[(bit >> 5) + 1], bit & 31) & ((1u << BITS) - 1u));
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        if (t < nb) {
+          float xv[8];
+          load8(xp[t] + g * 64 + i8 * 8, xv);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            cx[t] = fmaf(c[q], xv[q], cx[t]);
+            sx[t] += xv[q];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[t] = fmaf(s, cx[t], fmaf(z, sx[t], acc[t]));
+  }
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t] = warp_sum(acc[t]);
+}
+// codes this path takes: packed, group size 64, rows a whole number of words
+__host__ __device__ inline bool qmat_g64(const lrc_qmat& W) {
+  return W.dense == nullptr && W.packed != nullptr && W.group_size == 64 && (W.cols % 64) == 0 &&
+         (W.bits == 2 || W.bits == 3 || W.bits == 4) && ((static_cast<int64_t>(W.cols) * W.bits) % 32) == 0;
+}
+
 int route_tiles(int64_t B);
 // large-batch plan (router in routing-only mode, then a parallel counting sort)
 constexpr int kSerialPlanMaxPairs = 2048;
@@ -153,6 +224,7 @@ struct ExpertArgs {
   float* y;                   // [B][hidden] (accumulated)
   int max_pairs;
   int ne;                     // experts incl. shared; t is [B][ne][3][maxr]
+  int g64;                    // every expert's w1/w3/w2 take qrow_dot_g64 (generic path)
 };
 
 // Byte layout of the low-rank factor tiles that ride along with a weight tile
@@ -210,13 +282,13 @@ lrc_status launch_down_tiled(const ExpertArgs& a, int num_sms, int max_tokens_pe
                              int lr_down_max, cudaStream_t st, bool pdl);
 
 // tcgen05 prefill GEMM (prefill.cu)
-bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn, int maxr);
+bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn, int maxr, int* bits);
 int64_t prefill_lr_pack_elems(int hidden, int ffn, int maxr);  // bf16 elements per expert
 int prefill_tb_width(int maxr);
 lrc_status build_prefill_lr(const lrc_expert& e, int hidden, int ffn, int maxr, uint16_t* out, cudaStream_t st);
-int64_t prefill_pack_bytes(int hidden, int ffn);  // per expert
-lrc_status build_prefill_pack(const lrc_expert& e, int hidden, int ffn, uint8_t* out, cudaStream_t st);
+int64_t prefill_pack_bytes(int hidden, int ffn, int bits);  // per expert
+lrc_status build_prefill_pack(const lrc_expert& e, int hidden, int ffn, int bits, uint8_t* out, cudaStream_t st);
 lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp, uint16_t* tb,
-                          const uint8_t* ppk, cudaStream_t st, int* launches);
+                          const uint8_t* ppk, int bits, cudaStream_t st, int* launches);
 
 }  // namespace lrc

@@ -57,9 +57,15 @@ constexpr int kStageBytes = 2 * kSlabA + kSlabB;  // 48 KB
 constexpr int kProd = 256;
 constexpr int kThreads = kProd + 32;
 constexpr int kMmaWarp = kProd / 32;
-constexpr int kCB = 2560;  // prefill-pack block: 128 rows x (16 B codes) + 128 x (fp16 scale, fp16 zero)
-constexpr int kCR = 6;     // code ring depth (slabs), filled by cp.async.bulk
-constexpr int kSmemBytes = kStages * kStageBytes + kCR * 2 * kCB + 1024;
+// prefill-pack block: 128 rows x (8 BITS bytes of codes) + 128 x (fp16 scale, fp16 zero)
+__host__ __device__ constexpr int cb_bytes(int bits) { return 128 * 8 * bits + 512; }
+// code ring depth (slabs, filled by cp.async.bulk): 6 x 2 x 2,560 B (2-bit) or
+// 4 x 2 x 3,584 B (3-bit) in the same 30 KB
+__host__ __device__ constexpr int cr_depth(int bits) { return bits == 2 ? 6 : 4; }
+constexpr int kCR = 6;  // max ring depth
+constexpr int kRingBytes = 6 * 2 * cb_bytes(2);
+static_assert(4 * 2 * cb_bytes(3) <= kRingBytes, "3-bit code ring");
+constexpr int kSmemBytes = kStages * kStageBytes + kRingBytes + 1024;
 constexpr uint32_t kIdesc = umma::idesc_bf16(2 * kTM, kTN);
 
 enum Mode : int {
@@ -101,14 +107,15 @@ __host__ __device__ inline LrPack lr_pack_layout(int hidden, int ffn, int R) {
 struct PPack {
   int64_t w1, w3, w2, stride;  // byte offsets in an expert's pack
 };
-__host__ __device__ inline PPack ppack_layout(int hidden, int ffn) {
+__host__ __device__ inline PPack ppack_layout(int hidden, int ffn, int bits) {
   const int64_t up = static_cast<int64_t>((ffn + 127) / 128) * (hidden / 64);
   const int64_t dn = static_cast<int64_t>((hidden + 127) / 128) * (ffn / 64);
+  const int cb = cb_bytes(bits);
   PPack L;
   L.w1 = 0;
-  L.w3 = up * kCB;
-  L.w2 = 2 * up * kCB;
-  L.stride = (2 * up + dn) * kCB;
+  L.w3 = up * cb;
+  L.w2 = 2 * up * cb;
+  L.stride = (2 * up + dn) * cb;
   return L;
 }
 
@@ -123,6 +130,7 @@ struct PrefillArgs {
   int WT;
   const uint8_t* ppk;  // prefill packs [ne][PL.stride]
   PPack PL;
+  int bits, cb, cr;  // code width, pack block bytes, code ring depth
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -148,9 +156,10 @@ struct RowSlab {
   uint32_t s, z;
 };
 
-__global__ void build_ppack_kernel(lrc_expert E, int hidden, int ffn, PPack L, uint8_t* out) {
+__global__ void build_ppack_kernel(lrc_expert E, int hidden, int ffn, PPack L, int bits, uint8_t* out) {
   const int64_t up = static_cast<int64_t>((ffn + 127) / 128) * (hidden / 64);
-  const int64_t nblk = L.stride / kCB;
+  const int cb = cb_bytes(bits), rb = 8 * bits;  // block bytes, code bytes per row slab
+  const int64_t nblk = L.stride / cb;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nblk * 128;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t blk = i >> 7;
@@ -160,16 +169,18 @@ __global__ void build_ppack_kernel(lrc_expert E, int hidden, int ffn, PPack L, u
     const int K = blk < 2 * up ? hidden : ffn, M = blk < 2 * up ? ffn : hidden;
     const int nslab = K / 64;
     const int row = static_cast<int>(b / nslab) * 128 + r, s = static_cast<int>(b % nslab);
-    uint4 c = make_uint4(0, 0, 0, 0);
+    uint2 c[3] = {make_uint2(0, 0), make_uint2(0, 0), make_uint2(0, 0)};
     uint32_t sz = 0;
     if (row < M) {
-      c = *reinterpret_cast<const uint4*>(W.packed + ((static_cast<int64_t>(row) * K + s * 64) >> 2));
+      // the row slab's codes: 8 BITS bytes of the reference's LSB-first stream
+      const uint2* src = reinterpret_cast<const uint2*>(W.packed + ((static_cast<int64_t>(row) * K + s * 64) * bits >> 3));
+      for (int i = 0; i < bits; ++i) c[i] = src[i];
       const int64_t g = static_cast<int64_t>(row) * nslab + s;
       sz = static_cast<uint32_t>(W.scales[g]) | (static_cast<uint32_t>(W.zeros[g]) << 16);
     }
-    uint8_t* o = out + blk * kCB;
-    *reinterpret_cast<uint4*>(o + 16 * r) = c;
-    *reinterpret_cast<uint32_t*>(o + 2048 + 4 * r) = sz;
+    uint8_t* o = out + blk * cb;
+    for (int i = 0; i < bits; ++i) *reinterpret_cast<uint2*>(o + rb * r + 8 * i) = c[i];
+    *reinterpret_cast<uint32_t*>(o + 128 * rb + 4 * r) = sz;
   }
 }
 
@@ -198,6 +209,43 @@ __device__ __forceinline__ void store_row(uint32_t slab, int r, const RowSlab& v
       const float f0 = __uint_as_float(u0), f1 = __uint_as_float(u1);
       uint64_t t;
       asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f32x2(f0, f1)), "l"(mm));
+      asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(t), "l"(sp[j]), "l"(zz));
+      o[j] = bf16x2_of(t);
+    }
+    umma::sts128(slab + umma::sw128_chunk(r, ch), o[0], o[1], o[2], o[3]);
+  }
+}
+
+// 3-bit row slab: 64 codes in 6 words of the LSB-first stream.  Chunk ch (codes
+// 8ch..8ch+7) is the 24-bit field at bit 24ch (one funnel shift); code q of
+// the field is masked in place into the float 2^23 + c*2^3q (q = 7 is moved
+// down 3 bits first: 7*2^21 would carry into the exponent), then as above one
+// FADD2 and one FFMA2 with s*2^-3q.
+__device__ __forceinline__ void store_row3(uint32_t slab, int r, const uint32_t (&w)[6], uint32_t sb, uint32_t zb) {
+  const float s = h2f(static_cast<uint16_t>(sb)), z = h2f(static_cast<uint16_t>(zb));
+  uint64_t sp[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    sp[j] = f32x2(s * exp2f(-6.0f * j), s * exp2f(j == 3 ? -18.0f : -6.0f * j - 3.0f));
+  const uint64_t zz = f32x2(z, z), mm = f32x2(-8388608.0f, -8388608.0f);
+  uint32_t magic;
+  asm("mov.b32 %0, 0x4B000000;" : "=r"(magic));
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch) {
+    const int bit = 24 * ch;
+    const uint32_t f = __funnelshift_r(w[bit >> 5], w[min((bit >> 5) + 1, 5)], bit & 31);
+    const uint32_t f7 = f >> 3;
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t u0, u1;
+      asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(u0) : "r"(f), "r"(7u << (6 * j)), "r"(magic));
+      if (j == 3)
+        asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(u1) : "r"(f7), "r"(7u << 18), "r"(magic));
+      else
+        asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(u1) : "r"(f), "r"(7u << (6 * j + 3)), "r"(magic));
+      uint64_t t;
+      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f32x2(__uint_as_float(u0), __uint_as_float(u1))), "l"(mm));
       asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(t), "l"(sp[j]), "l"(zz));
       o[j] = bf16x2_of(t);
     }
@@ -369,25 +417,36 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
     // One slab: dequantize A from the code ring (filled kCR slabs ahead by
     // the bulk-copy loader) unless the slab is copied, wait for the slab's
     // cp.async group, publish the stage; then start the copies two slabs ahead.
-    const uint32_t ring = sbase + kStages * kStageBytes + mat * kCB;
+    const uint32_t ring = sbase + kStages * kStageBytes + mat * P.cb;
+    const int cr = P.cr;
     issue(0);
     if (nslab > 1) issue(1);
     for (int s = 0; s < nslab; ++s) {
       const int stage = s % kStages;
       if (s < main_slabs && !vx) {
-        const int slot = s % kCR;
-        umma::bar_wait(&rfull[slot], (s / kCR) & 1);
-        RowSlab v;
-        const uint32_t blk = ring + slot * 2 * kCB;
+        const int slot = s % cr;
+        umma::bar_wait(&rfull[slot], (s / cr) & 1);
+        const uint32_t blk = ring + slot * 2 * P.cb;
         uint32_t sz;
-        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(v.c.x), "=r"(v.c.y), "=r"(v.c.z), "=r"(v.c.w)
-                     : "r"(blk + 16 * rl));
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sz) : "r"(blk + 2048 + 4 * rl));
-        umma::bar_arrive(&rempty[slot]);
-        v.s = sz & 0xFFFFu;
-        v.z = sz >> 16;
-        store_row(sbase + stage * kStageBytes + mat * kSlabA, rl, v);
+        if (P.bits == 2) {
+          RowSlab v;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v.c.x), "=r"(v.c.y), "=r"(v.c.z), "=r"(v.c.w)
+                       : "r"(blk + 16 * rl));
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sz) : "r"(blk + 2048 + 4 * rl));
+          umma::bar_arrive(&rempty[slot]);
+          v.s = sz & 0xFFFFu;
+          v.z = sz >> 16;
+          store_row(sbase + stage * kStageBytes + mat * kSlabA, rl, v);
+        } else {
+          uint32_t w[6];
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[2 * i]), "=r"(w[2 * i + 1]) : "r"(blk + 24 * rl + 8 * i));
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(sz) : "r"(blk + 3072 + 4 * rl));
+          umma::bar_arrive(&rempty[slot]);
+          store_row3(sbase + stage * kStageBytes + mat * kSlabA, rl, w, sz & 0xFFFFu, sz >> 16);
+        }
       }
       if (s + 1 < nslab)
         umma::cp_async_wait<1>();  // slab s landed; slab s+1 may be in flight
@@ -426,29 +485,30 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
       const uint8_t* pk = P.ppk + static_cast<int64_t>(e) * P.PL.stride;
       const int nblkM = (P.M + kTM - 1) / kTM;
       const bool v1 = a1base < P.M, v3 = a3base < P.M;
+      const int cb = P.cb, cr = P.cr;
       const uint8_t* s1 = pk + (P.mode == kDown ? P.PL.w2 : P.PL.w1) +
-                          static_cast<int64_t>(min(a1base / kTM, nblkM - 1)) * main_slabs * kCB;
+                          static_cast<int64_t>(min(a1base / kTM, nblkM - 1)) * main_slabs * cb;
       const uint8_t* s3 = pk + (P.mode == kDown ? P.PL.w2 : P.PL.w3) +
-                          static_cast<int64_t>(min(a3base / kTM, nblkM - 1)) * main_slabs * kCB;
+                          static_cast<int64_t>(min(a3base / kTM, nblkM - 1)) * main_slabs * cb;
       const uint32_t ring0 = umma::smem_u32(sm) + kStages * kStageBytes;
       for (int s = 0; s < main_slabs; ++s) {
-        const int slot = s % kCR;
-        if (s >= kCR) umma::bar_wait(&rempty[slot], ((s / kCR) - 1) & 1);
+        const int slot = s % cr;
+        if (s >= cr) umma::bar_wait(&rempty[slot], ((s / cr) - 1) & 1);
         const uint32_t bar = umma::smem_u32(&rfull[slot]);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "r"((v1 ? kCB : 0) + (v3 ? kCB : 0))
+                     "r"((v1 ? cb : 0) + (v3 ? cb : 0))
                      : "memory");
-        const uint32_t dst = ring0 + slot * 2 * kCB;
+        const uint32_t dst = ring0 + slot * 2 * cb;
         if (v1)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-              "l"(s1 + static_cast<int64_t>(s) * kCB), "n"(kCB), "r"(bar)
+              "l"(s1 + static_cast<int64_t>(s) * cb), "r"(cb), "r"(bar)
               : "memory");
         if (v3)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  dst + kCB),
-              "l"(s3 + static_cast<int64_t>(s) * kCB), "n"(kCB), "r"(bar)
+                  dst + cb),
+              "l"(s3 + static_cast<int64_t>(s) * cb), "r"(cb), "r"(bar)
               : "memory");
       }
     }
@@ -541,15 +601,18 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs 
 
 }  // namespace
 
-bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn, int maxr) {
-  if (hidden % kKS != 0 || ffn % kKS != 0 || maxr > kTM) return false;
+bool prefill_eligible(const lrc_expert* experts, int n, int hidden, int ffn, int maxr, int* bits) {
+  if (hidden % kKS != 0 || ffn % kKS != 0 || maxr > kTM || n < 1) return false;
+  const int b = experts[0].w1.bits;  // one code width per layer (2 or 3)
+  if (b != 2 && b != 3) return false;
   for (int i = 0; i < n; ++i) {
     const lrc_qmat* ws[3] = {&experts[i].w1, &experts[i].w3, &experts[i].w2};
     for (auto w : ws)
-      if (w->dense != nullptr || w->packed == nullptr || w->bits != 2 || w->group_size != kKS ||
+      if (w->dense != nullptr || w->packed == nullptr || w->bits != b || w->group_size != kKS ||
           (reinterpret_cast<uintptr_t>(w->packed) & 15) != 0)
         return false;
   }
+  *bits = b;
   return true;
 }
 
@@ -570,16 +633,16 @@ lrc_status build_prefill_lr(const lrc_expert& e, int hidden, int ffn, int maxr, 
   return LRC_OK;
 }
 
-int64_t prefill_pack_bytes(int hidden, int ffn) { return ppack_layout(hidden, ffn).stride; }
+int64_t prefill_pack_bytes(int hidden, int ffn, int bits) { return ppack_layout(hidden, ffn, bits).stride; }
 
-lrc_status build_prefill_pack(const lrc_expert& e, int hidden, int ffn, uint8_t* out, cudaStream_t st) {
-  build_ppack_kernel<<<592, 256, 0, st>>>(e, hidden, ffn, ppack_layout(hidden, ffn), out);
+lrc_status build_prefill_pack(const lrc_expert& e, int hidden, int ffn, int bits, uint8_t* out, cudaStream_t st) {
+  build_ppack_kernel<<<592, 256, 0, st>>>(e, hidden, ffn, ppack_layout(hidden, ffn, bits), bits, out);
   LRC_CHECK_LAUNCH();
   return LRC_OK;
 }
 
 lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp, uint16_t* tb,
-                          const uint8_t* ppk, cudaStream_t st, int* launches) {
+                          const uint8_t* ppk, int bits, cudaStream_t st, int* launches) {
   static bool attr = false;
   if (!attr) {
     LRC_CUDA_TRY(cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
@@ -588,7 +651,10 @@ lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp
   PrefillArgs P{};
   P.a = a;
   P.ppk = ppk;
-  P.PL = ppack_layout(a.hidden, a.ffn);
+  P.PL = ppack_layout(a.hidden, a.ffn, bits);
+  P.bits = bits;
+  P.cb = cb_bytes(bits);
+  P.cr = cr_depth(bits);
   const int R = lrp ? a.maxr : 0;
   if (R) {
     P.lrp = lrp;

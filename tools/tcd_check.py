@@ -49,7 +49,7 @@ def timing(B=1, layers=8, steps=400, tcd=True, bits=2):
     idx = [torch.empty((B, 2), dtype=torch.int32, device="cuda") for _ in range(layers)]
     wts = [torch.empty((B, 2), dtype=torch.float32, device="cuda") for _ in range(layers)]
     out = {}
-    for mode in ("tcd", "tiled"):
+    for mode in (("tcd", "tiled") if tcd else ("tiled",)):
         for sl in sls:
             sl.layer.set_tcd_max(8 if mode == "tcd" else 0)
 
@@ -114,6 +114,7 @@ def main():
         timing(B=8, steps=200)
         timing(B=1, bits=3, steps=200)
         timing(B=8, bits=3, steps=100)
+        timing(B=64, bits=3, steps=50, tcd=False)
     elif not quick:
         timing(B=8, steps=200)
 
