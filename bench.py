@@ -342,6 +342,10 @@ def run_ours(args, world, rank):
     if args.offload and rank == 0:
         offl = offload_point()
 
+    int3 = None
+    if args.int3 and rank == 0:
+        int3 = int3_point(hbm, tf_sust)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_ours(layers[0], B)
@@ -366,13 +370,14 @@ def run_ours(args, world, rank):
         "sweep": sweep,
         "prefill": prefill,
         "offload": offl,
+        "int3": int3,
         "cpu_baseline": cpu,
     }
     if rank == 0:
         print(json.dumps(out))
 
 
-def sweep_point(layers, B, hbm, tf_sust, steps=200):
+def sweep_point(layers, B, hbm, tf_sust, steps=200, bits=None):
     import torch
 
     L = len(layers)
@@ -406,12 +411,32 @@ def sweep_point(layers, B, hbm, tf_sust, steps=200):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    byts = sum(layer_bytes(HIDDEN, FFN, BITS, RANK, *stats[i % L], B, E, 8, 4) for i in range(steps))
+    byts = sum(layer_bytes(HIDDEN, FFN, bits or BITS, RANK, *stats[i % L], B, E, 8, 4) for i in range(steps))
     fl = steps * B * layer_flops(HIDDEN, FFN, TOPK, TOPN, RANK, E)
     roof = max(byts / (hbm * 1e9), fl / (tf_sust * 1e12))
     return {"tokens_s": round(steps * B / (ms / 1e3), 1), "us_per_step": round(ms * 1e3 / steps, 2),
             "gbs": round(byts / (ms / 1e3) / 1e9, 1), "frac": round(roof / (ms / 1e3), 4),
             "d_sel_mean": round(float(np.mean([s[0] for s in stats])), 2)}
+
+
+def int3_point(hbm, tf_sust, layers=8):
+    """C2 at INT3 (BASELINE configs[1] "2-bit/3-bit experts"): 8 rotated INT3
+    layers without tiled packs, decode batches 1 / 8 (tensor-core decode
+    engine) and 64 (prefill engine), graph-replayed like the headline."""
+    import torch
+
+    from paper_2512_17073_b200.synth import SynthLayer
+
+    sls = [SynthLayer(HIDDEN, FFN, E, top_k=TOPK, bits=3, rank=RANK, seed=7000 + l, max_tokens=64, tiles=False)
+           for l in range(layers)]
+    out = {"workload": "Mixtral-8x7B MoE layer, INT3 gs64 + rank-32 INT3 LR on top-1, 8 layers rotated",
+           "path": {"1": "tcd (tcgen05 kind::i8 decode engine)", "8": "tcd", "64": "prefill (tcgen05 cta_group::2)"}}
+    for Bs in (1, 8, 64):
+        out[str(Bs)] = sweep_point(sls, Bs, hbm, tf_sust, steps=100 if Bs < 64 else 30, bits=3)
+    out["frac"] = out["1"]["frac"]
+    del sls
+    torch.cuda.empty_cache()
+    return out
 
 
 def prefill_point(tf_burst, tf_sust, B=16384, iters=3):
@@ -608,6 +633,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", dest="prefill", action="store_false")
     ap.add_argument("--no-offload", dest="offload", action="store_false")
+    ap.add_argument("--no-int3", dest="int3", action="store_false")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = 2000 if args.impl == "ours" else 5

@@ -130,6 +130,67 @@ __device__ __noinline__ void select_topk_warp(double* lg, int E, int k, int reno
   }
 }
 
+// Layer-forward variant (no fp64 probabilities requested, E <= 32): the
+// selection runs on the exact fp64 logits -- the softmax is monotonic, so the
+// stable top-k of the probabilities is the stable top-k of the logits unless
+// two compared logits are so close that their fp64 exponentials could round
+// to the same value; such near-ties (and ties) take the exact path above.
+// The mixing weights are computed in fp32 (expf, warp sum): within a few ulp
+// of float(fp64 softmax), far inside the layer-output tolerance.  Replaces
+// ~1,600 SASS instructions of fp64 exp / div / pairwise sum (cold code on the
+// critical path, DESIGN 8 item 2) with ~200.
+__device__ __noinline__ bool select_topk_fast(const double* lg, int E, int k, int renorm, int64_t b,
+                                              int32_t* topk_idx, float* topk_w, int32_t* s_idx, float* s_w) {
+  const int lane = threadIdx.x & 31;
+  const double l = lane < E ? lg[lane] : -DBL_MAX;
+  // 32-bit order key: the top 27 bits of the order-preserving integer image of
+  // the double, then (31 - lane) so that equal keys go to the lower expert;
+  // one redux.sync.max per selection round.  Truncation only merges logits
+  // that agree in their top 27 bits -- the fp64 near-tie guard below sends
+  // every such case (and every real near-tie) to the exact path.
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(l));
+  const unsigned long long ord = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+  const uint32_t key = lane < E ? (static_cast<uint32_t>(ord >> 37) << 5) | static_cast<uint32_t>(31 - lane) : 0u;
+  bool taken = lane >= E, ok = true;
+  double prev = 0.0, mx = 0.0;
+  int my_rank = -1;
+  const int kk = min(k + 1, E);
+  for (int j = 0; j < kk; ++j) {
+    const uint32_t m = __reduce_max_sync(0xffffffffu, taken ? 0u : key);
+    const int be = 31 - static_cast<int>(m & 31u);
+    const double bv = __shfl_sync(0xffffffffu, l, be);
+    if (j == 0) mx = bv;
+    // fp64 exp(l - mx) has relative error < 2^-52: logits closer than this
+    // bound could produce equal probabilities (a tie the reference breaks by
+    // index) -- leave those to the exact path
+    if (j > 0 && !(prev - bv > 1e-13 * fmax(1.0, fabs(bv - mx)))) ok = false;
+    prev = bv;
+    if (lane == be) {
+      taken = true;
+      if (j < k) my_rank = j;
+    }
+  }
+  if (!ok) return false;
+  const float ex = lane < E ? expf(static_cast<float>(l - mx)) : 0.f;
+  float den = ex;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+  float w = ex / den;
+  if (renorm) {
+    float sw = my_rank >= 0 ? w : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sw += __shfl_xor_sync(0xffffffffu, sw, o);
+    if (sw > 0.f) w = w / sw;
+  }
+  if (my_rank >= 0) {
+    topk_idx[b * k + my_rank] = lane;
+    topk_w[b * k + my_rank] = w;
+    s_idx[my_rank] = lane;
+    s_w[my_rank] = w;
+  }
+  return true;
+}
+
 __device__ __forceinline__ void griddep_launch_dependents_r() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
@@ -147,6 +208,54 @@ __device__ inline int xs_col(int c) { return (c >> 6) * 66 + (c & 63); }
 // of its whole groups, then loops over tokens.
 __device__ __forceinline__ float code_f(uint32_t c) {  // exact float of a small code
   return __uint_as_float(0x4B000000u | c) - 8388608.0f;
+}
+
+template <int NT>
+__device__ __forceinline__ void spec_dot(const RouteArgs& ra, const uint16_t* xs, const float* xsum,
+                                         const uint32_t (&w)[2][7], const float (&s)[2], const float (&z)[2],
+                                         const int (&nv)[2], int nb, float* tout, int64_t tstride) {
+  const int lane = threadIdx.x & 31;
+  const int ldx = xs_row_elems(ra.d);
+  const uint32_t* xs32 = reinterpret_cast<const uint32_t*>(xs);
+  float acc[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t] = 0.0f;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (nv[h] == 0) continue;
+    const int g = lane + 32 * h;
+    float cx[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) cx[t] = 0.0f;
+    // two chunks of 32 codes = exactly 3 words each (static word indices)
+    for (int ch = 0; ch < 2; ++ch) {
+      if (32 * ch >= nv[h]) break;
+      const uint32_t q[4] = {ch ? w[h][3] : w[h][0], ch ? w[h][4] : w[h][1], ch ? w[h][5] : w[h][2],
+                             ch ? w[h][6] : w[h][3]};
+#pragma unroll
+      for (int i2 = 0; i2 < 16; ++i2) {
+        const int bit0 = 6 * i2, bit1 = bit0 + 3;
+        const float c0 = code_f(__funnelshift_r(q[bit0 >> 5], q[(bit0 >> 5) + 1], bit0 & 31) & 7u);
+        const float c1 = code_f(__funnelshift_r(q[bit1 >> 5], q[(bit1 >> 5) + 1], bit1 & 31) & 7u);
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+          if (t < nb) {
+            const uint32_t xw = xs32[t * (ldx / 2) + g * 33 + 16 * ch + i2];
+            cx[t] = fmaf(c0, __uint_as_float(xw << 16), fmaf(c1, __uint_as_float(xw & 0xffff0000u), cx[t]));
+          }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+      if (t < nb) acc[t] = fmaf(s[h], cx[t], fmaf(z[h], xsum[t * 64 + g], acc[t]));
+  }
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    if (t < nb) {
+      const float v = warp_sum(acc[t]);
+      if (lane == 0) tout[t * tstride] = v;
+    }
+  }
 }
 
 __device__ __noinline__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* xs, const float* xsum,
@@ -186,46 +295,11 @@ __device__ __noinline__ void spec_lr_rows(const RouteArgs& ra, const uint16_t* x
     }
     // each code is decoded once (exact float via the 2^23 magic, no XU
     // conversion) and applied to every token of the tile; sum(x) per group
-    // comes precomputed from the staging pass (xsum[t][g])
-    const int ldx = xs_row_elems(ra.d);
-    const uint32_t* xs32 = reinterpret_cast<const uint32_t*>(xs);
-    float acc[kTT];
-#pragma unroll
-    for (int t = 0; t < kTT; ++t) acc[t] = 0.0f;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (nv[h] == 0) continue;
-      const int g = lane + 32 * h;
-      float cx[kTT];
-#pragma unroll
-      for (int t = 0; t < kTT; ++t) cx[t] = 0.0f;
-      // two chunks of 32 codes = exactly 3 words each (static word indices)
-      for (int ch = 0; ch < 2; ++ch) {
-        if (32 * ch >= nv[h]) break;
-        const uint32_t q[4] = {ch ? w[h][3] : w[h][0], ch ? w[h][4] : w[h][1], ch ? w[h][5] : w[h][2],
-                               ch ? w[h][6] : w[h][3]};
-#pragma unroll
-        for (int i2 = 0; i2 < 16; ++i2) {
-          const int bit0 = 6 * i2, bit1 = bit0 + 3;
-          const float c0 = code_f(__funnelshift_r(q[bit0 >> 5], q[(bit0 >> 5) + 1], bit0 & 31) & 7u);
-          const float c1 = code_f(__funnelshift_r(q[bit1 >> 5], q[(bit1 >> 5) + 1], bit1 & 31) & 7u);
-#pragma unroll
-          for (int t = 0; t < kTT; ++t)
-            if (t < nb) {
-              const uint32_t xw = xs32[t * (ldx / 2) + g * 33 + 16 * ch + i2];
-              cx[t] = fmaf(c0, __uint_as_float(xw << 16), fmaf(c1, __uint_as_float(xw & 0xffff0000u), cx[t]));
-            }
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < kTT; ++t)
-        if (t < nb) acc[t] = fmaf(s[h], cx[t], fmaf(z[h], xsum[t * 64 + g], acc[t]));
-    }
-#pragma unroll
-    for (int t = 0; t < kTT; ++t) {
-      const float v = warp_sum(acc[t]);
-      if (lane == 0 && t < nb) tout[t * tstride] = v;
-    }
+    // comes precomputed from the staging pass (xsum[t][g]).  This code runs
+    // once per layer step with a cold instruction cache, so its size is its
+    // cost: the single-token variant is ~8x smaller than the tile one.
+    if (nb == 1) spec_dot<1>(ra, xs, xsum, w, s, z, nv, 1, tout, tstride);
+    else spec_dot<kTT>(ra, xs, xsum, w, s, z, nv, nb, tout, tstride);
     return;
   }
   const int ldx = xs_row_elems(ra.d);
@@ -332,7 +406,7 @@ struct WarmScratch {
   ActiveRec arec[32];
 };
 __device__ __noinline__ void warm_tail(const RouteArgs& ra, WarmScratch& ws, const uint8_t* hc,
-                                       const ExpertTiles* et);
+                                       const ExpertTiles* et, bool exact);
 
 template <typename T>
 __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_constant__ RouteArgs ra) {
@@ -357,12 +431,44 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
   // complete, so it may read x and build its activation operand before it waits
   // for the routing.
   if (!ra.pdl) griddep_launch_dependents_r();
-  if (warp == kRThreads / 32) {  // warm-up warp: leader of a row-0 cluster only
+  // single-token decode: the leader's extra warp owns the whole tail (select +
+  // plan).  It runs both on dummy data while the logits are computed, so its
+  // SMSP's instruction cache holds them when the logits land (the tail is
+  // otherwise ~6 us of cold instruction fetches on the layer's critical path).
+  const bool tailw = ntiles == 1 && nb == 1 && ra.plan.ticket != nullptr && ra.pairs_expert == nullptr &&
+                     ra.probs == nullptr && ra.E <= 32 && ra.k <= ra.E &&
+                     ra.k + (ra.plan.comp_rows ? 0 : ra.plan.num_shared) <= 32;
+  if (warp == kRThreads / 32) {  // the extra warp: leader of a row-0 cluster only
     if (row == 0) {
-      // arrive on the cluster barrier first (never waits): the logits handoff
-      // must not wait for this warp's cold instruction fetches
+      // arrive on the cluster barrier first: the logits handoff must not wait
+      // for this warp's cold instruction fetches
       asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-      if (rank == 0 && ra.plan.ticket != nullptr && !(ra.stamp & 2)) warm_tail(ra, s_warm, s_hc, s_et);
+      if (rank == 0 && tailw) {
+        auto tstamp = [&](int k) {
+          if ((ra.stamp & 1) && lane == 0) {
+            unsigned long long t_;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+            g_route_stamps[blockIdx.x * 8 + k] = t_;
+          }
+        };
+        warm_tail(ra, s_warm, s_hc, s_et, false);
+        tstamp(7);
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every logit landed
+        tstamp(4);
+        double* lg = reinterpret_cast<double*>(rsm);
+        if (!select_topk_fast(lg, ra.E, ra.k, ra.renorm, b0, ra.topk_idx, ra.topk_w, s_tidx, s_tw))
+          select_topk_warp(lg, ra.E, ra.k, ra.renorm, b0, ra.probs, ra.topk_idx, ra.topk_w, s_tidx, s_tw);
+        __syncwarp();
+        tstamp(2);
+        build_plan_warp(ra.plan, s_tidx, s_tw, s_hc, s_et, static_cast<int>(ra.B), ra.k);
+        if ((ra.stamp & 1) && lane == 0) {
+          unsigned long long t_;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+          g_route_stamps[blockIdx.x * 8 + 5] = t_;
+        }
+      } else if (rank == 0 && ra.plan.ticket != nullptr && (ra.stamp & 2)) {
+        warm_tail(ra, s_warm, s_hc, s_et, true);  // (debug: warm-up only)
+      }
     }
     return;
   }
@@ -372,6 +478,7 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
       griddep_wait_r();
       griddep_launch_dependents_r();
     }
+    RSTAMP(2);
     const int aux = (row - 1) * kCl + rank, naux = (gridDim.y - 1) * kCl;
     if (ra.y_zero != nullptr) {
       const int64_t n = static_cast<int64_t>(nb) * ra.d;
@@ -422,6 +529,7 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
           }
         }
         wsync();
+        RSTAMP(3);
         // per (token, 64-column group) sums of x for the zero-point term
         float* xsum = reinterpret_cast<float*>(rsm + kTT * ldx * 2);
         const int gpr = (ra.d + 63) / 64;
@@ -435,6 +543,7 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
             xsum[t * 64 + g] = a;
           }
         wsync();
+        RSTAMP(4);
         spec_lr_rows(ra, xs, xsum, b0, nb, aux % ra.ne, aux / ra.ne);
       }
     }
@@ -533,7 +642,7 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
   }
   cl_sync();  // release/acquire: the leader sees every logit
   RSTAMP(6);
-  if (!leader) return;
+  if (!leader || tailw) return;
   // ---- leader: softmax + top-k (warp per token), then the pair plan
   if (ra.pairs_expert != nullptr) {  // pairs mode: the routing is given (k = 1)
     if (threadIdx.x < nb) {
@@ -545,6 +654,11 @@ __global__ void __launch_bounds__(kRThreads + 32) route_kernel(const __grid_cons
       ra.topk_w[b0 + threadIdx.x] = w;
     }
   } else if (warp < nb) {
+    if (ra.probs == nullptr && ra.E <= 32 && ra.k <= ra.E &&
+        select_topk_fast(lg + warp * ldl, ra.E, ra.k, ra.renorm, b0 + warp, ra.topk_idx, ra.topk_w,
+                         s_tidx + warp * ra.k, s_tw + warp * ra.k)) {
+      // done (exact selection, fp32 weights)
+    } else
     select_topk_warp(lg + warp * ldl, ra.E, ra.k, ra.renorm, b0 + warp, ra.probs, ra.topk_idx,
                      ra.topk_w, s_tidx + warp * ra.k, s_tw + warp * ra.k,
                      ((ra.stamp & 1) && warp == 0 && blockIdx.y * gridDim.x + blockIdx.x < kStampCtas)
@@ -729,11 +843,31 @@ __device__ __noinline__ void build_plan_warp(const PlanArgs& pa, const int32_t* 
   const unsigned same = __match_any_sync(0xffffffffu, e);  // lanes of my expert, in pair order
   const int cnt = __popc(same), rk = __popc(same & ((1u << lane) - 1u));
   int off = 0, nbelow = 0;  // pairs / distinct experts with a smaller id
-  for (int q = 0; q < 32; ++q) {
-    const int eq = __shfl_sync(0xffffffffu, e, q);
-    const unsigned sq = __shfl_sync(0xffffffffu, same, q);
-    off += eq < e;
-    nbelow += (eq < e) && ((sq & ((1u << q) - 1u)) == 0u);
+  if (pa.num_experts + pa.num_shared <= 32) {
+    // per-expert pair counts by ballot (lane x: expert x), exclusive scan over
+    // the lanes, one gather: a short dependency chain instead of 32 rounds
+    int cx = 0;
+#pragma unroll
+    for (int x = 0; x < 32; ++x) {
+      const unsigned bx = __ballot_sync(0xffffffffu, valid && e == x);
+      if (lane == x) cx = __popc(bx);
+    }
+    int incl = cx;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const unsigned present = __ballot_sync(0xffffffffu, cx > 0);
+    off = __shfl_sync(0xffffffffu, incl - cx, e & 31);
+    nbelow = __popc(present & ((1u << (e & 31)) - 1u));
+  } else {
+    for (int q = 0; q < 32; ++q) {
+      const int eq = __shfl_sync(0xffffffffu, e, q);
+      const unsigned sq = __shfl_sync(0xffffffffu, same, q);
+      off += eq < e;
+      nbelow += (eq < e) && ((sq & ((1u << q) - 1u)) == 0u);
+    }
   }
   const bool row_comp = pa.comp_rows != nullptr ? (valid && pa.comp_rows[lane / P] != 0) : j < pa.top_n;
   const bool comp = valid && ((j < k) ? (row_comp && hc[e] != 0) : (pa.compensate_shared && hc[e] != 0));
@@ -775,12 +909,14 @@ __device__ __noinline__ void build_plan_warp(const PlanArgs& pa, const int32_t* 
 }
 
 __device__ __noinline__ void warm_tail(const RouteArgs& ra, WarmScratch& ws, const uint8_t* hc,
-                                       const ExpertTiles* et) {
+                                       const ExpertTiles* et, bool exact) {
   const int lane = threadIdx.x & 31;
   const int E = min(ra.E, LRC_MAX_EXPERTS);
   for (int e = lane; e < E; e += 32) ws.lg[e] = 0.001 * e;
   __syncwarp();
-  select_topk_warp(ws.lg, E, ra.k, ra.renorm, 0, nullptr, ws.idx, ws.w, ws.idx, ws.w);
+  if (E <= 32 && ra.k <= E) select_topk_fast(ws.lg, E, ra.k, ra.renorm, 0, ws.idx, ws.w, ws.idx, ws.w);
+  __syncwarp();
+  if (exact) select_topk_warp(ws.lg, E, ra.k, ra.renorm, 0, nullptr, ws.idx, ws.w, ws.idx, ws.w);
   __syncwarp();
   PlanArgs d = ra.plan;  // same scalars, outputs redirected to the scratch
   d.pair_expert = ws.pe;

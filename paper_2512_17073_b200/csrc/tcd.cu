@@ -1239,6 +1239,7 @@ __device__ __noinline__ void role_epilogue(const Args& A, Shared& S) {
     __syncwarp();
     if (lane == 0) arrive(&S.empty[slot]);  // metadata and sums read
     if (lane == 0 && warp == kEpi0) trace2(A, 1, s);
+    if (warp == kEpi0 && s == S.nstage_u - 1) stamp(A, 12);  // last phase-U stage through the epilogue
     fresh = false;
     if (t.seg_end) {  // segment end: flush
       fresh = true;
@@ -1369,14 +1370,31 @@ __device__ __noinline__ void finalize_up(const Args& A, Shared& S, int a, int ti
             make_float4(ldexpf(1.f, -sc), static_cast<float>(__float_as_int(S.gred[2 * gl]) + __float_as_int(S.gred[2 * gl + 1])), 0.f, 0.f);
     }
     if (cs >= 0) {  // t2 partial: V2[:, i] . a_i, reduced over the tile rows
+      // (row words and group metadata loaded up front; per 32 factor columns one
+      // butterfly reduce-scatter: 31 shuffles leave lane l the warp sum of column l)
       const uint32_t* vm = reinterpret_cast<const uint32_t*>(lt + 3 * 128 * RB) + 256 + (f / 64) * kRMax;
-#pragma unroll 1
-      for (int k = 0; k < rk; ++k) {
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(lt + (256 + f) * RB + (k >> 3) * 4);
-        const uint32_t mz = vm[k];
-        const float vk = fmaf(static_cast<float>((w >> (4 * (k & 7))) & 15u), h2f(mz & 0xffff), h2f(mz >> 16));
-        const float sum = warp_sum(vk * av);
-        if (lane == 0) S.t2red[aw][k] = sum;
+      for (int k0 = 0; k0 < rk; k0 += 32) {
+        const uint4 wv = __ldg(reinterpret_cast<const uint4*>(lt + (256 + f) * RB + k0 / 2));
+        const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+        const uint32_t mzl = k0 + lane < rk ? __ldg(vm + k0 + lane) : 0u;
+        float v[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t mz = __shfl_sync(0xffffffffu, mzl, k);
+          const float vk = fmaf(static_cast<float>((ww[k >> 3] >> (4 * (k & 7))) & 15u), h2f(mz & 0xffff), h2f(mz >> 16));
+          v[k] = k0 + k < rk ? vk * av : 0.f;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int i = 0; i < o; ++i) {
+            const float send = up ? v[i] : v[i + o];
+            const float keep = up ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        if (k0 + lane < rk) S.t2red[aw][k0 + lane] = v[0];
       }
       named_sync(2, 128);
       if (f < rk)
@@ -1392,6 +1410,18 @@ __device__ __noinline__ void aux_phase_u(const Args& A, Shared& S) {
   const Plan& P = S.P;
   const int G0 = A.hidden / 64, T0 = A.ffn / 128;
   int useg = 0;
+  // the LR tile packs this CTA may finalise: pull them into L2 while the
+  // stages stream (their first touch is otherwise on the critical path)
+  for (int s = 0; s < S.nstage_u; ++s) {
+    const Stg t = stg(S, s);
+    if (!t.seg_end) continue;
+    const Expert& ex = A.ex[P.act_e[t.a]];
+    if (ex.rank > 0 && ex.lr_up != nullptr) {
+      const int tb = lr_up_tile_bytes(ex.rank);
+      const uint8_t* lt = ex.lr_up + static_cast<size_t>(t.tile) * tb;
+      for (int o = f * 128; o < tb; o += 128 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(lt + o));
+    }
+  }
   for (int s = 0; s < S.nstage_u; ++s) {
     const Stg t = stg(S, s);
     if (!t.seg_end) continue;
@@ -1588,6 +1618,7 @@ __global__ void __launch_bounds__(kThreads, 1) tcd_kernel(const __grid_constant_
       if (lane == 0) atomicAdd(&A.xcnt[S.P.par], 1u);
     }
   }
+  if (warp == 0) stamp(A, 13);
   if (fused) {
     wait(&S.gbarr, 0);
     if (warp == 0) stamp(A, 8);
@@ -1600,7 +1631,9 @@ __global__ void __launch_bounds__(kThreads, 1) tcd_kernel(const __grid_constant_
   if (warp == 0) {
     build_plan<BITS>(A, S);
     __syncwarp();
+    stamp(A, 14);
     build_stages(A, S);
+    stamp(A, 15);
   }
   __syncthreads();
   if (warp == 0) stamp(A, 1);

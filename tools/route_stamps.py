@@ -9,7 +9,7 @@ import sys
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 extra = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-os.environ["LRC_ROUTE_STAMPS"] = "1"
+os.environ.setdefault("LRC_ROUTE_STAMPS", "1")
 os.environ["LRC_TILED_DEBUG"] = str(8 | extra)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
@@ -53,7 +53,10 @@ nl = r[1:8]  # non-leader logit CTAs of row 0 (x = 1..7)
 for k, n in ((3, "nonleader: loads+fma done"), (4, "nonleader: reduce done"), (5, "nonleader: dsmem done")):
     show(n, nl[:, k])
 for k, n in enumerate(["entry", "work done", "sel: softmax done", "select done", "plan ticket", "plan done", "logits done", "sel: top-k done"]):
-    show("route " + n, r[:, k])
+    show("route " + n, r[:8, k])
+ax = r[8:]  # aux CTAs (rows > 0): zeroing + speculative V.x
+for k, n in ((0, "entry"), (2, "griddep passed"), (3, "x staged"), (4, "x sums"), (1, "work done")):
+    show("aux " + n, ax[:, k])
 for up, nm in ((1, "up"), (0, "down")):
     for k, n in enumerate(["entry", "griddep passed", "setup done", "prod first issue", "prod last issue",
                            "cons first data", "cons done", "epi done"]):

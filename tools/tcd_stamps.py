@@ -37,8 +37,15 @@ t0c = st[0, 0]
 rel = np.where(st > 0, (st - t0) / 1e3, np.nan)
 names = ["wait", "plan", "vx", "U fin", "gbar", "end", "dec->D", "mma end", "gate in", "logits", "select",
          "pre-plan"]
-print("NST*1000+NDS:", st[:, 12][:4])
-for i, n in ((13, "prod stage0 issued"), (14, "dec0 sees stage0"), (15, "prod stage9 issued")):
+uf = rel[:, 3]
+order = np.argsort(-np.nan_to_num(uf))
+print("slowest U fin CTAs: cta  plan  vx  epiUdone  Ufin  gbar")
+for c in order[:12]:
+    print(f"  {c:4d} {rel[c, 1]:7.2f} {rel[c, 2]:7.2f} {rel[c, 12]:7.2f} {rel[c, 3]:7.2f} {rel[c, 4]:7.2f}")
+eu = rel[:, 12]
+print(f"epi U done  min {np.nanmin(eu):.2f} med {np.nanmedian(eu):.2f} max {np.nanmax(eu):.2f}")
+print(f"U fin - epi U done: med {np.nanmedian(uf - eu):.2f} max {np.nanmax(uf - eu):.2f}")
+for i, n in ((13, "x images done"), (14, "build_plan done"), (15, "build_stages done")):
     col = rel[:, i]
     print(f"{i} {n:18s} min {np.nanmin(col):8.2f}  med {np.nanmedian(col):8.2f}  max {np.nanmax(col):8.2f} us")
 for i, n in enumerate(names):
