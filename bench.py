@@ -16,8 +16,11 @@ codes), so every step streams its experts from HBM (inputs larger than the
 oracle port of moe.forward(..., "compensated"), oracle/lrc.py) on the host
 cores with the same metric, one token per step.
 
-Multi-GPU (torchrun): every rank runs the same per-GPU workload (replicas,
-weak scaling); time = max over ranks.
+Multi-GPU (torchrun, --gpus N > 1): expert parallelism (run_ep): routed
+expert e on rank floor(e N / E), B decode tokens per rank dispatched to the
+owners with fixed-capacity NCCL all-to-alls (no host sync, graph-captured),
+weak scaling, time = max over ranks.  --replicas runs N independent copies of
+the single-GPU workload instead; --ep forces the EP arm on one GPU.
 """
 
 from __future__ import annotations
@@ -25,9 +28,11 @@ from __future__ import annotations
 import os
 
 os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # no NCCL banner on stdout: rank 0 prints ONE JSON line
 
 import argparse  # noqa: E402
 import json  # noqa: E402
+import sys  # noqa: E402
 import threading  # noqa: E402
 import time  # noqa: E402
 
@@ -377,6 +382,131 @@ def run_ours(args, world, rank):
         print(json.dumps(out))
 
 
+# ------------------------------------------------ expert-parallel arm (C5/e) --
+def run_ep(args, world, rank):
+    """Expert parallelism over the job's ranks (north_star item 5):
+    routed expert e lives on rank floor(e G / E); every rank routes its own
+    batch of B decode tokens, dispatches the (token, expert) pairs to the
+    owners with fixed-capacity NCCL all-to-alls (no host sync), the owners run
+    lrc_layer_forward_pairs, and the weighted rows come back for the combine.
+    Weak scaling: B tokens per rank; value = all ranks' tokens / max-over-ranks
+    time.  (Every rank holds the full synthetic layers -- same seeds -- but the
+    dispatch only ever hands it its own experts' rows.)"""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_17073_b200 import _lib, ep
+    from paper_2512_17073_b200.synth import SynthLayer
+
+    _lib.load()
+    hbm, tf_burst, tf_sust, peak_kind = load_peaks()
+    B, L = args.batch, args.layers
+    layers = [SynthLayer(HIDDEN, FFN, E, top_k=TOPK, bits=BITS, rank=RANK, seed=100 * l,
+                         max_tokens=max(64, world * B * TOPK)) for l in range(L)]
+    eps = [ep.from_device_layer(dist.group.WORLD, sl.layer, TOPK, TOPN, max_tokens=B) for sl in layers]
+    torch.manual_seed(1234 + rank)
+    nx = 2 * L
+    xs = [torch.randn((B, HIDDEN), device="cuda").to(torch.bfloat16) for _ in range(nx)]
+    ys = [None] * L
+
+    def step(i):
+        ys[i % L] = eps[i % L].forward(xs[i % nx])
+
+    # routed expert sets of the exact step sequence (for the byte model): the
+    # experts this rank owns that any rank's tokens select
+    owned = set(eps[0].local_experts())
+    sel_sets = []
+    for i in range(np.lcm(L, nx)):
+        idx, _ = eps[i % L].route_fn(xs[i % nx])
+        allidx = [torch.empty_like(idx) for _ in range(world)]
+        dist.all_gather(allidx, idx)
+        sel = set(int(v) for t in allidx for v in t.reshape(-1).tolist())
+        comp = set(int(v) for t in allidx for v in t[:, :TOPN].reshape(-1).tolist())
+        busy = sel & owned or {eps[0].first_expert(rank)}  # an idle rank still streams its first expert
+        sel_sets.append((len(busy), len(comp & owned)))
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    use_graph = True
+    try:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for i in range(3):
+                step(i)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            for i in range(args.steps):
+                step(i)
+        g.replay()
+        torch.cuda.synchronize()
+    except Exception as exc:  # NCCL without graph support: eager steps
+        use_graph = False
+        print(f"[bench ep] graph capture unavailable ({type(exc).__name__}: {str(exc)[:300]}); eager timing",
+              file=sys.stderr)
+        torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(index=torch.cuda.current_device()) as clk:
+        ev0.record()
+        if use_graph:
+            g.replay()
+        else:
+            for i in range(args.steps):
+                step(i)
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = dist_max(ev0.elapsed_time(ev1), world)
+    tok_s = world * args.steps * B / (ms / 1e3)
+    ncyc = len(sel_sets)
+    byts = sum(sel_sets[i % ncyc][0] * expert_bytes(HIDDEN, FFN, BITS) +
+               sel_sets[i % ncyc][1] * comp_bytes(HIDDEN, FFN, RANK) for i in range(args.steps))
+    # this rank's bytes over its own time; reported for rank 0 (max over ranks of the time)
+    frac = byts / (ms / 1e3) / 1e9 / hbm
+    # end to end: pinned host x in, y out, every step
+    xh = [torch.empty((B, HIDDEN), dtype=torch.bfloat16).pin_memory() for _ in range(nx)]
+    for i in range(nx):
+        xh[i].copy_(xs[i].cpu())
+    yh = torch.empty((B, HIDDEN), dtype=torch.float32).pin_memory()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        xd = xh[i % nx].to("cuda", non_blocking=True)
+        y = eps[i % L].forward(xd)
+        yh.copy_(y, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = dist_max(e0.elapsed_time(e1), world)
+    out = {
+        "metric": METRIC, "value": round(tok_s, 1), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int2 codes, bf16 x, fp32 accum",
+        "data": "synthetic (random INT2 codes, fp16 scale/zero, INT3 rank-32 factors, random bf16 tokens)",
+        "config": {"workload": f"Mixtral-8x7B MoE layer (d=4096, ffn=14336, 8 experts top-2), INT2 gs64 + rank-32 "
+                               f"INT3 LR on top-1, decode batch {B} per rank, expert-parallel over {world} GPU(s)",
+                   "batch_per_rank": B, "layers_rotated": L, "parallelism": f"ep{world}",
+                   "dispatch": "fixed-capacity NCCL all_to_all_single x2 + combine all_to_all, no host sync",
+                   "cuda_graph": use_graph, "l2": "inputs larger than L2 (8 layers rotated)"},
+        "roofline": {"bound": "hbm", "achieved": round(byts / (ms / 1e3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(frac, 4), "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "layer step on rank 0 (its experts' bytes / step time)"},
+        "e2e": {"value": round(world * args.steps * B / (e2e_ms / 1e3), 1), "unit": "tokens/s",
+                "h2d_bytes_per_step": B * HIDDEN * 2, "d2h_bytes_per_step": B * HIDDEN * 4,
+                "path": "ep.ExpertParallelLayer.forward with pinned host x/y copies per step"},
+        "gpu_launches": layers[0].layer.last_launches() * args.steps,
+        "clocks": clk.summary(),
+        "cpu_baseline": None,
+    }
+    if rank == 0:
+        print(json.dumps(out))
+
+
 def sweep_point(layers, B, hbm, tf_sust, steps=200, bits=None):
     import torch
 
@@ -634,6 +764,8 @@ def main():
     ap.add_argument("--no-prefill", dest="prefill", action="store_false")
     ap.add_argument("--no-offload", dest="offload", action="store_false")
     ap.add_argument("--no-int3", dest="int3", action="store_false")
+    ap.add_argument("--ep", action="store_true", help="expert-parallel arm (default when --gpus > 1)")
+    ap.add_argument("--replicas", action="store_true", help="N independent replicas instead of EP")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = 2000 if args.impl == "ours" else 5
@@ -641,11 +773,24 @@ def main():
         args.warmup = 10 if args.impl == "ours" else 1
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world, rank, _ = dist_setup(args)
+    use_ep = args.impl == "ours" and not args.replicas and (args.ep or world > 1)
+    if use_ep and world == 1:  # a 1-rank NCCL group (path check on one GPU)
+        import torch
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1)
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif use_ep:
+        if args.steps > 500:
+            args.steps = 500
+        run_ep(args, world, rank)
     else:
         run_ours(args, world, rank)
-    if world > 1:
+    if world > 1 or use_ep:
         import torch.distributed as dist
 
         dist.destroy_process_group()

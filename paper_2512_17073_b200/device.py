@@ -234,10 +234,12 @@ class LRCMoELayer:
                       _lib.ptr(topk_w), _lib.stream_ptr()))
         return y, topk_idx, topk_w
 
-    def forward_pairs(self, x, expert, weight, comp, y=None):
+    def forward_pairs(self, x, expert, weight, comp, y=None, validate: bool = True):
         """Given routing (expert-parallel receive side): row b of x (bf16 cuda)
         goes to expert[b] (int32) with weight[b] (f32); the low-rank term iff
-        comp[b] (uint8).  Returns y (B, hidden) f32 = weight * E(x) per row."""
+        comp[b] (uint8).  Returns y (B, hidden) f32 = weight * E(x) per row.
+        ``validate`` checks the ids on the host (one synchronisation); callers
+        that build the ids themselves (the EP layer) pass False."""
         torch = _lib.device_required()
         B = int(x.shape[0])
         if y is None:
@@ -247,7 +249,7 @@ class LRCMoELayer:
         self.ensure_capacity(B, 1)
         ne = self.num_experts + self.num_shared
         ex = expert.to(device="cuda", dtype=torch.int32).contiguous()
-        if int(ex.min()) < 0 or int(ex.max()) >= ne:
+        if validate and (int(ex.min()) < 0 or int(ex.max()) >= ne):
             raise ValueError(f"forward_pairs: expert ids must be in [0, {ne})")
         w = weight.to(device="cuda", dtype=torch.float32).contiguous()
         c = comp.to(device="cuda", dtype=torch.uint8).contiguous()

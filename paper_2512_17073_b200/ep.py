@@ -6,8 +6,9 @@ the token's own rank.  One step for a rank's local batch x (B, d):
 
 1. route locally (fp64 gate, stable top-k, top-n flags: ref/moe.py:165-193);
 2. dispatch: every (token, selected expert) pair is sent to the expert's owner
-   -- an all-to-all of the split sizes, then one all-to-all of the token rows
-   and one of the packed (expert, weight, compensated) metadata;
+   in fixed-capacity blocks (no host synchronisation, graph-capturable) -- one
+   all-to-all of the token rows and one of the packed (expert, weight,
+   compensated) metadata;
 3. the owner runs ``lrc_layer_forward_pairs`` on what it received: one launch
    sequence over its local experts, U.(V.x) applied for the flagged pairs;
 4. combine: the weighted rows go back with the reverse all-to-all and are summed
@@ -33,12 +34,17 @@ class ExpertParallelLayer:
     """One MoE layer sharded over ``group``; see the module docstring."""
 
     def __init__(self, group, num_experts: int, num_shared: int, top_k: int, top_n: int,
-                 route_fn, compute_fn, compensate_shared: bool = True):
+                 route_fn, compute_fn, compensate_shared: bool = True, comm_device=None,
+                 max_tokens: int = 64):
         import torch.distributed as dist
 
+        self.comm_device = comm_device  # None: collectives on x's device (NCCL); "cpu" for gloo
+        self.max_tokens = int(max_tokens)  # per rank and step; the same on every rank
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        if num_experts < self.world:
+            raise ValueError("expert parallelism needs at least one routed expert per rank")
         self.E, self.S, self.k, self.n = num_experts, num_shared, top_k, top_n
         self.route_fn, self.compute_fn = route_fn, compute_fn
         self.compensate_shared = compensate_shared
@@ -47,53 +53,76 @@ class ExpertParallelLayer:
         return [e for e in range(self.E) if owner_of(e, self.E, self.world) == self.rank]
 
     # ---------------------------------------------------------------- step --
+    def first_expert(self, r: int) -> int:
+        """Lowest routed expert id owned by rank r: ceil(r E / G)."""
+        return -(-r * self.E // self.world)
+
     def forward(self, x):
         """x (B, d) on this rank's device -> y (B, d) float32 (sum over the
-        token's experts, as ref/moe.py:forward in mode "compensated")."""
+        token's experts, as ref/moe.py:forward in mode "compensated").
+
+        No host synchronisation and static shapes (graph-capturable): every
+        rank sends a fixed-capacity block of C = max_tokens k rows to every
+        rank (the worst case, so nothing is ever dropped; max_tokens is the
+        same on every rank, the local batches B <= max_tokens may differ).  A (token, expert) pair's slot
+        in its owner's block is its rank among the pairs with the same owner
+        (a one-hot cumulative sum); unused slots carry a zero row for the
+        receiver's first expert with weight 0, which adds nothing (and only
+        keeps an expert busy on a rank that would otherwise idle)."""
         import torch
         import torch.distributed as dist
 
         B, d = int(x.shape[0]), int(x.shape[1])
         dev = x.device
+        W = self.world
         idx, w = self.route_fn(x)                      # (B, k) int, (B, k) float
         idx = idx.to(dev, torch.int64)
         w = w.to(dev, torch.float32)
-        k = idx.shape[1]
+        k = int(idx.shape[1])
+        if B > self.max_tokens:
+            raise ValueError(f"EP forward: {B} tokens above max_tokens={self.max_tokens}")
+        C = self.max_tokens * k
         token = torch.arange(B, device=dev).repeat_interleave(k)
         expert = idx.reshape(-1)
         weight = w.reshape(-1)
-        comp = (torch.arange(k, device=dev) < self.n).repeat(B).to(torch.int64)
-        dest = owner_of(expert, self.E, self.world)
-        order = torch.argsort(dest, stable=True)
-        token, expert, weight, comp, dest = token[order], expert[order], weight[order], comp[order], dest[order]
-        send = torch.bincount(dest, minlength=self.world).to(torch.int64)
-        recv = torch.empty_like(send)
-        dist.all_to_all_single(recv, send, group=self.group)
-        send_l, recv_l = send.tolist(), recv.tolist()
-        nrecv = int(sum(recv_l))
-        # token rows + packed metadata (expert id, weight bits, comp flag)
-        x_send = x[token].contiguous()
-        meta_send = torch.stack([expert.to(torch.int32), weight.view(torch.int32),
-                                 comp.to(torch.int32)], dim=1).contiguous()
-        x_recv = torch.empty((nrecv, d), dtype=x.dtype, device=dev)
-        meta_recv = torch.empty((nrecv, 3), dtype=torch.int32, device=dev)
-        dist.all_to_all_single(x_recv, x_send, recv_l, send_l, group=self.group)
-        dist.all_to_all_single(meta_recv, meta_send, recv_l, send_l, group=self.group)
+        comp = (torch.arange(k, device=dev) < self.n).repeat(B).to(torch.int32)
+        dest = owner_of(expert, self.E, W)
+        ranks = torch.arange(W, device=dev)
+        onehot = (dest[:, None] == ranks[None, :]).to(torch.int32)  # (no one_hot: it validates on the host)
+        pos = (onehot.cumsum(0) * onehot).sum(1) - 1
+        slot = dest * C + pos
+        first = (-(-ranks * self.E // W)).to(torch.int32)  # ceil(r E / G), computed on the device
+        meta = torch.zeros((W * C, 3), dtype=torch.int32, device=dev)
+        meta[:, 0] = first.repeat_interleave(C)
+        meta[slot, 0] = expert.to(torch.int32)
+        meta[slot, 1] = weight.view(torch.int32)
+        meta[slot, 2] = comp
+        src = torch.full((W * C,), B, dtype=torch.int64, device=dev)  # dummy slots -> row B
+        src[slot] = token
+        x_send = torch.zeros((W * C, d), dtype=x.dtype, device=dev)
+        x_send[slot] = x[token]
+        cdev = self.comm_device or dev
+        x_recv = torch.empty((W * C, d), dtype=x.dtype, device=cdev)
+        meta_recv = torch.empty((W * C, 3), dtype=torch.int32, device=cdev)
+        dist.all_to_all_single(x_recv, x_send.to(cdev), group=self.group)
+        dist.all_to_all_single(meta_recv, meta.to(cdev), group=self.group)
+        x_recv, meta_recv = x_recv.to(dev), meta_recv.to(dev)
         y_rows = self.compute_fn(x_recv, meta_recv[:, 0].contiguous(),
                                  meta_recv[:, 1].contiguous().view(torch.float32),
                                  meta_recv[:, 2].contiguous().to(torch.uint8))
         y_rows = y_rows.to(torch.float32).contiguous()
-        y_back = torch.empty((token.numel(), d), dtype=torch.float32, device=dev)
-        dist.all_to_all_single(y_back, y_rows, send_l, recv_l, group=self.group)
-        y = torch.zeros((B, d), dtype=torch.float32, device=dev)
-        y.index_add_(0, token, y_back)
+        y_back = torch.empty((W * C, d), dtype=torch.float32, device=cdev)
+        dist.all_to_all_single(y_back, y_rows.to(cdev), group=self.group)
+        y = torch.zeros((B + 1, d), dtype=torch.float32, device=dev)
+        y.index_add_(0, src, y_back.to(dev))
+        y = y[:B]
         if self.S:  # shared experts: replicated, computed on the token's own rank
             xs = x.repeat(self.S, 1)
             ex = torch.arange(self.E, self.E + self.S, device=dev).repeat_interleave(B).to(torch.int32)
             ws = torch.ones(B * self.S, dtype=torch.float32, device=dev)
             cs = torch.full((B * self.S,), int(self.compensate_shared), dtype=torch.uint8, device=dev)
             ys = self.compute_fn(xs, ex, ws, cs).to(torch.float32)
-            y += ys.reshape(self.S, B, d).sum(0)
+            y = y + ys.reshape(self.S, B, d).sum(0)
         return y
 
 
@@ -114,14 +143,15 @@ def cuda_route_fn(dl, top_k: int, top_n: int, renormalize: bool = False):
 
 
 def from_device_layer(group, dl, top_k: int, top_n: int, renormalize: bool = False,
-                      compensate_shared: bool = True) -> ExpertParallelLayer:
+                      compensate_shared: bool = True, comm_device=None,
+                      max_tokens: int = 64) -> ExpertParallelLayer:
     """EP layer over a rank-local ``LRCMoELayer`` that holds (at least) the
     experts this rank owns plus the shared experts (absent experts may be
     None records: they share one placeholder)."""
     return ExpertParallelLayer(group, dl.num_experts, dl.num_shared, top_k, top_n,
                                cuda_route_fn(dl, top_k, top_n, renormalize),
-                               lambda xr, e, w, c: dl.forward_pairs(xr, e, w, c),
-                               compensate_shared)
+                               lambda xr, e, w, c: dl.forward_pairs(xr, e, w, c, validate=False),
+                               compensate_shared, comm_device, max_tokens)
 
 
 def owned_records(records, num_experts: int, world: int, rank: int):

@@ -63,7 +63,7 @@ def _worker(rank, world, port, result_path):
                 assert ei >= E or ep.owner_of(ei, E, world) == rank, "row dispatched to a non-owner"
             return compute(xr, e, w, c)
 
-        layer_ep = ep.ExpertParallelLayer(dist.group.WORLD, E, S, K, N, route, guarded)
+        layer_ep = ep.ExpertParallelLayer(dist.group.WORLD, E, S, K, N, route, guarded, max_tokens=8)
         x = torch.from_numpy(O.to_bf16(O.gen_tokens(10 + rank, HID, 5 + rank))).double()
         y = layer_ep.forward(x).double().numpy()
         worst = 0.0
@@ -131,7 +131,7 @@ def test_ep_single_rank_nccl():
     dist.init_process_group("nccl", rank=0, world_size=1)
     try:
         sl = SynthLayer(512, 1024, 8, top_k=2, rank=16, seed=6, max_tokens=64)
-        layer_ep = ep.from_device_layer(dist.group.WORLD, sl.layer, 2, 1)
+        layer_ep = ep.from_device_layer(dist.group.WORLD, sl.layer, 2, 1, max_tokens=8)
         x = torch.randn((5, 512), device="cuda").to(torch.bfloat16)
         y = layer_ep.forward(x)
         y_ref, _, _ = sl.layer.forward(x, 2, 1)
@@ -139,3 +139,50 @@ def test_ep_single_rank_nccl():
         assert err < 1e-5, float(err)
     finally:
         dist.destroy_process_group()
+
+
+def _gpu_worker(rank, world, port, result_path):
+    """One rank of a world-2 EP layer on the SAME GPU: the CUDA router and
+    ``forward_pairs`` compute, the all-to-alls over gloo on host copies."""
+    import torch.distributed as dist
+    from paper_2512_17073_b200 import _lib
+    from paper_2512_17073_b200.synth import SynthLayer
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _lib.load()
+        sl = SynthLayer(512, 1024, 8, top_k=2, num_shared=1, rank=16, seed=8, max_tokens=64)
+        dl = sl.layer
+        layer_ep = ep.from_device_layer(dist.group.WORLD, dl, 2, 1, comm_device="cpu", max_tokens=8)
+        owned = set(layer_ep.local_experts())
+
+        def guarded(xr, e, w, c):  # every row this rank computes belongs to one of its experts
+            bad = [int(v) for v in e.cpu().tolist() if v < 8 and int(v) not in owned]
+            assert not bad, f"rows of experts {bad} dispatched to rank {rank}"
+            return dl.forward_pairs(xr, e, w, c, validate=False)
+
+        layer_ep.compute_fn = guarded
+        g = torch.Generator(device="cuda").manual_seed(100 + rank)
+        x = torch.randn((5 + rank, 512), device="cuda", generator=g).to(torch.bfloat16)
+        y = layer_ep.forward(x)
+        y_ref, _, _ = dl.forward(x, 2, 1)
+        err = float((y - y_ref).norm() / y_ref.norm())
+        with open(f"{result_path}.{rank}", "w") as f:
+            f.write(repr(err))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_ep_world2_cuda_compute(tmp_path):
+    """World-size-2 EP with the CUDA owner-side compute (forward_pairs) and the
+    CUDA router on both ranks vs the single-GPU routed layer forward."""
+    import torch.multiprocessing as mp
+
+    res = str(tmp_path / "err")
+    mp.spawn(_gpu_worker, args=(2, _free_port(), res), nprocs=2, join=True)
+    for r in range(2):
+        err = float(open(f"{res}.{r}").read())
+        assert err < 1e-5, f"rank {r}: EP output differs from the layer forward ({err:.2e})"
