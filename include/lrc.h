@@ -218,6 +218,25 @@ lrc_status lrc_layer_phase_ms(lrc_layer* layer, float* ms4);
  * Copies n values and clears the device buffer. */
 lrc_status lrc_debug_stamps(int which, uint64_t* host, int n);
 
+/* ------------------------------------------------------ expert parallel --- */
+/* Dispatch of a rank's routed pairs to the expert owners: pair
+ * p = b*top_k + j goes to rank floor(e*world/num_experts), e = topk_idx[p], at
+ * slot dest*capacity + (its rank among the pairs with that destination, in
+ * pair order).  Writes x_send (world*capacity, d) bf16 rows, meta_send
+ * (world*capacity, 3) int32 {expert, float bits of the weight, compensated =
+ * j < top_n} and slot_of[p]; unused slots get a zero row for the receiver's
+ * first expert ceil(r*num_experts/world) with weight 0.  Requires
+ * B*top_k <= capacity and world*capacity <= 4096.  Stream-ordered, no host
+ * synchronisation (the NCCL all-to-alls of x_send / meta_send go between
+ * this call and the owner's lrc_layer_forward_pairs). */
+lrc_status lrc_ep_dispatch(const int32_t* topk_idx, const float* topk_w, const uint16_t* x, int64_t B,
+                           int top_k, int top_n, int num_experts, int world, int capacity, int d,
+                           uint16_t* x_send, int32_t* meta_send, int32_t* slot_of, void* stream);
+/* Combine (ref/moe.py:237-258): y[b] = sum_j back[slot_of[b*top_k + j]] for the
+ * rows returned by the reverse all-to-all (already weighted by the owners). */
+lrc_status lrc_ep_combine(const float* back, const int32_t* slot_of, int64_t B, int top_k, int d, float* y,
+                          void* stream);
+
 /* Dense fp64 expert (mode="reference", ref/moe.py:241-243):
  * y (B, hidden) += w[b] * w2 @ (silu(w1 @ x_b) * (w3 @ x_b)); w may be NULL (=1). */
 lrc_status lrc_dense_expert_f64(const double* w1, const double* w3, const double* w2, int hidden,

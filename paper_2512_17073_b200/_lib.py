@@ -64,6 +64,9 @@ _SIGS = {
     "lrc_layer_forward_pairs": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
                                         c_void_p, c_void_p]),
     "lrc_layer_last_launches": (c_int, [c_void_p]),
+    "lrc_ep_dispatch": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int, c_int,
+                                c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "lrc_ep_combine": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p]),
     "lrc_layer_forward_host": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int,
                                        c_void_p, c_void_p]),
     "lrc_layer_set_profiling": (c_int, [c_void_p, c_int]),

@@ -76,12 +76,14 @@ class ExpertParallelLayer:
         dev = x.device
         W = self.world
         idx, w = self.route_fn(x)                      # (B, k) int, (B, k) float
-        idx = idx.to(dev, torch.int64)
-        w = w.to(dev, torch.float32)
         k = int(idx.shape[1])
         if B > self.max_tokens:
             raise ValueError(f"EP forward: {B} tokens above max_tokens={self.max_tokens}")
         C = self.max_tokens * k
+        if x.is_cuda and x.dtype == torch.bfloat16 and self.comm_device is None:
+            return self._forward_cuda(x, idx, w, B, d, k, C)
+        idx = idx.to(dev, torch.int64)
+        w = w.to(dev, torch.float32)
         token = torch.arange(B, device=dev).repeat_interleave(k)
         expert = idx.reshape(-1)
         weight = w.reshape(-1)
@@ -124,6 +126,54 @@ class ExpertParallelLayer:
             ys = self.compute_fn(xs, ex, ws, cs).to(torch.float32)
             y = y + ys.reshape(self.S, B, d).sum(0)
         return y
+
+
+def _shared_rows(self, x, y, B, d):
+    import torch
+
+    dev = x.device
+    xs = x.repeat(self.S, 1)
+    ex = torch.arange(self.E, self.E + self.S, device=dev).repeat_interleave(B).to(torch.int32)
+    ws = torch.ones(B * self.S, dtype=torch.float32, device=dev)
+    cs = torch.full((B * self.S,), int(self.compensate_shared), dtype=torch.uint8, device=dev)
+    ys = self.compute_fn(xs, ex, ws, cs).to(torch.float32)
+    return y + ys.reshape(self.S, B, d).sum(0)
+
+
+def _forward_cuda(self, x, idx, w, B, d, k, C):
+    """The same exchange with the dispatch and the combine as one CUDA kernel
+    each (lrc_ep_dispatch / lrc_ep_combine): route, dispatch, 2 all-to-alls,
+    the owner's forward_pairs, 1 all-to-all back, combine."""
+    import torch
+    import torch.distributed as dist
+
+    W = self.world
+    lib = _lib.lib()
+    idx = idx.to(torch.int32).contiguous()
+    w = w.to(torch.float32).contiguous()
+    x = x.contiguous()
+    x_send = torch.empty((W * C, d), dtype=torch.bfloat16, device=x.device)
+    meta = torch.empty((W * C, 3), dtype=torch.int32, device=x.device)
+    slot_of = torch.empty((B * k,), dtype=torch.int32, device=x.device)
+    _lib.check(lib.lrc_ep_dispatch(_lib.ptr(idx), _lib.ptr(w), _lib.ptr(x), B, k, self.n, self.E, W, C, d,
+                                   _lib.ptr(x_send), _lib.ptr(meta), _lib.ptr(slot_of), _lib.stream_ptr()))
+    x_recv = torch.empty_like(x_send)
+    meta_recv = torch.empty_like(meta)
+    dist.all_to_all_single(x_recv, x_send, group=self.group)
+    dist.all_to_all_single(meta_recv, meta, group=self.group)
+    y_rows = self.compute_fn(x_recv, meta_recv[:, 0].contiguous(),
+                             meta_recv[:, 1].contiguous().view(torch.float32),
+                             meta_recv[:, 2].contiguous().to(torch.uint8))
+    y_back = torch.empty_like(y_rows)
+    dist.all_to_all_single(y_back, y_rows.contiguous(), group=self.group)
+    y = torch.empty((B, d), dtype=torch.float32, device=x.device)
+    _lib.check(lib.lrc_ep_combine(_lib.ptr(y_back), _lib.ptr(slot_of), B, k, d, _lib.ptr(y), _lib.stream_ptr()))
+    if self.S:
+        y = _shared_rows(self, x, y, B, d)
+    return y
+
+
+ExpertParallelLayer._forward_cuda = _forward_cuda
 
 
 def cuda_route_fn(dl, top_k: int, top_n: int, renormalize: bool = False):
