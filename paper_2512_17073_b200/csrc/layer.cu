@@ -5,6 +5,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "layer.cuh"
 #include "tcd.cuh"
@@ -856,6 +858,15 @@ extern "C" lrc_status lrc_layer_set_tcd_max(lrc_layer* L, int max_tokens) {
 
 extern "C" int lrc_layer_tcd_eligible(const lrc_layer* L) { return L && L->tcd_ok ? 1 : 0; }
 
+// NVTX ranges: one per layer call, one per engine (visible in
+// nsys / ncu --nvtx; free when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int top_k, int top_n,
                                int renormalize, int compensate_shared, float* y, int32_t* topk_idx,
                                float* topk_w, void* stream, bool allow_tiled,
@@ -867,6 +878,7 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   if (top_k > L->E) return fail(LRC_ERR_INVALID, "top_k exceeds the number of experts");
   if (top_k > L->k_max) return fail(LRC_ERR_UNSUPPORTED, "top_k above the layer's workspace");
   if (B < 0 || B > L->max_tokens) return fail(LRC_ERR_UNSUPPORTED, "B above max_tokens");
+  NvtxRange nv_call(pairs_expert ? "lrc.layer_forward_pairs" : "lrc.layer_forward");
   cudaStream_t st = as_stream(stream);
   int launches = 0;
   const bool prof = L->profiling;
@@ -940,6 +952,7 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
     a.stamp = stamps ? 1 : 0;
     static const int dbg = getenv("LRC_TCD_DEBUG") ? atoi(getenv("LRC_TCD_DEBUG")) : 0;
     a.dbg = dbg;
+    NvtxRange nv_tcd("lrc.tcd");
     if ((s = tcd::launch(a, L->num_sms, st, pdl)) != LRC_OK) return s;
     ++launches;
     if (prof) {
@@ -994,7 +1007,9 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   const bool big_plan = np_bound > kSerialPlanMaxPairs;
   if (big_plan) ra.plan.ticket = nullptr;
   static const bool no_bulk = getenv("LRC_NO_BULK_ROUTE") != nullptr;
+  nvtxRangePushA("lrc.route");
   lrc_status s = (big_plan && !no_bulk) ? launch_route_bulk(ra, st) : launch_route(ra, st);
+  nvtxRangePop();
   if (s != LRC_OK) return s;
   ++launches;
   if (big_plan) {
@@ -1053,9 +1068,11 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
           return s;
         L->lrp_dirty[i] = 0;
       }
+    NvtxRange nv_pf("lrc.prefill");
     if ((s = launch_prefill(a, np_bound, L->lrp, L->tb, L->ppk, L->prefill_bits, st, &launches)) != LRC_OK) return s;
     if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));  // phases: up+mid+down lumped into [2]
   } else if (allow_tiled && L->tiled) {
+    NvtxRange nv_t("lrc.tiled");
     const int tok_bound = static_cast<int>(std::min<int64_t>(B, L->max_tokens));
     // programmatic dependent launch: the next kernel's CTAs are scheduled as SMs
     // free up and block in griddepcontrol.wait (no PDL while timing phases)
@@ -1067,6 +1084,7 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
       return s;
     launches += 2;
   } else {
+    NvtxRange nv_g("lrc.generic");
     const int grid = L->num_sms * 4;
     up_generic_kernel<<<grid, 256, 0, st>>>(a);
     LRC_CHECK_LAUNCH();
