@@ -647,12 +647,15 @@ def offload_point(layers=32, tokens=8, repeats=5):
     torch.cuda.synchronize()
     runs = []
     step_bytes = layers * eng.bytes_per_step(TOPK)  # B=1: top-k distinct experts per layer
-    for _ in range(repeats):
+    for rep in range(repeats):
+        if rep == repeats - 1:
+            eng.start_trace()  # routing of the last repeat's tokens, for the simulator
         t1 = time.perf_counter()
         for _ in range(tokens):
             x = eng.forward(x, normalize=True)
         torch.cuda.synchronize()
         runs.append((time.perf_counter() - t1, {"bytes": tokens * step_bytes}))
+    trace = eng.routing_trace()
     order = sorted(runs, key=lambda r: r[0])
     dt, stats = order[len(order) // 2]
     gbs = stats["bytes"] / dt / 1e9
@@ -664,8 +667,39 @@ def offload_point(layers=32, tokens=8, repeats=5):
            "runs_tok_s": [round(tokens / r[0], 2) for r in runs], "pool_gb": round(
                sum(he.nbytes for lay in host for he in lay) / 1e9, 2), "build_s": round(build_s, 1),
            "timing": "host wall clock around `tokens` decode steps + synchronize, median of repeats"}
+    out["simulator"] = simulator_calibration(trace, tokens / dt, h2d, int(stats["bytes"] / tokens))
     del eng, host
     torch.cuda.empty_cache()
+    return out
+
+
+def simulator_calibration(trace, measured_tok_s, h2d_gbs, moved_per_token):
+    """replay the routing trace of the measured C3 tokens through
+    the reference's cost model (paper_2512_17073_b200.simulate, checked against
+    the reference's own reports in tests/test_simulate.py) with this box's
+    measured B200 rates, and set the prediction against the measurement."""
+    from paper_2512_17073_b200 import simulate as sim
+
+    hbm, tf_burst, tf_sust, _ = load_peaks()
+    dims = sim.ModelDims(hidden=HIDDEN, ffn=FFN, num_layers=trace.num_layers(), num_experts=E, top_k=TOPK)
+    plan = sim.TransferPlan(name="int2-n1-r32", expert_bits=BITS, top_n=TOPN, rank=RANK, factor_bits=3)
+    out = {"trace_tokens": trace.num_tokens(), "plan": "INT2 codes, rank-32 3-bit factors on top-1, no cache",
+           "system": {"pcie_gbs": round(h2d_gbs, 2), "hbm_gbs": hbm, "bf16_tflops": tf_sust,
+                      "source": "measured (pinned H2D copy here; MEASURED_PEAKS.json)"},
+           "measured_tok_s": round(measured_tok_s, 3), "moved_bytes_per_token": moved_per_token}
+    for ov in (False, True):
+        r = sim.simulate(trace, plan, sim.b200_system(h2d_gbs, hbm, tf_sust, overlap=ov), dims, include_prefill=False)
+        key = "overlap" if ov else "serial"
+        out[key] = {"predicted_tok_s": round(r.tokens_per_s, 3),
+                    "sim_bytes_per_token": int(r.total_bytes_moved / r.output_len),
+                    "measured_over_predicted": round(measured_tok_s / r.tokens_per_s, 4)}
+    # the same model fed the bytes the engine really moves (codes + fp16 metadata
+    # + LR tiles + V factors per expert) isolates the byte model from the rest
+    scale = out["serial"]["sim_bytes_per_token"] / moved_per_token
+    out["serial_engine_bytes"] = {
+        "predicted_tok_s": round(out["serial"]["predicted_tok_s"] * scale, 3),
+        "measured_over_predicted": round(measured_tok_s / (out["serial"]["predicted_tok_s"] * scale), 4),
+        "note": "transfer-bound: prediction scaled by simulator bytes / engine bytes"}
     return out
 
 

@@ -287,6 +287,7 @@ class GpuPagerEngine(OffloadEngine):
                 row.append(blk)
             self.blocks.append(row)
         self.stats = {"bytes": 0, "steps": 0}
+        self._trace = None
         self._zw13 = _zero_qmat(ffn, hidden, self.keep)
         self._zw2 = _zero_qmat(hidden, ffn, self.keep)
         self._zfac = {}
@@ -302,9 +303,30 @@ class GpuPagerEngine(OffloadEngine):
             self.layers.append(dl)
 
     def forward_layer(self, layer: int, x):
-        y, _, _ = self.layers[layer].forward(x, self.k, self.n)
+        y, idx, w = self.layers[layer].forward(x, self.k, self.n)
         self.stats["steps"] += 1
+        if self._trace is not None:  # device copies only; read back by routing_trace()
+            self._trace.append((layer, idx.clone(), w.clone()))
         return y
+
+    def start_trace(self):
+        """Record the routing of every following layer step."""
+        self._trace = []
+
+    def routing_trace(self):
+        """The recorded steps as a ``moe.RoutingTrace`` (token = decode step;
+        one record per (token, layer) for the first row of each batch)."""
+        from .moe import RoutingTrace, TraceRecord
+
+        recs = []
+        steps = self._trace or []
+        nl = len(self.layers)
+        for i, (layer, idx, w) in enumerate(steps):
+            sel = [int(v) for v in idx[0].cpu().tolist()]
+            ww = w[0].double().cpu().numpy()
+            recs.append(TraceRecord(i // nl, layer, ww, sel, sel[: self.n]))
+        self._trace = None
+        return RoutingTrace(records=recs)
 
     def bytes_per_step(self, distinct_experts: int) -> int:
         """Host-link bytes of one layer step that selects ``distinct_experts``."""
