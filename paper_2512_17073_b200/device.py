@@ -42,12 +42,33 @@ def _qm_to_device(qm: QuantizedMatrix, keep: _Keep) -> _lib.LrcQmat:
     packed = keep.add(pack_codes_device(codes, qm.bits))
     # scale/zero rounded to fp16 on the host (numpy rounding; the parity oracle
     # applies the identical rounding)
-    s = keep.add(torch.from_numpy(np.ascontiguousarray(qm.scales, dtype=np.float16).view(np.uint16)).cuda())
-    z = keep.add(torch.from_numpy(np.ascontiguousarray(qm.zero_points, dtype=np.float16).view(np.uint16)).cuda())
+    s = keep.add(torch.from_numpy(_fp16_meta(qm.scales, "scale").view(np.uint16)).cuda())
+    z = keep.add(torch.from_numpy(_fp16_meta(qm.zero_points, "zero point").view(np.uint16)).cuda())
     m = _lib.LrcQmat()
     m.packed, m.scales, m.zeros, m.dense = packed.data_ptr(), s.data_ptr(), z.data_ptr(), None
     m.rows, m.cols, m.bits, m.group_size = qm.rows, qm.cols, qm.bits, qm.group_size
     return m
+
+
+def _fp16_meta(a, what: str):
+    """Group scale / zero metadata as fp16 (the kernels' format).  The
+    reference keeps them in f8 (ref/quant.py); a value that overflows fp16, or
+    a nonzero scale that flushes to 0, would silently corrupt the output, so
+    both raise ArtifactError.  (fp16 subnormals, |v| < 6.1e-5, keep an absolute
+    error below 3e-8: accepted.)"""
+    a64 = np.asarray(a, dtype=np.float64)
+    with np.errstate(over="ignore"):
+        h = a64.astype(np.float16)
+    bad = ~np.isfinite(h) & np.isfinite(a64)
+    if what == "scale":
+        bad |= (a64 != 0) & (h == 0)
+    bad |= ~np.isfinite(a64)
+    if bad.any():
+        from .artifact import ArtifactError
+
+        v = float(a64.ravel()[np.flatnonzero(bad.ravel())[0]])
+        raise ArtifactError(f"{what} value {v!r} does not fit the fp16 metadata the device kernels use")
+    return np.ascontiguousarray(h)
 
 
 def _packed_to_device(packed: bytes, rows, cols, bits, group_size, scales, zeros,
@@ -55,8 +76,8 @@ def _packed_to_device(packed: bytes, rows, cols, bits, group_size, scales, zeros
     """Reference on-disk form (ref/artifact.py:103-108) straight to HBM."""
     torch = _lib.device_required()
     p = keep.add(torch.frombuffer(bytearray(packed), dtype=torch.uint8).cuda())
-    s = keep.add(torch.from_numpy(np.ascontiguousarray(scales, dtype=np.float16).view(np.uint16)).cuda())
-    z = keep.add(torch.from_numpy(np.ascontiguousarray(zeros, dtype=np.float16).view(np.uint16)).cuda())
+    s = keep.add(torch.from_numpy(_fp16_meta(scales, "scale").view(np.uint16)).cuda())
+    z = keep.add(torch.from_numpy(_fp16_meta(zeros, "zero point").view(np.uint16)).cuda())
     m = _lib.LrcQmat()
     m.packed, m.scales, m.zeros, m.dense = p.data_ptr(), s.data_ptr(), z.data_ptr(), None
     m.rows, m.cols, m.bits, m.group_size = rows, cols, bits, group_size

@@ -329,15 +329,34 @@ def _forward_batch(xs: np.ndarray, layer: MoELayer, cfg: ForwardConfig, mode: st
         for s in layer.shared_experts:
             _dense_expert_accum(s, xd, None, y)
         return y.cpu().numpy()
-    dl = device_layer(artifacts, layer_id, layer, max_tokens=max(64, B), top_k=cfg.top_k)
-    xb = torch.from_numpy(np.ascontiguousarray(xs, dtype=np.float64)).cuda().to(torch.bfloat16)
-    top_n = cfg.top_n if mode == "compensated" else 0
-    comp_shared = cfg.compensate_shared and mode == "compensated"
-    y, idx, _ = dl.forward(xb, cfg.top_k, top_n, cfg.renormalize_topk, comp_shared)
+    # Routing runs on the fp64 tokens, exactly as the reference's forward
+    # (ref/moe.py:221-233 routes x itself): lrc_route in fp64, then the expert
+    # kernels take that selection as explicit (token, expert) pairs
+    # (lrc_layer_forward_pairs).  Only the expert compute sees the bf16 tokens.
+    P = cfg.top_k + layer.num_shared
+    dl = device_layer(artifacts, layer_id, layer, max_tokens=max(64, B * P), top_k=cfg.top_k)
+    xd = torch.from_numpy(np.ascontiguousarray(xs, dtype=np.float64)).cuda()
+    _, idx, mix = _route_batch(xd, layer.gate, cfg.top_k, 0, cfg.renormalize_topk)
     if dl.missing:
         _check_missing(dl, idx.cpu().numpy(), cfg.top_k, layer_id, layer.num_experts,
                        layer.num_shared)
-    return y.double().cpu().numpy()
+    xb = xd.to(torch.bfloat16)
+    top_n = cfg.top_n if mode == "compensated" else 0
+    comp_shared = cfg.compensate_shared and mode == "compensated"
+    k, S = cfg.top_k, layer.num_shared
+    ex = torch.empty((B, P), dtype=torch.int32, device="cuda")
+    wt = torch.ones((B, P), dtype=torch.float32, device="cuda")
+    cp = torch.zeros((B, P), dtype=torch.uint8, device="cuda")
+    if k:
+        ex[:, :k] = idx[:, :k]
+        wt[:, :k] = mix[:, :k]
+        cp[:, :min(top_n, k)] = 1
+    if S:
+        ex[:, k:] = torch.arange(layer.num_experts, layer.num_experts + S, dtype=torch.int32, device="cuda")
+        cp[:, k:] = int(comp_shared)
+    rows = xb.repeat_interleave(P, dim=0)
+    y = dl.forward_pairs(rows, ex.reshape(-1), wt.reshape(-1), cp.reshape(-1), validate=False)
+    return y.reshape(B, P, -1).sum(1).double().cpu().numpy()
 
 
 def forward(x: np.ndarray, layer: MoELayer, cfg: ForwardConfig, mode: str = "reference",

@@ -394,9 +394,9 @@ def test_api_renormalize(torch):
     st = _api_compress(model, 16)
     x = moe.gen_tokens(5, 32, 1)[0]
     for mode, art in (("reference", None), ("compensated", st)):
-        # the device path routes the bf16-rounded token; scale accordingly
-        rr = moe.route(x if art is None else lrc.to_bf16(x), model.layers[0],
-                       moe.ForwardConfig(top_k=2))
+        # every mode routes the fp64 token, as the reference does (ADVICE r1:
+        # the quantized / compensated device path used to route its bf16 copy)
+        rr = moe.route(x, model.layers[0], moe.ForwardConfig(top_k=2))
         scale = rr.weights[rr.selected].sum()
         y_plain = moe.forward(x, model.layers[0], moe.ForwardConfig(top_k=2), mode, art, 0)
         y_ren = moe.forward(x, model.layers[0], moe.ForwardConfig(top_k=2, renormalize_topk=True),

@@ -144,3 +144,18 @@ def test_product_never_imports_oracle():
             if f.endswith(".py") and f != "synth.py":
                 src = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_fp16_metadata_range_check():
+    """Artifact metadata that does not fit the kernels' fp16 format raises
+    (overflow -> inf, nonzero scales flushing to 0)."""
+    from paper_2512_17073_b200.artifact import ArtifactError
+    from paper_2512_17073_b200.device import _fp16_meta
+
+    assert _fp16_meta([0.01, 0.0, 1e-6], "scale").dtype == np.float16
+    assert _fp16_meta([1e-9, -3.0], "zero point")[0] == 0.0  # tiny zero points: < 3e-8 absolute error
+    for bad in ([7e4], [1e-9], [float("nan")]):
+        with pytest.raises(ArtifactError):
+            _fp16_meta(bad, "scale")
+    with pytest.raises(ArtifactError):
+        _fp16_meta([-1e5], "zero point")
