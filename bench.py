@@ -350,6 +350,9 @@ def run_ours(args, world, rank):
     int3 = None
     if args.int3 and rank == 0:
         int3 = int3_point(hbm, tf_sust)
+    c5 = None
+    if args.c5 and rank == 0:
+        c5 = c5_point(hbm, tf_sust)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -376,6 +379,7 @@ def run_ours(args, world, rank):
         "prefill": prefill,
         "offload": offl,
         "int3": int3,
+        "c5": c5,
         "cpu_baseline": cpu,
     }
     if rank == 0:
@@ -564,6 +568,61 @@ def int3_point(hbm, tf_sust, layers=8):
     for Bs in (1, 8, 64):
         out[str(Bs)] = sweep_point(sls, Bs, hbm, tf_sust, steps=100 if Bs < 64 else 30, bits=3)
     out["frac"] = out["1"]["frac"]
+    del sls
+    torch.cuda.empty_cache()
+    return out
+
+
+def c5_point(hbm, tf_sust, layers=4, E5=64, K5=8, N5=2, S5=2, D5=2048, F5=11008):
+    """C5 on one GPU (BASELINE configs[4] shape; ref/presets.py deepseek-16b
+    dims with top-8 / Top-2 restore and the preset's 2 shared experts, router
+    skew 0.8): decode batches 1 / 8 / 64, 4 layers rotated (4.4 GB), graph
+    replay.  Bytes: the distinct routed experts + the shared ones, their
+    compensators on top-2 (+ shared), gate, x, y."""
+    import torch
+
+    from paper_2512_17073_b200.synth import SynthLayer
+
+    sls = [SynthLayer(D5, F5, E5, top_k=K5, num_shared=S5, bits=2, rank=RANK, seed=5000 + l, router_skew=0.8,
+                      max_tokens=64) for l in range(layers)]
+    out = {"workload": f"DeepSeek-MoE-shaped layer d={D5} ffn={F5}, {E5} experts top-{K5} + {S5} shared, INT2 "
+                       f"+ rank-{RANK} LR on top-{N5} and the shared experts, skew 0.8, {layers} layers rotated"}
+    eb, cb = expert_bytes(D5, F5, 2), comp_bytes(D5, F5, RANK)
+    for B in (1, 8, 64):
+        xs = [torch.randn((B, D5), device="cuda").to(torch.bfloat16) for _ in range(layers)]
+        ys = [torch.empty((B, D5), dtype=torch.float32, device="cuda") for _ in range(layers)]
+        idx = [torch.empty((B, K5), dtype=torch.int32, device="cuda") for _ in range(layers)]
+        stats = []
+        for l in range(layers):
+            sls[l].layer.forward(xs[l], K5, N5, y=ys[l], topk_idx=idx[l])
+            sel = idx[l].cpu().numpy()
+            stats.append((len(np.unique(sel)), len(np.unique(sel[:, :N5]))))
+        steps = 100 if B < 64 else 30
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            for l in range(layers):
+                sls[l].layer.forward(xs[l], K5, N5, y=ys[l], topk_idx=idx[l])
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            for i in range(steps):
+                l = i % layers
+                sls[l].layer.forward(xs[l], K5, N5, y=ys[l], topk_idx=idx[l])
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        byts = sum((stats[i % layers][0] + S5) * eb + (stats[i % layers][1] + S5) * cb + D5 * E5 * 8 + B * D5 * 6
+                   for i in range(steps))
+        out[str(B)] = {"tokens_s": round(steps * B / (ms / 1e3), 1), "us_per_step": round(ms * 1e3 / steps, 2),
+                       "gbs": round(byts / (ms / 1e3) / 1e9, 1), "frac": round(byts / (ms / 1e3) / 1e9 / hbm, 4),
+                       "d_sel_mean": round(float(np.mean([x[0] for x in stats])), 2)}
     del sls
     torch.cuda.empty_cache()
     return out
@@ -798,6 +857,7 @@ def main():
     ap.add_argument("--no-prefill", dest="prefill", action="store_false")
     ap.add_argument("--no-offload", dest="offload", action="store_false")
     ap.add_argument("--no-int3", dest="int3", action="store_false")
+    ap.add_argument("--no-c5", dest="c5", action="store_false")
     ap.add_argument("--ep", action="store_true", help="expert-parallel arm (default when --gpus > 1)")
     ap.add_argument("--replicas", action="store_true", help="N independent replicas instead of EP")
     args = ap.parse_args()
