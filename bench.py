@@ -727,6 +727,57 @@ def offload_point(layers=32, tokens=8, repeats=5):
                sum(he.nbytes for lay in host for he in lay) / 1e9, 2), "build_s": round(build_s, 1),
            "timing": "host wall clock around `tokens` decode steps + synchronize, median of repeats"}
     out["simulator"] = simulator_calibration(trace, tokens / dt, h2d, int(stats["bytes"] / tokens))
+    del eng
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    # budgeted LRU in the pager (the reference cost model's cache_policy="lru"):
+    # 64 slots shared by the 32 layers (3.6 GB, a quarter of the 256 experts)
+    slots = 64
+    eng = offload.GpuPagerEngine(gates, host, HIDDEN, FFN, top_k=TOPK, top_n=TOPN, max_tokens=1, cache_slots=slots)
+    warm = 2
+    eng.start_trace()  # from the cold cache: the simulator replays the same history
+    for _ in range(warm):
+        x = eng.forward(x, normalize=True)
+    torch.cuda.synchronize()
+    h0 = eng.cache_stats()
+    t1 = time.perf_counter()
+    for _ in range(tokens):
+        x = eng.forward(x, normalize=True)
+    torch.cuda.synchronize()
+    dt_c = time.perf_counter() - t1
+    h1 = eng.cache_stats()
+    trace_c = eng.routing_trace()
+    hits, misses = h1[0] - h0[0], h1[1] - h0[1]
+    moved = misses * eng.block_bytes
+    out["lru_cache"] = {"slots": slots, "cache_gb": round(slots * eng.block_bytes / 1e9, 2),
+                        "tokens_s": round(tokens / dt_c, 3), "hit_rate": round(hits / max(1, hits + misses), 4),
+                        "host_bytes_per_token": int(moved / tokens),
+                        "h2d_achieved_gbs": round(moved / dt_c / 1e9, 2),
+                        "timing": f"{tokens} tokens after {warm} warm-up tokens from a cold cache"}
+    from paper_2512_17073_b200 import simulate as sim
+
+    hbm, _, tf_sust, _ = load_peaks()
+    dims = sim.ModelDims(hidden=HIDDEN, ffn=FFN, num_layers=layers, num_experts=E, top_k=TOPK)
+    plan = sim.TransferPlan(name="int2-n1-r32-lru64", expert_bits=BITS, top_n=TOPN, rank=RANK, factor_bits=3,
+                            cache_policy="lru", cache_budget_bytes=slots * sim.expert_weight_bytes(dims, BITS))
+    sysc = sim.b200_system(h2d, hbm, tf_sust)
+    # the timed tokens = the whole replay minus its first `warm` tokens (deterministic LRU state)
+    r_all = sim.simulate(trace_c, plan, sysc, dims, include_prefill=False, output_len=warm + tokens)
+    r_w = sim.simulate(trace_c, plan, sysc, dims, include_prefill=False, output_len=warm)
+    lookups_all = (warm + tokens) * layers * TOPK
+    hits_all = round(r_all.cache_hit_rate * lookups_all)
+    hits_w = round(r_w.cache_hit_rate * warm * layers * TOPK)
+    pred_tok_s = tokens / (r_all.decode_s - r_w.decode_s)
+    pred_hits = hits_all - hits_w
+    pred_bytes = r_all.total_bytes_moved - r_w.total_bytes_moved
+    out["lru_cache"]["simulator"] = {
+        "predicted_tok_s": round(pred_tok_s, 3), "predicted_hit_rate": round(pred_hits / (tokens * layers * TOPK), 4),
+        "measured_over_predicted": round((tokens / dt_c) / pred_tok_s, 4),
+        "predicted_tok_s_engine_bytes": round(pred_tok_s * pred_bytes / max(1, moved), 3),
+        "note": "same LRU decisions as the device (tests/test_offload.py asserts equal hit counts); "
+                "engine-bytes prediction scales by the simulator's codes-only bytes / the blocks moved"}
     del eng, host
     torch.cuda.empty_cache()
     return out

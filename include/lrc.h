@@ -196,6 +196,18 @@ lrc_status lrc_layer_set_prefill_min(lrc_layer* layer, int64_t min_tokens);
  * tiled decode kernels; no host synchronisation, graph-capturable. */
 lrc_status lrc_layer_set_pager(lrc_layer* layer, const void* const* host_blocks, const int64_t* offsets,
                                int64_t block_bytes, uint8_t* slots, int n_slots, int64_t slot_bytes);
+/* Budgeted LRU over the pager's slots, shared by every layer that uses the
+ * same slot pool (the reference cost model's cache_policy="lru",
+ * ref/simulate.py:127-167): a selected expert already resident in a slot moves
+ * nothing; a miss takes the least recently used slot not touched in the
+ * current step.  n_slots must equal the n_slots given to lrc_layer_set_pager;
+ * layer_key distinguishes the layers' experts.  Decisions are made on the
+ * device (no host round trip).  Stats = cumulative {hits, misses}. */
+typedef struct lrc_pager_cache lrc_pager_cache;
+lrc_status lrc_pager_cache_create(int n_slots, lrc_pager_cache** out);
+void lrc_pager_cache_destroy(lrc_pager_cache* cache);
+lrc_status lrc_pager_cache_stats(lrc_pager_cache* cache, int64_t* hits_misses);
+lrc_status lrc_layer_set_pager_cache(lrc_layer* layer, lrc_pager_cache* cache, int layer_key);
 int lrc_layer_prefill_eligible(const lrc_layer* layer);
 /* Batches of B <= max_tokens (at most 8) tokens run the tensor-core decode
  * engine when the layer is eligible (2- or 3-bit gs=64 weights, hidden and ffn

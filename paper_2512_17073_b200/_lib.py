@@ -75,6 +75,10 @@ _SIGS = {
     "lrc_layer_set_tcd_max": (c_int, [c_void_p, c_int]),
     "lrc_layer_tcd_eligible": (c_int, [c_void_p]),
     "lrc_layer_set_pager": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int, c_int64]),
+    "lrc_pager_cache_create": (c_int, [c_int, POINTER(c_void_p)]),
+    "lrc_pager_cache_destroy": (None, [c_void_p]),
+    "lrc_pager_cache_stats": (c_int, [c_void_p, POINTER(c_int64)]),
+    "lrc_layer_set_pager_cache": (c_int, [c_void_p, c_void_p, c_int]),
     "lrc_layer_phase_ms": (c_int, [c_void_p, POINTER(c_float)]),
     "lrc_debug_stamps": (c_int, [c_int, c_void_p, c_int]),
     "lrc_dense_expert_f64": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p,

@@ -311,14 +311,126 @@ struct PagerArgs {
   int64_t slot_bytes;
   lrc_expert* experts;  // device table
   PlanArgs plan;
+  // budgeted LRU over slots shared by every layer (lrc_pager_cache); null:
+  // slot a = active index a (no cross-step cache)
+  int64_t* owner;            // [n_cache] (layer key << 20 | expert) or -1
+  unsigned long long* stamp;  // [n_cache] last use: clock << 12 | order within the step
+  unsigned long long* clock;  // step counter
+  unsigned long long* stats;  // [2] hits, misses
+  int n_cache;
+  int layer_key;
+  int* slot_of;              // [E+S] per active index: its slot
+  int* miss;                 // [E+S] per active index: 1 = copy the block
 };
+
+// point expert e's descriptor and active record a at slot s
+__device__ void pager_repoint(const PagerArgs& g, int a, int e, int s) {
+  const uint8_t* base = g.slots + static_cast<int64_t>(s) * g.slot_bytes;
+  auto at = [&](int k) -> const uint8_t* { return g.off[k] >= 0 ? base + g.off[k] : nullptr; };
+  lrc_expert d = g.experts[e];
+  d.up_tiles = at(0);
+  d.down_tiles = at(1);
+  d.up_lr_tiles = at(2);
+  d.down_lr_tiles = at(3);
+  if (g.off[4] >= 0) {
+    d.v1.packed = at(4);
+    d.v1.scales = reinterpret_cast<const uint16_t*>(at(5));
+    d.v1.zeros = reinterpret_cast<const uint16_t*>(at(6));
+  }
+  if (g.off[7] >= 0) {
+    d.v3.packed = at(7);
+    d.v3.scales = reinterpret_cast<const uint16_t*>(at(8));
+    d.v3.zeros = reinterpret_cast<const uint16_t*>(at(9));
+  }
+  g.experts[e] = d;
+  if (g.plan.arec != nullptr) {
+    ActiveRec& R = g.plan.arec[a];
+    R.up_tiles = d.up_tiles;
+    R.down_tiles = d.down_tiles;
+    R.up_lr_tiles = d.up_lr_tiles;
+    R.down_lr_tiles = d.down_lr_tiles;
+  }
+}
+
+// LRU slot assignment for one layer step (one warp).  The step's experts are
+// looked up in the order of their first (token, rank) pair -- the reference
+// cost model's order (ref/simulate.py:219-227): a hit refreshes its slot; a
+// miss takes the least recently used slot not already touched in this step.
+__global__ void __launch_bounds__(32) pager_assign_kernel(const PagerArgs g) {
+  const int lane = threadIdx.x;
+  const int na = g.plan.counts[0];
+  const unsigned long long clk = *g.clock + 1;
+  // order of the active experts by their first pair (selection sort, na <= 64)
+  __shared__ int s_first[LRC_MAX_EXPERTS], s_order[LRC_MAX_EXPERTS];
+  for (int a = lane; a < na; a += 32) s_first[a] = g.plan.pair_list[g.plan.active_off[a]];
+  __syncwarp();
+  if (lane == 0) {
+    for (int i = 0; i < na; ++i) s_order[i] = i;
+    for (int i = 0; i < na; ++i)
+      for (int j = i + 1; j < na; ++j)
+        if (s_first[s_order[j]] < s_first[s_order[i]]) {
+          const int t = s_order[i];
+          s_order[i] = s_order[j];
+          s_order[j] = t;
+        }
+  }
+  __syncwarp();
+  unsigned long long hits = 0, misses = 0;
+  for (int i = 0; i < na; ++i) {
+    const int a = s_order[i], e = g.plan.active[a];
+    const int64_t key = (static_cast<int64_t>(g.layer_key) << 20) | e;
+    const unsigned long long now = (clk << 12) | static_cast<unsigned long long>(min(i, 4095));
+    int found = -1;
+    for (int s = lane; s < g.n_cache; s += 32)
+      if (g.owner[s] == key) found = s;
+    for (int o = 16; o > 0; o >>= 1) found = max(found, __shfl_xor_sync(0xffffffffu, found, o));
+    int slot = found;
+    if (slot < 0) {  // victim: min stamp among slots not touched this step (ties -> lower slot)
+      unsigned long long best = ~0ull;
+      int bs = 0x7fffffff;
+      for (int s = lane; s < g.n_cache; s += 32) {
+        const unsigned long long st = g.stamp[s];
+        if ((st >> 12) != clk && (st < best || (st == best && s < bs))) {
+          best = st;
+          bs = s;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+        if (ob < best || (ob == best && os < bs)) {
+          best = ob;
+          bs = os;
+        }
+      }
+      slot = bs;
+    }
+    if (lane == 0) {
+      g.owner[slot] = key;
+      g.stamp[slot] = now;
+      g.slot_of[a] = slot;
+      g.miss[a] = found < 0 ? 1 : 0;
+      pager_repoint(g, a, e, slot);
+    }
+    __syncwarp();
+    if (found < 0) ++misses;
+    else ++hits;
+  }
+  if (lane == 0) {
+    *g.clock = clk;
+    g.stats[0] += hits;
+    g.stats[1] += misses;
+  }
+}
 
 __global__ void __launch_bounds__(256) pager_kernel(const PagerArgs g) {
   const int a = blockIdx.y;
   if (a >= g.plan.counts[0]) return;
   const int e = g.plan.active[a];
+  if (g.owner != nullptr && !g.miss[a]) return;  // resident (cache hit): nothing moves
+  const int slot = g.owner != nullptr ? g.slot_of[a] : a;
   const uint4* src = reinterpret_cast<const uint4*>(g.host[e]);
-  uint4* dst = reinterpret_cast<uint4*>(g.slots + static_cast<int64_t>(a) * g.slot_bytes);
+  uint4* dst = reinterpret_cast<uint4*>(g.slots + static_cast<int64_t>(slot) * g.slot_bytes);
   const int64_t n = g.bytes / 16, stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   for (; i + 7 * stride < n; i += 8 * stride) {  // 8 loads in flight per thread (host-link latency)
@@ -329,33 +441,7 @@ __global__ void __launch_bounds__(256) pager_kernel(const PagerArgs g) {
     for (int u = 0; u < 8; ++u) __stcs(dst + i + u * stride, v[u]);
   }
   for (; i < n; i += stride) dst[i] = src[i];
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint8_t* base = g.slots + static_cast<int64_t>(a) * g.slot_bytes;
-    auto at = [&](int k) -> const uint8_t* { return g.off[k] >= 0 ? base + g.off[k] : nullptr; };
-    lrc_expert d = g.experts[e];
-    d.up_tiles = at(0);
-    d.down_tiles = at(1);
-    d.up_lr_tiles = at(2);
-    d.down_lr_tiles = at(3);
-    if (g.off[4] >= 0) {
-      d.v1.packed = at(4);
-      d.v1.scales = reinterpret_cast<const uint16_t*>(at(5));
-      d.v1.zeros = reinterpret_cast<const uint16_t*>(at(6));
-    }
-    if (g.off[7] >= 0) {
-      d.v3.packed = at(7);
-      d.v3.scales = reinterpret_cast<const uint16_t*>(at(8));
-      d.v3.zeros = reinterpret_cast<const uint16_t*>(at(9));
-    }
-    g.experts[e] = d;
-    if (g.plan.arec != nullptr) {
-      ActiveRec& R = g.plan.arec[a];
-      R.up_tiles = d.up_tiles;
-      R.down_tiles = d.down_tiles;
-      R.up_lr_tiles = d.up_lr_tiles;
-      R.down_lr_tiles = d.down_lr_tiles;
-    }
-  }
+  if (g.owner == nullptr && blockIdx.x == 0 && threadIdx.x == 0) pager_repoint(g, a, e, a);
 }
 }  // namespace lrc
 
@@ -382,6 +468,7 @@ struct lrc_layer {
   PagerArgs pg{};
   const uint8_t** pg_host = nullptr;  // device copy of the block pointers
   int pg_slots = 0;
+  int* pg_scratch = nullptr;  // [2][E+S] slot_of, miss (cache mode)
   int* plan_blk = nullptr;     // parallel plan: per-chunk histograms
   uint32_t* plan_cmask = nullptr;
   int* plan_ticket = nullptr;
@@ -632,6 +719,7 @@ extern "C" void lrc_layer_destroy(lrc_layer* L) {
   cudaFree(L->ws);
   cudaFree(L->lrp);
   cudaFree(L->pg_host);
+  cudaFree(L->pg_scratch);
   cudaFree(L->ppk);
   cudaFree(L->tcd_packs);
   cudaFree(L->d_tcd);
@@ -718,6 +806,67 @@ extern "C" lrc_status lrc_layer_set_pager(lrc_layer* L, const void* const* host_
   g.experts = L->d_experts;
   L->pg_slots = n_slots;
   L->pager = true;
+  return LRC_OK;
+}
+
+struct lrc_pager_cache {
+  int n = 0;
+  int64_t* owner = nullptr;
+  unsigned long long* stamp = nullptr;
+  unsigned long long* clock = nullptr;  // [0] clock, [1] hits, [2] misses
+};
+
+extern "C" lrc_status lrc_pager_cache_create(int n_slots, lrc_pager_cache** out) {
+  if (!out || n_slots <= 0) return fail(LRC_ERR_INVALID, "pager_cache_create: bad arguments");
+  auto* c = new lrc_pager_cache();
+  c->n = n_slots;
+  if (cudaMalloc(&c->owner, sizeof(int64_t) * n_slots) != cudaSuccess ||
+      cudaMalloc(&c->stamp, sizeof(unsigned long long) * n_slots) != cudaSuccess ||
+      cudaMalloc(&c->clock, sizeof(unsigned long long) * 3) != cudaSuccess) {
+    cudaFree(c->owner);
+    cudaFree(c->stamp);
+    delete c;
+    return fail(LRC_ERR_CUDA, "pager_cache_create: cudaMalloc");
+  }
+  cudaMemset(c->owner, 0xff, sizeof(int64_t) * n_slots);  // -1: empty
+  cudaMemset(c->stamp, 0, sizeof(unsigned long long) * n_slots);
+  cudaMemset(c->clock, 0, sizeof(unsigned long long) * 3);
+  *out = c;
+  return LRC_OK;
+}
+
+extern "C" void lrc_pager_cache_destroy(lrc_pager_cache* c) {
+  if (!c) return;
+  cudaFree(c->owner);
+  cudaFree(c->stamp);
+  cudaFree(c->clock);
+  delete c;
+}
+
+extern "C" lrc_status lrc_pager_cache_stats(lrc_pager_cache* c, int64_t* hits_misses) {
+  if (!c || !hits_misses) return fail(LRC_ERR_INVALID, "pager_cache_stats: null argument");
+  unsigned long long h[3];
+  LRC_CUDA_TRY(cudaMemcpy(h, c->clock, sizeof(h), cudaMemcpyDeviceToHost));
+  hits_misses[0] = static_cast<int64_t>(h[1]);
+  hits_misses[1] = static_cast<int64_t>(h[2]);
+  return LRC_OK;
+}
+
+extern "C" lrc_status lrc_layer_set_pager_cache(lrc_layer* L, lrc_pager_cache* c, int layer_key) {
+  if (!L || !c || layer_key < 0) return fail(LRC_ERR_INVALID, "set_pager_cache: bad arguments");
+  if (!L->pager) return fail(LRC_ERR_INVALID, "set_pager_cache: call lrc_layer_set_pager first");
+  if (c->n != L->pg_slots) return fail(LRC_ERR_INVALID, "set_pager_cache: cache size != the pager's slot count");
+  const int NE = L->E + L->S;
+  if (L->pg_scratch == nullptr) LRC_CUDA_TRY(cudaMalloc(&L->pg_scratch, sizeof(int) * 2 * NE));
+  PagerArgs& g = L->pg;
+  g.owner = c->owner;
+  g.stamp = c->stamp;
+  g.clock = c->clock;
+  g.stats = c->clock + 1;
+  g.n_cache = c->n;
+  g.layer_key = layer_key;
+  g.slot_of = L->pg_scratch;
+  g.miss = L->pg_scratch + NE;
   return LRC_OK;
 }
 
@@ -1021,7 +1170,13 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
   if (L->pager) {  // copy the active experts into their slots, repoint descriptors
     PagerArgs g = L->pg;
     g.plan = plan;
-    pager_kernel<<<dim3(static_cast<unsigned>(2 * L->num_sms), static_cast<unsigned>(L->pg_slots)), 256, 0, st>>>(g);
+    if (g.owner != nullptr) {
+      pager_assign_kernel<<<1, 32, 0, st>>>(g);
+      LRC_CHECK_LAUNCH();
+      ++launches;
+    }
+    const unsigned ny = static_cast<unsigned>(std::min(L->pg_slots, L->E + L->S));
+    pager_kernel<<<dim3(static_cast<unsigned>(2 * L->num_sms), ny), 256, 0, st>>>(g);
     LRC_CHECK_LAUNCH();
     ++launches;
   }

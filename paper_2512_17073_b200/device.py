@@ -173,6 +173,7 @@ class LRCMoELayer:
         self._prefill_min = None  # None: the library default (LRC_PREFILL_MIN or 128)
         self._tcd_max = None      # None: the library default (LRC_TCD_MAX or 8)
         self._pager = None        # lrc_layer_set_pager arguments (re-applied on re-create)
+        self._pager_cache = None  # (cache handle, layer key) for lrc_layer_set_pager_cache
         self._create()
 
     def _create(self):
@@ -191,6 +192,8 @@ class LRCMoELayer:
             _lib.check(lib.lrc_layer_set_tcd_max(h, int(self._tcd_max)))
         if self._pager is not None:
             _lib.check(lib.lrc_layer_set_pager(h, *self._pager))
+            if self._pager_cache is not None:
+                _lib.check(lib.lrc_layer_set_pager_cache(h, *self._pager_cache))
 
     def set_pager(self, host_blocks, offsets, block_bytes: int, slots_ptr: int, n_slots: int,
                   slot_bytes: int):
@@ -199,6 +202,12 @@ class LRCMoELayer:
                        int(slot_bytes))
         _lib.check(_lib.lib().lrc_layer_set_pager(self._handle, *self._pager))
 
+
+    def set_pager_cache(self, cache_handle, layer_key: int):
+        """Budgeted LRU over the pager's slots shared across layers
+        (lrc_layer_set_pager_cache); kept across workspace re-creates."""
+        self._pager_cache = (ctypes.c_void_p(cache_handle), int(layer_key))
+        _lib.check(_lib.lib().lrc_layer_set_pager_cache(self._handle, *self._pager_cache))
     def set_tcd_max(self, max_tokens: int):
         """Batches of <= max_tokens (<= 8) run the tensor-core decode engine when
         eligible; 0 disables it."""

@@ -254,17 +254,29 @@ class GpuPagerEngine(OffloadEngine):
     at fixed offsets); each layer forward copies its active experts into slots
     inside the stream (SM loads over the host link) and repoints their
     descriptors -- no host round trip per layer, so a token's whole layer chain
-    is asynchronous and graph-capturable.  No cross-token cache: slot a holds
-    the a-th active expert of the current step (the C3 "cache budget 0" case).
+    is asynchronous and graph-capturable.  Default: no cross-token cache, slot
+    a holds the a-th active expert of the current step (the C3 "cache budget
+    0" case).  ``cache_slots`` > 0: a budgeted LRU over that many slots shared
+    by all layers, decided on the device (``lrc_pager_cache``; hits move
+    nothing) -- the reference cost model's cache_policy="lru".
     """
 
-    def __init__(self, gates, experts, hidden: int, ffn: int, top_k: int, top_n: int, max_tokens: int = 1):
+    def __init__(self, gates, experts, hidden: int, ffn: int, top_k: int, top_n: int, max_tokens: int = 1,
+                 cache_slots: int = 0):
         torch = _lib.device_required()
         self.hidden, self.ffn, self.k, self.n = hidden, ffn, top_k, top_n
         self.E = len(experts[0])
         self.host = experts
         self.keep = _Keep()
         n_slots = min(self.E, max_tokens * max(top_k, 1))
+        self.cache = None
+        if cache_slots:
+            if cache_slots < n_slots:
+                raise ValueError(f"cache_slots must hold one step's experts (>= {n_slots})")
+            n_slots = int(cache_slots)
+            h = ctypes.c_void_p()
+            _lib.check(_lib.lib().lrc_pager_cache_create(n_slots, ctypes.byref(h)))
+            self.cache = h
         size = {n: max(int(he.bufs[n].numel()) for lay in experts for he in lay) for n in NAMES}
         self.offsets, o = {}, 0
         for n in NAMES:
@@ -300,6 +312,8 @@ class GpuPagerEngine(OffloadEngine):
             dl.set_tcd_max(0)
             ptrs = (ctypes.c_void_p * self.E)(*[b.data_ptr() for b in self.blocks[l]])
             dl.set_pager(ptrs, offs, self.block_bytes, self.slot_mem.data_ptr(), n_slots, self.block_bytes)
+            if self.cache is not None:
+                dl.set_pager_cache(self.cache.value, l)
             self.layers.append(dl)
 
     def forward_layer(self, layer: int, x):
@@ -308,6 +322,22 @@ class GpuPagerEngine(OffloadEngine):
         if self._trace is not None:  # device copies only; read back by routing_trace()
             self._trace.append((layer, idx.clone(), w.clone()))
         return y
+
+    def cache_stats(self):
+        """Cumulative (hits, misses) of the budgeted cache (None without one)."""
+        if self.cache is None:
+            return None
+        hm = (ctypes.c_int64 * 2)()
+        _lib.check(_lib.lib().lrc_pager_cache_stats(self.cache, hm))
+        return int(hm[0]), int(hm[1])
+
+    def __del__(self):
+        if getattr(self, "cache", None) is not None:
+            try:
+                _lib.lib().lrc_pager_cache_destroy(self.cache)
+            except Exception:
+                pass
+            self.cache = None
 
     def start_trace(self):
         """Record the routing of every following layer step."""

@@ -114,3 +114,36 @@ def test_gpu_pager_graph_capture():
     g.replay()
     torch.cuda.synchronize()
     assert float((out.float() - eager).norm() / eager.norm()) < 1e-6
+
+
+@pytest.mark.gpu
+def test_gpu_pager_lru_cache_matches_resident_and_simulator():
+    """Budgeted LRU in the GPU pager (lrc_pager_cache, 5 slots shared by 2
+    layers x 8 experts): every step matches the resident layers, resident hits
+    move nothing, and the device's hit / miss counts equal the reference cost
+    model's LRU (simulate.py, cache_policy="lru") on the recorded trace."""
+    from paper_2512_17073_b200 import simulate as sim
+
+    hidden, ffn, E, L = 512, 1024, 8, 2
+    layers = [SynthLayer(hidden, ffn, E, top_k=2, rank=16, seed=70 + l, max_tokens=8, router_skew=2.5)
+              for l in range(L)]
+    eng = offload.GpuPagerEngine([sl.gate for sl in layers], [offload.host_experts_from_synth(sl) for sl in layers],
+                                 hidden, ffn, top_k=2, top_n=1, max_tokens=1, cache_slots=5)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    eng.start_trace()
+    for step in range(24):
+        x = torch.randn((1, hidden), device="cuda", generator=gen).to(torch.bfloat16)
+        y = eng.forward(x)
+        ref = x
+        for sl in layers:
+            ref = sl.layer.forward(ref, 2, 1)[0].to(torch.bfloat16)
+        torch.cuda.synchronize()
+        assert float((y.float() - ref.float()).norm() / ref.float().norm()) < 1e-2, step
+    hits, misses = eng.cache_stats()
+    assert hits + misses == 24 * L * 2 and hits > 0
+    trace = eng.routing_trace()
+    dims = sim.ModelDims(hidden, ffn, L, E, 2)
+    plan = sim.TransferPlan(expert_bits=2, top_n=1, rank=16, cache_policy="lru",
+                            cache_budget_bytes=5 * sim.expert_weight_bytes(dims, 2))
+    rep = sim.simulate(trace, plan, sim.SYSTEM_PRESETS["gpu-only"], dims, include_prefill=False)
+    assert abs(rep.cache_hit_rate - hits / (hits + misses)) < 1e-12, (rep.cache_hit_rate, hits, misses)
