@@ -463,3 +463,42 @@ def test_lowrank_api(torch):
         np.testing.assert_allclose(s, G[f"svd{i}_s"], rtol=1e-6)
     c = lowrank.build_compensator(w, qm, 8)
     assert c.u.bits == 3 and c.u.shape == (24, 8) and c.v.shape == (8, 36)
+
+
+@pytest.fixture(scope="module")
+def c1_setup():
+    """C1 (BASELINE configs[0]): the reference's tiny model and its compressed
+    artifacts, rebuilt by the oracle -- bit-exact with the reference's own
+    compress_model (every record's SHA in c1.json is checked here)."""
+    import hashlib
+    import json
+
+    c1 = json.load(open(os.path.join(HERE, "golden", "c1.json")))
+    layers = lrc.gen_model(0, 512, 1024, 1, 8, router_skew=1.4)
+    st = lrc.compress(layers, bits=2, group_size=64, hqq_iters=20, rank=16, factor_bits=3, seed=0)
+
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+
+    for (l, e, p), rec in st.records.items():
+        r = c1["records"][f"{e}_{p}"]
+        assert sha(rec.qm.codes) == r["codes"] and sha(rec.comp.u.codes) == r["u_codes"], (e, p)
+    return c1, layers, st
+
+
+@pytest.mark.parametrize("mode", ["compensated", "quantized"])
+def test_c1_gpu_forward_vs_reference_outputs(torch, c1_setup, mode):
+    """The GPU path (moe.forward -> lrc_route + lrc_layer_forward_pairs) on the
+    reference's own C1 artifacts against the REFERENCE's outputs in c1.json
+    (ref/moe.py:217-259 run in the build container): routes identical, layer
+    outputs within 1e-2 relative L2 (bf16 tokens / fp16 metadata on the device)."""
+    from paper_2512_17073_b200 import moe
+
+    c1, layers, st = c1_setup
+    ml = moe.MoELayer(gate=layers[0].gate, experts=[moe.Expert(*e) for e in layers[0].experts])
+    cfg = moe.ForwardConfig(top_k=2, top_n=1)
+    for t, x in enumerate(lrc.gen_tokens(1, 512, 4)):
+        assert moe.route(x, ml, cfg).selected == c1["routes"][t]
+        y = moe.forward(x, ml, cfg, mode, st, 0)
+        want = np.asarray(c1[f"y_{mode}"][t])
+        assert rel_l2(y, want) <= TOL_Y, (t, rel_l2(y, want))
