@@ -1547,7 +1547,10 @@ __device__ __noinline__ void role_aux(const Args& A, Shared& S) {
   aux_phase_d(A, S);
 }
 
-template <int BITS>
+// ONE: the single-token specialisation (resident B operand, N = 8) -- a
+// separate instantiation so each kernel carries one set of role loops (the
+// code is one-shot per launch: its size is instruction-fetch latency)
+template <int BITS, bool ONE>
 __global__ void __launch_bounds__(kThreads, 1) tcd_kernel(const __grid_constant__ Args A) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ Shared S;
@@ -1641,15 +1644,12 @@ __global__ void __launch_bounds__(kThreads, 1) tcd_kernel(const __grid_constant_
   if (warp == kProdWarp) {
     role_producer<BITS>(A, S);
   } else if (warp == kMmaWarp) {
-    if (S.res) role_mma<true>(A, S, S.bop_off);
-    else role_mma<false>(A, S, S.bop_off);
+    role_mma<ONE>(A, S, S.bop_off);
     stamp(A, 7);
   } else if (warp < kDec) {
-    if (S.res) role_decode<BITS, true>(A, S);
-    else role_decode<BITS, false>(A, S);
+    role_decode<BITS, ONE>(A, S);
   } else if (warp < kEpi0 + kNEpi) {
-    if (S.res) role_epilogue<BITS, true>(A, S);
-    else role_epilogue<BITS, false>(A, S);
+    role_epilogue<BITS, ONE>(A, S);
   } else {
     role_aux(A, S);
   }
@@ -1806,17 +1806,17 @@ bool eligible(const lrc_expert* experts, int n, int hidden, int ffn, int* bits, 
   return true;
 }
 
-template <int BITS>
+template <int BITS, bool ONE>
 static lrc_status launch_t(const Args& a, int num_sms, cudaStream_t st, bool pdl) {
   static int smem = 0;
   if (smem == 0) {  // dynamic shared memory: everything the static state leaves
     cudaFuncAttributes fa{};
-    LRC_CUDA_TRY(cudaFuncGetAttributes(&fa, tcd_kernel<BITS>));
+    LRC_CUDA_TRY(cudaFuncGetAttributes(&fa, tcd_kernel<BITS, ONE>));
     int dev = 0, optin = 0;
     LRC_CUDA_TRY(cudaGetDevice(&dev));
     LRC_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     smem = (optin - static_cast<int>(fa.sharedSizeBytes) - 1024) & ~1023;
-    LRC_CUDA_TRY(cudaFuncSetAttribute(tcd_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    LRC_CUDA_TRY(cudaFuncSetAttribute(tcd_kernel<BITS, ONE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(num_sms);
@@ -1828,13 +1828,15 @@ static lrc_status launch_t(const Args& a, int num_sms, cudaStream_t st, bool pdl
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  LRC_CUDA_TRY(cudaLaunchKernelEx(&cfg, tcd_kernel<BITS>, a));
+  LRC_CUDA_TRY(cudaLaunchKernelEx(&cfg, tcd_kernel<BITS, ONE>, a));
   return LRC_OK;
 }
 
 lrc_status launch(const Args& a, int num_sms, cudaStream_t st, bool pdl) {
   if (a.B < 1 || a.B > kMaxTok) return fail(LRC_ERR_UNSUPPORTED, "tcd: 1..8 tokens");
-  return a.bits == 2 ? launch_t<2>(a, num_sms, st, pdl) : launch_t<3>(a, num_sms, st, pdl);
+  // (the resident-B single-token layout is chosen on the device from A.B == 1)
+  if (a.B == 1) return a.bits == 2 ? launch_t<2, true>(a, num_sms, st, pdl) : launch_t<3, true>(a, num_sms, st, pdl);
+  return a.bits == 2 ? launch_t<2, false>(a, num_sms, st, pdl) : launch_t<3, false>(a, num_sms, st, pdl);
 }
 
 void set_wait_mode(int) {}
