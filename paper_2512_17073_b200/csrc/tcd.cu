@@ -707,10 +707,19 @@ __device__ __noinline__ void build_plan(const Args& A, Shared& S) {
     const long long G0 = H / 64, T0 = F / 128, G1 = F / 64, T1 = H / 128;
     const long long tot0 = static_cast<long long>(P.n_act) * T0 * G0, tot1 = static_cast<long long>(P.n_act) * T1 * G1;
     const long long c = blockIdx.x, ncta = gridDim.x;
-    P.lo[0] = c * tot0 / ncta;
-    P.hi[0] = (c + 1) * tot0 / ncta;
-    P.lo[1] = c * tot1 / ncta;
-    P.hi[1] = (c + 1) * tot1 / ncta;
+    if ((ncta + 1) * (tot0 > tot1 ? tot0 : tot1) < (1ll << 32)) {  // 32-bit divisions (the common case)
+      const unsigned cu = static_cast<unsigned>(c), nu = static_cast<unsigned>(ncta);
+      const unsigned t0u = static_cast<unsigned>(tot0), t1u = static_cast<unsigned>(tot1);
+      P.lo[0] = cu * t0u / nu;
+      P.hi[0] = (cu + 1) * t0u / nu;
+      P.lo[1] = cu * t1u / nu;
+      P.hi[1] = (cu + 1) * t1u / nu;
+    } else {
+      P.lo[0] = c * tot0 / ncta;
+      P.hi[0] = (c + 1) * tot0 / ncta;
+      P.lo[1] = c * tot1 / ncta;
+      P.hi[1] = (c + 1) * tot1 / ncta;
+    }
     // stage layout: [codes + meta of <= gps groups x 2 matrices][B operand: per
     // group NT x 512-byte digit images][per token x group: {2^-S, sum}]
     // B operand rows: 8 per token (digits in rows 0..2), N = 8 NT
@@ -795,13 +804,21 @@ __device__ __noinline__ void build_stages(const Args& A, Shared& S) {
           }
         }
         const int at = base + pre - n, gat = gbase + gpre - (g1 - g0);
-        for (int k = 0; k < n && at + k < kMaxStages; ++k) {
-          const int g = g0 + k * gps, ns = min(gps, g1 - g);
-          const int segend = g + ns == g1 ? 1 : 0;
-          S.stab[at + k] = make_int2(g | ((tl % T) << 16), (tl / T) | (ph << 8) | (ns << 9) | (segend << 13) |
-                                                             ((g1 - g0) << 16));
-          // resident-B image index: U = the group's K index; D = position in this CTA's D groups
-          S.doff[at + k] = static_cast<uint16_t>(ph == 0 ? g : gat + k * gps);
+        // the tile parts one after another (a CTA has 1-3 per phase), each
+        // part's stages written by the lanes in parallel
+        for (unsigned m = __ballot_sync(0xffffffffu, n > 0); m; m &= m - 1) {
+          const int j = __ffs(m) - 1;
+          const int nj = __shfl_sync(0xffffffffu, n, j), g0j = __shfl_sync(0xffffffffu, g0, j);
+          const int g1j = __shfl_sync(0xffffffffu, g1, j), atj = __shfl_sync(0xffffffffu, at, j);
+          const int gatj = __shfl_sync(0xffffffffu, gat, j), tlj = tp0 + j;
+          const int hi_word = (tlj / T) | (ph << 8) | ((g1j - g0j) << 16), lo_word = (tlj % T) << 16;
+          for (int k = lane; k < nj && atj + k < kMaxStages; k += 32) {
+            const int g = g0j + k * gps, ns = min(gps, g1j - g);
+            const int segend = g + ns == g1j ? 1 : 0;
+            S.stab[atj + k] = make_int2(g | lo_word, hi_word | (ns << 9) | (segend << 13));
+            // resident-B image index: U = the group's K index; D = position in this CTA's D groups
+            S.doff[atj + k] = static_cast<uint16_t>(ph == 0 ? g : gatj + k * gps);
+          }
         }
         base += __shfl_sync(0xffffffffu, pre, 31);
         gbase += __shfl_sync(0xffffffffu, gpre, 31);
