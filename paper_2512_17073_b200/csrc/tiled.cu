@@ -4,18 +4,24 @@
 // 128-column group pairs.  Block (tile t, group-pair q, matrix i) is 640 B:
 //   [0,512)   codes: lane l holds 16 B = 4 words {A(g0), B(g0), A(g1), B(g1)}
 //             A = row t*16+gid, B = row t*16+gid+8 (gid = l>>2, tid = l&3);
-//             code (ks, p, e) of a word sits at bit 16e + 2(2ks+p) and is the
-//             weight at column g*64 + ks*16 + p*8 + tid*2 + e.
+//             code (m, h, b) of a word sits at bit 8b + 2(2m+h) and is the
+//             weight at column g*64 + 32m + 16h + 4tid + b -- the
+//             mma.m16n8k32 A-fragment order, so (w >> 2j) & 0x03030303 is
+//             one u8 operand register (4 codes).
 //   [512,640) fp16 scale/zero: 16 B per gid {s,z}(A,g0) {s,z}(A,g1) {s,z}(B,g0) {s,z}(B,g1)
 // Blocks are ordered (t, q, i), so one row tile over a K range is one contiguous
 // byte range -> one cp.async.bulk per work item.  The codes are exactly the
 // reference's (lrc_tiles_unpack inverts the layout bit-exactly).
 //
-// In-register unpack: (w >> sh) & (3 << pos) | 0x43004300 yields two bf16
-// values 128 + 2^pos * c, which feed mma.sync m16n8k16 directly.  The 2^pos
-// multiplier is folded into the activation operand (x' = x / 2^pos, exact in
-// bf16) and the +128 bias into the fp32 accumulator seed (C = -128 * sum x').
-// Per group:  y += s * (sum c x) + z * sum x   (fp32, ref/quant.py:216-224).
+// Core: mma.sync m16n8k32 u8 x s8 -> s32.  The activation operand is each
+// token's 64-column group as a 14-bit integer X = rint(x 2^S) (S per group and
+// token: |X| < 2^13), split into two signed 7-bit digits X = 128 d0 + d1 that
+// sit in adjacent N columns (one MMA covers 4 tokens); a lane's accumulator
+// pair is then {sum c d0, sum c d1} of one token, and 128 d0 + d1 lands
+// directly in a float's mantissa (seeded magic 1.5 * 2^23).
+// Per group:  y += s * 2^-S (sum c X) + z * sum x   (fp32, ref/quant.py:216-224).
+// The x rounding is relative 2^-14 of the group's largest |x| (below the bf16
+// rounding of the layer's own activations).
 #include <algorithm>
 #include <cstdlib>
 
@@ -56,13 +62,13 @@ __global__ void build_tiles_kernel(lrc_qmat m0, lrc_qmat m1, int ni, int64_t RT,
     for (int rs = 0; rs < 2; ++rs) {
       const int64_t r = t * 16 + gid + 8 * rs;
       uint32_t word = 0;
-      for (int ks = 0; ks < 4; ++ks)
-        for (int p = 0; p < 2; ++p)
-          for (int e = 0; e < 2; ++e) {
-            const int64_t k = (2 * q + h) * 64 + ks * 16 + p * 8 + tid * 2 + e;
+      for (int mm = 0; mm < 2; ++mm)
+        for (int hh = 0; hh < 2; ++hh)
+          for (int b = 0; b < 4; ++b) {
+            const int64_t k = (2 * q + h) * 64 + mm * 32 + hh * 16 + tid * 4 + b;
             uint32_t c = 0;
             if (r < m.rows && k < m.cols) c = read_code(m.packed, r * m.cols + k, m.bits, nbytes);
-            word |= c << (16 * e + 2 * (2 * ks + p));
+            word |= c << (8 * b + 2 * (2 * mm + hh));
           }
       w[h * 2 + rs] = word;
     }
@@ -104,11 +110,11 @@ __global__ void tiles_unpack_kernel(const uint8_t* __restrict__ tiles, int64_t r
   const int rr = static_cast<int>(r % 16), gid = rr & 7, rs = rr >> 3;
   const int64_t g = k / 64, q = g / 2;
   const int h = static_cast<int>(g & 1), w = static_cast<int>(k % 64);
-  const int ks = w / 16, p = (w % 16) / 8, tid = (w % 8) / 2, e = w % 2;
+  const int mm = w / 32, hh = (w % 32) / 16, tid = (w % 16) / 4, bb = w % 4;
   const int lane = gid * 4 + tid;
   const uint8_t* b = tiles + ((t * GP + q) * ni + which) * kBlk;
   const uint32_t word = reinterpret_cast<const uint32_t*>(b + lane * 16)[h * 2 + rs];
-  out[idx] = static_cast<uint8_t>((word >> (16 * e + 2 * (2 * ks + p))) & 3u);
+  out[idx] = static_cast<uint8_t>((word >> (8 * bb + 2 * (2 * mm + hh))) & 3u);
 }
 
 // -------------------------------------------------------- PTX primitives ---
@@ -173,27 +179,15 @@ __device__ __forceinline__ uint2 lds64(const void* p) {
   asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(smem_u32(p)));
   return v;
 }
-__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
-                                         uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+// D += A (u8, 16x32) . B (s8, 32x8), s32 accumulators
+__device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-
-// code slot j = 2*ks + p of a word -> bf16x2 {128 + m*c_lo, 128 + m*c_hi},
-// m = 1,4,16,1,4,16,1,4 for j = 0..7
-template <int J>
-__device__ __forceinline__ uint32_t unpack_j(uint32_t w) {
-  constexpr int sh = (J < 3) ? 0 : ((J < 6) ? 6 : 12);
-  constexpr int pos = 2 * (J - ((J < 3) ? 0 : ((J < 6) ? 3 : 6)));
-  return ((w >> sh) & (0x00030003u << pos)) | 0x43004300u;
-}
-__device__ __forceinline__ float inv_mult(int j) {
-  // 1 / m for slot j
-  return (j % 3 == 0) ? 1.0f : ((j % 3 == 1) ? 0.25f : 0.0625f);
-}
+constexpr int kMagicBits = 0x4B400000;   // 1.5 * 2^23: integer v added to its bits reads as 1.5*2^23 + v
+constexpr float kMagic = 12582912.0f;
 
 // ------------------------------------------------------------- LR tiles ---
 // Stream of a 16-row tile of factor rows: element (rr, j) at index rr*r + j
@@ -298,9 +292,9 @@ struct TiledParams {
   int stage_bytes;      // weight bytes per stage
   int lr_slot;          // low-rank tile bytes per stage (max over experts; 0 = none)
   int nstage;
-  int xs_stride;        // bf16 elements per x' row
-  int xs_rows;          // x' rows held in shared memory (<= 8*NT)
-  int prebuilt;         // UP with B <= 8*NT: x' rows = tokens, built before the grid-dependency wait
+  int xs_stride;        // bytes per x-digit row (stride % 128 == 32: conflict-free B-fragment loads)
+  int xs_rows;          // x-digit rows held in shared memory (<= TPP)
+  int prebuilt;         // UP with B <= TPP: digit rows = tokens, built before the grid-dependency wait
   int debug;            // LRC_TILED_DEBUG: bit0 skip MMA core, bit1 skip epilogue math
 };
 
@@ -313,13 +307,21 @@ struct SmemMap {
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
-template <int NI, int NT>
+// NQ token quads per pass: TPP = 4 NQ tokens, partials in NT = ceil(TPP / 8)
+// 16x8 tiles (token n -> tile n / 8, column n % 8)
+template <int NQ>
+struct Tpp {
+  static constexpr int TPP = 4 * NQ;
+  static constexpr int NT = (TPP + 7) / 8;
+};
+
+template <int NI, int NQ>
 __host__ __device__ inline SmemMap smem_map(const TiledParams& p) {
-  constexpr int TPP = 8 * NT;
+  constexpr int TPP = Tpp<NQ>::TPP, NT = Tpp<NQ>::NT;
   SmemMap m;
   int o = p.nstage * (p.stage_bytes + p.lr_slot);
   m.xs = o;
-  o = align16(o + p.xs_rows * p.xs_stride * 2);
+  o = align16(o + p.xs_rows * p.xs_stride);
   m.sums = o;
   o = align16(o + p.SPC * kSpanGP * 2 * TPP * 8);
   m.red = o;
@@ -356,13 +358,6 @@ __device__ __forceinline__ uint32_t smem_code(const uint32_t* w, int bit, uint32
   return __funnelshift_r(w[bit >> 5], w[(bit >> 5) + 1], bit & 31) & mask;
 }
 
-// (w & m) | 0x43004300 in ONE lop3 (nvcc otherwise splits it: one immediate per LOP3)
-__device__ __forceinline__ uint32_t lop_and_or(uint32_t w, uint32_t m) {
-  uint32_t r;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "r"(m), "r"(0x43004300u));
-  return r;
-}
-
 // (w & m) | c in one lop3
 __device__ __forceinline__ uint32_t lop3_and_or(uint32_t w, uint32_t m, uint32_t c) {
   uint32_t r;
@@ -385,83 +380,95 @@ struct EpiPass {
   LrLayout L;
 };
 
-// does pass `pass` (TPP = 8 * tpp8 pairs) hold a compensated pair? (ActiveRec::cmask)
-__device__ __forceinline__ bool pass_has_comp(uint32_t m, int pass, int tpp8) {
+// does pass `pass` (pairs [pass TPP, pass TPP + TPP)) hold a compensated pair?
+// (ActiveRec::cmask bit q: pairs [8q, 8q + 8))
+__device__ __forceinline__ bool pass_has_comp(uint32_t m, int pass, int tpp) {
   bool c = false;
-  for (int q = pass * tpp8; q < (pass + 1) * tpp8; ++q) c |= ((m >> min(q, 31)) & 1u) != 0;
+  for (int q = (pass * tpp) >> 3; q <= ((pass + 1) * tpp - 1) >> 3; ++q) c |= ((m >> min(q, 31)) & 1u) != 0;
   return c;
 }
 
 
-// x' rows (x / m per 8-column slot, bf16, in the permuted B-fragment order) and
-// per-(group, row) sums (X, -128 X') for `nrows` rows over columns
-// [k0, k0 + 64 ng) of the chunk.  Row n reads x row rowsrc[n] (token, UP) or
-// a16 row rowsrc[n] (pair, DOWN); rowsrc == nullptr: row n is token n.  One
-// 16-byte load per thread-task, two tasks in flight per thread; the 8 lanes of
-// a (row, group) reduce its sums by shuffles (nthr is a multiple of 32).
-template <bool UP, int NT>
-__device__ __forceinline__ void build_xprime(const ExpertArgs& A, const TiledParams& P, uint16_t* xs,
-                                             float2* sums, const int* rowsrc, int nrows, int k0, int ng,
-                                             int t0, int nthr) {
-  constexpr int TPP = 8 * NT;
-      // one 16-byte x load per thread-task (8 columns), two tasks in flight per
-      // thread; the 8 lanes of a (token, group) reduce its sums by shuffles
-      const int ntask = nrows * ng * 8;
-      for (int base = 0; base < ntask; base += 2 * nthr) {
-        uint4 raw[2];
-        int tn[2], tg[2];
-        bool ok[2];
-        const int c8 = t0 & 7;  // == task & 7 (base is a multiple of 8)
+// x-digit rows and per-(group, row) {2^-S, sum x} for `nrows` rows over
+// columns [k0, k0 + 64 ng) of the chunk.  Row n reads x row rowsrc[n] (token,
+// UP) or a16 row rowsrc[n] (pair, DOWN); rowsrc == nullptr: row n is token n.
+// Group gl of a row is 128 bytes: digit d (0: high, 1: low) of column
+// kk = 32m + 16h + 4t + b at byte 64d + 8(4m + t) + 4h + b (the m16n8k32
+// B-fragment order: lane (t, column) loads 8 bytes per m).  One 16-byte load
+// per thread-task (8 columns), two tasks in flight per thread; the 8 lanes of
+// a (row, group) reduce its max |x| and sum by shuffles (nthr % 32 == 0).
+template <bool UP, int TPP>
+__device__ __forceinline__ void build_xdigits(const ExpertArgs& A, const TiledParams& P, uint8_t* xs,
+                                              float2* sums, const int* rowsrc, int nrows, int k0, int ng,
+                                              int t0, int nthr) {
+  const int ntask = nrows * ng * 8;
+  const int c8 = t0 & 7;  // == task & 7 (base is a multiple of 8)
+  // byte offset of columns 8 c8 .. 8 c8 + 3 within a digit half (+8 for the next 4)
+  const int off = ((c8 >> 2) * 4 + 2 * (c8 & 1)) * 8 + ((c8 >> 1) & 1) * 4;
+  for (int base = 0; base < ntask; base += 2 * nthr) {
+    uint4 raw[2];
+    int tn[2], tg[2];
+    bool ok[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int task = base + u * nthr + t0;
-          ok[u] = task < ntask;
-          const int ng8 = ok[u] ? (task >> 3) : 0;
-          tn[u] = ng8 / ng;
-          tg[u] = ng8 - tn[u] * ng;
-          raw[u] = make_uint4(0u, 0u, 0u, 0u);
-          if (ok[u]) {
-            const int src = rowsrc ? rowsrc[tn[u]] : tn[u];
-            const uint16_t* row = UP ? A.x + static_cast<int64_t>(src) * A.hidden
-                                     : A.a16 + static_cast<int64_t>(src) * A.ffn;
-            const int kk = k0 + tg[u] * 64 + c8 * 8;
-            if (kk + 8 <= P.K && (reinterpret_cast<uintptr_t>(row + kk) & 15) == 0) {
-              raw[u] = __ldg(reinterpret_cast<const uint4*>(row + kk));
-            } else {
-              uint16_t h[8];
+    for (int u = 0; u < 2; ++u) {
+      const int task = base + u * nthr + t0;
+      ok[u] = task < ntask;
+      const int ng8 = ok[u] ? (task >> 3) : 0;
+      tn[u] = ng8 / ng;
+      tg[u] = ng8 - tn[u] * ng;
+      raw[u] = make_uint4(0u, 0u, 0u, 0u);
+      if (ok[u]) {
+        const int src = rowsrc ? rowsrc[tn[u]] : tn[u];
+        const uint16_t* row = UP ? A.x + static_cast<int64_t>(src) * A.hidden
+                                 : A.a16 + static_cast<int64_t>(src) * A.ffn;
+        const int kk = k0 + tg[u] * 64 + c8 * 8;
+        if (kk + 8 <= P.K && (reinterpret_cast<uintptr_t>(row + kk) & 15) == 0) {
+          raw[u] = __ldg(reinterpret_cast<const uint4*>(row + kk));
+        } else {
+          uint16_t h[8];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) h[j] = (kk + j < P.K) ? row[kk + j] : 0;
-              raw[u] = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16),
-                                  h[4] | (uint32_t(h[5]) << 16), h[6] | (uint32_t(h[7]) << 16));
-            }
-          }
-        }
-        const float im = inv_mult(c8);  // slot j = c8 for columns c8*8 .. c8*8+7
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          float xsum = 0.f, xpsum = 0.f;
-          if (ok[u]) {
-            uint32_t* dst = reinterpret_cast<uint32_t*>(xs + tn[u] * P.xs_stride + tg[u] * 64);
-            const uint32_t w4[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
-            // column c8*8 + 2*tj + e -> 16-block c8/2, position tj*4 + (c8&1)*2 + e
-#pragma unroll
-            for (int tj = 0; tj < 4; ++tj) {
-              const float lo = bf2f(w4[tj] & 0xffff), hi = bf2f(w4[tj] >> 16);
-              xsum += lo + hi;
-              const float plo = lo * im, phi = hi * im;
-              xpsum += plo + phi;
-              dst[((c8 >> 1) * 16 + tj * 4 + (c8 & 1) * 2) >> 1] =
-                  static_cast<uint32_t>(f2bf(plo)) | (static_cast<uint32_t>(f2bf(phi)) << 16);
-            }
-          }
-#pragma unroll
-          for (int o = 1; o < 8; o <<= 1) {
-            xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
-            xpsum += __shfl_xor_sync(0xffffffffu, xpsum, o);
-          }
-          if (ok[u] && c8 == 0) sums[tg[u] * TPP + tn[u]] = make_float2(xsum, -128.0f * xpsum);
+          for (int j = 0; j < 8; ++j) h[j] = (kk + j < P.K) ? row[kk + j] : 0;
+          raw[u] = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16),
+                              h[4] | (uint32_t(h[5]) << 16), h[6] | (uint32_t(h[7]) << 16));
         }
       }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t w4[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
+      float xv[8];
+      float xsum = 0.f, amax = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        xv[j] = bf2f((j & 1) ? (w4[j >> 1] >> 16) : (w4[j >> 1] & 0xffff));
+        xsum += xv[j];
+        amax = fmaxf(amax, fabsf(xv[j]));
+      }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      }
+      // amax < 2^(E - 126) for exponent field E: S = 139 - E puts |x| 2^S < 2^13
+      const int S = min(139 - static_cast<int>((__float_as_uint(amax) >> 23) & 255u), 126);
+      const float sc = __uint_as_float(static_cast<uint32_t>(S + 127) << 23);
+      if (ok[u]) {
+        uint32_t d0w[2] = {0u, 0u}, d1w[2] = {0u, 0u};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int X = __float2int_rn(xv[j] * sc);  // exact scaling, |X| <= 2^13
+          d0w[j >> 2] |= (static_cast<uint32_t>(X >> 7) & 0xffu) << (8 * (j & 3));
+          d1w[j >> 2] |= (static_cast<uint32_t>(X) & 0x7fu) << (8 * (j & 3));
+        }
+        uint8_t* g = xs + tn[u] * P.xs_stride + tg[u] * 128 + off;
+        *reinterpret_cast<uint32_t*>(g) = d0w[0];
+        *reinterpret_cast<uint32_t*>(g + 8) = d0w[1];
+        *reinterpret_cast<uint32_t*>(g + 64) = d1w[0];
+        *reinterpret_cast<uint32_t*>(g + 72) = d1w[1];
+        if (c8 == 0) sums[tg[u] * TPP + tn[u]] = make_float2(__uint_as_float(static_cast<uint32_t>(127 - S) << 23), xsum);
+      }
+    }
+  }
 }
 
 struct ItemDesc {
@@ -495,19 +502,20 @@ __device__ unsigned long long g_item_stamps[2][64][6];
     }                                                                      \
   } while (0)
 
-template <bool UP, int NT>
+template <bool UP, int NQ>
 __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constant__ TiledParams P) {
   // two interleaved matrices per tile: w1|w3 (UP) or the two row halves of W2
   // (DOWN: two independent accumulator chains, as for the up projection)
   constexpr int NI = 2;
-  constexpr int TPP = 8 * NT;  // tokens per pass
+  constexpr int TPP = Tpp<NQ>::TPP;  // tokens per pass
+  constexpr int NT = Tpp<NQ>::NT;    // 16x8 partial tiles per (warp, matrix)
   constexpr int kEpi0 = kNW, kProd = kNW + kNEpi;
   extern __shared__ __align__(128) uint8_t smem[];
-  const SmemMap SM = smem_map<NI, NT>(P);
+  const SmemMap SM = smem_map<NI, NQ>(P);
   uint8_t* stages = smem;
   const int slot_bytes = P.stage_bytes + P.lr_slot;
-  uint16_t* xs = reinterpret_cast<uint16_t*>(smem + SM.xs);
-  float2* sums = reinterpret_cast<float2*>(smem + SM.sums);  // [g_local][TPP] (X, -128 X')
+  uint8_t* xs = smem + SM.xs;                                 // [row][group] x digits
+  float2* sums = reinterpret_cast<float2*>(smem + SM.sums);  // [g_local][TPP] (2^-S, sum x)
   float* red = reinterpret_cast<float*>(smem + SM.red);      // [ring][warp][NI][NT][16][8]
   float* ts = reinterpret_cast<float*>(smem + SM.ts);        // [comp c][NI][maxr]
   float* act_s = reinterpret_cast<float*>(smem + SM.act);    // [TPP][16]
@@ -550,11 +558,9 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
   }
   if (UP && P.prebuilt) {
     // the router releases this grid only after the previous layer finished,
-    // so x is final: build x' for all B tokens while the routing completes
-    uint16_t* xs0 = reinterpret_cast<uint16_t*>(smem + SM.xs);
-    float2* sums0 = reinterpret_cast<float2*>(smem + SM.sums);
-    build_xprime<UP, NT>(A, P, xs0, sums0, nullptr, P.xs_rows, 0, static_cast<int>(2 * P.GP), threadIdx.x,
-                         blockDim.x);
+    // so x is final: build the digits of all B tokens while the routing completes
+    build_xdigits<UP, TPP>(A, P, xs, sums, nullptr, P.xs_rows, 0, static_cast<int>(2 * P.GP), threadIdx.x,
+                           blockDim.x);
   }
   if (UP) griddep_wait();
   griddep_launch_dependents();
@@ -604,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
         const int tile = r % static_cast<int>(P.RT);
         r /= static_cast<int>(P.RT);
         const int chunk = r % P.nchunk, pass = r / P.nchunk;
-        const bool c_comp = pass_has_comp(s_acmask[ai], pass, NT);
+        const bool c_comp = pass_has_comp(s_acmask[ai], pass, TPP);
         const int gp0 = chunk * P.SPC * kSpanGP;
         const int gp1 = static_cast<int>(min(P.GP, static_cast<int64_t>(gp0) + P.SPC * kSpanGP));
         const uint8_t* src = s_wsrc[ai] + ((static_cast<int64_t>(tile) * P.GP + gp0) * NI) * kBlk;
@@ -843,7 +849,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
     const ItemDesc dsc = s_desc[s];
     const int gp0 = dsc.gp0, gp1 = dsc.gp1;
     if (dsc.ai != cur_ai || dsc.pass != cur_pass || dsc.chunk != cur_chunk) {
-      // ---- (re)build the activation operand x' (consumers only)
+      // ---- (re)build the activation digits (consumers only)
       consumer_sync();  // every consumer is past the previous item's MMA
       const bool new_pass = (dsc.ai != cur_ai || dsc.pass != cur_pass);
       cur_ai = dsc.ai;
@@ -865,39 +871,36 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
       if (!P.prebuilt) {
         // only real token rows are built (empty MMA columns read row 0: their
         // accumulators are never read -- MMA columns are independent)
-        build_xprime<UP, NT>(A, P, xs, sums, UP ? s_ctok : s_cpair, pass_tok, gp0 * 128, (gp1 - gp0) * 2,
-                             ctid, kNW * 32);
+        build_xdigits<UP, TPP>(A, P, xs, sums, UP ? s_ctok : s_cpair, pass_tok, gp0 * 128, (gp1 - gp0) * 2,
+                               ctid, kNW * 32);
       }
       consumer_sync();
     }
     const uint8_t* st = stages + static_cast<size_t>(s) * slot_bytes;
 
     // ---------------------------------------------------------- MMA core ----
-    float acc[NI][NT][4];
+    // acc[i][nq][r]: matrix i, token nq*4 + tid, row gid (r = 0) / gid + 8 (r = 1)
+    float acc[NI][NQ][2];
 #pragma unroll
     for (int i = 0; i < NI; ++i)
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[i][nt][c] = 0.0f;
+      for (int nq = 0; nq < NQ; ++nq) acc[i][nq][0] = acc[i][nq][1] = 0.0f;
 
     const int ngp = gp1 - gp0;
     const int nspan = (ngp + kSpanGP - 1) / kSpanGP;
-    // B-fragment row of this lane per N-tile: token column nt*8+gid (empty columns
-    // read row 0; their results are discarded)
-    // x' / sums row of a token column: its pass position, or (prebuilt) its token
-    const uint16_t* xrow[NT];
-    int srow[NT][2];
+    // B-fragment column gid of quad nq = digit gid & 1 of token nq*4 + gid/2
+    // (empty columns read row 0: MMA columns are independent and the lanes
+    // holding them are never read); the digit / sums row of a token is its pass
+    // position, or (prebuilt) the token itself
+    const uint8_t* brow[NQ];
+    int srow[NQ];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int n = nt * 8 + gid;
-      xrow[nt] = xs + (n < pass_tok ? (P.prebuilt ? s_ctok[n] : n) : 0) * P.xs_stride + tid * 4;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int col = nt * 8 + 2 * tid + c;
-        srow[nt][c] = col < pass_tok ? (P.prebuilt ? s_ctok[col] : col) : 0;
-      }
+    for (int nq = 0; nq < NQ; ++nq) {
+      const int nb = nq * 4 + (gid >> 1), nc = nq * 4 + tid;
+      brow[nq] = xs + (nb < pass_tok ? (P.prebuilt ? s_ctok[nb] : nb) : 0) * P.xs_stride + (gid & 1) * 64 + tid * 8;
+      srow[nq] = nc < pass_tok ? (P.prebuilt ? s_ctok[nc] : nc) : 0;
     }
+    constexpr uint32_t kM = 0x03030303u;
     for (int sp = warp; sp < ((P.debug & 1) ? 0 : nspan); sp += kNW) {
       const int q0 = sp * kSpanGP, q1 = min(ngp, q0 + kSpanGP);
 #pragma unroll 1
@@ -912,62 +915,34 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int gl = q * 2 + h;  // group index within the chunk
-          float4 xx[NT];
-          float d[NI][NT][4];
+          uint2 b0[NQ], b1[NQ];
+          float2 sx[NQ];
+          float nm[NQ];
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            // (X, -128X') of this lane's two token columns
-            const float2 s0 = sums[gl * TPP + srow[nt][0]], s1 = sums[gl * TPP + srow[nt][1]];
-            xx[nt] = make_float4(s0.x, s0.y, s1.x, s1.y);
-#pragma unroll
-            for (int i = 0; i < NI; ++i) {
-              d[i][nt][0] = xx[nt].y;
-              d[i][nt][1] = xx[nt].w;
-              d[i][nt][2] = xx[nt].y;
-              d[i][nt][3] = xx[nt].w;
-            }
-          }
-          // the two code words per matrix and their shifted copies (j >= 3 slots)
-          uint32_t wa[NI][3], wb[NI][3];
-#pragma unroll
-          for (int i = 0; i < NI; ++i) {
-            wa[i][0] = h ? cw[i].z : cw[i].x;
-            wb[i][0] = h ? cw[i].w : cw[i].y;
-            wa[i][1] = wa[i][0] >> 6;
-            wb[i][1] = wb[i][0] >> 6;
-            wa[i][2] = wa[i][0] >> 12;
-            wb[i][2] = wb[i][0] >> 12;
-          }
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            uint32_t b0[NT], b1[NT];
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              const uint2 bv = *reinterpret_cast<const uint2*>(xrow[nt] + gl * 64 + ks * 16);
-              b0[nt] = bv.x;
-              b1[nt] = bv.y;
-            }
-            // slot j = 2ks (regs a0/a1) and 2ks+1 (a2/a3): word (j/3 shift), mask 3 << 2*(j%3)
-            const int j0 = 2 * ks, j1 = 2 * ks + 1;
-#pragma unroll
-            for (int i = 0; i < NI; ++i) {
-              const uint32_t m0 = 0x00030003u << (2 * (j0 % 3)), m1 = 0x00030003u << (2 * (j1 % 3));
-              const uint32_t a0 = lop_and_or(wa[i][j0 / 3], m0), a1 = lop_and_or(wb[i][j0 / 3], m0);
-              const uint32_t a2 = lop_and_or(wa[i][j1 / 3], m1), a3 = lop_and_or(wb[i][j1 / 3], m1);
-#pragma unroll
-              for (int nt = 0; nt < NT; ++nt) mma_bf16(d[i][nt], a0, a1, a2, a3, b0[nt], b1[nt]);
-            }
+          for (int nq = 0; nq < NQ; ++nq) {
+            b0[nq] = lds64(brow[nq] + gl * 128);       // m = 0
+            b1[nq] = lds64(brow[nq] + gl * 128 + 32);  // m = 1
+            sx[nq] = sums[gl * TPP + srow[nq]];          // (2^-S, sum x) of token nq*4 + tid
+            nm[nq] = -kMagic * sx[nq].x;
           }
 #pragma unroll
           for (int i = 0; i < NI; ++i) {
+            const uint32_t wa = h ? cw[i].z : cw[i].x, wb = h ? cw[i].w : cw[i].y;
+            // planes j = 2m + h' of the A (row gid) and B (row gid+8) words
+            const uint32_t a0 = wa & kM, a1 = (wa >> 2) & kM, a2 = (wa >> 4) & kM, a3 = (wa >> 6) & kM;
+            const uint32_t c0 = wb & kM, c1 = (wb >> 2) & kM, c2 = (wb >> 4) & kM, c3 = (wb >> 6) & kM;
             const float2 mA = h2f2(h ? mw[i].y : mw[i].x);  // {s, z} row gid
             const float2 mB = h2f2(h ? mw[i].w : mw[i].z);  // {s, z} row gid+8
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              acc[i][nt][0] = fmaf(mA.x, d[i][nt][0], fmaf(mA.y, xx[nt].x, acc[i][nt][0]));
-              acc[i][nt][1] = fmaf(mA.x, d[i][nt][1], fmaf(mA.y, xx[nt].z, acc[i][nt][1]));
-              acc[i][nt][2] = fmaf(mB.x, d[i][nt][2], fmaf(mB.y, xx[nt].x, acc[i][nt][2]));
-              acc[i][nt][3] = fmaf(mB.x, d[i][nt][3], fmaf(mB.y, xx[nt].z, acc[i][nt][3]));
+            for (int nq = 0; nq < NQ; ++nq) {
+              int d[4] = {0, kMagicBits, 0, kMagicBits};
+              mma_u8s8(d, a0, c0, a1, c1, b0[nq].x, b0[nq].y);
+              mma_u8s8(d, a2, c2, a3, c3, b1[nq].x, b1[nq].y);
+              // 2^-S sum c X, exact: (1.5*2^23 + v) 2^-S - 1.5*2^23 2^-S
+              const float ta = fmaf(__int_as_float(d[0] * 128 + d[1]), sx[nq].x, nm[nq]);
+              const float tb = fmaf(__int_as_float(d[2] * 128 + d[3]), sx[nq].x, nm[nq]);
+              acc[i][nq][0] = fmaf(mA.x, ta, fmaf(mA.y, sx[nq].y, acc[i][nq][0]));
+              acc[i][nq][1] = fmaf(mB.x, tb, fmaf(mB.y, sx[nq].y, acc[i][nq][1]));
             }
           }
         }
@@ -988,10 +963,11 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
 #pragma unroll
       for (int i = 0; i < NI; ++i)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          float* q = rb + (i * NT + nt) * 128;
-          *reinterpret_cast<float2*>(q + gid * 8 + 2 * tid) = make_float2(acc[i][nt][0], acc[i][nt][1]);
-          *reinterpret_cast<float2*>(q + (gid + 8) * 8 + 2 * tid) = make_float2(acc[i][nt][2], acc[i][nt][3]);
+        for (int nq = 0; nq < NQ; ++nq) {
+          const int n = nq * 4 + tid;  // token column of this lane
+          float* q = rb + (i * NT + (n >> 3)) * 128 + (n & 7);
+          q[gid * 8] = acc[i][nq][0];
+          q[(gid + 8) * 8] = acc[i][nq][1];
         }
     }
     __syncwarp();
@@ -1015,13 +991,13 @@ void tiled_stamps_copy(uint64_t* host, int n) {
   }
 }
 
-template <bool UP, int NT>
+template <bool UP, int NQ>
 static lrc_status launch_one(const TiledParams& P, int num_sms, cudaStream_t st, bool pdl) {
   constexpr int NI = 2;
-  const SmemMap m = smem_map<NI, NT>(P);
-  auto fn = tiled_kernel<UP, NT>;
-  static int configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
-  if (configured[UP][NT] < m.total) {
+  const SmemMap m = smem_map<NI, NQ>(P);
+  auto fn = tiled_kernel<UP, NQ>;
+  static int configured[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};
+  if (configured[UP][NQ] < m.total) {
     cudaFuncAttributes fa{};
     LRC_CUDA_TRY(cudaFuncGetAttributes(&fa, fn));
     int dev = 0, optin = 0;
@@ -1031,7 +1007,7 @@ static lrc_status launch_one(const TiledParams& P, int num_sms, cudaStream_t st,
       return fail(LRC_ERR_UNSUPPORTED, "tiled kernel: shared memory budget");
     LRC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       optin - static_cast<int>(fa.sharedSizeBytes)));
-    configured[UP][NT] = optin - static_cast<int>(fa.sharedSizeBytes);
+    configured[UP][NQ] = optin - static_cast<int>(fa.sharedSizeBytes);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(num_sms);
@@ -1065,29 +1041,29 @@ static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, in
     P.nchunk = (P.NS + kNW - 1) / kNW;
     P.SPC = (P.NS + P.nchunk - 1) / P.nchunk;
   }
-  P.xs_stride = P.SPC * kSpanGP * 128 + 16;
+  P.xs_stride = P.SPC * kSpanGP * 2 * 128 + 32;
   P.stage_bytes = P.SPC * kSpanGP * NI * kBlk;
   P.lr_slot = lr_max;
   P.debug = getenv("LRC_TILED_DEBUG") ? atoi(getenv("LRC_TILED_DEBUG")) : 0;
   const int budget = 227 * 1024 - 12 * 1024;  // static shared (~10 KB) + slack
-  auto fits = [&](int nt) {
-    P.xs_rows = min(8 * nt, max(max_tok, 1));  // x' rows actually needed
-    return (nt == 1 ? smem_map<NI, 1>(P).total : smem_map<NI, 2>(P).total) <= budget;
+  auto fits = [&](int nq) {
+    P.xs_rows = min(4 * nq, max(max_tok, 1));  // digit rows actually needed
+    const int tot = nq == 1 ? smem_map<NI, 1>(P).total : nq == 2 ? smem_map<NI, 2>(P).total
+                                                                  : smem_map<NI, 4>(P).total;
+    return tot <= budget;
   };
-  int nt = 1;
-  if (max_tok > 8) {
-    for (P.nstage = 3; P.nstage >= 2; --P.nstage)
-      if (fits(2)) break;
-    if (P.nstage >= 2) nt = 2;
-  }
-  if (nt == 1) {
+  // token quads per pass: the fewest that hold the largest expert batch (<= 4)
+  int nq = max_tok <= 4 ? 1 : (max_tok <= 8 ? 2 : 4);
+  for (;; nq >>= 1) {
     for (P.nstage = 4; P.nstage >= 2; --P.nstage)
-      if (fits(1)) break;
-    if (P.nstage < 2) return fail(LRC_ERR_UNSUPPORTED, "tiled kernel: K too large for smem");
+      if (fits(nq)) break;
+    if (P.nstage >= 2 || nq == 1) break;
   }
-  fits(nt);  // final x' row count for the chosen N-tiling
-  P.prebuilt = (UP && max_tok >= 1 && max_tok <= 8 * nt) ? 1 : 0;
-  return (nt == 1) ? launch_one<UP, 1>(P, num_sms, st, pdl) : launch_one<UP, 2>(P, num_sms, st, pdl);
+  if (P.nstage < 2) return fail(LRC_ERR_UNSUPPORTED, "tiled kernel: K too large for smem");
+  fits(nq);  // final digit-row count for the chosen pass width
+  P.prebuilt = (UP && max_tok >= 1 && max_tok <= 4 * nq) ? 1 : 0;
+  return nq == 1 ? launch_one<UP, 1>(P, num_sms, st, pdl)
+                 : nq == 2 ? launch_one<UP, 2>(P, num_sms, st, pdl) : launch_one<UP, 4>(P, num_sms, st, pdl);
 }
 
 lrc_status launch_up_tiled(const ExpertArgs& a, int num_sms, int max_tok, int lr_max,

@@ -306,7 +306,111 @@ void run_gn(int warps) {
   cudaFree(cyc);
 }
 
+// IMMA core (mma.sync m16n8k32 u8 x s8): I8 tile words hold code (m, h, b) of
+// lane tid at bit 8b + 2(2m+h) (K = 32m + 16h + 4 tid + b); x as two signed
+// 7-bit digits in N columns 2t, 2t+1 (token t <= 3); per (group, token) the
+// sums hold {2^-S, -1.5*2^23*2^-S, X, 0}.  The d1 accumulator is seeded with
+// the float bits of 1.5*2^23 so 128 d0 + d1 is a float (magic) directly.
+__device__ __forceinline__ void imma(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                     uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+template <int NI, int UNR, int SP>
+__device__ __forceinline__ void core_i8(const uint8_t* st, const uint8_t* xd, const float4* sums, int xd_stride,
+                                        int warp, int nwarps, float (&acc)[NI][2]) {
+  const int lane = threadIdx.x & 31, gid = lane >> 2, tid = lane & 3;
+  const uint8_t* brow = xd + (gid >> 1) * xd_stride + (gid & 1) * 64 + tid * 8;
+  const int nspan = GPI / SP;
+  constexpr uint32_t M = 0x03030303u;
+  for (int sp = warp; sp < nspan; sp += nwarps) {
+    const int q0 = sp * SP, q1 = q0 + SP;
+#pragma unroll UNR
+    for (int q = q0; q < q1; ++q) {
+      const uint8_t* blk = st + q * NI * kBlk;
+      uint4 cw[NI], mw[NI];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        cw[i] = *reinterpret_cast<const uint4*>(blk + i * kBlk + lane * 16);
+        mw[i] = *reinterpret_cast<const uint4*>(blk + i * kBlk + kCodeBytes + gid * 16);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gl = q * 2 + h;
+        const uint2 bv = *reinterpret_cast<const uint2*>(brow + gl * 128);  // m = 0; m = 1 at +32
+        const uint2 bw = *reinterpret_cast<const uint2*>(brow + gl * 128 + 32);
+        const float4 sx = sums[gl * 4 + tid];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const uint32_t wa = h ? cw[i].z : cw[i].x, wb = h ? cw[i].w : cw[i].y;
+          int d[4] = {0, 0x4B400000, 0, 0x4B400000};
+          imma(d, wa & M, wb & M, (wa >> 2) & M, (wb >> 2) & M, bv.x, bv.y);
+          imma(d, (wa >> 4) & M, (wb >> 4) & M, (wa >> 6) & M, (wb >> 6) & M, bw.x, bw.y);
+          const float fa = __int_as_float(d[0] * 128 + d[1]), fb = __int_as_float(d[2] * 128 + d[3]);
+          const float ta = fmaf(fa, sx.x, sx.y), tb = fmaf(fb, sx.x, sx.y);
+          const float2 mA = h2f2(h ? mw[i].y : mw[i].x);
+          const float2 mB = h2f2(h ? mw[i].w : mw[i].z);
+          acc[i][0] = fmaf(mA.x, ta, fmaf(mA.y, sx.z, acc[i][0]));
+          acc[i][1] = fmaf(mB.x, tb, fmaf(mB.y, sx.z, acc[i][1]));
+        }
+      }
+    }
+  }
+}
+
+template <int NI, int UNR, int SP>
+__global__ void bench_i8(int items, float* out, long long* cyc) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int xd_stride = GPI * 2 * 128 + 16;
+  uint8_t* st = sm;
+  uint8_t* xd = sm + GPI * NI * kBlk;
+  float4* sums = reinterpret_cast<float4*>(sm + GPI * NI * kBlk + 4 * xd_stride);
+  const int total = GPI * NI * kBlk + 4 * xd_stride + GPI * 2 * 4 * 16;
+  for (int i = threadIdx.x; i < total / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(sm)[i] = (i * 2654435761u) & 0x3c003c00u;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  float acc[NI][2] = {};
+  const long long t0 = clock64();
+  for (int it = 0; it < items; ++it) core_i8<NI, UNR, SP>(st, xd, sums, xd_stride, warp, nwarps, acc);
+  const long long t1 = clock64();
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) s += acc[i][0] + acc[i][1];
+  if (s == 1.2345f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+
+template <int NI, int UNR, int SP = 4>
+void run_i8(int warps) {
+  const int xd_stride = GPI * 2 * 128 + 16;
+  const int smem = GPI * NI * kBlk + 4 * xd_stride + GPI * 2 * 4 * 16;
+  cudaFuncSetAttribute(bench_i8<NI, UNR, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  float* out;
+  long long* cyc;
+  cudaMalloc(&out, 4);
+  cudaMallocManaged(&cyc, 8);
+  const int items = 200;
+  bench_i8<NI, UNR, SP><<<148, warps * 32, smem>>>(items, out, cyc);
+  cudaDeviceSynchronize();
+  bench_i8<NI, UNR, SP><<<148, warps * 32, smem>>>(items, out, cyc);
+  cudaError_t e = cudaDeviceSynchronize();
+  const double cpi = double(*cyc) / items;
+  const double bytes = GPI * NI * kBlk;
+  printf("IMMA NI=%d unroll=%d span=%d warps=%2d:   %7.0f cycles/item  -> %6.1f B/cycle/SM  = %5.2f TB/s  (%s)\n", NI,
+         UNR, SP, warps, cpi, bytes / cpi, bytes / cpi * 1.965e9 * 148 / 1e12, cudaGetErrorString(e));
+  cudaFree(out);
+  cudaFree(cyc);
+}
+
 int main() {
+  run_i8<2, 1>(8);
+  run_i8<2, 2>(8);
+  run_i8<2, 1, 2>(16);
+  run_i8<2, 2, 2>(16);
+  run_i8<2, 1, 1>(32);
+  run_i8<2, 1, 2>(8);
   run<2, 1, 0>(8);
   run<2, 1, 2>(8);
   run<2, 1, 2, 2>(16);
