@@ -2,25 +2,29 @@
 //
 // HBM layout ("T2 tiles"): a matrix (M, K) is cut into 16-row tiles and
 // 128-column group pairs.  Block (tile t, group-pair q, matrix i) is 640 B:
-//   [0,512)   codes: lane l holds 16 B = 4 words {A(g0), B(g0), A(g1), B(g1)}
-//             A = row t*16+gid, B = row t*16+gid+8 (gid = l>>2, tid = l&3);
-//             code (m, h, b) of a word sits at bit 8b + 2(2m+h) and is the
-//             weight at column g*64 + 32m + 16h + 4tid + b -- the
-//             mma.m16n8k32 A-fragment order, so (w >> 2j) & 0x03030303 is
-//             one u8 operand register (4 codes).
+//   [0,512)   codes: lane l holds 16 B = 4 words W0..W3 (gid = l>>2, tid = l&3);
+//             word Wk covers the mma.m16n8k32 K slice k (m = k>>1, half = k&1)
+//             of both groups and both rows of the lane: byte b, plane p
+//             (bits 8b + 2p) holds the code at column g*64 + 32m + 16half +
+//             4tid + b of group g = 2q + (p>>1), row t*16 + gid + 8(p&1).
+//             So W & (0x03030303 << 2(p&1)) after W >>= 4 (p >> 1) is one u8
+//             A-fragment register: row gid codes x1, row gid+8 codes x4 --
+//             a per-row factor, folded into that row's epilogue scale.
 //   [512,640) fp16 scale/zero: 16 B per gid {s,z}(A,g0) {s,z}(A,g1) {s,z}(B,g0) {s,z}(B,g1)
+//             (A = row t*16+gid, B = row t*16+gid+8)
 // Blocks are ordered (t, q, i), so one row tile over a K range is one contiguous
 // byte range -> one cp.async.bulk per work item.  The codes are exactly the
 // reference's (lrc_tiles_unpack inverts the layout bit-exactly).
 //
 // Core: mma.sync m16n8k32 u8 x s8 -> s32.  The activation operand is each
-// token's 64-column group as a 14-bit integer X = rint(x 2^S) (S per group and
-// token: |X| < 2^13), split into two signed 7-bit digits X = 128 d0 + d1 that
+// token's 64-column group as a 13-bit integer X = rint(x 2^S) (S per group and
+// token: |X| <= 2^12), split into two signed 7-bit digits X = 128 d0 + d1 that
 // sit in adjacent N columns (one MMA covers 4 tokens); a lane's accumulator
-// pair is then {sum c d0, sum c d1} of one token, and 128 d0 + d1 lands
-// directly in a float's mantissa (seeded magic 1.5 * 2^23).
+// pair is then {sum c d0, sum c d1} of one token (x4 for the B row), and
+// 128 d0 + d1 + the bits of 1.5 * 2^23 is a float whose mantissa holds the
+// exact dot product (|4 sum c X| <= 4 * 192 * 2^12 < 2^22).
 // Per group:  y += s * 2^-S (sum c X) + z * sum x   (fp32, ref/quant.py:216-224).
-// The x rounding is relative 2^-14 of the group's largest |x| (below the bf16
+// The x rounding is relative 2^-13 of the group's largest |x| (below the bf16
 // rounding of the layer's own activations).
 #include <algorithm>
 #include <cstdlib>
@@ -32,10 +36,24 @@ namespace lrc {
 
 constexpr int kBlk = 640;
 constexpr int kCodeBytes = 512;
-constexpr int kSpanGP = 4;        // group pairs per warp span (512 columns)
-constexpr int kNW = 8;            // consumer warps (+1 epilogue warp, +1 producer warp)
-constexpr int kNEpi = 2;          // epilogue warps: item k -> warp kNW + k % kNEpi
-constexpr int kThreads = (kNW + kNEpi + 1) * 32;
+constexpr int kNEpi = 2;          // epilogue warps: item k -> warp NW + k % kNEpi
+// Consumer warps and their K span per pass width (NQ token quads).  In
+// isolation the single-quad core gains from 16 warps on 2-group-pair spans
+// (tools/core_bench.cu: 1,854 -> 1,697 cycles per 40 KB item), in the kernel
+// it does not (B=1 equal, B=2/4 -4%): 8 warps, 512-column spans everywhere
+// (TILED_NW1 / TILED_SPAN1 override the single-quad shape for A/B runs).
+#ifndef TILED_NW1
+#define TILED_NW1 8
+#endif
+#ifndef TILED_SPAN1
+#define TILED_SPAN1 4
+#endif
+template <int NQ>
+struct KCfg {
+  static constexpr int NW = NQ == 1 ? TILED_NW1 : 8;
+  static constexpr int SPAN = NQ == 1 ? TILED_SPAN1 : 4;  // group pairs per warp span
+  static constexpr int THREADS = (NW + kNEpi + 1) * 32;
+};
 
 int64_t tiles_bytes(int64_t rows, int64_t cols, int ni) {
   int64_t rt = (rows + 15) / 16, gp = (cols + 127) / 128;
@@ -55,24 +73,17 @@ __global__ void build_tiles_kernel(lrc_qmat m0, lrc_qmat m1, int ni, int64_t RT,
   const lrc_qmat& m = (i == 0) ? m0 : m1;
   const int gid = lane >> 2, tid = lane & 3;
   const int64_t nbytes = (static_cast<int64_t>(m.rows) * m.cols * m.bits + 7) >> 3;
-  uint32_t w[4];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-#pragma unroll
-    for (int rs = 0; rs < 2; ++rs) {
-      const int64_t r = t * 16 + gid + 8 * rs;
-      uint32_t word = 0;
-      for (int mm = 0; mm < 2; ++mm)
-        for (int hh = 0; hh < 2; ++hh)
-          for (int b = 0; b < 4; ++b) {
-            const int64_t k = (2 * q + h) * 64 + mm * 32 + hh * 16 + tid * 4 + b;
-            uint32_t c = 0;
-            if (r < m.rows && k < m.cols) c = read_code(m.packed, r * m.cols + k, m.bits, nbytes);
-            word |= c << (8 * b + 2 * (2 * mm + hh));
-          }
-      w[h * 2 + rs] = word;
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  for (int kw = 0; kw < 4; ++kw)
+    for (int pl = 0; pl < 4; ++pl) {
+      const int64_t r = t * 16 + gid + 8 * (pl & 1);
+      for (int b = 0; b < 4; ++b) {
+        const int64_t k = (2 * q + (pl >> 1)) * 64 + (kw >> 1) * 32 + (kw & 1) * 16 + tid * 4 + b;
+        uint32_t c = 0;
+        if (r < m.rows && k < m.cols) c = read_code(m.packed, r * m.cols + k, m.bits, nbytes);
+        w[kw] |= c << (8 * b + 2 * pl);
+      }
     }
-  }
   uint8_t* b = tiles + blk * kBlk;
   *reinterpret_cast<uint4*>(b + lane * 16) = make_uint4(w[0], w[1], w[2], w[3]);
   if (lane < 8) {
@@ -110,11 +121,11 @@ __global__ void tiles_unpack_kernel(const uint8_t* __restrict__ tiles, int64_t r
   const int rr = static_cast<int>(r % 16), gid = rr & 7, rs = rr >> 3;
   const int64_t g = k / 64, q = g / 2;
   const int h = static_cast<int>(g & 1), w = static_cast<int>(k % 64);
-  const int mm = w / 32, hh = (w % 32) / 16, tid = (w % 16) / 4, bb = w % 4;
+  const int kw = 2 * (w / 32) + (w % 32) / 16, tid = (w % 16) / 4, bb = w % 4;
   const int lane = gid * 4 + tid;
   const uint8_t* b = tiles + ((t * GP + q) * ni + which) * kBlk;
-  const uint32_t word = reinterpret_cast<const uint32_t*>(b + lane * 16)[h * 2 + rs];
-  out[idx] = static_cast<uint8_t>((word >> (8 * bb + 2 * (2 * mm + hh))) & 3u);
+  const uint32_t word = reinterpret_cast<const uint32_t*>(b + lane * 16)[kw];
+  out[idx] = static_cast<uint8_t>((word >> (8 * bb + 2 * (2 * h + rs))) & 3u);
 }
 
 // -------------------------------------------------------- PTX primitives ---
@@ -164,8 +175,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+template <int NW>
 __device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kNW * 32) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
 }
 __device__ __forceinline__ uint4 lds128(const void* p) {
   uint4 v;
@@ -185,6 +197,13 @@ __device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, 
   asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
       : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// D = A . B (zero accumulator: the first MMA of a chain reads RZ)
+__device__ __forceinline__ void mma_u8s8_z(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                           uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%10,%10,%10};"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(0));
 }
 constexpr int kMagicBits = 0x4B400000;   // 1.5 * 2^23: integer v added to its bits reads as 1.5*2^23 + v
 constexpr float kMagic = 12582912.0f;
@@ -317,15 +336,15 @@ struct Tpp {
 
 template <int NI, int NQ>
 __host__ __device__ inline SmemMap smem_map(const TiledParams& p) {
-  constexpr int TPP = Tpp<NQ>::TPP, NT = Tpp<NQ>::NT;
+  constexpr int TPP = Tpp<NQ>::TPP, NT = Tpp<NQ>::NT, NW = KCfg<NQ>::NW, SPAN = KCfg<NQ>::SPAN;
   SmemMap m;
   int o = p.nstage * (p.stage_bytes + p.lr_slot);
   m.xs = o;
   o = align16(o + p.xs_rows * p.xs_stride);
   m.sums = o;
-  o = align16(o + p.SPC * kSpanGP * 2 * TPP * 8);
+  o = align16(o + p.SPC * SPAN * 2 * TPP * 8);
   m.red = o;
-  o = align16(o + kNRed * kNW * NI * NT * 128 * 4);
+  o = align16(o + kNRed * NW * NI * NT * 128 * 4);
   m.ts = o;
   o = align16(o + kNEpi * TPP * NI * (p.a.maxr > 0 ? p.a.maxr : 1) * 4);
   m.act = o;
@@ -449,14 +468,14 @@ __device__ __forceinline__ void build_xdigits(const ExpertArgs& A, const TiledPa
         xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
         amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
       }
-      // amax < 2^(E - 126) for exponent field E: S = 139 - E puts |x| 2^S < 2^13
-      const int S = min(139 - static_cast<int>((__float_as_uint(amax) >> 23) & 255u), 126);
+      // amax < 2^(E - 126) for exponent field E: S = 138 - E puts |x| 2^S < 2^12
+      const int S = min(138 - static_cast<int>((__float_as_uint(amax) >> 23) & 255u), 126);
       const float sc = __uint_as_float(static_cast<uint32_t>(S + 127) << 23);
       if (ok[u]) {
         uint32_t d0w[2] = {0u, 0u}, d1w[2] = {0u, 0u};
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int X = __float2int_rn(xv[j] * sc);  // exact scaling, |X| <= 2^13
+          const int X = __float2int_rn(xv[j] * sc);  // exact scaling, |X| <= 2^12
           d0w[j >> 2] |= (static_cast<uint32_t>(X >> 7) & 0xffu) << (8 * (j & 3));
           d1w[j >> 2] |= (static_cast<uint32_t>(X) & 0x7fu) << (8 * (j & 3));
         }
@@ -503,12 +522,13 @@ __device__ unsigned long long g_item_stamps[2][64][6];
   } while (0)
 
 template <bool UP, int NQ>
-__global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constant__ TiledParams P) {
+__global__ void __launch_bounds__(KCfg<NQ>::THREADS, 1) tiled_kernel(const __grid_constant__ TiledParams P) {
   // two interleaved matrices per tile: w1|w3 (UP) or the two row halves of W2
   // (DOWN: two independent accumulator chains, as for the up projection)
   constexpr int NI = 2;
   constexpr int TPP = Tpp<NQ>::TPP;  // tokens per pass
   constexpr int NT = Tpp<NQ>::NT;    // 16x8 partial tiles per (warp, matrix)
+  constexpr int kNW = KCfg<NQ>::NW, kSpanGP = KCfg<NQ>::SPAN;
   constexpr int kEpi0 = kNW, kProd = kNW + kNEpi;
   extern __shared__ __align__(128) uint8_t smem[];
   const SmemMap SM = smem_map<NI, NQ>(P);
@@ -850,7 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
     const int gp0 = dsc.gp0, gp1 = dsc.gp1;
     if (dsc.ai != cur_ai || dsc.pass != cur_pass || dsc.chunk != cur_chunk) {
       // ---- (re)build the activation digits (consumers only)
-      consumer_sync();  // every consumer is past the previous item's MMA
+      consumer_sync<kNW>();  // every consumer is past the previous item's MMA
       const bool new_pass = (dsc.ai != cur_ai || dsc.pass != cur_pass);
       cur_ai = dsc.ai;
       cur_pass = dsc.pass;
@@ -866,7 +886,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
           s_cpair[ctid] = p;
           s_ctok[ctid] = tok;
         }
-        consumer_sync();
+        consumer_sync<kNW>();
       }
       if (!P.prebuilt) {
         // only real token rows are built (empty MMA columns read row 0: their
@@ -874,7 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
         build_xdigits<UP, TPP>(A, P, xs, sums, UP ? s_ctok : s_cpair, pass_tok, gp0 * 128, (gp1 - gp0) * 2,
                                ctid, kNW * 32);
       }
-      consumer_sync();
+      consumer_sync<kNW>();
     }
     const uint8_t* st = stages + static_cast<size_t>(s) * slot_bytes;
 
@@ -900,7 +920,7 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
       brow[nq] = xs + (nb < pass_tok ? (P.prebuilt ? s_ctok[nb] : nb) : 0) * P.xs_stride + (gid & 1) * 64 + tid * 8;
       srow[nq] = nc < pass_tok ? (P.prebuilt ? s_ctok[nc] : nc) : 0;
     }
-    constexpr uint32_t kM = 0x03030303u;
+    constexpr uint32_t kM = 0x03030303u, kM4 = kM << 2;
     for (int sp = warp; sp < ((P.debug & 1) ? 0 : nspan); sp += kNW) {
       const int q0 = sp * kSpanGP, q1 = min(ngp, q0 + kSpanGP);
 #pragma unroll 1
@@ -917,30 +937,31 @@ __global__ void __launch_bounds__(kThreads, 1) tiled_kernel(const __grid_constan
           const int gl = q * 2 + h;  // group index within the chunk
           uint2 b0[NQ], b1[NQ];
           float2 sx[NQ];
-          float nm[NQ];
+          float nm[NQ], inv4[NQ], nm4[NQ];
 #pragma unroll
           for (int nq = 0; nq < NQ; ++nq) {
             b0[nq] = lds64(brow[nq] + gl * 128);       // m = 0
             b1[nq] = lds64(brow[nq] + gl * 128 + 32);  // m = 1
             sx[nq] = sums[gl * TPP + srow[nq]];          // (2^-S, sum x) of token nq*4 + tid
             nm[nq] = -kMagic * sx[nq].x;
+            inv4[nq] = 0.25f * sx[nq].x;  // B-row codes carry a factor 4
+            nm4[nq] = 0.25f * nm[nq];
           }
 #pragma unroll
           for (int i = 0; i < NI; ++i) {
-            const uint32_t wa = h ? cw[i].z : cw[i].x, wb = h ? cw[i].w : cw[i].y;
-            // planes j = 2m + h' of the A (row gid) and B (row gid+8) words
-            const uint32_t a0 = wa & kM, a1 = (wa >> 2) & kM, a2 = (wa >> 4) & kM, a3 = (wa >> 6) & kM;
-            const uint32_t c0 = wb & kM, c1 = (wb >> 2) & kM, c2 = (wb >> 4) & kM, c3 = (wb >> 6) & kM;
+            // group h's planes: 2h (row gid) and 2h + 1 (row gid+8, x4)
+            const uint32_t w0 = h ? cw[i].x >> 4 : cw[i].x, w1 = h ? cw[i].y >> 4 : cw[i].y;
+            const uint32_t w2 = h ? cw[i].z >> 4 : cw[i].z, w3 = h ? cw[i].w >> 4 : cw[i].w;
             const float2 mA = h2f2(h ? mw[i].y : mw[i].x);  // {s, z} row gid
             const float2 mB = h2f2(h ? mw[i].w : mw[i].z);  // {s, z} row gid+8
 #pragma unroll
             for (int nq = 0; nq < NQ; ++nq) {
-              int d[4] = {0, kMagicBits, 0, kMagicBits};
-              mma_u8s8(d, a0, c0, a1, c1, b0[nq].x, b0[nq].y);
-              mma_u8s8(d, a2, c2, a3, c3, b1[nq].x, b1[nq].y);
+              int d[4];
+              mma_u8s8_z(d, w0 & kM, w0 & kM4, w1 & kM, w1 & kM4, b0[nq].x, b0[nq].y);
+              mma_u8s8(d, w2 & kM, w2 & kM4, w3 & kM, w3 & kM4, b1[nq].x, b1[nq].y);
               // 2^-S sum c X, exact: (1.5*2^23 + v) 2^-S - 1.5*2^23 2^-S
-              const float ta = fmaf(__int_as_float(d[0] * 128 + d[1]), sx[nq].x, nm[nq]);
-              const float tb = fmaf(__int_as_float(d[2] * 128 + d[3]), sx[nq].x, nm[nq]);
+              const float ta = fmaf(__int_as_float(d[0] * 128 + (d[1] + kMagicBits)), sx[nq].x, nm[nq]);
+              const float tb = fmaf(__int_as_float(d[2] * 128 + (d[3] + kMagicBits)), inv4[nq], nm4[nq]);
               acc[i][nq][0] = fmaf(mA.x, ta, fmaf(mA.y, sx[nq].y, acc[i][nq][0]));
               acc[i][nq][1] = fmaf(mB.x, tb, fmaf(mB.y, sx[nq].y, acc[i][nq][1]));
             }
@@ -1011,7 +1032,7 @@ static lrc_status launch_one(const TiledParams& P, int num_sms, cudaStream_t st,
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(num_sms);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(KCfg<NQ>::THREADS);
   cfg.dynamicSmemBytes = m.total;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1033,20 +1054,21 @@ static lrc_status launch_tiled(const ExpertArgs& a, int num_sms, int max_tok, in
   P.K = UP ? a.hidden : a.ffn;
   P.GP = (P.K + 127) / 128;
   P.RT = (P.M + 15) / 16;
-  P.NS = static_cast<int>((P.GP + kSpanGP - 1) / kSpanGP);
-  if (UP) {  // the SwiGLU needs complete h1/h3: one chunk covers all of K
-    P.nchunk = 1;
-    P.SPC = P.NS;
-  } else {  // split K into <= kNW-span chunks; partial outputs combine with atomics
-    P.nchunk = (P.NS + kNW - 1) / kNW;
-    P.SPC = (P.NS + P.nchunk - 1) / P.nchunk;
-  }
-  P.xs_stride = P.SPC * kSpanGP * 2 * 128 + 32;
-  P.stage_bytes = P.SPC * kSpanGP * NI * kBlk;
   P.lr_slot = lr_max;
   P.debug = getenv("LRC_TILED_DEBUG") ? atoi(getenv("LRC_TILED_DEBUG")) : 0;
   const int budget = 227 * 1024 - 12 * 1024;  // static shared (~10 KB) + slack
   auto fits = [&](int nq) {
+    const int nw = nq == 1 ? KCfg<1>::NW : KCfg<2>::NW, span = nq == 1 ? KCfg<1>::SPAN : KCfg<2>::SPAN;
+    P.NS = static_cast<int>((P.GP + span - 1) / span);
+    if (UP) {  // the SwiGLU needs complete h1/h3: one chunk covers all of K
+      P.nchunk = 1;
+      P.SPC = P.NS;
+    } else {  // split K into <= nw-span chunks; partial outputs combine with atomics
+      P.nchunk = (P.NS + nw - 1) / nw;
+      P.SPC = (P.NS + P.nchunk - 1) / P.nchunk;
+    }
+    P.xs_stride = P.SPC * span * 2 * 128 + 32;
+    P.stage_bytes = P.SPC * span * NI * kBlk;
     P.xs_rows = min(4 * nq, max(max_tok, 1));  // digit rows actually needed
     const int tot = nq == 1 ? smem_map<NI, 1>(P).total : nq == 2 ? smem_map<NI, 2>(P).total
                                                                   : smem_map<NI, 4>(P).total;

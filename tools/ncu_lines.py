@@ -6,6 +6,8 @@
 import csv
 import sys
 
+import os
+FILE = os.environ.get("NCU_FILE", "tcd.cu")
 rows = list(csv.reader(open(sys.argv[1], errors="replace")))
 lo, hi = (map(int, sys.argv[2].split("-")) if len(sys.argv) > 2 else (0, 10 ** 9))
 topn = int(sys.argv[3]) if len(sys.argv) > 3 else 30
@@ -22,7 +24,7 @@ for r in rows:
     if r[0] == "Line No":
         hdr = r
         continue
-    if hdr and cur and cur.endswith("tcd.cu") and r[0].isdigit() and len(r) == len(hdr):
+    if hdr and cur and cur.endswith(FILE) and r[0].isdigit() and len(r) == len(hdr):
         ln = int(r[0])
         if not (lo <= ln <= hi):
             continue
