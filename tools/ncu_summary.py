@@ -17,7 +17,7 @@ def short(name):
     name = re.sub(r"\((?!.*<).*$", "", name)
     m = re.match(r"tiled_kernel<(\d), *(\d)>", name)
     if m:
-        return f"tiled_kernel<{'UP' if m.group(1) == '1' else 'DOWN'}, NT={m.group(2)}>"
+        return f"tiled_kernel<{'UP' if m.group(1) == '1' else 'DOWN'}, NQ={m.group(2)}>"
     return name
 
 
