@@ -1224,7 +1224,7 @@ static lrc_status forward_impl(lrc_layer* L, const uint16_t* x, int64_t B, int t
         L->lrp_dirty[i] = 0;
       }
     NvtxRange nv_pf("lrc.prefill");
-    if ((s = launch_prefill(a, np_bound, L->lrp, L->tb, L->ppk, L->prefill_bits, st, &launches)) != LRC_OK) return s;
+    if ((s = launch_prefill(a, np_bound, static_cast<int>(B), L->lrp, L->tb, L->ppk, L->prefill_bits, st, &launches)) != LRC_OK) return s;
     if (prof) LRC_CUDA_TRY(cudaEventRecord(L->ev[3], st));  // phases: up+mid+down lumped into [2]
   } else if (allow_tiled && L->tiled) {
     NvtxRange nv_t("lrc.tiled");

@@ -288,7 +288,7 @@ int prefill_tb_width(int maxr);
 lrc_status build_prefill_lr(const lrc_expert& e, int hidden, int ffn, int maxr, uint16_t* out, cudaStream_t st);
 int64_t prefill_pack_bytes(int hidden, int ffn, int bits);  // per expert
 lrc_status build_prefill_pack(const lrc_expert& e, int hidden, int ffn, int bits, uint8_t* out, cudaStream_t st);
-lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp, uint16_t* tb,
+lrc_status launch_prefill(const ExpertArgs& a, int np_bound, int max_tok, const uint16_t* lrp, uint16_t* tb,
                           const uint8_t* ppk, int bits, cudaStream_t st, int* launches);
 
 }  // namespace lrc

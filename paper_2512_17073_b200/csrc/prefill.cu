@@ -39,6 +39,8 @@
 // bf16 activations pair-major in the idle stage memory and writes 16-byte rows.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "layer.cuh"
 #include "umma.cuh"
@@ -47,8 +49,8 @@ namespace lrc {
 namespace {
 
 constexpr int kTM = 128;  // rows per accumulator per CTA (256 per pair)
-constexpr int kTN = 256;  // pairs per tile (MMA N)
-constexpr int kBN = 128;  // B rows per CTA
+constexpr int kTN = 256;  // max pairs per tile (MMA N); the kernel takes TN in {64, 128, 256}
+constexpr int kBN = 128;  // max B rows per CTA (TN / 2)
 constexpr int kKS = 64;   // K slab
 constexpr int kStages = 4;
 constexpr int kSlabA = kTM * 128;
@@ -66,7 +68,6 @@ constexpr int kCR = 6;  // max ring depth
 constexpr int kRingBytes = 6 * 2 * cb_bytes(2);
 static_assert(4 * 2 * cb_bytes(3) <= kRingBytes, "3-bit code ring");
 constexpr int kSmemBytes = kStages * kStageBytes + kRingBytes + 1024;
-constexpr uint32_t kIdesc = umma::idesc_bf16(2 * kTM, kTN);
 
 enum Mode : int {
   kUp = 0,      // A = W1 | W3 rows, B = x rows       -> SwiGLU -> a16
@@ -282,7 +283,13 @@ __global__ void build_lr_pack_kernel(lrc_expert E, int hidden, int ffn, int R, L
   }
 }
 
+// TN = pairs per tile (MMA N): small batches take N = 64 / 128 so the tensor
+// work follows the expert's token count instead of a fixed 256 columns
+template <int TN>
 __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const PrefillArgs P) {
+  constexpr int kTN = TN, kBN = TN / 2;
+  constexpr uint32_t kIdesc = umma::idesc_bf16(2 * kTM, kTN);
+  static_assert(kBN % (kProd / 8) == 0, "B gather: rows bn0 + 32 i");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[kStages], empty[kStages], done, rfull[kCR], rempty[kCR];
@@ -641,13 +648,20 @@ lrc_status build_prefill_pack(const lrc_expert& e, int hidden, int ffn, int bits
   return LRC_OK;
 }
 
-lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp, uint16_t* tb,
+lrc_status launch_prefill(const ExpertArgs& a, int np_bound, int max_tok, const uint16_t* lrp, uint16_t* tb,
                           const uint8_t* ppk, int bits, cudaStream_t st, int* launches) {
   static bool attr = false;
   if (!attr) {
-    LRC_CUDA_TRY(cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    LRC_CUDA_TRY(cudaFuncSetAttribute(prefill_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    LRC_CUDA_TRY(cudaFuncSetAttribute(prefill_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    LRC_CUDA_TRY(cudaFuncSetAttribute(prefill_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
     attr = true;
   }
+  // MMA N per tile: the smallest that holds the largest possible expert batch
+  // (an expert sees at most B pairs); LRC_PREFILL_TN overrides
+  static const int tn_env = getenv("LRC_PREFILL_TN") ? atoi(getenv("LRC_PREFILL_TN")) : 0;
+  const int tn = tn_env == 64 || tn_env == 128 || tn_env == 256 ? tn_env
+                 : (max_tok <= 64 ? 64 : (max_tok <= 128 ? 128 : 256));
   PrefillArgs P{};
   P.a = a;
   P.ppk = ppk;
@@ -662,7 +676,7 @@ lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp
     P.tb = tb;
     P.WT = prefill_tb_width(R);
   }
-  const int ytiles = (np_bound + kTN - 1) / kTN + a.ne;  // >= sum over experts of ceil(cnt / kTN)
+  const int ytiles = (np_bound + tn - 1) / tn + a.ne;  // >= sum over experts of ceil(cnt / tn)
   auto launch = [&](int mode, int M, int K, int lr_slabs, int rows_per_pair) -> lrc_status {
     P.mode = mode;
     P.M = M;
@@ -680,7 +694,12 @@ lrc_status launch_prefill(const ExpertArgs& a, int np_bound, const uint16_t* lrp
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    LRC_CUDA_TRY(cudaLaunchKernelEx(&cfg, prefill_kernel, P));
+    if (tn == 64)
+      LRC_CUDA_TRY(cudaLaunchKernelEx(&cfg, prefill_kernel<64>, P));
+    else if (tn == 128)
+      LRC_CUDA_TRY(cudaLaunchKernelEx(&cfg, prefill_kernel<128>, P));
+    else
+      LRC_CUDA_TRY(cudaLaunchKernelEx(&cfg, prefill_kernel<256>, P));
     ++*launches;
     return LRC_OK;
   };

@@ -117,3 +117,16 @@ def test_e128_top8_two_shared_all_tokens(torch):
                     max_tokens=32)
     for B in (1, 16):
         check_layer(torch, sl, B, 8, 2, seed=900 + B, n_shared=2)
+
+
+@pytest.mark.parametrize("B", [16, 64])
+def test_int2_small_batch_prefill_all_tokens(torch, int2_layer, B):
+    """The tensor-core grouped GEMM at batch sizes below the default prefill
+    threshold (MMA N = 64 tiles), every token vs the oracle."""
+    L = int2_layer.layer
+    assert L.prefill_eligible
+    L.set_prefill_min(1)
+    try:
+        check_layer(torch, int2_layer, B, 2, 1, seed=700 + B)
+    finally:
+        L.set_prefill_min(128)
