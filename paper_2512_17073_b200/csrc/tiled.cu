@@ -45,6 +45,10 @@ constexpr int kNEpi = 2;          // epilogue warps: item k -> warp NW + k % kNE
 #ifndef TILED_NW1
 #define TILED_NW1 8
 #endif
+#ifndef TILED_QUNROLL
+#define TILED_QUNROLL 1
+#endif
+constexpr int kQUnroll = TILED_QUNROLL;  // group pairs per consumer loop body
 #ifndef TILED_SPAN1
 #define TILED_SPAN1 4
 #endif
@@ -923,7 +927,7 @@ __global__ void __launch_bounds__(KCfg<NQ>::THREADS, 1) tiled_kernel(const __gri
     constexpr uint32_t kM = 0x03030303u, kM4 = kM << 2;
     for (int sp = warp; sp < ((P.debug & 1) ? 0 : nspan); sp += kNW) {
       const int q0 = sp * kSpanGP, q1 = min(ngp, q0 + kSpanGP);
-#pragma unroll 1
+#pragma unroll kQUnroll
       for (int q = q0; q < q1; ++q) {
         const uint8_t* blk = st + q * NI * kBlk;
         uint4 cw[NI], mw[NI];
