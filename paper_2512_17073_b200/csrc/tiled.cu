@@ -303,10 +303,10 @@ __device__ __forceinline__ float lr_deq(const uint8_t* codes, int idx, int bits,
 
 // --------------------------------------------------------- tiled kernel ---
 // Work item = (active expert, token pass, K chunk, 16-row tile).  One CTA per
-// SM: warp kNW (producer) streams items with cp.async.bulk into a ring of
-// shared-memory stages; kNW consumer warps each own a 2-group-pair (256
-// column) span of the item, unpack the codes in registers and issue
-// mma.sync m16n8k16 with the activation operand x' from shared memory.
+// SM: warp kNW + kNEpi (producer) streams items with cp.async.bulk into a
+// ring of shared-memory stages; kNW consumer warps each own a 4-group-pair
+// (512-column) span of the item, unpack the codes in registers and issue
+// mma.sync m16n8k32 u8 x s8 with the activation digits from shared memory.
 struct TiledParams {
   ExpertArgs a;
   int M, K;             // rows / cols of the streamed matrix (per interleaved matrix)
