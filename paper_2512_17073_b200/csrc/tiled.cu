@@ -24,8 +24,9 @@
 // 128 d0 + d1 + the bits of 1.5 * 2^23 is a float whose mantissa holds the
 // exact dot product (|4 sum c X| <= 4 * 192 * 2^12 < 2^22).
 // Per group:  y += s * 2^-S (sum c X) + z * sum x   (fp32, ref/quant.py:216-224).
-// The x rounding is relative 2^-13 of the group's largest |x| (below the bf16
-// rounding of the layer's own activations).
+// The x rounding moves each x by at most 2^-12 of the group's largest |x|
+// (tests/test_host.py::test_tiled_core_digit_arithmetic; the layer's own
+// activations carry bf16 rounding, 2^-9 relative).
 #include <algorithm>
 #include <cstdlib>
 

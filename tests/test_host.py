@@ -159,3 +159,42 @@ def test_fp16_metadata_range_check():
             _fp16_meta(bad, "scale")
     with pytest.raises(ArtifactError):
         _fp16_meta([-1e5], "zero point")
+
+
+def test_tiled_core_digit_arithmetic():
+    """The integer arithmetic of the tiled decode core (csrc/tiled.cu), restated
+    in numpy: per (token, 64-column group) X = rint(x 2^S) with S = 138 - E
+    (E = exponent field of max|x|), digits d0 = X >> 7, d1 = X & 127 fit s8;
+    the u8 x s8 sums of 2-bit codes (x1 row, x4 row) stay inside the exact
+    window of the 1.5 * 2^23 magic float; and the group dot product is within
+    2^-12 max|x| sum(c) of the exact one (each x moves by at most half a unit
+    2^-S <= 2^-12 max|x|)."""
+    rng = np.random.default_rng(3)
+    magic = np.float32(12582912.0)
+    for scale in (1e-30, 1e-3, 1.0, 7.5, 3e4):
+        x = (rng.standard_normal((256, 64)) * scale).astype(np.float32)
+        x[0] = 0.0
+        x[1, :] = scale  # all equal: the rounding edge |X| = 2^12
+        amax = np.abs(x).max(axis=1)
+        E = (amax.view(np.uint32) >> 23) & 255
+        S = np.minimum(138 - E.astype(np.int64), 126)
+        X = np.rint(x.astype(np.float64) * np.exp2(S)[:, None]).astype(np.int64)
+        assert np.abs(X).max() <= 4096
+        d0, d1 = X >> 7, X & 127
+        assert d0.min() >= -128 and d0.max() <= 127 and d1.min() >= 0 and d1.max() <= 127
+        assert np.array_equal(128 * d0 + d1, X)
+        c = rng.integers(0, 4, size=(256, 64))
+        for mult in (1, 4):  # row gid codes x1, row gid+8 codes x4
+            v = 128 * (mult * c * d0).sum(axis=1) + (mult * c * d1).sum(axis=1)
+            assert np.abs(v).max() < 2 ** 22
+            f = (np.full(256, magic).view(np.int32) + v.astype(np.int32)).view(np.float32)
+            inv = np.exp2(-S).astype(np.float32) / mult
+            t = (f.astype(np.float64) * inv - magic.astype(np.float64) * inv)
+            exact = (c * X).sum(axis=1) * np.exp2(-S)
+            assert np.array_equal(t, exact)  # the magic float holds the dot product exactly
+            err = np.abs(exact - (c * x.astype(np.float64)).sum(axis=1))
+            bound = 0.5 * np.exp2(-S) * c.sum(axis=1)
+            assert np.all(err <= bound + 1e-300)
+            live = amax > 0  # an all-zero group is exact (X = 0)
+            assert np.all(err[~live] == 0)
+            assert np.all(bound[live] <= np.exp2(-12) * amax[live] * c.sum(axis=1)[live])
